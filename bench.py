@@ -1,0 +1,561 @@
+"""MG-WFBP on B200: ResNet-50 iteration time at N GPUs (+ WFBP / SyncEASGD on the same
+kernels, the fitted alpha/beta model, all-reduce bus GB/s vs size, rooflines).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...          (N > 1, one rank per GPU)
+
+A *step* is one emulated training iteration (Algorithm 2) of the ResNet-50 layer
+profile: simulated backward on a compute stream, every merge group packed (K1),
+all-reduced over NVLink (K2/K3, N > 1) and unpacked (K4) on a comm stream as soon as
+its head layer's gradient exists.  The headline is the MG-WFBP plan, planned from an
+(a, b) fitted on this box; WFBP and SyncEASGD run on the same kernels.
+
+Prints ONE JSON line on rank 0 (contract in the task statement).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import pathlib
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "ResNet-50 iter time + scaling eff. at 1/2/4/8 B200; allreduce bus GB/s vs size"
+# Backward/forward seconds of torchvision ResNet-50 at the paper's batch size 32
+# (PAPER.md:468), fp32 weights, measured on one B200 by scripts/measure_backward.py
+# (profiles/backward_times_b200.json).  Only the totals enter resnet50_like(); the
+# per-layer split is the reference's FLOPs proxy (model_profile.py:193-208).
+PROFILE_TIMES = ROOT / "profiles" / "backward_times_b200.json"
+FIT_SIZES = [1 << k for k in range(12, 27)]  # 4 KiB .. 64 MiB (BASELINE sweep)
+L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+
+
+def b200_profile():
+    from paper_1811_11141_b200 import resnet50_like
+
+    bwd, fwd = 0.0171, 0.0085  # fallback if the measurement file is absent
+    if PROFILE_TIMES.exists():
+        doc = json.loads(PROFILE_TIMES.read_text())
+        bwd, fwd = doc["resnet50_bs32"]["backward_s"], doc["resnet50_bs32"]["forward_s"]
+    return resnet50_like(backward_seconds=bwd, forward_seconds=fwd), bwd, fwd
+
+
+def peaks():
+    path = ROOT / "MEASURED_PEAKS.json"
+    if path.exists():
+        doc = json.loads(path.read_text())
+        return float(doc["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+NVLINK_PEAK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md); 900 nominal
+
+
+# --------------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (rank 0)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        if not getattr(self, "lines", None):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except (ValueError, IndexError):
+                continue
+            for name, flag in zip(names, parts[5:9]):
+                if flag.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# --------------------------------------------------------------- our arm
+
+
+def _dist_setup(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}; launch N>1 with torchrun")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def _barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def _max_over_ranks(values, world, device):
+    import torch
+
+    t = torch.tensor(values, dtype=torch.float64, device=device)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.tolist()
+
+
+def _group_exchange_times(session, comm, world, device, sizes, repeats=20, warmups=3):
+    """Median device seconds of one group exchange (pack + all-reduce + unpack; N=1:
+    pack + unpack) per size, CUDA events on the comm stream, max over ranks."""
+    import ctypes
+
+    import torch
+
+    from paper_1811_11141_b200 import _native
+
+    stream = torch.cuda.Stream(device=device)
+    out = []
+    scratch = torch.empty(max(sizes) // 4, dtype=torch.float32, device=device)
+    local_bucket = torch.empty_like(scratch) if world == 1 else None
+    for nbytes in sizes:
+        n = nbytes // 4
+        src = scratch[:n]
+        table = _native.DeviceTable([(src.data_ptr(), n, 0)])
+        marks = []
+        with torch.cuda.stream(stream):
+            for r in range(warmups + repeats):
+                src.fill_(1.0)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                h = stream.cuda_stream
+                if world == 1:
+                    _native.call("mgw_pack", table.ptr, 1, local_bucket.data_ptr(), n, ctypes.c_float(1.0), h)
+                    _native.call("mgw_unpack", table.ptr, 1, local_bucket.data_ptr(), n, h)
+                else:
+                    _native.call("mgw_comm_pack", comm, table.ptr, 1, n, ctypes.c_float(1.0), h)
+                    _native.call("mgw_allreduce", comm, n, _native.ALGO_AUTO, h)
+                    _native.call("mgw_unpack", table.ptr, 1, session.result_ptr(), n, h)
+                b.record(stream)
+                if r >= warmups:
+                    marks.append((a, b))
+        stream.synchronize()
+        table.close()
+        out.append(statistics.median(x.elapsed_time(y) * 1e-3 for x, y in marks))
+    if session is not None:
+        session.raise_if_failed()
+    return _max_over_ranks(out, world, device)
+
+
+def _allreduce_sweep(session, comm, world, device, sizes, repeats=20, warmups=3):
+    """Bus GB/s of our one-shot / two-shot kernels alone and of ncclAllReduce."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1811_11141_b200 import _native
+
+    stream = torch.cuda.Stream(device=device)
+    rows = []
+    buf = torch.ones(max(sizes) // 4, dtype=torch.float32, device=device)
+    for nbytes in sizes:
+        n = nbytes // 4
+        res = {"bytes": nbytes}
+        for label, algo in (("oneshot", _native.ALGO_ONESHOT), ("twoshot", _native.ALGO_TWOSHOT)):
+            if algo == _native.ALGO_ONESHOT and nbytes > (64 << 20):
+                continue
+            marks = []
+            with torch.cuda.stream(stream):
+                for r in range(warmups + repeats):
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(stream)
+                    _native.call("mgw_allreduce", comm, n, algo, stream.cuda_stream)
+                    b.record(stream)
+                    if r >= warmups:
+                        marks.append((a, b))
+            stream.synchronize()
+            res[label + "_s"] = statistics.median(x.elapsed_time(y) * 1e-3 for x, y in marks)
+        x = buf[:n]
+        marks = []
+        with torch.cuda.stream(stream):
+            for r in range(warmups + repeats):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                dist.all_reduce(x)
+                b.record(stream)
+                if r >= warmups:
+                    marks.append((a, b))
+        stream.synchronize()
+        res["nccl_s"] = statistics.median(x_.elapsed_time(y_) * 1e-3 for x_, y_ in marks)
+        rows.append(res)
+    session.raise_if_failed()
+    keys = [k for k in ("oneshot_s", "twoshot_s", "nccl_s")]
+    flat = [r.get(k, 0.0) for r in rows for k in keys]
+    flat = _max_over_ranks(flat, world, device)
+    out = []
+    for i, r in enumerate(rows):
+        entry = {"bytes": r["bytes"]}
+        for j, k in enumerate(keys):
+            t = flat[i * len(keys) + j]
+            if t > 0:
+                entry[k.replace("_s", "_us")] = round(t * 1e6, 2)
+                entry[k.replace("_s", "_busbw_gbs")] = round(2 * (world - 1) / world * r["bytes"] / t / 1e9, 1)
+        out.append(entry)
+    return out
+
+
+def run_ours(args) -> dict | None:
+    import torch
+
+    from paper_1811_11141_b200 import (
+        CommModel,
+        Measurement,
+        MergePlan,
+        find_merge_plan,
+        fit_ab,
+        simulate_mgwfbp,
+        simulate_sync_easgd,
+        simulate_wfbp,
+    )
+    from paper_1811_11141_b200.allreduce_net import open_session_dist
+    from paper_1811_11141_b200.overlap import OverlappedIteration
+
+    rank, world, local = _dist_setup(args)
+    device = torch.device("cuda", local)
+    profile, bwd, fwd = b200_profile()
+    n = profile.num_layers
+    session = comm = None
+    if world > 1:
+        _, session = open_session_dist(capacity_bytes=4 * profile.total_params)
+        comm = session.comm
+
+    # 1. fit the startup/bandwidth model of one group exchange on this box
+    exch = _group_exchange_times(session, comm, world, device, FIT_SIZES)
+    fit_pts = [(s, t) for s, t in zip(FIT_SIZES, exch) if s <= 32 << 20]
+    model = fit_ab([Measurement(s, t, max(world, 2)) for s, t in fit_pts])
+    plans = {
+        "wfbp": MergePlan(frozenset(), n),
+        "synceasgd": MergePlan(frozenset(range(2, n + 1)), n),
+        "mgwfbp": find_merge_plan(profile, model),
+    }
+    predicted = {
+        "wfbp": simulate_wfbp(profile, model),
+        "synceasgd": simulate_sync_easgd(profile, model),
+        "mgwfbp": simulate_mgwfbp(profile, model, plans["mgwfbp"]),
+    }
+
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=device)
+    results = {}
+    headline = None
+    for name in ("wfbp", "synceasgd", "mgwfbp"):
+        it = OverlappedIteration(profile, plans[name], comm=comm, rank=rank, world=world, device=device,
+                                 fill=True, graph=not args.no_graph)
+        try:
+            for _ in range(args.warmup):
+                with torch.cuda.stream(it.compute_stream):
+                    flush.zero_()
+                it.run()
+            if not it.verify():
+                raise RuntimeError(f"{name}: reduced gradients differ from the expected sums")
+            _barrier(world)
+            torch.cuda.synchronize()
+            sampler = ClockSampler(local) if (rank == 0 and name == "mgwfbp") else None
+            if sampler:
+                sampler.__enter__()
+            wall0 = time.perf_counter()
+            t_iter, compute, exposed, kern = [], [], [], []
+            for _ in range(args.steps):
+                with torch.cuda.stream(it.compute_stream):
+                    flush.zero_()  # L2 flush between iterations, outside the iteration's events
+                times = it.run()
+                t_iter.append(times.t_iter)
+                compute.append(times.compute_time)
+                exposed.append(times.t_c_no)
+                kern.append(it.kernel_times())
+            torch.cuda.synchronize()
+            wall = time.perf_counter() - wall0
+            _barrier(world)
+            if sampler:
+                sampler.__exit__(None, None, None)
+            if session is not None:
+                session.raise_if_failed()
+            ok = it.verify()
+            t_iter_max = _max_over_ranks(t_iter, world, device)
+            compute_max = _max_over_ranks(compute, world, device)
+            exposed_max = _max_over_ranks(exposed, world, device)
+            gbytes = it.group_bytes()
+            res = {
+                "t_iter_ms": round(statistics.fmean(t_iter_max) * 1e3, 4),
+                "t_iter_ms_min": round(min(t_iter_max) * 1e3, 4),
+                "compute_ms": round(statistics.fmean(compute_max) * 1e3, 4),
+                "t_c_no_us": round(statistics.fmean(exposed_max) * 1e6, 2),
+                "scaling_eff": round(statistics.fmean(compute_max) / statistics.fmean(t_iter_max), 5),
+                "predicted_t_iter_ms": round(predicted[name].t_iter * 1e3, 4),
+                "predicted_t_c_no_us": round(predicted[name].t_c_no * 1e6, 2),
+                "groups": len(gbytes),
+                "verified": ok,
+                "wall_s": round(wall, 4),
+            }
+            results[name] = res
+            if name == "mgwfbp":
+                headline = (it, kern, gbytes, sampler, t_iter_max, wall)
+                launches = it.launches_per_iteration
+        finally:
+            if name != "mgwfbp":
+                it.close()
+
+    it, kern, gbytes, sampler, t_iter_max, wall = headline
+    # roofline of the dominant kernel inside the MG-WFBP timed region
+    pack_s = sum(sum(k[0]) for k in kern)
+    ar_s = sum(sum(k[1]) for k in kern)
+    unpack_s = sum(sum(k[2]) for k in kern)
+    launches_of = {"pack": len(kern) * sum(1 for b in gbytes if b), "unpack": len(kern) * sum(1 for b in gbytes if b)}
+    hbm_peak, hbm_src = peaks()
+    kernels = {"pack": pack_s, "unpack": unpack_s}
+    if world > 1:
+        kernels["allreduce"] = ar_s
+    dominant = max(kernels, key=kernels.get)
+    total_bytes = sum(gbytes)
+    if dominant in ("pack", "unpack"):
+        algo_bytes = 2 * total_bytes * len(kern)  # read + write of every bucket byte
+        achieved = algo_bytes / kernels[dominant] / 1e9
+        roofline = {"bound": "hbm", "kernel": f"K1 {dominant}" if dominant == "pack" else "K4 unpack",
+                    "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                    "frac": round(achieved / hbm_peak, 4), "peak_source": hbm_src,
+                    "bytes_per_step": 2 * total_bytes, "launches_per_step": launches_of[dominant] // max(1, len(kern))}
+    else:
+        bus = 2 * (world - 1) / world * total_bytes * len(kern)
+        achieved = bus / ar_s / 1e9
+        roofline = {"bound": "nvlink", "kernel": "K2/K3 all-reduce", "achieved": round(achieved, 1),
+                    "peak": NVLINK_PEAK_GBS, "unit": "GB/s", "frac": round(achieved / NVLINK_PEAK_GBS, 4),
+                    "peak_source": "measured peer copy per direction, B200_PROFILING.md (900 nominal)",
+                    "bytes_per_step": int(2 * (world - 1) / world * total_bytes)}
+    traffic_file = ROOT / "profiles" / "roofline_traffic.json"
+    roofline["traffic"] = None
+    if traffic_file.exists():
+        roofline["traffic"] = json.loads(traffic_file.read_text()).get(f"{roofline['kernel']}@N{world}")
+    roofline["kernel_ms_per_step"] = {k: round(v / len(kern) * 1e3, 4) for k, v in kernels.items()}
+
+    # e2e: the same MG-WFBP iteration with host buffers (H2D of every layer's gradient,
+    # D2H of every reduced gradient) inside the timed region
+    e2e_it = OverlappedIteration(profile, plans["mgwfbp"], comm=comm, rank=rank, world=world, device=device,
+                                 host_io=True, graph=not args.no_graph)
+    try:
+        for _ in range(args.warmup):
+            e2e_it.run()
+        _barrier(world)
+        e2e_times = []
+        for _ in range(args.steps):
+            with torch.cuda.stream(e2e_it.compute_stream):
+                flush.zero_()
+            e2e_times.append(e2e_it.run().t_iter)
+        e2e_ok = e2e_it.verify()
+        h2d, d2h = e2e_it.io_bytes()
+    finally:
+        e2e_it.close()
+    e2e_max = _max_over_ranks(e2e_times, world, device)
+
+    sweep = None
+    if world > 1 and not args.no_sweep:
+        sweep = _allreduce_sweep(session, comm, world, device, FIT_SIZES)
+    it.close()
+    if session is not None:
+        session.close()
+    if rank != 0:
+        return None
+
+    mg = results["mgwfbp"]
+    line = {
+        "metric": METRIC,
+        "value": mg["t_iter_ms"],
+        "unit": "ms",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": mg["t_iter_ms"],
+        "higher_is_better": False,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "fp32",
+        "data": "synthetic (reference gradient pattern rank+1+layer%5, rewritten every iteration)",
+        "config": {
+            "workload": "resnet50_like (54 layers, 25,503,912 fp32 params = 102,015,648 B), MG-WFBP iteration",
+            "backward_s": bwd,
+            "forward_s": fwd,
+            "timings": "B200-class: torchvision ResNet-50 bs32 fwd/bwd measured on one B200, split by the "
+                       "reference FLOPs proxy",
+            "strategy": "mgwfbp",
+            "plan_groups": len(plans["mgwfbp"].groups()),
+            "merged_layers": sorted(plans["mgwfbp"].merged_layers),
+            "fitted_a_us": round(model.a * 1e6, 3),
+            "fitted_b_ns_per_byte": model.b * 1e9,
+            "parallelism": f"dp{world}",
+            "l2": "flushed between iterations (256 MiB write on the compute stream, outside the timed events)",
+            "cuda_graph": not args.no_graph,
+        },
+        "strategies": results,
+        "roofline": roofline,
+        "e2e": {"value": round(statistics.fmean(e2e_max) * 1e3, 4), "unit": "ms",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "verified": e2e_ok},
+        "gpu_launches": launches * args.steps,
+        "group_exchange_us": {str(s): round(t * 1e6, 2) for s, t in zip(FIT_SIZES, exch)},
+        "timed_wall_s": round(wall, 4),
+    }
+    if sweep is not None:
+        line["allreduce_sweep"] = sweep
+    if sampler is not None:
+        line["clocks"] = sampler.summary()
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(profile, plans["mgwfbp"], world, args.cpu_seconds)
+    return line
+
+
+# --------------------------------------------------------- reference arm (CPU)
+
+
+def _cpu_plan(profile, n_ranks):
+    """The reference workflow on its own transport: fit (a, b) on the CPU ring, plan."""
+    from oracle import emulation
+    from paper_1811_11141_b200 import Measurement, MergePlan, find_merge_plan, fit_ab
+
+    if n_ranks < 2:
+        return MergePlan(frozenset(), profile.num_layers), None
+    sizes = [1 << k for k in range(14, 25, 2)]
+    ms = [Measurement(s, emulation.ring_seconds(n_ranks, s, repeats=3), n_ranks) for s in sizes]
+    model = fit_ab(ms)
+    return find_merge_plan(profile, model), model
+
+
+def cpu_baseline(profile, plan, n_ranks, seconds):
+    from oracle import emulation
+
+    walls, ok = emulation.emulate(profile, plan, n_ranks, 10_000, warmup=1, time_budget_s=seconds)
+    return {
+        "value": round(statistics.fmean(walls) * 1e3, 3),
+        "unit": "ms",
+        "cores": max(1, n_ranks),
+        "kind": "port",
+        "sample": f"{len(walls)} Algorithm-2 iterations of the same resnet50_like profile/plan with {n_ranks} "
+                  f"simulated rank(s) (oracle/emulation.py: reference _delay + C ring, one thread per rank), "
+                  f"~{seconds:.0f} s budget, verified={ok}",
+    }
+
+
+def run_reference(args) -> dict | None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    profile, bwd, fwd = b200_profile()
+    n_ranks = args.gpus
+    plan, model = _cpu_plan(profile, n_ranks)
+    from oracle import emulation
+
+    _, _ = emulation.emulate(profile, plan, n_ranks, args.warmup, warmup=0)
+    t0 = time.perf_counter()
+    walls, ok = emulation.emulate(profile, plan, n_ranks, args.steps, warmup=0,
+                                  time_budget_s=max(10.0, args.cpu_seconds))
+    wall = time.perf_counter() - t0
+    value = round(statistics.fmean(walls) * 1e3, 3)
+    cores = max(1, n_ranks)
+    return {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": "ms",
+        "n_gpus": args.gpus,
+        "steps": len(walls),
+        "warmup": args.warmup,
+        "ms_per_step": value,
+        "higher_is_better": False,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "fp32",
+        "data": "synthetic (reference gradient pattern rank+1+layer%5)",
+        "config": {
+            "workload": "resnet50_like (54 layers, 25,503,912 fp32 params = 102,015,648 B), MG-WFBP iteration",
+            "backward_s": bwd,
+            "forward_s": fwd,
+            "strategy": "mgwfbp",
+            "plan_groups": len(plan.groups()),
+            "fitted_a_us": None if model is None else round(model.a * 1e6, 3),
+            "fitted_b_ns_per_byte": None if model is None else model.b * 1e9,
+            "parallelism": f"{n_ranks} simulated ranks on host cores",
+        },
+        "cpu_baseline": {"value": value, "unit": "ms", "cores": cores, "kind": "port",
+                         "sample": f"{len(walls)} iterations, {n_ranks} simulated rank(s), oracle/emulation.py "
+                                   f"(reference Algorithm 2: _delay agent thread + C ring one thread per rank), "
+                                   f"verified={ok}, wall {wall:.1f} s"},
+        "e2e": {"value": value, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-graph", action="store_true", help="eager stream schedule instead of CUDA-graph replay")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the all-reduce bus-bandwidth sweep (N > 1)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    line = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    if args.impl == "ours" and args.gpus > 1:
+        import torch.distributed as dist
+
+        if dist.is_initialized():
+            dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    raise SystemExit(main())

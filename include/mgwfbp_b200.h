@@ -1,0 +1,139 @@
+/*
+ * mgwfbp_b200.h -- C ABI of the B200-native MG-WFBP merged-gradient data path.
+ *
+ * Plain C types only (pointers, sizes, ints); no torch types cross this
+ * boundary.  Every function returns an int status:
+ *
+ *   MGW_OK     0  success
+ *   MGW_EINVAL 1  invalid argument                     -> Python ValueError
+ *   MGW_EPROTO 2  peer / length / timeout disagreement -> Python ProtocolError
+ *   MGW_ECUDA  3  CUDA runtime failure                 -> Python RuntimeError
+ *
+ * and leaves a message readable with mgw_last_error().  Data-path calls are
+ * asynchronous on the caller's cudaStream_t (passed as void*).
+ *
+ * Which reference interface each entry point replaces
+ * (reference = /root/reference/pkg/src/mgwfbp):
+ *
+ *   mgw_spin_ns / sched spins    <- allreduce_net.py:448-460  (_delay, simulated backward)
+ *   mgw_pack / mgw_comm_pack     <- allreduce_net.py:544-546  (per-layer fill of the group
+ *                                   buffer, layout :495-509: layer `high` at offset 0)
+ *   mgw_comm_create / open_peers <- allreduce_net.py:180-262  (rendezvous + RingSession:
+ *                                   here CUDA-IPC handles instead of TCP ports)
+ *   mgw_allreduce                <- allreduce_net.py:370-411  (ring_allreduce; same per-
+ *                                   element fold order)
+ *   mgw_comm_error               <- allreduce_net.py:309-357  (frame/header validation ->
+ *                                   ProtocolError; here a device error word)
+ *   mgw_unpack                   <- (no reference counterpart: the reference verifies the
+ *                                   reduced buffer in place, allreduce_net.py:556)
+ *   mgw_sched_*                  <- allreduce_net.py:463-578  (run_emulation: compute agent
+ *                                   thread + queue -> compute stream + comm stream)
+ *   mgw_check_const              <- allreduce_net.py:556      (np.array_equal verification)
+ */
+#ifndef MGWFBP_B200_H
+#define MGWFBP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MGW_OK 0
+#define MGW_EINVAL 1
+#define MGW_EPROTO 2
+#define MGW_ECUDA 3
+
+#define MGW_MAX_RANKS 8
+#define MGW_IPC_HANDLE_BYTES 64
+
+/* device error word values (mgw_comm_error) */
+#define MGW_DEV_OK 0
+#define MGW_DEV_LENGTH_MISMATCH 1 /* ranks disagree on the bucket length */
+#define MGW_DEV_TIMEOUT 2         /* a peer never arrived at the barrier */
+#define MGW_DEV_PEER_ABORT 3      /* a peer detected an error and aborted */
+
+/* all-reduce algorithm selection */
+#define MGW_ALGO_AUTO 0
+#define MGW_ALGO_ONESHOT 1
+#define MGW_ALGO_TWOSHOT 2
+
+/* schedule flags */
+#define MGW_SCHED_FILL 1u  /* "backward" writes fill_values into each layer before its deadline */
+#define MGW_SCHED_GRAPH 2u /* capture the iteration once into a CUDA graph and replay it */
+#define MGW_SCHED_HOSTIO 4u /* e2e: H2D of each layer from host_src, D2H of the result to host_dst */
+
+typedef struct mgw_comm mgw_comm;
+typedef struct mgw_sched mgw_sched;
+
+/* One layer tensor inside a bucket: `count` fp32 elements at `ptr` (device, or
+ * pinned host for host_src/host_dst) occupying bucket elements
+ * [offset, offset + count). */
+typedef struct {
+  float* ptr;
+  int64_t count;
+  int64_t offset;
+} mgw_tensor_desc;
+
+/* One merge group of a schedule, given in send order (descending layer index). */
+typedef struct {
+  int32_t head_layer; /* lowest layer of the group: the sender (merge_planner.py:67-84) */
+  int32_t desc_begin; /* first row of the schedule's descriptor table for this group */
+  int32_t desc_count; /* rows belonging to this group (layers high..low) */
+  int32_t algo;       /* MGW_ALGO_* */
+  int64_t n_elem;     /* bucket elements = sum of the group's layer params */
+  int64_t ready_ns;   /* tau_b[head] + t_b[head]: when the head's gradient exists (ns from
+                         iteration start, schedule_sim.py:103-127) */
+} mgw_group;
+
+/* ---- library ---------------------------------------------------------- */
+const char* mgw_version(void);
+int mgw_last_error(char* buf, size_t len);
+int mgw_device_count(int* out);
+
+/* ---- K5: simulated backward ------------------------------------------- */
+int mgw_spin_ns(int64_t ns, void* stream);
+
+/* ---- K1 pack+scale / K4 unpack ---------------------------------------- */
+int mgw_desc_upload(const mgw_tensor_desc* rows, int n, void** dev_table);
+int mgw_desc_free(void* dev_table);
+int mgw_pack(const void* dev_table, int n, float* bucket, int64_t bucket_elems, float scale, void* stream);
+int mgw_unpack(const void* dev_table, int n, const float* bucket, int64_t bucket_elems, void* stream);
+int mgw_fill_const(const void* dev_table, int n, const float* values_dev, void* stream);
+int mgw_check_const(const void* dev_table, int n, const float* values_dev, int64_t* mismatches, void* stream);
+
+/* ---- communicator: CUDA-IPC peer buckets over NVLink/NVSwitch --------- */
+int mgw_comm_create(int rank, int world, int device, int64_t capacity_bytes, mgw_comm** out,
+                    uint8_t* ipc_handle_out);
+int mgw_comm_open_peers(mgw_comm* comm, const uint8_t* handles /* world * 64 bytes */);
+int mgw_comm_destroy(mgw_comm* comm);
+int mgw_comm_set_timeout_ms(mgw_comm* comm, int64_t ms);
+int mgw_comm_set_oneshot_max(mgw_comm* comm, int64_t bytes);
+int mgw_comm_input(mgw_comm* comm, float** slot); /* slot the next collective reads (syncs) */
+int mgw_comm_result(mgw_comm* comm, float** result);
+int mgw_comm_pack(mgw_comm* comm, const void* dev_table, int n, int64_t n_elem, float scale, void* stream);
+int mgw_allreduce(mgw_comm* comm, int64_t n_elem, int algo, void* stream);
+int mgw_comm_error(mgw_comm* comm, int* code);
+int mgw_comm_calls(mgw_comm* comm, int64_t* calls);
+
+/* ---- emulated ranks on one device (test path; no barriers) ------------ */
+int mgw_allreduce_emulated(float* const* ins, float* const* outs, int world, int64_t n_elem, int algo,
+                           void* stream);
+
+/* ---- Algorithm 2 on streams ------------------------------------------- */
+int mgw_sched_create(mgw_comm* comm /* NULL: single rank */, const mgw_tensor_desc* rows, int n_rows,
+                     const mgw_group* groups, int n_groups, float scale, uint32_t flags,
+                     const float* fill_values /* per row, or NULL */, float* const* host_src /* per row */,
+                     float* const* host_dst /* per row */, mgw_sched** out);
+int mgw_sched_run(mgw_sched* sched, void* compute_stream, void* comm_stream);
+int mgw_sched_times(mgw_sched* sched, double* t_iter_s, double* compute_s, double* group_comm_s);
+int mgw_sched_kernel_times(mgw_sched* sched, double* pack_s, double* allreduce_s, double* unpack_s);
+int mgw_sched_launches(mgw_sched* sched, int* kernels_per_iteration);
+int mgw_sched_destroy(mgw_sched* sched);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MGWFBP_B200_H */

@@ -1,0 +1,169 @@
+"""K1 pack+scale, K4 unpack, fill/check, K5 spin, and the K2/K3 fold order -- on one B200.
+
+Multi-rank all-reduce on one device uses the emulated-rank entry point (one launch
+per rank and phase, no barriers, the same device reduction code), which is how the
+fold order is checked bit-exactly against the reference's ring outputs without
+running mutually-waiting kernels on one GPU."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+from conftest import golden_ring
+from oracle import ring_oracle
+from paper_1811_11141_b200 import _native
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    torch.cuda.set_device(0)
+    return torch
+
+
+def _rows_for(tensors, counts):
+    rows, off = [], 0
+    for t, p in zip(tensors, counts):
+        rows.append((t.data_ptr(), p, off))
+        off += p
+    return rows, off
+
+
+@pytest.mark.parametrize("counts,shift", [
+    ([4096, 2359296, 1000, 3, 0 + 17, 9408], 0),   # resnet-ish + odd sizes
+    ([1, 2, 3, 5, 7, 11, 13, 1 << 16], 1),         # misaligned tensor starts
+    ([768] * 40 + [3072, 23440896 // 64], 3),      # many small BERT-like tensors
+])
+def test_pack_unpack_bitwise(torch_cuda, counts, shift):
+    torch = torch_cuda
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    bases = [torch.randn(p + shift, generator=gen, device="cuda") for p in counts]
+    tensors = [b[shift:] for b in bases]
+    rows, total = _rows_for(tensors, counts)
+    table = _native.DeviceTable(rows)
+    bucket = torch.full((total,), float("nan"), device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+    _native.call("mgw_pack", table.ptr, table.n, bucket.data_ptr(), total, ctypes.c_float(1.0), stream)
+    want = ring_oracle.pack_group({k + 1: t.cpu().numpy() for k, t in enumerate(reversed(tensors))},
+                                  list(reversed(counts)), 1, len(counts))
+    assert np.array_equal(bucket.cpu().numpy().view("<u4"), want.view("<u4"))
+    outs = [torch.zeros(p + shift, device="cuda")[shift:] for p in counts]
+    out_rows, _ = _rows_for(outs, counts)
+    out_table = _native.DeviceTable(out_rows)
+    _native.call("mgw_unpack", out_table.ptr, out_table.n, bucket.data_ptr(), total, stream)
+    for a, b in zip(outs, tensors):
+        assert torch.equal(a.view(torch.int32), b.view(torch.int32))
+    table.close()
+    out_table.close()
+
+
+def test_pack_scale_is_exact_power_of_two(torch_cuda):
+    torch = torch_cuda
+    x = torch.randn(100003, device="cuda")
+    table = _native.DeviceTable([(x.data_ptr(), x.numel(), 0)])
+    bucket = torch.empty_like(x)
+    _native.call("mgw_pack", table.ptr, 1, bucket.data_ptr(), x.numel(), ctypes.c_float(0.125),
+                 torch.cuda.current_stream().cuda_stream)
+    want = x.cpu().numpy() * np.float32(0.125)
+    assert np.array_equal(bucket.cpu().numpy().view("<u4"), want.view("<u4"))
+    table.close()
+
+
+def test_fill_and_check(torch_cuda):
+    torch = torch_cuda
+    counts = [5, 4096, 33, 1 << 20]
+    tensors = [torch.zeros(p, device="cuda") for p in counts]
+    rows, _ = _rows_for(tensors, counts)
+    table = _native.DeviceTable(rows)
+    vals = torch.tensor([1.0, 2.0, 3.0, 4.0], device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    _native.call("mgw_fill_const", table.ptr, table.n, vals.data_ptr(), s)
+    for t, v in zip(tensors, (1.0, 2.0, 3.0, 4.0)):
+        assert bool((t == v).all())
+    bad = ctypes.c_int64()
+    _native.call("mgw_check_const", table.ptr, table.n, vals.data_ptr(), ctypes.byref(bad), s)
+    assert bad.value == 0
+    tensors[3][17] = 0.5
+    tensors[0][4] = 9.0
+    _native.call("mgw_check_const", table.ptr, table.n, vals.data_ptr(), ctypes.byref(bad), s)
+    assert bad.value == 2
+    table.close()
+
+
+def test_spin_ns_duration(torch_cuda):
+    torch = torch_cuda
+    s = torch.cuda.current_stream()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    _native.call("mgw_spin_ns", 100_000, s.cuda_stream)
+    a.record(s)
+    _native.call("mgw_spin_ns", 2_000_000, s.cuda_stream)
+    b.record(s)
+    b.synchronize()
+    ms = a.elapsed_time(b)
+    assert 1.99 <= ms < 2.3
+
+
+def _emulated(torch, ins, algo, in_place=False):
+    n = ins[0].numel()
+    world = len(ins)
+    outs = list(ins) if in_place else [torch.full((max(n, 1),), float("nan"), device="cuda")[:n] for _ in ins]
+    ip = (ctypes.c_void_p * world)(*[t.data_ptr() for t in ins])
+    op = (ctypes.c_void_p * world)(*[t.data_ptr() for t in outs])
+    _native.call("mgw_allreduce_emulated", ip, op, world, n, algo, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    return outs
+
+
+@pytest.mark.parametrize("algo", [_native.ALGO_ONESHOT, _native.ALGO_TWOSHOT])
+@pytest.mark.parametrize("n_ranks", [2, 3, 4, 8])
+@pytest.mark.parametrize("n", [1, 17, 1001, 4099])
+def test_fold_order_bit_exact_vs_reference_ring(torch_cuda, algo, n_ranks, n):
+    torch = torch_cuda
+    g = golden_ring()
+    ins = [torch.from_numpy(g[f"in_N{n_ranks}_n{n}_r{r}"].copy()).cuda() for r in range(n_ranks)]
+    want = g[f"out_N{n_ranks}_n{n}"]
+    for out in _emulated(torch, ins, algo):
+        assert np.array_equal(out.cpu().numpy().view("<u4"), want.view("<u4"))
+
+
+@pytest.mark.parametrize("algo", [_native.ALGO_ONESHOT, _native.ALGO_TWOSHOT])
+@pytest.mark.parametrize("n_ranks", [2, 5, 7, 8])
+def test_fold_order_large_vs_oracle(torch_cuda, algo, n_ranks):
+    torch = torch_cuda
+    n = (1 << 20) + 3
+    rng = np.random.default_rng(n_ranks)
+    host = [(rng.standard_normal(n) * 10.0 ** rng.integers(-3, 4, n)).astype("<f4") for _ in range(n_ranks)]
+    want = ring_oracle.ring_allreduce(host)[0]
+    ins = [torch.from_numpy(h.copy()).cuda() for h in host]
+    for out in _emulated(torch, ins, algo):
+        assert np.array_equal(out.cpu().numpy().view("<u4"), want.view("<u4"))
+
+
+def test_twoshot_in_place(torch_cuda):
+    torch = torch_cuda
+    n = 12345
+    host = [np.random.default_rng(r).standard_normal(n).astype("<f4") for r in range(4)]
+    want = ring_oracle.ring_allreduce(host)[0]
+    ins = [torch.from_numpy(h.copy()).cuda() for h in host]
+    for out in _emulated(torch, ins, _native.ALGO_TWOSHOT, in_place=True):
+        assert np.array_equal(out.cpu().numpy().view("<u4"), want.view("<u4"))
+
+
+def test_integer_payloads_exact(torch_cuda):
+    """The reference's exact-sum payloads (allreduce_net tests): arange + rank, rank + 1."""
+    torch = torch_cuda
+    for world in (2, 3, 4, 8):
+        ins = [torch.arange(23, dtype=torch.float32, device="cuda") + r for r in range(world)]
+        want = torch.arange(23, dtype=torch.float32, device="cuda") * world + world * (world - 1) / 2
+        for algo in (_native.ALGO_ONESHOT, _native.ALGO_TWOSHOT):
+            for out in _emulated(torch, ins, algo):
+                assert torch.equal(out, want)
+        ones = [torch.full((1_000_000,), float(r + 1), device="cuda") for r in range(world)]
+        for out in _emulated(torch, ones, _native.ALGO_TWOSHOT):
+            assert bool((out == world * (world + 1) / 2).all())

@@ -1,0 +1,106 @@
+"""The reference's collective and emulation tests, run through the real multi-process
+CUDA-IPC path (one process per GPU).  Skipped unless >= 2 GPUs are visible; run with
+`gpurun --gpus 2|4 -- python -m pytest tests -m gpu`."""
+
+from functools import partial
+
+import numpy as np
+import pytest
+
+import _mp_tasks
+from conftest import cuda_devices, golden_ring, make_profile
+from paper_1811_11141_b200 import (
+    EmulationReport,
+    MergePlan,
+    bench_local,
+    emulate_local,
+    find_merge_plan,
+    fit_ab,
+    run_workers,
+    simulate_mgwfbp,
+    synth_profile,
+)
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+
+@pytest.fixture(autouse=True)
+def _two_gpus():
+    if cuda_devices() < 2:
+        pytest.skip("needs >= 2 GPUs (one process per GPU)")
+
+
+def _worlds():
+    n = cuda_devices()
+    return [w for w in (2, 3, 4, 8) if w <= n]
+
+
+def test_exact_sums_and_counters():
+    for n in _worlds():
+        results = run_workers(n, _mp_tasks.sum_task)
+        assert set(results) == set(range(n))
+        assert all(frames == 2 for frames in results.values())
+
+
+def test_payload_smaller_than_group():
+    n = max(_worlds())
+    assert all(run_workers(n, _mp_tasks.single_element_task).values())
+
+
+def test_length_mismatch_is_a_protocol_error():
+    with pytest.raises(RuntimeError) as err:
+        run_workers(2, _mp_tasks.mismatched_task, timeout=60)
+    assert "buffer lengths" in str(err.value) or "ProtocolError" in str(err.value)
+
+
+def test_criterion_7_collective_correctness():
+    for n in _worlds():
+        for verdicts in run_workers(n, _mp_tasks.collective_task).values():
+            assert all(verdicts)
+
+
+def test_random_payloads_bit_exact_vs_reference_ring():
+    g = golden_ring()
+    for n in _worlds():
+        arrays = [{f"n{size}": g[f"in_N{n}_n{size}_r{r}"] for size in (1, 17, 1001, 4099)} for r in range(n)]
+        results = run_workers(n, partial(_mp_tasks.random_task, arrays=arrays))
+        for size in (1, 17, 1001, 4099):
+            want = g[f"out_N{n}_n{size}"].view("<u4")
+            for r in range(n):
+                assert np.array_equal(results[r][f"n{size}"].view("<u4"), want)
+                assert np.array_equal(results[r][f"n{size}_tensor"].view("<u4"), want)
+
+
+def test_bench_local_measurement_shape():
+    ms = bench_local(2, [4096, 65536, 1 << 22], repeats=3, warmups=2)
+    assert [m.nbytes for m in ms] == [4096, 65536, 1 << 22]
+    assert all(m.n_nodes == 2 and 0 < m.seconds < 1e-2 for m in ms)
+    with pytest.raises((RuntimeError, ValueError), match="multiples of 4"):
+        bench_local(2, [10], repeats=1, warmups=0)
+
+
+def test_emulate_local_verified_report():
+    profile = make_profile([40, 0, 24, 16], [4e-3, 3e-3, 3e-3, 2e-3], 5e-3)
+    plan = MergePlan(frozenset({4}), 4)
+    reports = emulate_local(2, profile, plan, 3, warmup=1)
+    assert set(reports) == {0, 1}
+    for r in reports.values():
+        assert isinstance(r, EmulationReport) and r.verified
+        assert len(r.iteration_seconds) == 3
+        assert r.allreduce_count == 2 * 4
+        assert set(r.group_comm_seconds) == {1, 3}
+        assert r.mean_seconds >= profile.forward_time + profile.total_backward_time - 1e-4
+
+
+def test_criterion_8_calibrate_then_predict():
+    n = max(_worlds())
+    sizes = [32768, 131072, 262144, 524288, 1048576, 2097152, 4194304, 8388608]
+    model = fit_ab(bench_local(n, sizes, repeats=20, warmups=3))
+    profile = synth_profile(8, param_range=(1e4, 2e5), time_scale=15e-3, seed=1)
+    for plan in (find_merge_plan(profile, model), MergePlan(frozenset(range(2, 9)), 8)):
+        predicted = simulate_mgwfbp(profile, model, plan).t_iter
+        for graph in (False, True):
+            reports = emulate_local(n, profile, plan, 20, warmup=2, graph=graph)
+            assert all(r.verified for r in reports.values())
+            measured = max(r.mean_seconds for r in reports.values())
+            assert abs(measured - predicted) / predicted <= 0.05, (measured, predicted)

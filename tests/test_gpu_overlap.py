@@ -1,0 +1,82 @@
+"""Algorithm 2 on streams (single GPU): the iteration engine reproduces the simulated
+compute timeline, verifies the reference's expected values, and the graph replay
+matches eager execution."""
+
+import pytest
+
+from paper_1811_11141_b200 import CommModel, MergePlan, find_merge_plan, resnet50_like, simulate_mgwfbp, synth_profile
+from paper_1811_11141_b200.overlap import OverlappedIteration
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    torch.cuda.set_device(0)
+    return torch
+
+
+def _plans(profile):
+    n = profile.num_layers
+    model = CommModel(a=2e-5, b=1.5e-12)
+    return {
+        "wfbp": MergePlan(frozenset(), n),
+        "synceasgd": MergePlan(frozenset(range(2, n + 1)), n),
+        "mgwfbp": find_merge_plan(profile, model),
+    }
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_single_gpu_iteration_matches_profile(torch_cuda, graph):
+    profile = resnet50_like(backward_seconds=4e-3, forward_seconds=2e-3)
+    compute = profile.forward_time + profile.total_backward_time
+    for name, plan in _plans(profile).items():
+        it = OverlappedIteration(profile, plan, comm=None, rank=0, world=1, device="cuda:0", graph=graph)
+        try:
+            for _ in range(3):
+                t = it.run()
+            assert it.verify(), name
+            assert abs(t.compute_time - compute) / compute < 0.02, (name, t)
+            assert t.t_iter >= t.compute_time
+            assert 0.0 <= t.t_c_no < 2e-3, (name, t)
+            assert len(t.group_comm) == len(plan.groups())
+        finally:
+            it.close()
+
+
+def test_host_io_end_to_end(torch_cuda):
+    profile = resnet50_like(backward_seconds=8e-3, forward_seconds=4e-3)
+    it = OverlappedIteration(profile, MergePlan(frozenset(), profile.num_layers), comm=None, rank=0, world=1,
+                             device="cuda:0", fill=False, host_io=True)
+    try:
+        it.run()
+        assert it.verify()
+        assert it.io_bytes() == (4 * profile.total_params, 4 * profile.total_params)
+    finally:
+        it.close()
+
+
+def test_many_small_groups_graph(torch_cuda):
+    profile = synth_profile(300, param_range=(1024, 65536), time_scale=2e-5, seed=3)
+    it = OverlappedIteration(profile, None, comm=None, rank=0, world=1, device="cuda:0", graph=True)
+    try:
+        for _ in range(3):
+            t = it.run()
+        assert it.verify()
+        assert t.t_iter >= t.compute_time
+    finally:
+        it.close()
+
+
+def test_launch_count_reported(torch_cuda):
+    profile = resnet50_like(backward_seconds=4e-3, forward_seconds=2e-3)
+    it = OverlappedIteration(profile, None, comm=None, rank=0, world=1, device="cuda:0")
+    try:
+        # mark + per group: spin, fill, pack, unpack
+        assert it.launches_per_iteration == 1 + 4 * profile.num_layers
+    finally:
+        it.close()
