@@ -78,7 +78,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"],
+                 "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
@@ -150,9 +150,10 @@ def _max_over_ranks(values, world, device):
     return t.tolist()
 
 
-def _group_exchange_times(session, comm, world, device, sizes, repeats=20, warmups=3):
-    """Median device seconds of one group exchange (pack + all-reduce + unpack; N=1:
-    pack + unpack) per size, CUDA events on the comm stream, max over ranks."""
+def _exchange_times(comm, world, device, sizes, kind=0, algo=0, repeats=20, warmups=3):
+    """Device seconds per exchange step (kind 0: pack + all-reduce + unpack, N=1: pack +
+    unpack; kind 1: all-reduce kernel alone) per size: `repeats` back-to-back steps under
+    one CUDA event pair (mgw_time_exchange), max over ranks."""
     import ctypes
 
     import torch
@@ -161,91 +162,73 @@ def _group_exchange_times(session, comm, world, device, sizes, repeats=20, warmu
 
     stream = torch.cuda.Stream(device=device)
     out = []
-    scratch = torch.empty(max(sizes) // 4, dtype=torch.float32, device=device)
+    scratch = torch.ones(max(sizes) // 4, dtype=torch.float32, device=device)
     local_bucket = torch.empty_like(scratch) if world == 1 else None
     for nbytes in sizes:
         n = nbytes // 4
-        src = scratch[:n]
-        table = _native.DeviceTable([(src.data_ptr(), n, 0)])
-        marks = []
-        with torch.cuda.stream(stream):
-            for r in range(warmups + repeats):
-                src.fill_(1.0)
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(stream)
-                h = stream.cuda_stream
-                if world == 1:
-                    _native.call("mgw_pack", table.ptr, 1, local_bucket.data_ptr(), n, ctypes.c_float(1.0), h)
-                    _native.call("mgw_unpack", table.ptr, 1, local_bucket.data_ptr(), n, h)
-                else:
-                    _native.call("mgw_comm_pack", comm, table.ptr, 1, n, ctypes.c_float(1.0), h)
-                    _native.call("mgw_allreduce", comm, n, _native.ALGO_AUTO, h)
-                    _native.call("mgw_unpack", table.ptr, 1, session.result_ptr(), n, h)
-                b.record(stream)
-                if r >= warmups:
-                    marks.append((a, b))
-        stream.synchronize()
+        table = _native.DeviceTable([(scratch.data_ptr(), n, 0)])
+        sec = ctypes.c_double()
+        _native.call("mgw_time_exchange", comm, table.ptr, 1, n,
+                     None if local_bucket is None else local_bucket.data_ptr(), algo, kind,
+                     repeats, warmups, ctypes.byref(sec), stream.cuda_stream)
         table.close()
-        out.append(statistics.median(x.elapsed_time(y) * 1e-3 for x, y in marks))
-    if session is not None:
-        session.raise_if_failed()
+        out.append(sec.value)
     return _max_over_ranks(out, world, device)
 
 
-def _allreduce_sweep(session, comm, world, device, sizes, repeats=20, warmups=3):
-    """Bus GB/s of our one-shot / two-shot kernels alone and of ncclAllReduce."""
+def _nccl_times(world, device, sizes, repeats=20, warmups=3):
+    """ncclAllReduce (torch.distributed, comparison only), same loop timing."""
     import torch
     import torch.distributed as dist
 
     from paper_1811_11141_b200 import _native
 
     stream = torch.cuda.Stream(device=device)
-    rows = []
     buf = torch.ones(max(sizes) // 4, dtype=torch.float32, device=device)
-    for nbytes in sizes:
-        n = nbytes // 4
-        res = {"bytes": nbytes}
-        for label, algo in (("oneshot", _native.ALGO_ONESHOT), ("twoshot", _native.ALGO_TWOSHOT)):
-            if algo == _native.ALGO_ONESHOT and nbytes > (64 << 20):
-                continue
-            marks = []
-            with torch.cuda.stream(stream):
-                for r in range(warmups + repeats):
-                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    a.record(stream)
-                    _native.call("mgw_allreduce", comm, n, algo, stream.cuda_stream)
-                    b.record(stream)
-                    if r >= warmups:
-                        marks.append((a, b))
-            stream.synchronize()
-            res[label + "_s"] = statistics.median(x.elapsed_time(y) * 1e-3 for x, y in marks)
-        x = buf[:n]
-        marks = []
-        with torch.cuda.stream(stream):
-            for r in range(warmups + repeats):
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(stream)
-                dist.all_reduce(x)
-                b.record(stream)
-                if r >= warmups:
-                    marks.append((a, b))
-        stream.synchronize()
-        res["nccl_s"] = statistics.median(x_.elapsed_time(y_) * 1e-3 for x_, y_ in marks)
-        rows.append(res)
-    session.raise_if_failed()
-    keys = [k for k in ("oneshot_s", "twoshot_s", "nccl_s")]
-    flat = [r.get(k, 0.0) for r in rows for k in keys]
-    flat = _max_over_ranks(flat, world, device)
     out = []
-    for i, r in enumerate(rows):
-        entry = {"bytes": r["bytes"]}
-        for j, k in enumerate(keys):
-            t = flat[i * len(keys) + j]
-            if t > 0:
-                entry[k.replace("_s", "_us")] = round(t * 1e6, 2)
-                entry[k.replace("_s", "_busbw_gbs")] = round(2 * (world - 1) / world * r["bytes"] / t / 1e9, 1)
-        out.append(entry)
-    return out
+    with torch.cuda.stream(stream):
+        for nbytes in sizes:
+            x = buf[: nbytes // 4]
+            for _ in range(warmups):
+                dist.all_reduce(x)
+            _native.call("mgw_spin_ns", 1_000_000 + 20_000 * repeats, stream.cuda_stream)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(repeats):
+                dist.all_reduce(x)
+            b.record(stream)
+            b.synchronize()
+            out.append(a.elapsed_time(b) * 1e-3 / repeats)
+    return _max_over_ranks(out, world, device)
+
+
+def _allreduce_sweep(session, comm, world, device, sizes):
+    """Bus GB/s vs size: our one-shot and two-shot kernels alone, the full group
+    exchange (pack + all-reduce + unpack), and ncclAllReduce."""
+    from paper_1811_11141_b200 import _native
+
+    one = _exchange_times(comm, world, device, sizes, kind=1, algo=_native.ALGO_ONESHOT)
+    two = _exchange_times(comm, world, device, sizes, kind=1, algo=_native.ALGO_TWOSHOT)
+    nccl = _nccl_times(world, device, sizes)
+    session.raise_if_failed()
+    rows = []
+    for nbytes, t1, t2, tn in zip(sizes, one, two, nccl):
+        bus = 2 * (world - 1) / world * nbytes
+        rows.append({"bytes": nbytes,
+                     "oneshot_us": round(t1 * 1e6, 2), "oneshot_busbw_gbs": round(bus / t1 / 1e9, 1),
+                     "twoshot_us": round(t2 * 1e6, 2), "twoshot_busbw_gbs": round(bus / t2 / 1e9, 1),
+                     "nccl_us": round(tn * 1e6, 2), "nccl_busbw_gbs": round(bus / tn / 1e9, 1)})
+    return rows
+
+
+def _fit(sizes, times, world):
+    from paper_1811_11141_b200 import CommModel, Measurement, fit_ab
+
+    pts = [(s, t) for s, t in zip(sizes, times) if s <= 32 << 20]
+    try:
+        return fit_ab([Measurement(s, t, max(world, 2)) for s, t in pts]), True
+    except ValueError:  # e.g. under a profiler that serialises launches
+        return CommModel(a=min(times), b=0.0), False
 
 
 def run_ours(args) -> dict | None:
@@ -274,9 +257,10 @@ def run_ours(args) -> dict | None:
         comm = session.comm
 
     # 1. fit the startup/bandwidth model of one group exchange on this box
-    exch = _group_exchange_times(session, comm, world, device, FIT_SIZES)
-    fit_pts = [(s, t) for s, t in zip(FIT_SIZES, exch) if s <= 32 << 20]
-    model = fit_ab([Measurement(s, t, max(world, 2)) for s, t in fit_pts])
+    exch = _exchange_times(comm, world, device, FIT_SIZES)
+    if session is not None:
+        session.raise_if_failed()
+    model, fit_ok = _fit(FIT_SIZES, exch, world)
     plans = {
         "wfbp": MergePlan(frozenset(), n),
         "synceasgd": MergePlan(frozenset(range(2, n + 1)), n),
@@ -294,6 +278,9 @@ def run_ours(args) -> dict | None:
     for name in ("wfbp", "synceasgd", "mgwfbp"):
         it = OverlappedIteration(profile, plans[name], comm=comm, rank=rank, world=world, device=device,
                                  fill=True, graph=not args.no_graph)
+        sampler = ClockSampler(local) if (rank == 0 and name == "mgwfbp") else None
+        if sampler:
+            sampler.__enter__()
         try:
             for _ in range(args.warmup):
                 with torch.cuda.stream(it.compute_stream):
@@ -303,9 +290,6 @@ def run_ours(args) -> dict | None:
                 raise RuntimeError(f"{name}: reduced gradients differ from the expected sums")
             _barrier(world)
             torch.cuda.synchronize()
-            sampler = ClockSampler(local) if (rank == 0 and name == "mgwfbp") else None
-            if sampler:
-                sampler.__enter__()
             wall0 = time.perf_counter()
             t_iter, compute, exposed, kern = [], [], [], []
             for _ in range(args.steps):
@@ -319,8 +303,6 @@ def run_ours(args) -> dict | None:
             torch.cuda.synchronize()
             wall = time.perf_counter() - wall0
             _barrier(world)
-            if sampler:
-                sampler.__exit__(None, None, None)
             if session is not None:
                 session.raise_if_failed()
             ok = it.verify()
@@ -349,36 +331,51 @@ def run_ours(args) -> dict | None:
                 it.close()
 
     it, kern, gbytes, sampler, t_iter_max, wall = headline
-    # roofline of the dominant kernel inside the MG-WFBP timed region
-    pack_s = sum(sum(k[0]) for k in kern)
-    ar_s = sum(sum(k[1]) for k in kern)
-    unpack_s = sum(sum(k[2]) for k in kern)
-    launches_of = {"pack": len(kern) * sum(1 for b in gbytes if b), "unpack": len(kern) * sum(1 for b in gbytes if b)}
-    hbm_peak, hbm_src = peaks()
-    kernels = {"pack": pack_s, "unpack": unpack_s}
+    # roofline of the dominant kernel inside the MG-WFBP timed region; kernel spans are
+    # %globaltimer stamps written by the kernels (first CTA entry .. last CTA exit)
+    steps = len(kern)
+    spans = {"pack": sum(sum(k[0]) for k in kern), "unpack": sum(sum(k[2]) for k in kern)}
     if world > 1:
-        kernels["allreduce"] = ar_s
-    dominant = max(kernels, key=kernels.get)
+        spans["allreduce"] = sum(sum(k[1]) for k in kern)
+    dominant = max(spans, key=spans.get)
     total_bytes = sum(gbytes)
+    sending = sum(1 for b in gbytes if b)
+    hbm_peak, hbm_src = peaks()
     if dominant in ("pack", "unpack"):
-        algo_bytes = 2 * total_bytes * len(kern)  # read + write of every bucket byte
-        achieved = algo_bytes / kernels[dominant] / 1e9
-        roofline = {"bound": "hbm", "kernel": f"K1 {dominant}" if dominant == "pack" else "K4 unpack",
+        per_step = 2 * total_bytes  # read + write of every bucket byte
+        achieved = per_step * steps / spans[dominant] / 1e9
+        roofline = {"bound": "hbm", "kernel": "K1 pack" if dominant == "pack" else "K4 unpack",
                     "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-                    "frac": round(achieved / hbm_peak, 4), "peak_source": hbm_src,
-                    "bytes_per_step": 2 * total_bytes, "launches_per_step": launches_of[dominant] // max(1, len(kern))}
+                    "frac": round(achieved / hbm_peak, 4), "peak_source": hbm_src}
     else:
-        bus = 2 * (world - 1) / world * total_bytes * len(kern)
-        achieved = bus / ar_s / 1e9
+        per_step = int(2 * (world - 1) / world * total_bytes)  # nccl-tests bus bytes
+        achieved = per_step * steps / spans["allreduce"] / 1e9
         roofline = {"bound": "nvlink", "kernel": "K2/K3 all-reduce", "achieved": round(achieved, 1),
                     "peak": NVLINK_PEAK_GBS, "unit": "GB/s", "frac": round(achieved / NVLINK_PEAK_GBS, 4),
-                    "peak_source": "measured peer copy per direction, B200_PROFILING.md (900 nominal)",
-                    "bytes_per_step": int(2 * (world - 1) / world * total_bytes)}
+                    "peak_source": "measured peer copy per direction, B200_PROFILING.md (900 nominal)"}
+    roofline.update({
+        "bytes_per_step": per_step,
+        "launches_per_step": sending,
+        "avg_launch_us": round(spans[dominant] / (steps * max(1, sending)) * 1e6, 3),
+        "timing": "kernel-written %globaltimer spans over the timed region (CUDA event records cost ~6.5 us "
+                  "per pair inside a graph on this B200, see profiles/microbench_r01.json)",
+        "kernel_ms_per_step": {k: round(v / steps * 1e3, 4) for k, v in spans.items()},
+    })
     traffic_file = ROOT / "profiles" / "roofline_traffic.json"
     roofline["traffic"] = None
     if traffic_file.exists():
         roofline["traffic"] = json.loads(traffic_file.read_text()).get(f"{roofline['kernel']}@N{world}")
-    roofline["kernel_ms_per_step"] = {k: round(v / len(kern) * 1e3, 4) for k, v in kernels.items()}
+    # the same kernel on the whole-model bucket, back to back under one event pair
+    big = _exchange_times(comm, world, device, [4 * profile.total_params],
+                          kind={"pack": 2, "allreduce": 1, "unpack": 3}[dominant] if world > 1 else 2)[0]
+    if dominant in ("pack", "unpack") or world == 1:
+        big_bw = 2 * 4 * profile.total_params / big / 1e9
+    else:
+        big_bw = 2 * (world - 1) / world * 4 * profile.total_params / big / 1e9
+    roofline["whole_model_bucket"] = {"bytes": 4 * profile.total_params, "us": round(big * 1e6, 2),
+                                      "achieved": round(big_bw, 1),
+                                      "frac": round(big_bw / (hbm_peak if roofline["bound"] == "hbm" else NVLINK_PEAK_GBS), 4),
+                                      "timing": "one CUDA event pair around 20 back-to-back launches"}
 
     # e2e: the same MG-WFBP iteration with host buffers (H2D of every layer's gradient,
     # D2H of every reduced gradient) inside the timed region
@@ -398,6 +395,8 @@ def run_ours(args) -> dict | None:
     finally:
         e2e_it.close()
     e2e_max = _max_over_ranks(e2e_times, world, device)
+    if sampler is not None:
+        sampler.__exit__(None, None, None)
 
     sweep = None
     if world > 1 and not args.no_sweep:
@@ -433,6 +432,7 @@ def run_ours(args) -> dict | None:
             "merged_layers": sorted(plans["mgwfbp"].merged_layers),
             "fitted_a_us": round(model.a * 1e6, 3),
             "fitted_b_ns_per_byte": model.b * 1e9,
+            "fit_ok": fit_ok,
             "parallelism": f"dp{world}",
             "l2": "flushed between iterations (256 MiB write on the compute stream, outside the timed events)",
             "cuda_graph": not args.no_graph,
@@ -546,7 +546,16 @@ def main(argv=None) -> int:
     args = ap.parse_args(argv)
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
-    line = run_reference(args) if args.impl == "reference" else run_ours(args)
+    # keep stdout for the one JSON line: library chatter (e.g. "NCCL version") goes to stderr
+    sys.stdout.flush()
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
+    try:
+        line = run_reference(args) if args.impl == "reference" else run_ours(args)
+    finally:
+        sys.stdout.flush()
+        os.dup2(json_fd, 1)
+        os.close(json_fd)
     if line is not None:
         print(json.dumps(line), flush=True)
     if args.impl == "ours" and args.gpus > 1:

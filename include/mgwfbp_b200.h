@@ -117,6 +117,12 @@ int mgw_allreduce(mgw_comm* comm, int64_t n_elem, int algo, void* stream);
 int mgw_comm_error(mgw_comm* comm, int* code);
 int mgw_comm_calls(mgw_comm* comm, int64_t* calls);
 
+/* Device seconds per step of `reps` back-to-back exchange steps under one event pair
+ * (the (a, b) fit's input and the bus-bandwidth sweep).  kind: 0 pack+all-reduce+unpack,
+ * 1 all-reduce only, 2 pack only, 3 unpack only.  comm NULL: single rank, local_bucket. */
+int mgw_time_exchange(mgw_comm* comm, const void* dev_table, int n_rows, int64_t n_elem, float* local_bucket,
+                      int algo, int kind, int reps, int warmups, double* seconds_per_rep, void* stream);
+
 /* ---- emulated ranks on one device (test path; no barriers) ------------ */
 int mgw_allreduce_emulated(float* const* ins, float* const* outs, int world, int64_t n_elem, int algo,
                            void* stream);
@@ -128,6 +134,8 @@ int mgw_sched_create(mgw_comm* comm /* NULL: single rank */, const mgw_tensor_de
                      float* const* host_dst /* per row */, mgw_sched** out);
 int mgw_sched_run(mgw_sched* sched, void* compute_stream, void* comm_stream);
 int mgw_sched_times(mgw_sched* sched, double* t_iter_s, double* compute_s, double* group_comm_s);
+/* per-group kernel execution spans of the last iteration, from %globaltimer stamps the
+ * kernels write themselves (first CTA entry .. last CTA exit) */
 int mgw_sched_kernel_times(mgw_sched* sched, double* pack_s, double* allreduce_s, double* unpack_s);
 int mgw_sched_launches(mgw_sched* sched, int* kernels_per_iteration);
 int mgw_sched_destroy(mgw_sched* sched);

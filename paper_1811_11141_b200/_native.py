@@ -70,6 +70,7 @@ _SIGNATURES = {
     "mgw_allreduce": ([_P, _I64, _I, _P], _I),
     "mgw_comm_error": ([_P, ctypes.POINTER(_I)], _I),
     "mgw_comm_calls": ([_P, ctypes.POINTER(_I64)], _I),
+    "mgw_time_exchange": ([_P, _P, _I, _I64, _P, _I, _I, _I, _I, ctypes.POINTER(ctypes.c_double), _P], _I),
     "mgw_allreduce_emulated": ([ctypes.POINTER(_P), ctypes.POINTER(_P), _I, _I64, _I, _P], _I),
     "mgw_sched_create": (
         [_P, ctypes.POINTER(TensorDesc), _I, ctypes.POINTER(Group), _I, ctypes.c_float, ctypes.c_uint32,

@@ -482,14 +482,14 @@ def bench_allreduce(
     repeats: int = 5,
     warmups: int = 3,
 ) -> list[Measurement]:
-    """Median device time of one group exchange (pack + all-reduce + unpack)
-    per payload size, timed with CUDA events on the comm stream.
+    """Median device time of one group exchange (pack + all-reduce + unpack) per
+    payload size (allreduce_net.py:414-445 semantics: sizes are positive multiples
+    of 4 bytes; rank 0 returns the Measurements, other ranks an empty list).
 
-    Sizes are positive multiples of 4 bytes.  Reps run back to back on one
-    stream, so every rep after the first is in lock-step across ranks (the
-    kernel barrier aligns them); each rep refills the buffer with ``rank + 1``
-    outside its timed span (allreduce_net.py:436-442).  Rank 0 returns the
-    Measurements, other ranks an empty list.
+    Each of the ``repeats`` samples is the mean of 8 back-to-back exchanges timed
+    with one CUDA event pair on the comm stream (the kernel barrier keeps the ranks
+    in lock-step), so neither host launch latency nor per-launch event cost enters
+    the fit.  Every size is also checked once for the exact sum ``N(N+1)/2``.
     """
     if repeats < 1:
         raise ValueError("repeats must be >= 1")
@@ -502,33 +502,32 @@ def bench_allreduce(
     out: list[Measurement] = []
     world = config.n_workers
     handle = session.stream.cuda_stream
+    loop = 8
     with torch.cuda.device(session.device), torch.cuda.stream(session.stream):
         for nbytes in sizes:
             n = nbytes // 4
             buf = torch.empty(n, dtype=torch.float32, device=session.device)
             table = _native.DeviceTable([(buf.data_ptr(), n, 0)])
             algo = _algo_for(session, n)
-            result = session.result_ptr()
-            marks = []
-            for r in range(warmups + repeats):
+            times = []
+            try:
+                for r in range(repeats):
+                    buf.fill_(float(config.rank + 1))
+                    sec = ctypes.c_double()
+                    _native.call("mgw_time_exchange", session.comm, table.ptr, 1, n, None, _native.ALGO_AUTO, 0,
+                                 loop, warmups if r == 0 else 0, ctypes.byref(sec), handle)
+                    times.append(sec.value)
+                    session.account(n, algo)
                 buf.fill_(float(config.rank + 1))
-                start = torch.cuda.Event(enable_timing=True)
-                stop = torch.cuda.Event(enable_timing=True)
-                start.record(session.stream)
                 _native.call("mgw_comm_pack", session.comm, table.ptr, 1, n, ctypes.c_float(1.0), handle)
                 _native.call("mgw_allreduce", session.comm, n, algo, handle)
-                _native.call("mgw_unpack", table.ptr, 1, result, n, handle)
-                stop.record(session.stream)
-                if r >= warmups:
-                    marks.append((start, stop))
-                session.account(n, algo)
-            session.stream.synchronize()
-            session.raise_if_failed()
-            want = float(world * (world + 1) // 2)
-            if not bool((buf == want).all()):
-                raise RuntimeError(f"rank {config.rank}: wrong all-reduce result at {nbytes} B")
-            table.close()
-            times = [a.elapsed_time(b) * 1e-3 for a, b in marks]
+                _native.call("mgw_unpack", table.ptr, 1, session.result_ptr(), n, handle)
+                session.stream.synchronize()
+                session.raise_if_failed()
+                if not bool((buf == float(world * (world + 1) // 2)).all()):
+                    raise RuntimeError(f"rank {config.rank}: wrong all-reduce result at {nbytes} B")
+            finally:
+                table.close()
             if config.rank == 0:
                 out.append(Measurement(nbytes=nbytes, seconds=statistics.median(times), n_nodes=world))
     return out

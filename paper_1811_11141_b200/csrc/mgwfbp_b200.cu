@@ -118,6 +118,20 @@ __device__ __forceinline__ uint32_t load_volatile32(const uint32_t* p) {
   return *reinterpret_cast<const volatile uint32_t*>(p);
 }
 
+// Kernel span stamps: every CTA folds its entry time into stamp[0] (min) and its
+// exit time into stamp[1] (max), so [stamp[0], stamp[1]] is the kernel's execution
+// span without the ~6.5 us an event record pair costs inside a CUDA graph.
+__device__ __forceinline__ void stamp_enter(uint64_t* stamp) {
+  if (stamp != nullptr && threadIdx.x == 0) atomicMin(reinterpret_cast<unsigned long long*>(stamp), (unsigned long long)global_ns());
+}
+
+__device__ __forceinline__ void stamp_exit(uint64_t* stamp) {
+  if (stamp != nullptr) {
+    __syncthreads();
+    if (threadIdx.x == 0) atomicMax(reinterpret_cast<unsigned long long*>(stamp + 1), (unsigned long long)global_ns());
+  }
+}
+
 __device__ __forceinline__ float4 fadd4(float4 a, float4 b) {
   return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
 }
@@ -206,7 +220,8 @@ template <RowOp kOp, bool kScale>
 __global__ void __launch_bounds__(kThreads) rows_kernel(const Row* __restrict__ rows, int n_rows, float* bucket,
                                                         int64_t total, float scale, const float* __restrict__ values,
                                                         const uint32_t* calls, int64_t slot_stride_elems,
-                                                        unsigned long long* mismatches) {
+                                                        unsigned long long* mismatches, uint64_t* stamp) {
+  stamp_enter(stamp);
   if (calls != nullptr) {
     // epoch of the collective this pack feeds = completed calls + 1
     const uint32_t epoch = load_volatile32(calls) + 1u;
@@ -224,6 +239,7 @@ __global__ void __launch_bounds__(kThreads) rows_kernel(const Row* __restrict__ 
       span_op<kOp, kScale>(r.ptr + (lo - r.offset), bucket + lo, hi - lo, scale, v, mismatches);
     }
   }
+  stamp_exit(stamp);
 }
 
 int rows_grid(int64_t total) {
@@ -235,16 +251,16 @@ int rows_grid(int64_t total) {
 template <RowOp kOp>
 int launch_rows(const void* table, int n, float* bucket, int64_t total, float scale, const float* values,
                 const uint32_t* calls, int64_t slot_stride_elems, unsigned long long* mismatches,
-                cudaStream_t stream) {
+                cudaStream_t stream, uint64_t* stamp = nullptr) {
   if (total <= 0 || n <= 0) return MGW_OK;
   const Row* rows = static_cast<const Row*>(table);
   const int grid = rows_grid(total);
   if (kOp == RowOp::kPack && scale != 1.0f)
     rows_kernel<kOp, true><<<grid, kThreads, 0, stream>>>(rows, n, bucket, total, scale, values, calls,
-                                                          slot_stride_elems, mismatches);
+                                                          slot_stride_elems, mismatches, stamp);
   else
     rows_kernel<kOp, false><<<grid, kThreads, 0, stream>>>(rows, n, bucket, total, scale, values, calls,
-                                                           slot_stride_elems, mismatches);
+                                                           slot_stride_elems, mismatches, stamp);
   MGW_CHECK_LAUNCH();
   return MGW_OK;
 }
@@ -255,6 +271,13 @@ __global__ void spin_relative_kernel(int64_t ns) {
   if (threadIdx.x != 0) return;
   const uint64_t t0 = global_ns();
   while ((int64_t)(global_ns() - t0) < ns) __nanosleep(128);
+}
+
+__global__ void stamps_reset_kernel(uint64_t* stamps, int pairs) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < pairs; i += gridDim.x * blockDim.x) {
+    stamps[2 * i] = ~0ull;
+    stamps[2 * i + 1] = 0ull;
+  }
 }
 
 __global__ void clock_mark_kernel(uint64_t* clock) {
@@ -277,6 +300,7 @@ struct ArArgs {
   float* out[kMaxRanks];       // result buffer (real mode uses out[rank])
   uint32_t* state;             // local device [completed calls, finished CTAs]; null = no epochs
   int* err;                    // local device error word
+  uint64_t* stamp;             // optional kernel span stamps [2]
   int64_t slot_stride;         // bytes from slot 0 to slot 1
   int64_t n;                   // elements
   uint64_t timeout_ns;
@@ -382,6 +406,7 @@ __device__ int cta_barrier(uint64_t* const* flags, int parity, uint32_t epoch, u
 
 // Last CTA out advances the call counter (epochs and slot parity come from it).
 __device__ __forceinline__ void finish_call(const ArArgs& a) {
+  stamp_exit(a.stamp);
   if (a.state == nullptr) return;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -435,6 +460,7 @@ __device__ __forceinline__ void load_slots(const ArArgs& a, int parity, const fl
 template <int N>
 __global__ void __launch_bounds__(kThreads) oneshot_kernel(ArArgs a) {
   __shared__ const float* s_in[kMaxRanks];
+  stamp_enter(a.stamp);
   uint32_t epoch = 0;
   if (a.state != nullptr) epoch = load_volatile32(a.state) + 1u;
   const int parity = (int)(epoch & 1u);
@@ -482,6 +508,7 @@ __global__ void __launch_bounds__(kThreads) oneshot_kernel(ArArgs a) {
 template <int N>
 __global__ void __launch_bounds__(kThreads) twoshot_kernel(ArArgs a) {
   __shared__ const float* s_in[kMaxRanks];
+  stamp_enter(a.stamp);
   uint32_t epoch = 0;
   if (a.state != nullptr) epoch = load_volatile32(a.state) + 1u;
   const int parity = (int)(epoch & 1u);
@@ -571,6 +598,7 @@ int grid_for(int64_t vectors_per_cta_work, int64_t min_per_cta, int max_ctas) {
 
 int launch_allreduce(const ArArgs& a, int algo, int max_ctas, cudaStream_t stream) {
   const int64_t nv = a.n >> 2;
+  max_ctas = std::min(max_ctas, kMaxBlocks);  // one barrier flag slot per CTA
   if (algo == MGW_ALGO_ONESHOT) {
     const int grid = grid_for(nv, 1024, max_ctas);
 #define MGW_ONESHOT_CASE(NN) \
@@ -632,7 +660,7 @@ struct mgw_comm {
   float* result = nullptr;
   uint64_t timeout_ns = 30ull * 1000000000ull;
   int64_t oneshot_max_bytes = 1 << 20;
-  int max_ctas = 2 * kSMs;
+  int max_ctas = kSMs;
 };
 
 struct mgw_sched {
@@ -644,17 +672,19 @@ struct mgw_sched {
   float* d_fill = nullptr;
   float* local_bucket = nullptr;  // single-rank bucket
   uint64_t* d_clock = nullptr;
+  uint64_t* d_stamps = nullptr;   // per group: pack, all-reduce, unpack spans (3 x [start, end])
+  std::vector<uint64_t> h_stamps;
   float scale = 1.f;
   uint32_t flags = 0;
   std::vector<float*> host_src, host_dst;
-  // dependency events (fork/join) and timing events (external records)
+  // dependency events (fork/join) and the three timing events of an iteration
   cudaEvent_t dep_fork = nullptr, dep_join = nullptr, dep_compute = nullptr;
   std::vector<cudaEvent_t> dep_ready;
   cudaEvent_t t_start = nullptr, t_compute = nullptr, t_end = nullptr;
-  std::vector<cudaEvent_t> t_g0, t_gp, t_ga, t_g1;  // group start, after pack, after all-reduce, end
   cudaGraphExec_t graph_exec = nullptr;
   cudaGraph_t graph = nullptr;
   int launches = 0;
+  bool capturing = false;
 };
 
 namespace {
@@ -688,7 +718,7 @@ int pick_algo(const mgw_comm* c, int64_t n, int algo) {
   return n * 4 <= c->oneshot_max_bytes ? MGW_ALGO_ONESHOT : MGW_ALGO_TWOSHOT;
 }
 
-int comm_allreduce(mgw_comm* c, int64_t n, int algo, cudaStream_t stream) {
+int comm_allreduce(mgw_comm* c, int64_t n, int algo, cudaStream_t stream, uint64_t* stamp = nullptr) {
   if (n < 0 || n * 4 > c->slot_bytes) return set_error(MGW_EINVAL, "bucket of %lld elements exceeds slot capacity %lld B", (long long)n, (long long)c->slot_bytes);
   if (c->world == 1) {
     if (n > 0) MGW_CUDA(cudaMemcpyAsync(c->result, c->region + kCtrlBytes, n * 4, cudaMemcpyDeviceToDevice, stream));
@@ -696,14 +726,17 @@ int comm_allreduce(mgw_comm* c, int64_t n, int algo, cudaStream_t stream) {
   }
   if (!c->peers_open) return set_error(MGW_EINVAL, "peers not opened (call mgw_comm_open_peers)");
   ArArgs a = make_args(c, n);
+  a.stamp = stamp;
   return launch_allreduce(a, pick_algo(c, n, algo), c->max_ctas, stream);
 }
 
-int comm_pack(mgw_comm* c, const void* table, int n_rows, int64_t n, float scale, cudaStream_t stream) {
+int comm_pack(mgw_comm* c, const void* table, int n_rows, int64_t n, float scale, cudaStream_t stream,
+              uint64_t* stamp = nullptr) {
   if (n * 4 > c->slot_bytes) return set_error(MGW_EINVAL, "bucket of %lld elements exceeds slot capacity %lld B", (long long)n, (long long)c->slot_bytes);
   float* slot0 = reinterpret_cast<float*>(c->region + kCtrlBytes);
   const uint32_t* calls = c->world > 1 ? c->state : nullptr;
-  return launch_rows<RowOp::kPack>(table, n_rows, slot0, n, scale, nullptr, calls, c->slot_bytes / 4, nullptr, stream);
+  return launch_rows<RowOp::kPack>(table, n_rows, slot0, n, scale, nullptr, calls, c->slot_bytes / 4, nullptr, stream,
+                                   stamp);
 }
 
 }  // namespace
@@ -979,6 +1012,61 @@ int mgw_allreduce_emulated(float* const* ins, float* const* outs, int world, int
   return MGW_OK;
 }
 
+// Device time of back-to-back group-exchange steps, timed as one event pair around
+// `reps` repetitions (after `warmups` untimed ones) so no per-launch event cost
+// enters the figure.  kind: 0 = pack -> all-reduce -> unpack (single rank: pack ->
+// unpack into `local_bucket`), 1 = all-reduce kernel only, 2 = pack only, 3 = unpack only.
+int mgw_time_exchange(mgw_comm* c, const void* table, int n_rows, int64_t n_elem, float* local_bucket, int algo,
+                      int kind, int reps, int warmups, double* seconds_per_rep, void* stream) {
+  if (!table || reps < 1 || warmups < 0 || !seconds_per_rep || n_elem <= 0 || kind < 0 || kind > 3)
+    return set_error(MGW_EINVAL, "bad timing arguments");
+  const bool multi = c && c->world > 1;
+  if (!multi && !local_bucket) return set_error(MGW_EINVAL, "single-rank timing needs a local bucket");
+  if (kind == 1 && !multi) return set_error(MGW_EINVAL, "all-reduce timing needs a multi-rank communicator");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  auto step = [&]() -> int {
+    int rc = MGW_OK;
+    if (multi) {
+      if (kind == 0 || kind == 2) rc = comm_pack(c, table, n_rows, n_elem, 1.f, s);
+      if (rc == MGW_OK && (kind == 0 || kind == 1)) rc = comm_allreduce(c, n_elem, algo, s);
+      if (rc == MGW_OK && (kind == 0 || kind == 3))
+        rc = launch_rows<RowOp::kUnpack>(table, n_rows, c->result, n_elem, 1.f, nullptr, nullptr, 0, nullptr, s);
+    } else {
+      if (kind == 0 || kind == 2)
+        rc = launch_rows<RowOp::kPack>(table, n_rows, local_bucket, n_elem, 1.f, nullptr, nullptr, 0, nullptr, s);
+      if (rc == MGW_OK && (kind == 0 || kind == 3))
+        rc = launch_rows<RowOp::kUnpack>(table, n_rows, local_bucket, n_elem, 1.f, nullptr, nullptr, 0, nullptr, s);
+    }
+    return rc;
+  };
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  MGW_CUDA(cudaEventCreate(&ev0));
+  cudaError_t e = cudaEventCreate(&ev1);
+  if (e != cudaSuccess) {
+    cudaEventDestroy(ev0);
+    return set_error(MGW_ECUDA, "cudaEventCreate: %s", cudaGetErrorString(e));
+  }
+  int rc = MGW_OK;
+  for (int r = 0; r < warmups && rc == MGW_OK; ++r) rc = step();
+  // hold the stream while the host enqueues the timed reps
+  if (rc == MGW_OK) spin_relative_kernel<<<1, 32, 0, s>>>(1000000 + 20000LL * reps);
+  if (rc == MGW_OK) cudaEventRecord(ev0, s);
+  for (int r = 0; r < reps && rc == MGW_OK; ++r) rc = step();
+  if (rc == MGW_OK) {
+    cudaEventRecord(ev1, s);
+    e = cudaEventSynchronize(ev1);
+    float ms = 0.f;
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, ev0, ev1);
+    if (e != cudaSuccess)
+      rc = set_error(MGW_ECUDA, "timing loop: %s", cudaGetErrorString(e));
+    else
+      *seconds_per_rep = ms * 1e-3 / reps;
+  }
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  return rc;
+}
+
 // ------------------------------------------------------------ schedule engine
 
 static void sched_release(mgw_sched* s) {
@@ -986,26 +1074,22 @@ static void sched_release(mgw_sched* s) {
   if (s->graph_exec) cudaGraphExecDestroy(s->graph_exec);
   if (s->graph) cudaGraphDestroy(s->graph);
   for (auto e : s->dep_ready) cudaEventDestroy(e);
-  for (auto e : s->t_g0) cudaEventDestroy(e);
-  for (auto e : s->t_g1) cudaEventDestroy(e);
-  for (auto e : s->t_gp) cudaEventDestroy(e);
-  for (auto e : s->t_ga) cudaEventDestroy(e);
   for (cudaEvent_t e : {s->dep_fork, s->dep_join, s->dep_compute, s->t_start, s->t_compute, s->t_end})
     if (e) cudaEventDestroy(e);
-  if (s->d_rows) cudaFree(s->d_rows);
-  if (s->d_fill) cudaFree(s->d_fill);
-  if (s->local_bucket) cudaFree(s->local_bucket);
-  if (s->d_clock) cudaFree(s->d_clock);
+  for (void* p : {(void*)s->d_rows, (void*)s->d_fill, (void*)s->local_bucket, (void*)s->d_clock, (void*)s->d_stamps})
+    if (p) cudaFree(p);
   delete s;
 }
 
 int mgw_sched_create(mgw_comm* comm, const mgw_tensor_desc* rows, int n_rows, const mgw_group* groups, int n_groups,
                      float scale, uint32_t flags, const float* fill_values, float* const* host_src,
                      float* const* host_dst, mgw_sched** out) {
-  if (!out || (n_rows > 0 && !rows) || !groups || n_rows < 0 || n_groups <= 0) return set_error(MGW_EINVAL, "bad schedule arguments");
+  if (!out || (n_rows > 0 && !rows) || !groups || n_rows < 0 || n_groups <= 0)
+    return set_error(MGW_EINVAL, "bad schedule arguments");
   *out = nullptr;
   if ((flags & MGW_SCHED_FILL) && !fill_values) return set_error(MGW_EINVAL, "MGW_SCHED_FILL needs fill_values");
-  if ((flags & MGW_SCHED_HOSTIO) && (!host_src || !host_dst)) return set_error(MGW_EINVAL, "MGW_SCHED_HOSTIO needs host_src and host_dst");
+  if ((flags & MGW_SCHED_HOSTIO) && (!host_src || !host_dst))
+    return set_error(MGW_EINVAL, "MGW_SCHED_HOSTIO needs host_src and host_dst");
   int64_t max_elems = 0;
   for (int g = 0; g < n_groups; ++g) {
     const mgw_group& gr = groups[g];
@@ -1016,14 +1100,16 @@ int mgw_sched_create(mgw_comm* comm, const mgw_tensor_desc* rows, int n_rows, co
       if (rows[k].offset != expect) return set_error(MGW_EINVAL, "group %d: rows must tile the bucket contiguously", g);
       expect += rows[k].count;
     }
-    if (expect != gr.n_elem) return set_error(MGW_EINVAL, "group %d: n_elem %lld != rows total %lld", g, (long long)gr.n_elem, (long long)expect);
+    if (expect != gr.n_elem)
+      return set_error(MGW_EINVAL, "group %d: n_elem %lld != rows total %lld", g, (long long)gr.n_elem, (long long)expect);
     if (gr.ready_ns < 0) return set_error(MGW_EINVAL, "group %d: negative ready time", g);
     if (g > 0 && gr.ready_ns < groups[g - 1].ready_ns) return set_error(MGW_EINVAL, "groups must be in send order");
     max_elems = std::max(max_elems, gr.n_elem);
   }
   const int world = comm ? comm->world : 1;
   if (comm && max_elems * 4 > comm->slot_bytes)
-    return set_error(MGW_EINVAL, "largest group (%lld B) exceeds the communicator slot (%lld B)", (long long)(max_elems * 4), (long long)comm->slot_bytes);
+    return set_error(MGW_EINVAL, "largest group (%lld B) exceeds the communicator slot (%lld B)",
+                     (long long)(max_elems * 4), (long long)comm->slot_bytes);
   mgw_sched* s = new mgw_sched();
   s->comm = comm;
   s->world = world;
@@ -1035,15 +1121,19 @@ int mgw_sched_create(mgw_comm* comm, const mgw_tensor_desc* rows, int n_rows, co
     s->host_src.assign(host_src, host_src + n_rows);
     s->host_dst.assign(host_dst, host_dst + n_rows);
   }
+  s->h_stamps.assign((size_t)n_groups * 6, 0);
   cudaError_t e = cudaMalloc(&s->d_rows, sizeof(Row) * (size_t)std::max(1, n_rows));
   if (e == cudaSuccess && n_rows > 0) e = cudaMemcpy(s->d_rows, rows, sizeof(Row) * (size_t)n_rows, cudaMemcpyHostToDevice);
   if (e == cudaSuccess && (flags & MGW_SCHED_FILL)) {
     e = cudaMalloc(&s->d_fill, sizeof(float) * (size_t)std::max(1, n_rows));
-    if (e == cudaSuccess && n_rows > 0) e = cudaMemcpy(s->d_fill, fill_values, sizeof(float) * (size_t)n_rows, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && n_rows > 0)
+      e = cudaMemcpy(s->d_fill, fill_values, sizeof(float) * (size_t)n_rows, cudaMemcpyHostToDevice);
   }
   if (e == cudaSuccess && world == 1) e = cudaMalloc(&s->local_bucket, std::max<size_t>(256, (size_t)max_elems * 4));
   if (e == cudaSuccess) e = cudaMalloc(&s->d_clock, sizeof(uint64_t));
   if (e == cudaSuccess) e = cudaMemset(s->d_clock, 0, sizeof(uint64_t));
+  if (e == cudaSuccess) e = cudaMalloc(&s->d_stamps, sizeof(uint64_t) * (size_t)n_groups * 6);
+  if (e == cudaSuccess) e = cudaMemset(s->d_stamps, 0, sizeof(uint64_t) * (size_t)n_groups * 6);
   auto mk = [&](cudaEvent_t* ev, bool timing) {
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, timing ? cudaEventDefault : cudaEventDisableTiming);
   };
@@ -1054,49 +1144,47 @@ int mgw_sched_create(mgw_comm* comm, const mgw_tensor_desc* rows, int n_rows, co
   mk(&s->t_compute, true);
   mk(&s->t_end, true);
   s->dep_ready.assign(n_groups, nullptr);
-  s->t_g0.assign(n_groups, nullptr);
-  s->t_g1.assign(n_groups, nullptr);
-  s->t_gp.assign(n_groups, nullptr);
-  s->t_ga.assign(n_groups, nullptr);
-  for (int g = 0; g < n_groups; ++g) {
-    mk(&s->dep_ready[g], false);
-    mk(&s->t_g0[g], true);
-    mk(&s->t_gp[g], true);
-    mk(&s->t_ga[g], true);
-    mk(&s->t_g1[g], true);
-  }
+  for (int g = 0; g < n_groups; ++g) mk(&s->dep_ready[g], false);
   if (e != cudaSuccess) {
     sched_release(s);
     return set_error(MGW_ECUDA, "schedule setup: %s", cudaGetErrorString(e));
   }
-  int launches = 1 + (world > 1 ? 1 : 0);  // clock mark (+ start barrier)
+  int launches = 2 + (world > 1 ? 1 : 0);  // stamp reset + clock mark (+ start barrier)
   for (int g = 0; g < n_groups; ++g) {
-    launches += 1;                                                      // spin
+    launches += 1;  // spin
     if (groups[g].n_elem == 0) continue;
-    launches += (flags & MGW_SCHED_FILL) ? 1 : 0;                       // fill
-    launches += 2;                                                      // pack + unpack
-    launches += world > 1 ? 1 : 0;                                      // all-reduce
+    launches += (flags & MGW_SCHED_FILL) ? 1 : 0;  // gradient production
+    launches += 2;                                 // pack + unpack
+    launches += world > 1 ? 1 : 0;                 // all-reduce
   }
   s->launches = launches;
   *out = s;
   return MGW_OK;
 }
 
+// Timing events: inside a stream capture they must be external record nodes; in
+// eager mode they are plain records.
+static cudaError_t record_timing(const mgw_sched* s, cudaEvent_t ev, cudaStream_t st) {
+  return s->capturing ? cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal) : cudaEventRecord(ev, st);
+}
+
 static int sched_enqueue(mgw_sched* s, cudaStream_t cs, cudaStream_t ms) {
   const Row* d_rows = s->d_rows;
+  const int n_groups = (int)s->groups.size();
   if (s->world > 1) {
     // align the ranks' iteration starts: a zero-length collective is a barrier
     int rc = comm_allreduce(s->comm, 0, MGW_ALGO_ONESHOT, cs);
     if (rc) return rc;
   }
-  MGW_CUDA(cudaEventRecordWithFlags(s->t_start, cs, cudaEventRecordExternal));
+  stamps_reset_kernel<<<1, 256, 0, cs>>>(s->d_stamps, n_groups * 3);
+  MGW_CHECK_LAUNCH();
+  MGW_CUDA(record_timing(s, s->t_start, cs));
   MGW_CUDA(cudaEventRecord(s->dep_fork, cs));
   clock_mark_kernel<<<1, 32, 0, cs>>>(s->d_clock);
   MGW_CHECK_LAUNCH();
-  const int n_groups = (int)s->groups.size();
   for (int g = 0; g < n_groups; ++g) {
     const mgw_group& gr = s->groups[g];
-    if (s->flags & MGW_SCHED_HOSTIO) {
+    if ((s->flags & MGW_SCHED_HOSTIO) && gr.n_elem > 0) {
       for (int k = gr.desc_begin; k < gr.desc_begin + gr.desc_count; ++k)
         if (s->rows[k].count)
           MGW_CUDA(cudaMemcpyAsync(s->rows[k].ptr, s->host_src[k], s->rows[k].count * 4, cudaMemcpyHostToDevice, cs));
@@ -1110,49 +1198,41 @@ static int sched_enqueue(mgw_sched* s, cudaStream_t cs, cudaStream_t ms) {
     MGW_CHECK_LAUNCH();
     MGW_CUDA(cudaEventRecord(s->dep_ready[g], cs));
   }
-  MGW_CUDA(cudaEventRecordWithFlags(s->t_compute, cs, cudaEventRecordExternal));
+  MGW_CUDA(record_timing(s, s->t_compute, cs));
   MGW_CUDA(cudaEventRecord(s->dep_compute, cs));
 
   MGW_CUDA(cudaStreamWaitEvent(ms, s->dep_fork, 0));
   for (int g = 0; g < n_groups; ++g) {
     const mgw_group& gr = s->groups[g];
     const Row* grows = d_rows + gr.desc_begin;
+    uint64_t* st = s->d_stamps + 6 * (size_t)g;
     MGW_CUDA(cudaStreamWaitEvent(ms, s->dep_ready[g], 0));
-    MGW_CUDA(cudaEventRecordWithFlags(s->t_g0[g], ms, cudaEventRecordExternal));
+    if (gr.n_elem == 0) continue;  // silent group: nothing to send (allreduce_net.py:549)
     int rc;
-    if (gr.n_elem == 0) {
-      // silent group: nothing to send (allreduce_net.py:549)
-      MGW_CUDA(cudaEventRecordWithFlags(s->t_gp[g], ms, cudaEventRecordExternal));
-      MGW_CUDA(cudaEventRecordWithFlags(s->t_ga[g], ms, cudaEventRecordExternal));
-    } else if (s->world == 1) {
+    if (s->world == 1) {
       rc = launch_rows<RowOp::kPack>(grows, gr.desc_count, s->local_bucket, gr.n_elem, s->scale, nullptr, nullptr, 0,
-                                     nullptr, ms);
+                                     nullptr, ms, st);
       if (rc) return rc;
-      MGW_CUDA(cudaEventRecordWithFlags(s->t_gp[g], ms, cudaEventRecordExternal));
-      MGW_CUDA(cudaEventRecordWithFlags(s->t_ga[g], ms, cudaEventRecordExternal));
       rc = launch_rows<RowOp::kUnpack>(grows, gr.desc_count, s->local_bucket, gr.n_elem, 1.f, nullptr, nullptr, 0,
-                                       nullptr, ms);
+                                       nullptr, ms, st + 4);
       if (rc) return rc;
     } else {
-      rc = comm_pack(s->comm, grows, gr.desc_count, gr.n_elem, s->scale, ms);
+      rc = comm_pack(s->comm, grows, gr.desc_count, gr.n_elem, s->scale, ms, st);
       if (rc) return rc;
-      MGW_CUDA(cudaEventRecordWithFlags(s->t_gp[g], ms, cudaEventRecordExternal));
-      rc = comm_allreduce(s->comm, gr.n_elem, gr.algo, ms);
+      rc = comm_allreduce(s->comm, gr.n_elem, gr.algo, ms, st + 2);
       if (rc) return rc;
-      MGW_CUDA(cudaEventRecordWithFlags(s->t_ga[g], ms, cudaEventRecordExternal));
       rc = launch_rows<RowOp::kUnpack>(grows, gr.desc_count, s->comm->result, gr.n_elem, 1.f, nullptr, nullptr, 0,
-                                       nullptr, ms);
+                                       nullptr, ms, st + 4);
       if (rc) return rc;
     }
-    if ((s->flags & MGW_SCHED_HOSTIO) && gr.n_elem > 0) {
+    if (s->flags & MGW_SCHED_HOSTIO) {
       for (int k = gr.desc_begin; k < gr.desc_begin + gr.desc_count; ++k)
         if (s->rows[k].count)
           MGW_CUDA(cudaMemcpyAsync(s->host_dst[k], s->rows[k].ptr, s->rows[k].count * 4, cudaMemcpyDeviceToHost, ms));
     }
-    MGW_CUDA(cudaEventRecordWithFlags(s->t_g1[g], ms, cudaEventRecordExternal));
   }
   MGW_CUDA(cudaStreamWaitEvent(ms, s->dep_compute, 0));  // iteration ends no earlier than backward
-  MGW_CUDA(cudaEventRecordWithFlags(s->t_end, ms, cudaEventRecordExternal));
+  MGW_CUDA(record_timing(s, s->t_end, ms));
   MGW_CUDA(cudaEventRecord(s->dep_join, ms));
   MGW_CUDA(cudaStreamWaitEvent(cs, s->dep_join, 0));
   return MGW_OK;
@@ -1166,7 +1246,9 @@ int mgw_sched_run(mgw_sched* s, void* compute_stream, void* comm_stream) {
   if (!(s->flags & MGW_SCHED_GRAPH)) return sched_enqueue(s, cs, ms);
   if (!s->graph_exec) {
     MGW_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    s->capturing = true;
     int rc = sched_enqueue(s, cs, ms);
+    s->capturing = false;
     cudaGraph_t graph = nullptr;
     cudaError_t e = cudaStreamEndCapture(cs, &graph);
     if (rc) {
@@ -1181,9 +1263,20 @@ int mgw_sched_run(mgw_sched* s, void* compute_stream, void* comm_stream) {
   return MGW_OK;
 }
 
+static int sched_fetch_stamps(mgw_sched* s) {
+  MGW_CUDA(cudaEventSynchronize(s->t_end));
+  MGW_CUDA(cudaMemcpy(s->h_stamps.data(), s->d_stamps, sizeof(uint64_t) * s->h_stamps.size(), cudaMemcpyDeviceToHost));
+  return MGW_OK;
+}
+
+static double span_s(const uint64_t* st) {
+  return (st[0] == ~0ull || st[1] < st[0]) ? 0.0 : (double)(st[1] - st[0]) * 1e-9;
+}
+
 int mgw_sched_times(mgw_sched* s, double* t_iter_s, double* compute_s, double* group_comm_s) {
   if (!s) return set_error(MGW_EINVAL, "schedule is null");
-  MGW_CUDA(cudaEventSynchronize(s->t_end));
+  int rc = sched_fetch_stamps(s);
+  if (rc) return rc;
   float ms = 0.f;
   if (t_iter_s) {
     MGW_CUDA(cudaEventElapsedTime(&ms, s->t_start, s->t_end));
@@ -1195,8 +1288,9 @@ int mgw_sched_times(mgw_sched* s, double* t_iter_s, double* compute_s, double* g
   }
   if (group_comm_s) {
     for (size_t g = 0; g < s->groups.size(); ++g) {
-      MGW_CUDA(cudaEventElapsedTime(&ms, s->t_g0[g], s->t_g1[g]));
-      group_comm_s[g] = ms * 1e-3;
+      const uint64_t* st = &s->h_stamps[6 * g];
+      // pack entry .. unpack exit: the group's whole exchange on the comm stream
+      group_comm_s[g] = (st[0] == ~0ull || st[5] < st[0]) ? 0.0 : (double)(st[5] - st[0]) * 1e-9;
     }
   }
   return MGW_OK;
@@ -1204,15 +1298,13 @@ int mgw_sched_times(mgw_sched* s, double* t_iter_s, double* compute_s, double* g
 
 int mgw_sched_kernel_times(mgw_sched* s, double* pack_s, double* allreduce_s, double* unpack_s) {
   if (!s || !pack_s || !allreduce_s || !unpack_s) return set_error(MGW_EINVAL, "bad arguments");
-  MGW_CUDA(cudaEventSynchronize(s->t_end));
-  float ms = 0.f;
+  int rc = sched_fetch_stamps(s);
+  if (rc) return rc;
   for (size_t g = 0; g < s->groups.size(); ++g) {
-    MGW_CUDA(cudaEventElapsedTime(&ms, s->t_g0[g], s->t_gp[g]));
-    pack_s[g] = ms * 1e-3;
-    MGW_CUDA(cudaEventElapsedTime(&ms, s->t_gp[g], s->t_ga[g]));
-    allreduce_s[g] = ms * 1e-3;
-    MGW_CUDA(cudaEventElapsedTime(&ms, s->t_ga[g], s->t_g1[g]));
-    unpack_s[g] = ms * 1e-3;
+    const uint64_t* st = &s->h_stamps[6 * g];
+    pack_s[g] = span_s(st);
+    allreduce_s[g] = span_s(st + 2);
+    unpack_s[g] = span_s(st + 4);
   }
   return MGW_OK;
 }

@@ -76,7 +76,7 @@ def test_launch_count_reported(torch_cuda):
     profile = resnet50_like(backward_seconds=4e-3, forward_seconds=2e-3)
     it = OverlappedIteration(profile, None, comm=None, rank=0, world=1, device="cuda:0")
     try:
-        # mark + per group: spin, fill, pack, unpack
-        assert it.launches_per_iteration == 1 + 4 * profile.num_layers
+        # stamp reset + mark + per group: spin, fill, pack, unpack
+        assert it.launches_per_iteration == 2 + 4 * profile.num_layers
     finally:
         it.close()
