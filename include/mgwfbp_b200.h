@@ -96,8 +96,10 @@ int mgw_device_count(int* out);
 int mgw_spin_ns(int64_t ns, void* stream);
 
 /* ---- K1 pack+scale / K4 unpack ---------------------------------------- */
-int mgw_desc_upload(const mgw_tensor_desc* rows, int n, void** dev_table);
-int mgw_desc_free(void* dev_table);
+/* A descriptor table handle: rows (layer `high` first) must tile [0, extent)
+ * contiguously; the handle keeps a device copy and a host mirror. */
+int mgw_desc_upload(const mgw_tensor_desc* rows, int n, void** table);
+int mgw_desc_free(void* table);
 int mgw_pack(const void* dev_table, int n, float* bucket, int64_t bucket_elems, float scale, void* stream);
 int mgw_unpack(const void* dev_table, int n, const float* bucket, int64_t bucket_elems, void* stream);
 int mgw_fill_const(const void* dev_table, int n, const float* values_dev, void* stream);
@@ -110,6 +112,7 @@ int mgw_comm_open_peers(mgw_comm* comm, const uint8_t* handles /* world * 64 byt
 int mgw_comm_destroy(mgw_comm* comm);
 int mgw_comm_set_timeout_ms(mgw_comm* comm, int64_t ms);
 int mgw_comm_set_oneshot_max(mgw_comm* comm, int64_t bytes);
+int mgw_comm_set_max_ctas(mgw_comm* comm, int ctas);
 int mgw_comm_input(mgw_comm* comm, float** slot); /* slot the next collective reads (syncs) */
 int mgw_comm_result(mgw_comm* comm, float** result);
 int mgw_comm_pack(mgw_comm* comm, const void* dev_table, int n, int64_t n_elem, float scale, void* stream);

@@ -1,0 +1,347 @@
+// allreduce.cuh -- K2 one-shot and K3 two-shot all-reduce over CUDA-IPC peer memory.
+//
+// Fold order (bit-exact with allreduce_net.py:360-411): element e lies in segment
+// s = seg(e) of `_segments(n, N)` (q, r = divmod(n, N); the first r segments hold
+// q + 1 elements); the reference ring accumulates it as
+//     ((x_s + x_{s+1}) + x_{s+2}) + ... + x_{s+N-1}      (ranks mod N)
+// Both kernels evaluate exactly that left fold with __fadd_rn.  The *work* split is
+// free: K3 partitions the bucket into N 16-B aligned parts (not the reference's
+// segments), so both of its phases stream equal, aligned chunks; every 16-B slot
+// still looks up its own fold start.  Slots straddling a segment boundary (at most
+// N-1 of them) take a scalar path.
+//
+// Synchronisation: per-CTA flag barriers in every rank's IPC control area
+// (st.release.sys / ld.acquire.sys), flags tagged (epoch << 32 | n mod 2^32) so a
+// length disagreement between ranks is detected at the barrier; epochs come from a
+// device call counter (graph-replay safe); bounded spins set a device error word and
+// raise a sticky abort flag on every rank.
+#pragma once
+
+#include "common.cuh"
+
+namespace mgw {
+
+enum : int { kNoBarrier = 1, kSkipPhase1 = 2, kSkipPhase2 = 4 };
+
+struct ArArgs {
+  char* slot[kMaxRanks];       // slot-0 base of every rank (peer mapped; own at [rank])
+  uint64_t* arrive[kMaxRanks]; // per-rank entry-barrier flags [2][kMaxBlocks][kMaxRanks]
+  uint64_t* mid[kMaxRanks];    // per-rank mid-barrier flags   [2][kMaxBlocks][kMaxRanks]
+  uint32_t* abort_flag[kMaxRanks];
+  float* out[kMaxRanks];       // result buffer (a real rank uses out[rank])
+  uint32_t* state;             // local [completed calls, finished CTAs]; null: no epochs
+  int* err;                    // local device error word
+  uint64_t* stamp;             // optional kernel span stamps [2]
+  int64_t slot_stride;         // bytes from slot 0 to slot 1
+  int64_t n;                   // elements
+  uint64_t timeout_ns;
+  int rank;
+  int world;
+  int flags;
+};
+
+// Loads in flight per thread ~ 8: unroll the slot loop by 8 / N.
+template <int N>
+struct Unroll {
+  static constexpr int value = N <= 2 ? 4 : (N <= 4 ? 2 : 1);
+};
+
+// One barrier round for this CTA.  Thread t < world signals rank t and waits for
+// rank t's matching CTA.
+__device__ __noinline__ int cta_barrier(uint64_t* const* flags, int parity, uint32_t epoch, uint32_t tag,
+                                        const ArArgs& a) {
+  __shared__ int s_status;
+  if (threadIdx.x == 0) s_status = 0;
+  __syncthreads();  // also orders this CTA's earlier stores before the release below
+  const int t = threadIdx.x;
+  if (t < a.world) {
+    const size_t base = ((size_t)parity * kMaxBlocks + blockIdx.x) * kMaxRanks;
+    store_release_sys(flags[t] + base + a.rank, ((uint64_t)epoch << 32) | tag);
+    const uint64_t* mine = flags[a.rank] + base + t;
+    const uint64_t start = global_ns();
+    int status = MGW_DEV_OK;
+    for (uint32_t spin = 0;; ++spin) {
+      const uint64_t v = load_acquire_sys(mine);
+      if ((uint32_t)(v >> 32) == epoch) {
+        if ((uint32_t)v != tag) status = MGW_DEV_LENGTH_MISMATCH;
+        break;
+      }
+      if ((spin & 63) == 63) {
+        if (load_relaxed_sys32(a.abort_flag[a.rank]) != 0u) {
+          status = MGW_DEV_PEER_ABORT;
+          break;
+        }
+        if (global_ns() - start > a.timeout_ns) {
+          status = MGW_DEV_TIMEOUT;
+          break;
+        }
+      }
+    }
+    if (status != MGW_DEV_OK) atomicCAS(&s_status, 0, status);
+  }
+  __syncthreads();
+  const int status = s_status;
+  if (status != MGW_DEV_OK && threadIdx.x == 0) {
+    atomicCAS(a.err, 0, status);
+    if (status != MGW_DEV_PEER_ABORT)
+      for (int r = 0; r < a.world; ++r) store_release_sys32(a.abort_flag[r], 1u);
+  }
+  return status;
+}
+
+// Last CTA out advances the call counter (epochs and slot parity come from it).
+// Kernel completion publishes the counter to the next kernel on the stream.
+__device__ __forceinline__ void finish_call(const ArArgs& a) {
+  stamp_exit(a.stamp);
+  if (a.state == nullptr) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t ticket = atomicAdd(&a.state[1], 1u);
+    if (ticket == gridDim.x - 1) {
+      a.state[1] = 0u;
+      atomicAdd(&a.state[0], 1u);
+    }
+  }
+}
+
+template <int N>
+__device__ __forceinline__ float fold1(const float* const* in, int s, int64_t e) {
+  float x[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    const int src = s + k >= N ? s + k - N : s + k;
+    x[k] = __ldcg(in[src] + e);
+  }
+  float acc = x[0];
+#pragma unroll
+  for (int k = 1; k < N; ++k) acc = __fadd_rn(acc, x[k]);
+  return acc;
+}
+
+// fold start of element e: advance a per-thread segment cursor (monotone in e)
+__device__ __forceinline__ int advance_segment(int s, int64_t e, const int64_t* seg_end) {
+  while (e >= seg_end[s]) ++s;
+  return s;
+}
+
+// U slots of 16 B starting at vector v, stride `step` vectors: fold every slot that
+// lies inside one segment; write results to dst0 (and dst1 when non-null).
+template <int N, int U>
+__device__ __forceinline__ void reduce_slots(const float* const* in, const int64_t* seg_end, int& seg, int64_t v,
+                                             int64_t v_end, int64_t step, float* dst0, float* dst1) {
+  float4 x[U][N];
+  int su[U];
+  bool ok[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t vv = v + u * step;
+    ok[u] = false;
+    su[u] = seg;
+    if (vv < v_end) {
+      const int64_t e = vv << 2;
+      seg = advance_segment(seg, e, seg_end);
+      su[u] = seg;
+      ok[u] = e + 3 < seg_end[seg];
+      if (ok[u]) {
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          const int src = seg + k >= N ? seg + k - N : seg + k;
+          x[u][k] = __ldcg(reinterpret_cast<const float4*>(in[src] + e));
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t vv = v + u * step;
+    if (vv >= v_end) continue;
+    const int64_t e = vv << 2;
+    if (ok[u]) {
+      float4 acc = x[u][0];
+#pragma unroll
+      for (int k = 1; k < N; ++k) acc = fadd4(acc, x[u][k]);
+      *reinterpret_cast<float4*>(dst0 + e) = acc;
+      if (dst1) *reinterpret_cast<float4*>(dst1 + e) = acc;
+    } else {
+      int s = su[u];
+      for (int j = 0; j < 4; ++j) {
+        s = advance_segment(s, e + j, seg_end);
+        const float y = fold1<N>(in, s, e + j);
+        dst0[e + j] = y;
+        if (dst1) dst1[e + j] = y;
+      }
+    }
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void reduce_tail(const float* const* in, const int64_t* seg_end, int64_t e0, int64_t e1,
+                                            float* dst0, float* dst1) {
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+    int s = advance_segment(0, e, seg_end);
+    const float y = fold1<N>(in, s, e);
+    dst0[e] = y;
+    if (dst1) dst1[e] = y;
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void kernel_prologue(const ArArgs& a, uint32_t& epoch, int& parity, const float** s_in,
+                                                int64_t* s_end) {
+  stamp_enter(a.stamp);
+  epoch = a.state != nullptr ? load_volatile32(a.state) + 1u : 0u;
+  parity = (int)(epoch & 1u);
+  if (threadIdx.x < N) {
+    const int t = threadIdx.x;
+    s_in[t] = reinterpret_cast<const float*>(a.slot[t] + (int64_t)parity * a.slot_stride);
+    const int64_t q = a.n / N, r = a.n % N;
+    s_end[t] = (int64_t)(t + 1) * q + (t + 1 < r ? t + 1 : r);  // end of reference segment t
+  }
+  __syncthreads();
+}
+
+// K2: every rank reads all N buckets and writes the whole reduced vector.
+template <int N>
+__global__ void __launch_bounds__(kThreads, 2) oneshot_kernel(const __grid_constant__ ArArgs a) {
+  constexpr int U = Unroll<N>::value;
+  __shared__ const float* s_in[kMaxRanks];
+  __shared__ int64_t s_end[kMaxRanks];
+  uint32_t epoch;
+  int parity;
+  kernel_prologue<N>(a, epoch, parity, s_in, s_end);
+  int status = MGW_DEV_OK;
+  if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, (uint32_t)a.n, a);
+  if (status == MGW_DEV_OK && a.n > 0) {
+    float* out = a.out[a.rank];
+    const int64_t nv = a.n >> 2;
+    const int64_t per = (nv + gridDim.x - 1) / gridDim.x;
+    const int64_t v0 = (int64_t)blockIdx.x * per;
+    const int64_t v1 = v0 + per < nv ? v0 + per : nv;
+    int seg = advance_segment(0, (v0 + threadIdx.x) << 2 < a.n ? (v0 + threadIdx.x) << 2 : 0, s_end);
+    for (int64_t v = v0 + threadIdx.x; v < v1; v += (int64_t)U * kThreads)
+      reduce_slots<N, U>(s_in, s_end, seg, v, v1, kThreads, out, nullptr);
+    if (blockIdx.x == gridDim.x - 1) reduce_tail<N>(s_in, s_end, nv << 2, a.n, out, nullptr);
+  }
+  finish_call(a);
+}
+
+// 16-B aligned work parts of the two-shot: rank p owns vectors [part(p), part(p+1));
+// the n % 4 tail elements belong to rank N-1.
+__device__ __forceinline__ int64_t part_begin(int p, int64_t nv, int world) { return (int64_t)p * nv / world; }
+
+// K3: phase 1 reduces this rank's part (fold order per slot) into its own slot (in
+// place) and into out; phase 2 copies every peer's reduced part into out.
+template <int N>
+__global__ void __launch_bounds__(kThreads, 2) twoshot_kernel(const __grid_constant__ ArArgs a) {
+  constexpr int U = Unroll<N>::value;
+  constexpr int UC = N <= 2 ? 8 : (N <= 3 ? 4 : (N <= 5 ? 2 : 1));  // copy slots per peer per step
+  __shared__ const float* s_in[kMaxRanks];
+  __shared__ int64_t s_end[kMaxRanks];
+  uint32_t epoch;
+  int parity;
+  kernel_prologue<N>(a, epoch, parity, s_in, s_end);
+  const int me = a.rank;
+  const int b = blockIdx.x, G = gridDim.x;
+  const int64_t nv = a.n >> 2;
+  float* out = a.out[me];
+  float* own = const_cast<float*>(s_in[me]);
+  float* second = out != own ? out : nullptr;
+  int status = MGW_DEV_OK;
+
+  if (!(a.flags & kSkipPhase1)) {
+    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, (uint32_t)a.n, a);
+    if (status == MGW_DEV_OK && a.n > 0) {
+      const int64_t p0 = part_begin(me, nv, N), p1 = part_begin(me + 1, nv, N);
+      const int64_t per = (p1 - p0 + G - 1) / G;
+      const int64_t v0 = p0 + (int64_t)b * per;
+      const int64_t v1 = v0 + per < p1 ? v0 + per : p1;
+      int seg = advance_segment(0, ((v0 + threadIdx.x) << 2) < a.n ? (v0 + threadIdx.x) << 2 : 0, s_end);
+      for (int64_t v = v0 + threadIdx.x; v < v1; v += (int64_t)U * kThreads)
+        reduce_slots<N, U>(s_in, s_end, seg, v, v1, kThreads, own, second);
+      if (me == N - 1 && b == G - 1) reduce_tail<N>(s_in, s_end, nv << 2, a.n, own, second);
+    }
+  }
+
+  if (status == MGW_DEV_OK && !(a.flags & kSkipPhase2)) {
+    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.mid, parity, epoch, (uint32_t)a.n, a);
+    if (status == MGW_DEV_OK && a.n > 0) {
+      // chunk b of every peer part; peers interleaved so N-1 streams are in flight.
+      // Chunk bounds live in shared memory to keep the copy loop's registers for data.
+      __shared__ int64_t s_lo[kMaxRanks], s_len[kMaxRanks];
+      if (threadIdx.x > 0 && threadIdx.x < N) {
+        const int k = threadIdx.x;
+        const int p = me + k >= N ? me + k - N : me + k;
+        const int64_t q0 = part_begin(p, nv, N), q1 = part_begin(p + 1, nv, N);
+        const int64_t per = (q1 - q0 + G - 1) / G;
+        const int64_t c0 = q0 + (int64_t)b * per;
+        const int64_t c1 = c0 + per < q1 ? c0 + per : q1;
+        s_lo[k] = c0;
+        s_len[k] = c1 > c0 ? c1 - c0 : 0;
+      }
+      __syncthreads();
+      int64_t longest = 0;
+      for (int k = 1; k < N; ++k) longest = s_len[k] > longest ? s_len[k] : longest;
+      float4* out4 = reinterpret_cast<float4*>(out);
+      for (int64_t i = threadIdx.x; i < longest; i += (int64_t)UC * kThreads) {
+        float4 x[UC][N];
+#pragma unroll
+        for (int u = 0; u < UC; ++u)
+#pragma unroll
+          for (int k = 1; k < N; ++k) {
+            const int64_t ii = i + (int64_t)u * kThreads;
+            const int p = me + k >= N ? me + k - N : me + k;
+            if (ii < s_len[k]) x[u][k] = __ldcg(reinterpret_cast<const float4*>(s_in[p]) + s_lo[k] + ii);
+          }
+#pragma unroll
+        for (int u = 0; u < UC; ++u)
+#pragma unroll
+          for (int k = 1; k < N; ++k) {
+            const int64_t ii = i + (int64_t)u * kThreads;
+            if (ii < s_len[k]) out4[s_lo[k] + ii] = x[u][k];
+          }
+      }
+      if (me != N - 1 && b == G - 1)
+        for (int64_t e = (nv << 2) + threadIdx.x; e < a.n; e += blockDim.x) out[e] = __ldcg(s_in[N - 1] + e);
+    }
+  }
+  finish_call(a);
+}
+
+inline int grid_for(int64_t vectors, int64_t per_cta, int max_ctas) {
+  int64_t g = (vectors + per_cta - 1) / per_cta;
+  if (g < 1) g = 1;
+  if (g > max_ctas) g = max_ctas;
+  return (int)g;
+}
+
+template <int N>
+int launch_allreduce_n(const ArArgs& a, int algo, int max_ctas, cudaStream_t stream) {
+  constexpr int U = Unroll<N>::value;
+  const int64_t nv = a.n >> 2;
+  if (algo == MGW_ALGO_ONESHOT) {
+    const int grid = grid_for(nv, (int64_t)kThreads * U, max_ctas);
+    oneshot_kernel<N><<<grid, kThreads, 0, stream>>>(a);
+  } else {
+    const int grid = grid_for(nv / N, (int64_t)kThreads * U, max_ctas);
+    twoshot_kernel<N><<<grid, kThreads, 0, stream>>>(a);
+  }
+  MGW_CHECK_LAUNCH();
+  return MGW_OK;
+}
+
+inline int launch_allreduce(const ArArgs& a, int algo, int max_ctas, cudaStream_t stream) {
+  max_ctas = max_ctas < kMaxBlocks ? max_ctas : kMaxBlocks;  // one barrier flag slot per CTA
+  switch (a.world) {
+    case 1: return launch_allreduce_n<1>(a, algo, max_ctas, stream);
+    case 2: return launch_allreduce_n<2>(a, algo, max_ctas, stream);
+    case 3: return launch_allreduce_n<3>(a, algo, max_ctas, stream);
+    case 4: return launch_allreduce_n<4>(a, algo, max_ctas, stream);
+    case 5: return launch_allreduce_n<5>(a, algo, max_ctas, stream);
+    case 6: return launch_allreduce_n<6>(a, algo, max_ctas, stream);
+    case 7: return launch_allreduce_n<7>(a, algo, max_ctas, stream);
+    case 8: return launch_allreduce_n<8>(a, algo, max_ctas, stream);
+    default: return set_error(MGW_EINVAL, "world %d outside 1..%d", a.world, kMaxRanks);
+  }
+}
+
+}  // namespace mgw

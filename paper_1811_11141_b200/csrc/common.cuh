@@ -1,0 +1,129 @@
+// common.cuh -- constants, error plumbing and device helpers shared by the kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "mgwfbp_b200.h"
+
+namespace mgw {
+
+// ------------------------------------------------------------------ errors
+
+inline std::string& last_error_slot() {
+  thread_local std::string msg;
+  return msg;
+}
+
+inline int set_error(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  last_error_slot() = buf;
+  return code;
+}
+
+#define MGW_CUDA(call)                                                                             \
+  do {                                                                                             \
+    cudaError_t err_ = (call);                                                                     \
+    if (err_ != cudaSuccess)                                                                       \
+      return ::mgw::set_error(MGW_ECUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(err_), __FILE__, \
+                              __LINE__);                                                           \
+  } while (0)
+
+#define MGW_CHECK_LAUNCH()                                                                         \
+  do {                                                                                             \
+    cudaError_t err_ = cudaGetLastError();                                                         \
+    if (err_ != cudaSuccess)                                                                       \
+      return ::mgw::set_error(MGW_ECUDA, "kernel launch: %s (%s:%d)", cudaGetErrorString(err_),   \
+                              __FILE__, __LINE__);                                                 \
+  } while (0)
+
+// --------------------------------------------------------------- constants
+
+constexpr int kMaxRanks = MGW_MAX_RANKS;
+constexpr int kMaxBlocks = 512;     // barrier flag slots per parity (>= any grid we launch)
+constexpr int kThreads = 512;       // threads per CTA of every bulk kernel
+constexpr int kSMs = 148;
+constexpr int64_t kTile = 16384;    // pack/unpack tile: 64 KB of bucket per CTA step
+constexpr int kInlineRows = 40;     // descriptor rows passed by value as kernel parameters
+
+// IPC region layout (per rank): [arrive | mid | abort | pad] [slot 0] [slot 1]
+constexpr size_t kFlagsPerParity = (size_t)kMaxBlocks * kMaxRanks;
+constexpr size_t kArriveOff = 0;
+constexpr size_t kMidOff = kArriveOff + 2 * kFlagsPerParity * sizeof(uint64_t);
+constexpr size_t kAbortOff = kMidOff + 2 * kFlagsPerParity * sizeof(uint64_t);
+constexpr size_t kCtrlBytes = 262144;
+static_assert(kAbortOff + 256 <= kCtrlBytes, "control area overflow");
+
+struct Row {  // identical layout to mgw_tensor_desc
+  float* ptr;
+  int64_t count;
+  int64_t offset;
+};
+static_assert(sizeof(Row) == sizeof(mgw_tensor_desc), "Row must mirror mgw_tensor_desc");
+
+// ------------------------------------------------------------ device utils
+
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void store_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ void store_release_sys32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint64_t load_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ uint32_t load_relaxed_sys32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ uint32_t load_volatile32(const uint32_t* p) {
+  return *reinterpret_cast<const volatile uint32_t*>(p);
+}
+
+// Kernel span stamps: every CTA folds its entry time into stamp[0] (min) and its
+// exit time into stamp[1] (max), so [stamp[0], stamp[1]] is the kernel's execution
+// span without the ~6.5 us an event-record pair costs inside a CUDA graph.
+__device__ __forceinline__ void stamp_enter(uint64_t* stamp) {
+  if (stamp != nullptr && threadIdx.x == 0)
+    atomicMin(reinterpret_cast<unsigned long long*>(stamp), (unsigned long long)global_ns());
+}
+
+__device__ __forceinline__ void stamp_exit(uint64_t* stamp) {
+  if (stamp != nullptr) {
+    __syncthreads();
+    if (threadIdx.x == 0) atomicMax(reinterpret_cast<unsigned long long*>(stamp + 1), (unsigned long long)global_ns());
+  }
+}
+
+__device__ __forceinline__ float4 fadd4(float4 a, float4 b) {
+  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
+}
+
+__device__ __forceinline__ float4 fmul4(float4 a, float s) {
+  return make_float4(__fmul_rn(a.x, s), __fmul_rn(a.y, s), __fmul_rn(a.z, s), __fmul_rn(a.w, s));
+}
+
+inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+}  // namespace mgw

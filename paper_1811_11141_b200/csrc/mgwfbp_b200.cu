@@ -1,269 +1,36 @@
-// mgwfbp_b200.cu -- sm_100a kernels and C ABI of the MG-WFBP merged-gradient data path.
+// mgwfbp_b200.cu -- C ABI of the MG-WFBP merged-gradient data path (sm_100a).
 //
 //   K1 pack+scale   gather a merge group's layer gradients into one contiguous
-//                   bucket (layer `high` at offset 0; allreduce_net.py:495-509)
+//                   bucket (layer `high` at offset 0; allreduce_net.py:495-509)  rows.cuh
 //   K2 one-shot     every rank pulls all N peer buckets over NVLink (CUDA IPC)
-//                   and folds them in the reference ring's per-element order
-//   K3 two-shot     reduce-scatter of the rank's own `_segments` slice, then
-//                   all-gather of the peers' reduced slices, same fold order
-//   K4 unpack       scatter the reduced bucket back to the layer tensors
-//   K5 spin         simulated backward on the compute stream (%globaltimer)
+//                   and folds them in the reference ring's per-element order    allreduce.cuh
+//   K3 two-shot     reduce-scatter of an aligned 1/N part, then all-gather of
+//                   the peers' reduced parts, same per-element fold order        allreduce.cuh
+//   K4 unpack       scatter the reduced bucket back to the layer tensors         rows.cuh
+//   K5 spin         simulated backward on the compute stream (%globaltimer)      below
 //
-// Fold order (bit-exact with allreduce_net.py:360-411): element e of the bucket
-// lies in segment s = seg(e) of `_segments(n, N)`; the ring accumulates it as
-// ((x_s + x_{s+1}) + x_{s+2}) + ... + x_{s+N-1} (ranks mod N).  Both K2 and K3
-// reproduce exactly that left fold with __fadd_rn (no contraction).
-//
-// Synchronisation: per-block flag barriers in the IPC control area of every
-// rank (system-scope release/acquire), epochs taken from a device-side call
-// counter so the whole iteration can be replayed from a CUDA graph, bounded
-// spins that set a device error word (-> ProtocolError on the host).
+// Host side: the communicator (IPC buckets, flags, peer mappings), descriptor
+// tables, the Algorithm-2 schedule engine (streams, events, CUDA graph) and the
+// timing helpers.  Every entry point returns MGW_* status codes.
 
 #include "mgwfbp_b200.h"
 
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <cstdarg>
 #include <cstdint>
-#include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
+#include "allreduce.cuh"
+#include "common.cuh"
+#include "rows.cuh"
+
+using namespace mgw;
+
 namespace {
-
-// ------------------------------------------------------------------ errors
-
-thread_local std::string g_last_error;
-
-int set_error(int code, const char* fmt, ...) {
-  char buf[1024];
-  va_list ap;
-  va_start(ap, fmt);
-  vsnprintf(buf, sizeof(buf), fmt, ap);
-  va_end(ap);
-  g_last_error = buf;
-  return code;
-}
-
-#define MGW_CUDA(call)                                                                            \
-  do {                                                                                            \
-    cudaError_t err_ = (call);                                                                    \
-    if (err_ != cudaSuccess)                                                                      \
-      return set_error(MGW_ECUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(err_), __FILE__, __LINE__); \
-  } while (0)
-
-#define MGW_CHECK_LAUNCH()                                                                        \
-  do {                                                                                            \
-    cudaError_t err_ = cudaGetLastError();                                                        \
-    if (err_ != cudaSuccess)                                                                      \
-      return set_error(MGW_ECUDA, "kernel launch: %s (%s:%d)", cudaGetErrorString(err_), __FILE__, __LINE__); \
-  } while (0)
-
-// --------------------------------------------------------------- constants
-
-constexpr int kMaxRanks = MGW_MAX_RANKS;
-constexpr int kMaxBlocks = 256;          // per-block barrier slots per parity
-constexpr int kThreads = 512;            // threads per CTA for every bulk kernel
-constexpr int64_t kTile = 16384;         // pack/unpack tile: 64 KB of bucket per CTA step
-constexpr int kSMs = 148;
-
-// IPC region layout (per rank):  [arrive | mid | abort | pad] [slot 0] [slot 1]
-constexpr size_t kFlagsPerParity = (size_t)kMaxBlocks * kMaxRanks;
-constexpr size_t kArriveOff = 0;
-constexpr size_t kMidOff = kArriveOff + 2 * kFlagsPerParity * sizeof(uint64_t);
-constexpr size_t kAbortOff = kMidOff + 2 * kFlagsPerParity * sizeof(uint64_t);
-constexpr size_t kCtrlBytes = 131072;
-static_assert(kAbortOff + 256 <= kCtrlBytes, "control area overflow");
-
-enum : int { kNoBarrier = 1, kSkipPhase1 = 2, kSkipPhase2 = 4 };
-
-struct Row {  // identical layout to mgw_tensor_desc
-  float* ptr;
-  int64_t count;
-  int64_t offset;
-};
-static_assert(sizeof(Row) == sizeof(mgw_tensor_desc), "Row must mirror mgw_tensor_desc");
-
-// ------------------------------------------------------------ device utils
-
-__device__ __forceinline__ uint64_t global_ns() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
-__device__ __forceinline__ void store_relaxed_sys(uint64_t* p, uint64_t v) {
-  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-__device__ __forceinline__ void store_relaxed_sys32(uint32_t* p, uint32_t v) {
-  asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-__device__ __forceinline__ uint64_t load_acquire_sys(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ uint32_t load_acquire_sys32(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ uint32_t load_volatile32(const uint32_t* p) {
-  return *reinterpret_cast<const volatile uint32_t*>(p);
-}
-
-// Kernel span stamps: every CTA folds its entry time into stamp[0] (min) and its
-// exit time into stamp[1] (max), so [stamp[0], stamp[1]] is the kernel's execution
-// span without the ~6.5 us an event record pair costs inside a CUDA graph.
-__device__ __forceinline__ void stamp_enter(uint64_t* stamp) {
-  if (stamp != nullptr && threadIdx.x == 0) atomicMin(reinterpret_cast<unsigned long long*>(stamp), (unsigned long long)global_ns());
-}
-
-__device__ __forceinline__ void stamp_exit(uint64_t* stamp) {
-  if (stamp != nullptr) {
-    __syncthreads();
-    if (threadIdx.x == 0) atomicMax(reinterpret_cast<unsigned long long*>(stamp + 1), (unsigned long long)global_ns());
-  }
-}
-
-__device__ __forceinline__ float4 fadd4(float4 a, float4 b) {
-  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
-}
-
-__device__ __forceinline__ float4 fmul4(float4 a, float s) {
-  return make_float4(__fmul_rn(a.x, s), __fmul_rn(a.y, s), __fmul_rn(a.z, s), __fmul_rn(a.w, s));
-}
-
-// ======================================================== K1 / K4: pack, unpack
-//
-// The bucket of a group is tiled in kTile-element steps; a CTA binary-searches
-// the first descriptor row overlapping its tile and walks the rows it covers.
-// Each (row, tile) span is copied block-cooperatively: 128-bit accesses when
-// tensor and bucket addresses agree modulo 16 B (true for every torch
-// allocation and every profile whose layer sizes are multiples of 4), scalar
-// coalesced accesses otherwise.
-
-enum class RowOp { kPack, kUnpack, kFill, kCheck };
-
-template <RowOp kOp, bool kScale>
-__device__ __forceinline__ void span_op(float* __restrict__ tensor, float* __restrict__ bucket, int64_t len,
-                                        float scale, float value, unsigned long long* mismatches) {
-  const int t = threadIdx.x;
-  const int nt = blockDim.x;
-  if constexpr (kOp == RowOp::kFill) {
-    const uintptr_t a = reinterpret_cast<uintptr_t>(tensor);
-    int64_t head = (int64_t)(((16 - (a & 15)) & 15) >> 2);
-    head = head < len ? head : len;
-    for (int64_t i = t; i < head; i += nt) tensor[i] = value;
-    float4* d4 = reinterpret_cast<float4*>(tensor + head);
-    const int64_t nv = (len - head) >> 2;
-    const float4 v4 = make_float4(value, value, value, value);
-    for (int64_t i = t; i < nv; i += nt) d4[i] = v4;
-    for (int64_t i = head + (nv << 2) + t; i < len; i += nt) tensor[i] = value;
-  } else if constexpr (kOp == RowOp::kCheck) {
-    unsigned long long bad = 0;
-    for (int64_t i = t; i < len; i += nt) bad += (tensor[i] != value);
-    if (bad) atomicAdd(mismatches, bad);
-  } else {
-    const float* __restrict__ src = (kOp == RowOp::kUnpack) ? bucket : tensor;
-    float* __restrict__ dst = (kOp == RowOp::kUnpack) ? tensor : bucket;
-    const uintptr_t sa = reinterpret_cast<uintptr_t>(src);
-    const uintptr_t da = reinterpret_cast<uintptr_t>(dst);
-    if (((sa ^ da) & 15) == 0) {
-      int64_t head = (int64_t)(((16 - (da & 15)) & 15) >> 2);
-      head = head < len ? head : len;
-      for (int64_t i = t; i < head; i += nt) dst[i] = kScale ? __fmul_rn(src[i], scale) : src[i];
-      const float4* __restrict__ s4 = reinterpret_cast<const float4*>(src + head);
-      float4* __restrict__ d4 = reinterpret_cast<float4*>(dst + head);
-      const int64_t nv = (len - head) >> 2;
-      int64_t i = t;
-      for (; i + 3 * nt < nv; i += 4 * nt) {
-        float4 r0 = s4[i], r1 = s4[i + nt], r2 = s4[i + 2 * nt], r3 = s4[i + 3 * nt];
-        if (kScale) {
-          r0 = fmul4(r0, scale);
-          r1 = fmul4(r1, scale);
-          r2 = fmul4(r2, scale);
-          r3 = fmul4(r3, scale);
-        }
-        d4[i] = r0;
-        d4[i + nt] = r1;
-        d4[i + 2 * nt] = r2;
-        d4[i + 3 * nt] = r3;
-      }
-      for (; i < nv; i += nt) d4[i] = kScale ? fmul4(s4[i], scale) : s4[i];
-      for (int64_t j = head + (nv << 2) + t; j < len; j += nt) dst[j] = kScale ? __fmul_rn(src[j], scale) : src[j];
-    } else {
-      for (int64_t i = t; i < len; i += nt) dst[i] = kScale ? __fmul_rn(src[i], scale) : src[i];
-    }
-  }
-}
-
-__device__ __forceinline__ int first_row_covering(const Row* __restrict__ rows, int n, int64_t e) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (rows[mid].offset + rows[mid].count > e)
-      hi = mid;
-    else
-      lo = mid + 1;
-  }
-  return lo;
-}
-
-template <RowOp kOp, bool kScale>
-__global__ void __launch_bounds__(kThreads) rows_kernel(const Row* __restrict__ rows, int n_rows, float* bucket,
-                                                        int64_t total, float scale, const float* __restrict__ values,
-                                                        const uint32_t* calls, int64_t slot_stride_elems,
-                                                        unsigned long long* mismatches, uint64_t* stamp) {
-  stamp_enter(stamp);
-  if (calls != nullptr) {
-    // epoch of the collective this pack feeds = completed calls + 1
-    const uint32_t epoch = load_volatile32(calls) + 1u;
-    bucket += (int64_t)(epoch & 1u) * slot_stride_elems;
-  }
-  for (int64_t t0 = (int64_t)blockIdx.x * kTile; t0 < total; t0 += (int64_t)gridDim.x * kTile) {
-    const int64_t t1 = t0 + kTile < total ? t0 + kTile : total;
-    for (int k = first_row_covering(rows, n_rows, t0); k < n_rows; ++k) {
-      const Row r = rows[k];
-      if (r.offset >= t1) break;
-      const int64_t lo = r.offset > t0 ? r.offset : t0;
-      const int64_t hi = (r.offset + r.count) < t1 ? (r.offset + r.count) : t1;
-      if (hi <= lo) continue;
-      const float v = values ? values[k] : 0.f;
-      span_op<kOp, kScale>(r.ptr + (lo - r.offset), bucket + lo, hi - lo, scale, v, mismatches);
-    }
-  }
-  stamp_exit(stamp);
-}
-
-int rows_grid(int64_t total) {
-  int64_t tiles = (total + kTile - 1) / kTile;
-  int64_t cap = (int64_t)kSMs * 4;
-  return (int)std::max<int64_t>(1, std::min(tiles, cap));
-}
-
-template <RowOp kOp>
-int launch_rows(const void* table, int n, float* bucket, int64_t total, float scale, const float* values,
-                const uint32_t* calls, int64_t slot_stride_elems, unsigned long long* mismatches,
-                cudaStream_t stream, uint64_t* stamp = nullptr) {
-  if (total <= 0 || n <= 0) return MGW_OK;
-  const Row* rows = static_cast<const Row*>(table);
-  const int grid = rows_grid(total);
-  if (kOp == RowOp::kPack && scale != 1.0f)
-    rows_kernel<kOp, true><<<grid, kThreads, 0, stream>>>(rows, n, bucket, total, scale, values, calls,
-                                                          slot_stride_elems, mismatches, stamp);
-  else
-    rows_kernel<kOp, false><<<grid, kThreads, 0, stream>>>(rows, n, bucket, total, scale, values, calls,
-                                                           slot_stride_elems, mismatches, stamp);
-  MGW_CHECK_LAUNCH();
-  return MGW_OK;
-}
 
 // ============================================================ K5: spin kernels
 
@@ -290,361 +57,17 @@ __global__ void spin_until_kernel(const uint64_t* clock, int64_t deadline_ns) {
   while (global_ns() < until) __nanosleep(128);
 }
 
-// ====================================================== K2 / K3: all-reduce
-
-struct ArArgs {
-  char* slot[kMaxRanks];       // slot-0 base of every rank (peer mapped; own at [rank])
-  uint64_t* arrive[kMaxRanks]; // per-rank entry-barrier flags  [2][kMaxBlocks][kMaxRanks]
-  uint64_t* mid[kMaxRanks];    // per-rank mid-barrier flags    [2][kMaxBlocks][kMaxRanks]
-  uint32_t* abort_flag[kMaxRanks];
-  float* out[kMaxRanks];       // result buffer (real mode uses out[rank])
-  uint32_t* state;             // local device [completed calls, finished CTAs]; null = no epochs
-  int* err;                    // local device error word
-  uint64_t* stamp;             // optional kernel span stamps [2]
-  int64_t slot_stride;         // bytes from slot 0 to slot 1
-  int64_t n;                   // elements
-  uint64_t timeout_ns;
-  int rank;
-  int world;
-  int flags;
-};
-
-// segment of bucket element e under _segments(n, N): q, r = divmod(n, N); the
-// first r segments hold q+1 elements (allreduce_net.py:360-367)
-__device__ __forceinline__ int segment_of(int64_t e, int64_t q, int64_t r) {
-  const int64_t big = r * (q + 1);
-  return e < big ? (int)(e / (q + 1)) : (int)(r + (e - big) / q);
-}
-
-__device__ __forceinline__ void segment_range(int s, int64_t q, int64_t r, int64_t& off, int64_t& len) {
-  len = q + (s < r ? 1 : 0);
-  off = (int64_t)s * q + (s < r ? s : r);
-}
-
-// Work a CTA owns inside one segment: a scalar head (CTA 0), a slice of the
-// 16-B aligned vector body, and a scalar tail (last CTA).  Deterministic in
-// (segment, cta, grid) so a CTA on another rank can find what this CTA wrote.
-struct Chunk {
-  int64_t v0, v1;  // vector indices (4 floats each) into the bucket
-  int64_t h0, h1;  // scalar head elements
-  int64_t t0, t1;  // scalar tail elements
-};
-
-__device__ __forceinline__ Chunk chunk_of(int64_t off, int64_t len, int b, int G) {
-  Chunk c{0, 0, 0, 0, 0, 0};
-  const int64_t end = off + len;
-  const int64_t a0 = (off + 3) & ~int64_t(3);
-  const int64_t a1 = end & ~int64_t(3);
-  if (a0 >= a1) {
-    if (b == 0) {
-      c.h0 = off;
-      c.h1 = end;
-    }
-    return c;
-  }
-  if (b == 0) {
-    c.h0 = off;
-    c.h1 = a0;
-  }
-  if (b == G - 1) {
-    c.t0 = a1;
-    c.t1 = end;
-  }
-  const int64_t nv = (a1 - a0) >> 2;
-  const int64_t per = (nv + G - 1) / G;
-  const int64_t lo = (int64_t)b * per < nv ? (int64_t)b * per : nv;
-  const int64_t hi = (int64_t)(b + 1) * per < nv ? (int64_t)(b + 1) * per : nv;
-  c.v0 = (a0 >> 2) + lo;
-  c.v1 = (a0 >> 2) + hi;
-  return c;
-}
-
-// Per-CTA barrier across ranks.  Thread t < world signals rank t and waits for
-// rank t's matching CTA.  Flags carry (epoch << 32 | n mod 2^32) so a length
-// disagreement is detected at the barrier (replaces the frame header check,
-// allreduce_net.py:342-347).  Parity-split slots keep epoch e's flags intact
-// until every rank has passed e.
-__device__ int cta_barrier(uint64_t* const* flags, int parity, uint32_t epoch, uint32_t tag, const ArArgs& a) {
-  __shared__ int s_status;
-  if (threadIdx.x == 0) s_status = 0;
-  __syncthreads();
-  const int t = threadIdx.x;
-  if (t < a.world) {
-    const size_t base = ((size_t)parity * kMaxBlocks + blockIdx.x) * kMaxRanks;
-    __threadfence_system();
-    store_relaxed_sys(flags[t] + base + a.rank, ((uint64_t)epoch << 32) | tag);
-    const uint64_t* mine = flags[a.rank] + base + t;
-    const uint64_t start = global_ns();
-    int status = MGW_DEV_OK;
-    for (;;) {
-      const uint64_t v = load_acquire_sys(mine);
-      if ((uint32_t)(v >> 32) == epoch) {
-        if ((uint32_t)v != tag) status = MGW_DEV_LENGTH_MISMATCH;
-        break;
-      }
-      if (load_acquire_sys32(a.abort_flag[a.rank]) != 0u) {
-        status = MGW_DEV_PEER_ABORT;
-        break;
-      }
-      if (global_ns() - start > a.timeout_ns) {
-        status = MGW_DEV_TIMEOUT;
-        break;
-      }
-    }
-    __threadfence_system();
-    if (status != MGW_DEV_OK) atomicCAS(&s_status, 0, status);
-  }
-  __syncthreads();
-  const int status = s_status;
-  if (status != MGW_DEV_OK && threadIdx.x == 0) {
-    atomicCAS(a.err, 0, status);
-    if (status != MGW_DEV_PEER_ABORT)
-      for (int r = 0; r < a.world; ++r) store_relaxed_sys32(a.abort_flag[r], 1u);
-  }
-  return status;
-}
-
-// Last CTA out advances the call counter (epochs and slot parity come from it).
-__device__ __forceinline__ void finish_call(const ArArgs& a) {
-  stamp_exit(a.stamp);
-  if (a.state == nullptr) return;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const uint32_t ticket = atomicAdd(&a.state[1], 1u);
-    if (ticket == gridDim.x - 1) {
-      a.state[1] = 0u;
-      __threadfence();
-      atomicAdd(&a.state[0], 1u);
-    }
-  }
-}
-
-template <int N>
-__device__ __forceinline__ float4 fold4(const float* const* in, int s, int64_t e) {
-  float4 x[N];
-#pragma unroll
-  for (int k = 0; k < N; ++k) {
-    int src = s + k;
-    src = src >= N ? src - N : src;
-    x[k] = __ldcg(reinterpret_cast<const float4*>(in[src] + e));
-  }
-  float4 acc = x[0];
-#pragma unroll
-  for (int k = 1; k < N; ++k) acc = fadd4(acc, x[k]);
-  return acc;
-}
-
-template <int N>
-__device__ __forceinline__ float fold1(const float* const* in, int s, int64_t e) {
-  float x[N];
-#pragma unroll
-  for (int k = 0; k < N; ++k) {
-    int src = s + k;
-    src = src >= N ? src - N : src;
-    x[k] = __ldcg(in[src] + e);
-  }
-  float acc = x[0];
-#pragma unroll
-  for (int k = 1; k < N; ++k) acc = __fadd_rn(acc, x[k]);
-  return acc;
-}
-
-template <int N>
-__device__ __forceinline__ void load_slots(const ArArgs& a, int parity, const float** s_in) {
-  if (threadIdx.x < N) s_in[threadIdx.x] = reinterpret_cast<const float*>(a.slot[threadIdx.x] + (int64_t)parity * a.slot_stride);
-  __syncthreads();
-}
-
-// K2: every rank reads all N buckets and writes the full reduced vector.
-template <int N>
-__global__ void __launch_bounds__(kThreads) oneshot_kernel(ArArgs a) {
-  __shared__ const float* s_in[kMaxRanks];
-  stamp_enter(a.stamp);
-  uint32_t epoch = 0;
-  if (a.state != nullptr) epoch = load_volatile32(a.state) + 1u;
-  const int parity = (int)(epoch & 1u);
-  load_slots<N>(a, parity, s_in);
-  int status = MGW_DEV_OK;
-  if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, (uint32_t)a.n, a);
-  if (status == MGW_DEV_OK) {
-    float* __restrict__ out = a.out[a.rank];
-    const int64_t n = a.n, q = n / N, r = n % N;
-    const int64_t nv = n >> 2;
-    const int64_t per = (nv + gridDim.x - 1) / gridDim.x;
-    const int64_t v0 = (int64_t)blockIdx.x * per;
-    const int64_t v1 = v0 + per < nv ? v0 + per : nv;
-    int64_t v = v0 + threadIdx.x;
-    for (; v + blockDim.x < v1; v += 2 * blockDim.x) {
-      const int64_t e0 = v << 2, e1 = (v + blockDim.x) << 2;
-      const int s0 = segment_of(e0, q, r), s1 = segment_of(e1, q, r);
-      if (s0 == segment_of(e0 + 3, q, r) && s1 == segment_of(e1 + 3, q, r)) {
-        const float4 y0 = fold4<N>(s_in, s0, e0);
-        const float4 y1 = fold4<N>(s_in, s1, e1);
-        *reinterpret_cast<float4*>(out + e0) = y0;
-        *reinterpret_cast<float4*>(out + e1) = y1;
-      } else {
-        for (int j = 0; j < 4; ++j) out[e0 + j] = fold1<N>(s_in, segment_of(e0 + j, q, r), e0 + j);
-        for (int j = 0; j < 4; ++j) out[e1 + j] = fold1<N>(s_in, segment_of(e1 + j, q, r), e1 + j);
-      }
-    }
-    for (; v < v1; v += blockDim.x) {
-      const int64_t e = v << 2;
-      const int s = segment_of(e, q, r);
-      if (s == segment_of(e + 3, q, r)) {
-        *reinterpret_cast<float4*>(out + e) = fold4<N>(s_in, s, e);
-      } else {
-        for (int j = 0; j < 4; ++j) out[e + j] = fold1<N>(s_in, segment_of(e + j, q, r), e + j);
-      }
-    }
-    if (blockIdx.x == gridDim.x - 1)
-      for (int64_t e = (nv << 2) + threadIdx.x; e < n; e += blockDim.x) out[e] = fold1<N>(s_in, segment_of(e, q, r), e);
-  }
-  finish_call(a);
-}
-
-// K3: reduce-scatter own segment (in place in the own slot, copy to out), then
-// all-gather the peers' reduced segments into out.
-template <int N>
-__global__ void __launch_bounds__(kThreads) twoshot_kernel(ArArgs a) {
-  __shared__ const float* s_in[kMaxRanks];
-  stamp_enter(a.stamp);
-  uint32_t epoch = 0;
-  if (a.state != nullptr) epoch = load_volatile32(a.state) + 1u;
-  const int parity = (int)(epoch & 1u);
-  load_slots<N>(a, parity, s_in);
-  const int me = a.rank;
-  const int b = blockIdx.x, G = gridDim.x;
-  const int64_t n = a.n, q = n / N, r = n % N;
-  float* __restrict__ out = a.out[me];
-  float* own = const_cast<float*>(s_in[me]);
-  const bool copy_out = out != own;
-  int status = MGW_DEV_OK;
-
-  if (!(a.flags & kSkipPhase1)) {
-    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, (uint32_t)a.n, a);
-    if (status == MGW_DEV_OK) {
-      int64_t off, len;
-      segment_range(me, q, r, off, len);
-      const Chunk c = chunk_of(off, len, b, G);
-      for (int64_t e = c.h0 + threadIdx.x; e < c.h1; e += blockDim.x) {
-        const float y = fold1<N>(s_in, me, e);
-        own[e] = y;
-        if (copy_out) out[e] = y;
-      }
-      int64_t v = c.v0 + threadIdx.x;
-      for (; v + blockDim.x < c.v1; v += 2 * blockDim.x) {
-        const int64_t e0 = v << 2, e1 = (v + blockDim.x) << 2;
-        const float4 y0 = fold4<N>(s_in, me, e0);
-        const float4 y1 = fold4<N>(s_in, me, e1);
-        *reinterpret_cast<float4*>(own + e0) = y0;
-        *reinterpret_cast<float4*>(own + e1) = y1;
-        if (copy_out) {
-          *reinterpret_cast<float4*>(out + e0) = y0;
-          *reinterpret_cast<float4*>(out + e1) = y1;
-        }
-      }
-      for (; v < c.v1; v += blockDim.x) {
-        const int64_t e = v << 2;
-        const float4 y = fold4<N>(s_in, me, e);
-        *reinterpret_cast<float4*>(own + e) = y;
-        if (copy_out) *reinterpret_cast<float4*>(out + e) = y;
-      }
-      for (int64_t e = c.t0 + threadIdx.x; e < c.t1; e += blockDim.x) {
-        const float y = fold1<N>(s_in, me, e);
-        own[e] = y;
-        if (copy_out) out[e] = y;
-      }
-    }
-  }
-
-  if (status == MGW_DEV_OK && !(a.flags & kSkipPhase2)) {
-    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.mid, parity, epoch, (uint32_t)a.n, a);
-    if (status == MGW_DEV_OK) {
-#pragma unroll 1
-      for (int k = 1; k < N; ++k) {
-        int s = me + k;
-        s = s >= N ? s - N : s;
-        int64_t off, len;
-        segment_range(s, q, r, off, len);
-        const Chunk c = chunk_of(off, len, b, G);
-        const float* __restrict__ src = s_in[s];
-        for (int64_t e = c.h0 + threadIdx.x; e < c.h1; e += blockDim.x) out[e] = __ldcg(src + e);
-        const float4* __restrict__ s4 = reinterpret_cast<const float4*>(src);
-        float4* __restrict__ d4 = reinterpret_cast<float4*>(out);
-        const int64_t step = blockDim.x;
-        int64_t v = c.v0 + threadIdx.x;
-        for (; v + 3 * step < c.v1; v += 4 * step) {
-          const float4 x0 = __ldcg(s4 + v), x1 = __ldcg(s4 + v + step), x2 = __ldcg(s4 + v + 2 * step),
-                       x3 = __ldcg(s4 + v + 3 * step);
-          d4[v] = x0;
-          d4[v + step] = x1;
-          d4[v + 2 * step] = x2;
-          d4[v + 3 * step] = x3;
-        }
-        for (; v < c.v1; v += step) d4[v] = __ldcg(s4 + v);
-        for (int64_t e = c.t0 + threadIdx.x; e < c.t1; e += blockDim.x) out[e] = __ldcg(src + e);
-      }
-    }
-  }
-  finish_call(a);
-}
-
-int grid_for(int64_t vectors_per_cta_work, int64_t min_per_cta, int max_ctas) {
-  int64_t g = (vectors_per_cta_work + min_per_cta - 1) / min_per_cta;
-  g = std::max<int64_t>(1, std::min<int64_t>(g, max_ctas));
-  return (int)g;
-}
-
-int launch_allreduce(const ArArgs& a, int algo, int max_ctas, cudaStream_t stream) {
-  const int64_t nv = a.n >> 2;
-  max_ctas = std::min(max_ctas, kMaxBlocks);  // one barrier flag slot per CTA
-  if (algo == MGW_ALGO_ONESHOT) {
-    const int grid = grid_for(nv, 1024, max_ctas);
-#define MGW_ONESHOT_CASE(NN) \
-  case NN:                   \
-    oneshot_kernel<NN><<<grid, kThreads, 0, stream>>>(a); \
-    break;
-    switch (a.world) {
-      MGW_ONESHOT_CASE(1)
-      MGW_ONESHOT_CASE(2)
-      MGW_ONESHOT_CASE(3)
-      MGW_ONESHOT_CASE(4)
-      MGW_ONESHOT_CASE(5)
-      MGW_ONESHOT_CASE(6)
-      MGW_ONESHOT_CASE(7)
-      MGW_ONESHOT_CASE(8)
-      default:
-        return set_error(MGW_EINVAL, "world %d outside 1..%d", a.world, kMaxRanks);
-    }
-#undef MGW_ONESHOT_CASE
-  } else {
-    const int grid = grid_for(nv / std::max(1, a.world), 1024, max_ctas);
-#define MGW_TWOSHOT_CASE(NN) \
-  case NN:                   \
-    twoshot_kernel<NN><<<grid, kThreads, 0, stream>>>(a); \
-    break;
-    switch (a.world) {
-      MGW_TWOSHOT_CASE(1)
-      MGW_TWOSHOT_CASE(2)
-      MGW_TWOSHOT_CASE(3)
-      MGW_TWOSHOT_CASE(4)
-      MGW_TWOSHOT_CASE(5)
-      MGW_TWOSHOT_CASE(6)
-      MGW_TWOSHOT_CASE(7)
-      MGW_TWOSHOT_CASE(8)
-      default:
-        return set_error(MGW_EINVAL, "world %d outside 1..%d", a.world, kMaxRanks);
-    }
-#undef MGW_TWOSHOT_CASE
-  }
-  MGW_CHECK_LAUNCH();
-  return MGW_OK;
-}
-
 }  // namespace
 
 // =================================================================== C ABI
+
+// Descriptor table handle: device rows plus a host mirror (the host copy feeds the
+// kernels' inline parameters).  Rows tile [0, extent) contiguously in order.
+struct mgw_table_t {
+  Row* dev = nullptr;
+  std::vector<Row> host;
+  int64_t extent = 0;
+};
 
 struct mgw_comm {
   int rank = 0;
@@ -660,7 +83,7 @@ struct mgw_comm {
   float* result = nullptr;
   uint64_t timeout_ns = 30ull * 1000000000ull;
   int64_t oneshot_max_bytes = 1 << 20;
-  int max_ctas = kSMs;
+  int max_ctas = 2 * kSMs;
 };
 
 struct mgw_sched {
@@ -689,8 +112,6 @@ struct mgw_sched {
 
 namespace {
 
-inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
-
 ArArgs make_args(const mgw_comm* c, int64_t n) {
   ArArgs a;
   memset(&a, 0, sizeof(a));
@@ -709,7 +130,6 @@ ArArgs make_args(const mgw_comm* c, int64_t n) {
   a.timeout_ns = c->timeout_ns;
   a.rank = c->rank;
   a.world = c->world;
-  a.flags = 0;
   return a;
 }
 
@@ -719,7 +139,9 @@ int pick_algo(const mgw_comm* c, int64_t n, int algo) {
 }
 
 int comm_allreduce(mgw_comm* c, int64_t n, int algo, cudaStream_t stream, uint64_t* stamp = nullptr) {
-  if (n < 0 || n * 4 > c->slot_bytes) return set_error(MGW_EINVAL, "bucket of %lld elements exceeds slot capacity %lld B", (long long)n, (long long)c->slot_bytes);
+  if (n < 0 || n * 4 > c->slot_bytes)
+    return set_error(MGW_EINVAL, "bucket of %lld elements exceeds slot capacity %lld B", (long long)n,
+                     (long long)c->slot_bytes);
   if (c->world == 1) {
     if (n > 0) MGW_CUDA(cudaMemcpyAsync(c->result, c->region + kCtrlBytes, n * 4, cudaMemcpyDeviceToDevice, stream));
     return MGW_OK;
@@ -730,27 +152,42 @@ int comm_allreduce(mgw_comm* c, int64_t n, int algo, cudaStream_t stream, uint64
   return launch_allreduce(a, pick_algo(c, n, algo), c->max_ctas, stream);
 }
 
-int comm_pack(mgw_comm* c, const void* table, int n_rows, int64_t n, float scale, cudaStream_t stream,
-              uint64_t* stamp = nullptr) {
-  if (n * 4 > c->slot_bytes) return set_error(MGW_EINVAL, "bucket of %lld elements exceeds slot capacity %lld B", (long long)n, (long long)c->slot_bytes);
+int comm_pack(mgw_comm* c, const Row* host_rows, const Row* dev_rows, int n_rows, int64_t n, float scale,
+              cudaStream_t stream, uint64_t* stamp = nullptr) {
+  if (n * 4 > c->slot_bytes)
+    return set_error(MGW_EINVAL, "bucket of %lld elements exceeds slot capacity %lld B", (long long)n,
+                     (long long)c->slot_bytes);
   float* slot0 = reinterpret_cast<float*>(c->region + kCtrlBytes);
   const uint32_t* calls = c->world > 1 ? c->state : nullptr;
-  return launch_rows<RowOp::kPack>(table, n_rows, slot0, n, scale, nullptr, calls, c->slot_bytes / 4, nullptr, stream,
-                                   stamp);
+  return launch_rows<RowOp::kPack>(host_rows, dev_rows, n_rows, slot0, n, scale, nullptr, calls, c->slot_bytes / 4,
+                                   nullptr, stream, stamp);
+}
+
+const mgw_table_t* as_table(const void* t) { return static_cast<const mgw_table_t*>(t); }
+
+int check_table(const void* t, int n, int64_t elems) {
+  if (!t) return set_error(MGW_EINVAL, "table is null");
+  const mgw_table_t* tb = as_table(t);
+  if (n != (int)tb->host.size()) return set_error(MGW_EINVAL, "table has %d rows, %d given", (int)tb->host.size(), n);
+  if (elems >= 0 && elems != tb->extent)
+    return set_error(MGW_EINVAL, "bucket of %lld elements does not match the table extent %lld", (long long)elems,
+                     (long long)tb->extent);
+  return MGW_OK;
 }
 
 }  // namespace
 
 extern "C" {
 
-const char* mgw_version(void) { return "mgwfbp_b200 0.1.0 (sm_100a)"; }
+const char* mgw_version(void) { return "mgwfbp_b200 0.2.0 (sm_100a)"; }
 
 int mgw_last_error(char* buf, size_t len) {
+  const std::string& msg = last_error_slot();
   if (buf && len) {
-    strncpy(buf, g_last_error.c_str(), len - 1);
+    strncpy(buf, msg.c_str(), len - 1);
     buf[len - 1] = '\0';
   }
-  return (int)g_last_error.size();
+  return (int)msg.size();
 }
 
 int mgw_device_count(int* out) {
@@ -772,73 +209,85 @@ int mgw_spin_ns(int64_t ns, void* stream) {
   return MGW_OK;
 }
 
-int mgw_desc_upload(const mgw_tensor_desc* rows, int n, void** dev_table) {
-  if (!dev_table || n < 0 || (n > 0 && !rows)) return set_error(MGW_EINVAL, "bad descriptor table arguments");
+int mgw_desc_upload(const mgw_tensor_desc* rows, int n, void** table) {
+  if (!table || n < 1 || !rows) return set_error(MGW_EINVAL, "bad descriptor table arguments");
+  int64_t expect = 0;
   for (int i = 0; i < n; ++i) {
-    if (rows[i].count < 0 || rows[i].offset < 0) return set_error(MGW_EINVAL, "row %d: negative count/offset", i);
-    if (i > 0 && rows[i].offset < rows[i - 1].offset + rows[i - 1].count)
-      return set_error(MGW_EINVAL, "row %d: rows must be sorted by offset and non-overlapping", i);
+    if (rows[i].count < 0 || !rows[i].ptr) return set_error(MGW_EINVAL, "row %d: negative count or null pointer", i);
+    if (rows[i].offset != expect)
+      return set_error(MGW_EINVAL, "row %d: rows must tile the bucket contiguously (offset %lld, expected %lld)", i,
+                       (long long)rows[i].offset, (long long)expect);
+    expect += rows[i].count;
   }
-  void* p = nullptr;
-  MGW_CUDA(cudaMalloc(&p, std::max<size_t>(1, sizeof(Row) * (size_t)n)));
-  if (n) MGW_CUDA(cudaMemcpy(p, rows, sizeof(Row) * (size_t)n, cudaMemcpyHostToDevice));
-  *dev_table = p;
+  mgw_table_t* t = new mgw_table_t();
+  t->host.assign(reinterpret_cast<const Row*>(rows), reinterpret_cast<const Row*>(rows) + n);
+  t->extent = expect;
+  cudaError_t e = cudaMalloc(&t->dev, sizeof(Row) * (size_t)n);
+  if (e == cudaSuccess) e = cudaMemcpy(t->dev, rows, sizeof(Row) * (size_t)n, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    if (t->dev) cudaFree(t->dev);
+    delete t;
+    return set_error(MGW_ECUDA, "descriptor upload: %s", cudaGetErrorString(e));
+  }
+  *table = t;
   return MGW_OK;
 }
 
-int mgw_desc_free(void* dev_table) {
-  if (dev_table) MGW_CUDA(cudaFree(dev_table));
+int mgw_desc_free(void* table) {
+  if (table) {
+    mgw_table_t* t = static_cast<mgw_table_t*>(table);
+    if (t->dev) cudaFree(t->dev);
+    delete t;
+  }
   return MGW_OK;
 }
 
-int mgw_pack(const void* dev_table, int n, float* bucket, int64_t bucket_elems, float scale, void* stream) {
-  if (!dev_table || !bucket || bucket_elems < 0) return set_error(MGW_EINVAL, "bad pack arguments");
-  return launch_rows<RowOp::kPack>(dev_table, n, bucket, bucket_elems, scale, nullptr, nullptr, 0, nullptr,
+int mgw_pack(const void* table, int n, float* bucket, int64_t bucket_elems, float scale, void* stream) {
+  if (!bucket) return set_error(MGW_EINVAL, "bucket is null");
+  int rc = check_table(table, n, bucket_elems);
+  if (rc) return rc;
+  const mgw_table_t* t = as_table(table);
+  return launch_rows<RowOp::kPack>(t->host.data(), t->dev, n, bucket, bucket_elems, scale, nullptr, nullptr, 0, nullptr,
                                    static_cast<cudaStream_t>(stream));
 }
 
-int mgw_unpack(const void* dev_table, int n, const float* bucket, int64_t bucket_elems, void* stream) {
-  if (!dev_table || !bucket || bucket_elems < 0) return set_error(MGW_EINVAL, "bad unpack arguments");
-  return launch_rows<RowOp::kUnpack>(dev_table, n, const_cast<float*>(bucket), bucket_elems, 1.f, nullptr, nullptr,
-                                     0, nullptr, static_cast<cudaStream_t>(stream));
-}
-
-static int table_extent(const void* dev_table, int n, cudaStream_t stream, int64_t* out) {
-  // extent of a device table = last row's offset + count (read back once)
-  if (n <= 0) {
-    *out = 0;
-    return MGW_OK;
-  }
-  Row last;
-  MGW_CUDA(cudaMemcpyAsync(&last, static_cast<const Row*>(dev_table) + (n - 1), sizeof(Row), cudaMemcpyDeviceToHost, stream));
-  MGW_CUDA(cudaStreamSynchronize(stream));
-  *out = last.offset + last.count;
-  return MGW_OK;
-}
-
-int mgw_fill_const(const void* dev_table, int n, const float* values_dev, void* stream) {
-  if (!dev_table || !values_dev) return set_error(MGW_EINVAL, "bad fill arguments");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  int64_t total = 0;
-  int rc = table_extent(dev_table, n, s, &total);
+int mgw_unpack(const void* table, int n, const float* bucket, int64_t bucket_elems, void* stream) {
+  if (!bucket) return set_error(MGW_EINVAL, "bucket is null");
+  int rc = check_table(table, n, bucket_elems);
   if (rc) return rc;
-  return launch_rows<RowOp::kFill>(dev_table, n, nullptr, total, 1.f, values_dev, nullptr, 0, nullptr, s);
+  const mgw_table_t* t = as_table(table);
+  return launch_rows<RowOp::kUnpack>(t->host.data(), t->dev, n, const_cast<float*>(bucket), bucket_elems, 1.f, nullptr,
+                                     nullptr, 0, nullptr, static_cast<cudaStream_t>(stream));
 }
 
-int mgw_check_const(const void* dev_table, int n, const float* values_dev, int64_t* mismatches, void* stream) {
-  if (!dev_table || !values_dev || !mismatches) return set_error(MGW_EINVAL, "bad check arguments");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  int64_t total = 0;
-  int rc = table_extent(dev_table, n, s, &total);
+int mgw_fill_const(const void* table, int n, const float* values_dev, void* stream) {
+  if (!values_dev) return set_error(MGW_EINVAL, "values are null");
+  int rc = check_table(table, n, -1);
   if (rc) return rc;
+  const mgw_table_t* t = as_table(table);
+  return launch_rows<RowOp::kFill>(t->host.data(), t->dev, n, nullptr, t->extent, 1.f, values_dev, nullptr, 0, nullptr,
+                                   static_cast<cudaStream_t>(stream));
+}
+
+int mgw_check_const(const void* table, int n, const float* values_dev, int64_t* mismatches, void* stream) {
+  if (!values_dev || !mismatches) return set_error(MGW_EINVAL, "bad check arguments");
+  int rc = check_table(table, n, -1);
+  if (rc) return rc;
+  const mgw_table_t* t = as_table(table);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
   unsigned long long* d_bad = nullptr;
   MGW_CUDA(cudaMalloc(&d_bad, sizeof(unsigned long long)));
-  MGW_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(unsigned long long), s));
-  rc = launch_rows<RowOp::kCheck>(dev_table, n, nullptr, total, 1.f, values_dev, nullptr, 0, d_bad, s);
+  cudaError_t e = cudaMemsetAsync(d_bad, 0, sizeof(unsigned long long), s);
+  if (e != cudaSuccess) {
+    cudaFree(d_bad);
+    return set_error(MGW_ECUDA, "check: %s", cudaGetErrorString(e));
+  }
+  rc = launch_rows<RowOp::kCheck>(t->host.data(), t->dev, n, nullptr, t->extent, 1.f, values_dev, nullptr, 0, d_bad, s);
   unsigned long long bad = 0;
   if (rc == MGW_OK) {
-    MGW_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost, s));
-    MGW_CUDA(cudaStreamSynchronize(s));
+    e = cudaMemcpyAsync(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) rc = set_error(MGW_ECUDA, "check: %s", cudaGetErrorString(e));
   }
   cudaFree(d_bad);
   *mismatches = (int64_t)bad;
@@ -927,6 +376,12 @@ int mgw_comm_set_oneshot_max(mgw_comm* c, int64_t bytes) {
   return MGW_OK;
 }
 
+int mgw_comm_set_max_ctas(mgw_comm* c, int ctas) {
+  if (!c || ctas < 1 || ctas > kMaxBlocks) return set_error(MGW_EINVAL, "CTA cap must lie in 1..%d", kMaxBlocks);
+  c->max_ctas = ctas;
+  return MGW_OK;
+}
+
 int mgw_comm_input(mgw_comm* c, float** slot) {
   if (!c || !slot) return set_error(MGW_EINVAL, "bad arguments");
   uint32_t calls = 0;
@@ -946,9 +401,12 @@ int mgw_comm_result(mgw_comm* c, float** result) {
   return MGW_OK;
 }
 
-int mgw_comm_pack(mgw_comm* c, const void* dev_table, int n, int64_t n_elem, float scale, void* stream) {
-  if (!c || !dev_table) return set_error(MGW_EINVAL, "bad arguments");
-  return comm_pack(c, dev_table, n, n_elem, scale, static_cast<cudaStream_t>(stream));
+int mgw_comm_pack(mgw_comm* c, const void* table, int n, int64_t n_elem, float scale, void* stream) {
+  if (!c) return set_error(MGW_EINVAL, "comm is null");
+  int rc = check_table(table, n, n_elem);
+  if (rc) return rc;
+  const mgw_table_t* t = as_table(table);
+  return comm_pack(c, t->host.data(), t->dev, n, n_elem, scale, static_cast<cudaStream_t>(stream));
 }
 
 int mgw_allreduce(mgw_comm* c, int64_t n_elem, int algo, void* stream) {
@@ -976,18 +434,19 @@ int mgw_comm_calls(mgw_comm* c, int64_t* calls) {
 }
 
 int mgw_allreduce_emulated(float* const* ins, float* const* outs, int world, int64_t n, int algo, void* stream) {
-  if (!ins || !outs || world < 1 || world > kMaxRanks || n < 0) return set_error(MGW_EINVAL, "bad emulated all-reduce arguments");
-  if (algo != MGW_ALGO_ONESHOT && algo != MGW_ALGO_TWOSHOT) return set_error(MGW_EINVAL, "emulated all-reduce needs an explicit algorithm");
+  if (!ins || !outs || world < 1 || world > kMaxRanks || n < 0)
+    return set_error(MGW_EINVAL, "bad emulated all-reduce arguments");
+  if (algo != MGW_ALGO_ONESHOT && algo != MGW_ALGO_TWOSHOT)
+    return set_error(MGW_EINVAL, "emulated all-reduce needs an explicit algorithm");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   ArArgs a;
   memset(&a, 0, sizeof(a));
   for (int r = 0; r < world; ++r) {
     a.slot[r] = reinterpret_cast<char*>(ins[r]);
     a.out[r] = outs[r];
-    if (algo == MGW_ALGO_ONESHOT) {
+    if (algo == MGW_ALGO_ONESHOT)
       for (int q = 0; q < world; ++q)
         if (outs[r] == ins[q]) return set_error(MGW_EINVAL, "one-shot output may not alias an input");
-    }
   }
   a.n = n;
   a.world = world;
@@ -1018,26 +477,32 @@ int mgw_allreduce_emulated(float* const* ins, float* const* outs, int world, int
 // unpack into `local_bucket`), 1 = all-reduce kernel only, 2 = pack only, 3 = unpack only.
 int mgw_time_exchange(mgw_comm* c, const void* table, int n_rows, int64_t n_elem, float* local_bucket, int algo,
                       int kind, int reps, int warmups, double* seconds_per_rep, void* stream) {
-  if (!table || reps < 1 || warmups < 0 || !seconds_per_rep || n_elem <= 0 || kind < 0 || kind > 3)
+  if (reps < 1 || warmups < 0 || !seconds_per_rep || n_elem <= 0 || kind < 0 || kind > 3)
     return set_error(MGW_EINVAL, "bad timing arguments");
+  int rc = check_table(table, n_rows, n_elem);
+  if (rc) return rc;
+  const mgw_table_t* t = as_table(table);
   const bool multi = c && c->world > 1;
   if (!multi && !local_bucket) return set_error(MGW_EINVAL, "single-rank timing needs a local bucket");
   if (kind == 1 && !multi) return set_error(MGW_EINVAL, "all-reduce timing needs a multi-rank communicator");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   auto step = [&]() -> int {
-    int rc = MGW_OK;
+    int r = MGW_OK;
     if (multi) {
-      if (kind == 0 || kind == 2) rc = comm_pack(c, table, n_rows, n_elem, 1.f, s);
-      if (rc == MGW_OK && (kind == 0 || kind == 1)) rc = comm_allreduce(c, n_elem, algo, s);
-      if (rc == MGW_OK && (kind == 0 || kind == 3))
-        rc = launch_rows<RowOp::kUnpack>(table, n_rows, c->result, n_elem, 1.f, nullptr, nullptr, 0, nullptr, s);
+      if (kind == 0 || kind == 2) r = comm_pack(c, t->host.data(), t->dev, n_rows, n_elem, 1.f, s);
+      if (r == MGW_OK && (kind == 0 || kind == 1)) r = comm_allreduce(c, n_elem, algo, s);
+      if (r == MGW_OK && (kind == 0 || kind == 3))
+        r = launch_rows<RowOp::kUnpack>(t->host.data(), t->dev, n_rows, c->result, n_elem, 1.f, nullptr, nullptr, 0,
+                                        nullptr, s);
     } else {
       if (kind == 0 || kind == 2)
-        rc = launch_rows<RowOp::kPack>(table, n_rows, local_bucket, n_elem, 1.f, nullptr, nullptr, 0, nullptr, s);
-      if (rc == MGW_OK && (kind == 0 || kind == 3))
-        rc = launch_rows<RowOp::kUnpack>(table, n_rows, local_bucket, n_elem, 1.f, nullptr, nullptr, 0, nullptr, s);
+        r = launch_rows<RowOp::kPack>(t->host.data(), t->dev, n_rows, local_bucket, n_elem, 1.f, nullptr, nullptr, 0,
+                                      nullptr, s);
+      if (r == MGW_OK && (kind == 0 || kind == 3))
+        r = launch_rows<RowOp::kUnpack>(t->host.data(), t->dev, n_rows, local_bucket, n_elem, 1.f, nullptr, nullptr, 0,
+                                        nullptr, s);
     }
-    return rc;
+    return r;
   };
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   MGW_CUDA(cudaEventCreate(&ev0));
@@ -1046,7 +511,6 @@ int mgw_time_exchange(mgw_comm* c, const void* table, int n_rows, int64_t n_elem
     cudaEventDestroy(ev0);
     return set_error(MGW_ECUDA, "cudaEventCreate: %s", cudaGetErrorString(e));
   }
-  int rc = MGW_OK;
   for (int r = 0; r < warmups && rc == MGW_OK; ++r) rc = step();
   // hold the stream while the host enqueues the timed reps
   if (rc == MGW_OK) spin_relative_kernel<<<1, 32, 0, s>>>(1000000 + 20000LL * reps);
@@ -1190,8 +654,8 @@ static int sched_enqueue(mgw_sched* s, cudaStream_t cs, cudaStream_t ms) {
           MGW_CUDA(cudaMemcpyAsync(s->rows[k].ptr, s->host_src[k], s->rows[k].count * 4, cudaMemcpyHostToDevice, cs));
     }
     if ((s->flags & MGW_SCHED_FILL) && gr.n_elem > 0) {
-      int rc = launch_rows<RowOp::kFill>(d_rows + gr.desc_begin, gr.desc_count, nullptr, gr.n_elem, 1.f,
-                                         s->d_fill + gr.desc_begin, nullptr, 0, nullptr, cs);
+      int rc = launch_rows<RowOp::kFill>(s->rows.data() + gr.desc_begin, d_rows + gr.desc_begin, gr.desc_count, nullptr,
+                                         gr.n_elem, 1.f, s->d_fill + gr.desc_begin, nullptr, 0, nullptr, cs);
       if (rc) return rc;
     }
     spin_until_kernel<<<1, 32, 0, cs>>>(s->d_clock, gr.ready_ns);
@@ -1205,23 +669,24 @@ static int sched_enqueue(mgw_sched* s, cudaStream_t cs, cudaStream_t ms) {
   for (int g = 0; g < n_groups; ++g) {
     const mgw_group& gr = s->groups[g];
     const Row* grows = d_rows + gr.desc_begin;
+    const Row* hrows = s->rows.data() + gr.desc_begin;
     uint64_t* st = s->d_stamps + 6 * (size_t)g;
     MGW_CUDA(cudaStreamWaitEvent(ms, s->dep_ready[g], 0));
     if (gr.n_elem == 0) continue;  // silent group: nothing to send (allreduce_net.py:549)
     int rc;
     if (s->world == 1) {
-      rc = launch_rows<RowOp::kPack>(grows, gr.desc_count, s->local_bucket, gr.n_elem, s->scale, nullptr, nullptr, 0,
-                                     nullptr, ms, st);
+      rc = launch_rows<RowOp::kPack>(hrows, grows, gr.desc_count, s->local_bucket, gr.n_elem, s->scale, nullptr, nullptr,
+                                     0, nullptr, ms, st);
       if (rc) return rc;
-      rc = launch_rows<RowOp::kUnpack>(grows, gr.desc_count, s->local_bucket, gr.n_elem, 1.f, nullptr, nullptr, 0,
+      rc = launch_rows<RowOp::kUnpack>(hrows, grows, gr.desc_count, s->local_bucket, gr.n_elem, 1.f, nullptr, nullptr, 0,
                                        nullptr, ms, st + 4);
       if (rc) return rc;
     } else {
-      rc = comm_pack(s->comm, grows, gr.desc_count, gr.n_elem, s->scale, ms, st);
+      rc = comm_pack(s->comm, hrows, grows, gr.desc_count, gr.n_elem, s->scale, ms, st);
       if (rc) return rc;
       rc = comm_allreduce(s->comm, gr.n_elem, gr.algo, ms, st + 2);
       if (rc) return rc;
-      rc = launch_rows<RowOp::kUnpack>(grows, gr.desc_count, s->comm->result, gr.n_elem, 1.f, nullptr, nullptr, 0,
+      rc = launch_rows<RowOp::kUnpack>(hrows, grows, gr.desc_count, s->comm->result, gr.n_elem, 1.f, nullptr, nullptr, 0,
                                        nullptr, ms, st + 4);
       if (rc) return rc;
     }
