@@ -82,15 +82,18 @@ __global__ void __launch_bounds__(kThreads) rows_kernel(const __grid_constant__ 
       float* tp[kRowsUnroll];
       float value[kRowsUnroll];
       bool fast[kRowsUnroll];
+      int ku[kRowsUnroll];
 #pragma unroll
       for (int u = 0; u < kRowsUnroll; ++u) {
         const int64_t e = base + (int64_t)u * 4 * kThreads;
         fast[u] = false;
         tp[u] = nullptr;
         value[u] = 0.f;
+        ku[u] = k;
         if (e < t1) {
           Row r = row_at(p, k);
           while (e >= r.offset + r.count) r = row_at(p, ++k);
+          ku[u] = k;
           tp[u] = r.ptr + (e - r.offset);
           if constexpr (kOp == RowOp::kFill || kOp == RowOp::kCheck) value[u] = p.values[k];
           fast[u] = e + 4 <= t1 && e + 4 <= r.offset + r.count && (reinterpret_cast<uintptr_t>(tp[u]) & 15) == 0;
@@ -128,7 +131,7 @@ __global__ void __launch_bounds__(kThreads) rows_kernel(const __grid_constant__ 
       for (int u = 0; u < kRowsUnroll; ++u) {
         const int64_t e = base + (int64_t)u * 4 * kThreads;
         if (fast[u] || e >= t1) continue;
-        int kk = k;
+        int kk = ku[u];
         for (int j = 0; j < 4 && e + j < t1; ++j) {
           Row r = row_at(p, kk);
           while (e + j >= r.offset + r.count) r = row_at(p, ++kk);  // rows tile the bucket in order
