@@ -257,7 +257,7 @@ def run_ours(args) -> dict | None:
         comm = session.comm
 
     # 1. fit the startup/bandwidth model of one group exchange on this box
-    exch = _exchange_times(comm, world, device, FIT_SIZES)
+    exch = _exchange_times(comm, world, device, FIT_SIZES, kind=4 if (world > 1 and not args.unfused) else 0)
     if session is not None:
         session.raise_if_failed()
     model, fit_ok = _fit(FIT_SIZES, exch, world)
@@ -277,7 +277,7 @@ def run_ours(args) -> dict | None:
     headline = None
     for name in ("wfbp", "synceasgd", "mgwfbp"):
         it = OverlappedIteration(profile, plans[name], comm=comm, rank=rank, world=world, device=device,
-                                 fill=True, graph=not args.no_graph)
+                                 fill=True, graph=not args.no_graph, fused=not args.unfused)
         sampler = ClockSampler(local) if (rank == 0 and name == "mgwfbp") else None
         if sampler:
             sampler.__enter__()
@@ -350,7 +350,9 @@ def run_ours(args) -> dict | None:
     else:
         per_step = int(2 * (world - 1) / world * total_bytes)  # nccl-tests bus bytes
         achieved = per_step * steps / spans["allreduce"] / 1e9
-        roofline = {"bound": "nvlink", "kernel": "K2/K3 all-reduce", "achieved": round(achieved, 1),
+        roofline = {"bound": "nvlink",
+                    "kernel": "fused K1+K2/K3+K4" if (not args.unfused) else "K2/K3 all-reduce",
+                    "achieved": round(achieved, 1),
                     "peak": NVLINK_PEAK_GBS, "unit": "GB/s", "frac": round(achieved / NVLINK_PEAK_GBS, 4),
                     "peak_source": "measured peer copy per direction, B200_PROFILING.md (900 nominal)"}
     roofline.update({
@@ -366,8 +368,8 @@ def run_ours(args) -> dict | None:
     if traffic_file.exists():
         roofline["traffic"] = json.loads(traffic_file.read_text()).get(f"{roofline['kernel']}@N{world}")
     # the same kernel on the whole-model bucket, back to back under one event pair
-    big = _exchange_times(comm, world, device, [4 * profile.total_params],
-                          kind={"pack": 2, "allreduce": 1, "unpack": 3}[dominant] if world > 1 else 2)[0]
+    big_kind = {"pack": 2, "allreduce": 1 if args.unfused else 4, "unpack": 3}[dominant] if world > 1 else 2
+    big = _exchange_times(comm, world, device, [4 * profile.total_params], kind=big_kind)[0]
     if dominant in ("pack", "unpack") or world == 1:
         big_bw = 2 * 4 * profile.total_params / big / 1e9
     else:
@@ -380,7 +382,7 @@ def run_ours(args) -> dict | None:
     # e2e: the same MG-WFBP iteration with host buffers (H2D of every layer's gradient,
     # D2H of every reduced gradient) inside the timed region
     e2e_it = OverlappedIteration(profile, plans["mgwfbp"], comm=comm, rank=rank, world=world, device=device,
-                                 host_io=True, graph=not args.no_graph)
+                                 host_io=True, graph=not args.no_graph, fused=not args.unfused)
     try:
         for _ in range(args.warmup):
             e2e_it.run()
@@ -436,6 +438,7 @@ def run_ours(args) -> dict | None:
             "parallelism": f"dp{world}",
             "l2": "flushed between iterations (256 MiB write on the compute stream, outside the timed events)",
             "cuda_graph": not args.no_graph,
+            "fused_group_kernel": world > 1 and not args.unfused,
         },
         "strategies": results,
         "roofline": roofline,
@@ -540,6 +543,7 @@ def main(argv=None) -> int:
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-graph", action="store_true", help="eager stream schedule instead of CUDA-graph replay")
+    ap.add_argument("--unfused", action="store_true", help="separate pack / all-reduce / unpack kernels per group")
     ap.add_argument("--no-sweep", action="store_true", help="skip the all-reduce bus-bandwidth sweep (N > 1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)

@@ -63,6 +63,7 @@ extern "C" {
 #define MGW_SCHED_FILL 1u  /* "backward" writes fill_values into each layer before its deadline */
 #define MGW_SCHED_GRAPH 2u /* capture the iteration once into a CUDA graph and replay it */
 #define MGW_SCHED_HOSTIO 4u /* e2e: H2D of each layer from host_src, D2H of the result to host_dst */
+#define MGW_SCHED_FUSED 8u  /* one kernel per group: pack + all-reduce + unpack (N > 1) */
 
 typedef struct mgw_comm mgw_comm;
 typedef struct mgw_sched mgw_sched;
@@ -117,18 +118,24 @@ int mgw_comm_input(mgw_comm* comm, float** slot); /* slot the next collective re
 int mgw_comm_result(mgw_comm* comm, float** result);
 int mgw_comm_pack(mgw_comm* comm, const void* dev_table, int n, int64_t n_elem, float scale, void* stream);
 int mgw_allreduce(mgw_comm* comm, int64_t n_elem, int algo, void* stream);
+/* pack -> all-reduce -> unpack of one group in one kernel, in place on the layer tensors */
+int mgw_allreduce_fused(mgw_comm* comm, const void* table, int n_rows, int64_t n_elem, float scale, int algo,
+                        void* stream);
 int mgw_comm_error(mgw_comm* comm, int* code);
 int mgw_comm_calls(mgw_comm* comm, int64_t* calls);
 
 /* Device seconds per step of `reps` back-to-back exchange steps under one event pair
  * (the (a, b) fit's input and the bus-bandwidth sweep).  kind: 0 pack+all-reduce+unpack,
- * 1 all-reduce only, 2 pack only, 3 unpack only.  comm NULL: single rank, local_bucket. */
+ * 1 all-reduce only, 2 pack only, 3 unpack only, 4 fused kernel.  comm NULL: single rank. */
 int mgw_time_exchange(mgw_comm* comm, const void* dev_table, int n_rows, int64_t n_elem, float* local_bucket,
                       int algo, int kind, int reps, int warmups, double* seconds_per_rep, void* stream);
 
 /* ---- emulated ranks on one device (test path; no barriers) ------------ */
 int mgw_allreduce_emulated(float* const* ins, float* const* outs, int world, int64_t n_elem, int algo,
                            void* stream);
+
+int mgw_allreduce_fused_emulated(void* const* tables, float* const* slots, int world, int64_t n_elem, float scale,
+                                 int algo, void* stream);
 
 /* ---- Algorithm 2 on streams ------------------------------------------- */
 int mgw_sched_create(mgw_comm* comm /* NULL: single rank */, const mgw_tensor_desc* rows, int n_rows,

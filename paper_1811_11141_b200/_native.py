@@ -19,7 +19,7 @@ LIB_PATH = LIB_DIR / "libmgwfbp_b200.so"
 
 MGW_OK, MGW_EINVAL, MGW_EPROTO, MGW_ECUDA = 0, 1, 2, 3
 ALGO_AUTO, ALGO_ONESHOT, ALGO_TWOSHOT = 0, 1, 2
-SCHED_FILL, SCHED_GRAPH, SCHED_HOSTIO = 1, 2, 4
+SCHED_FILL, SCHED_GRAPH, SCHED_HOSTIO, SCHED_FUSED = 1, 2, 4, 8
 DEV_OK, DEV_LENGTH_MISMATCH, DEV_TIMEOUT, DEV_PEER_ABORT = 0, 1, 2, 3
 IPC_HANDLE_BYTES = 64
 MAX_RANKS = 8
@@ -69,6 +69,8 @@ _SIGNATURES = {
     "mgw_comm_result": ([_P, ctypes.POINTER(_P)], _I),
     "mgw_comm_pack": ([_P, _P, _I, _I64, ctypes.c_float, _P], _I),
     "mgw_allreduce": ([_P, _I64, _I, _P], _I),
+    "mgw_allreduce_fused": ([_P, _P, _I, _I64, ctypes.c_float, _I, _P], _I),
+    "mgw_allreduce_fused_emulated": ([ctypes.POINTER(_P), ctypes.POINTER(_P), _I, _I64, ctypes.c_float, _I, _P], _I),
     "mgw_comm_error": ([_P, ctypes.POINTER(_I)], _I),
     "mgw_comm_calls": ([_P, ctypes.POINTER(_I64)], _I),
     "mgw_time_exchange": ([_P, _P, _I, _I64, _P, _I, _I, _I, _I, ctypes.POINTER(ctypes.c_double), _P], _I),

@@ -461,11 +461,11 @@ def ring_allreduce(
         algo = _algo_for(session, n)
         handle = stream.cuda_stream
         if n:
+            # one kernel: pack -> all-reduce -> unpack, in place on the payload
             table = session.table(ptr, n)
-            _native.call("mgw_comm_pack", session.comm, table.ptr, 1, n, ctypes.c_float(1.0), handle)
-        _native.call("mgw_allreduce", session.comm, n, algo, handle)
-        if n:
-            _native.call("mgw_unpack", table.ptr, 1, session.result_ptr(), n, handle)
+            _native.call("mgw_allreduce_fused", session.comm, table.ptr, 1, n, ctypes.c_float(1.0), algo, handle)
+        else:
+            _native.call("mgw_allreduce", session.comm, 0, algo, handle)  # still collective
         stream.synchronize()
         session.raise_if_failed()
         if numpy_payload and n:
@@ -542,6 +542,7 @@ def run_emulation(
     *,
     warmup: int = 2,
     graph: bool = False,
+    fused: bool = True,
 ) -> EmulationReport:
     """Measure the overlapped iteration (Algorithm 2) on the GPUs.
 
@@ -579,6 +580,7 @@ def run_emulation(
             device=session.device,
             fill=True,
             graph=graph,
+            fused=fused,
         )
         try:
             walls, computes, exposed = [], [], []

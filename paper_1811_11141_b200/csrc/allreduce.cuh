@@ -21,7 +21,7 @@
 
 namespace mgw {
 
-enum : int { kNoBarrier = 1, kSkipPhase1 = 2, kSkipPhase2 = 4 };
+enum : int { kNoBarrier = 1, kSkipPhase1 = 2, kSkipPhase2 = 4, kSkipPack = 8 };
 
 struct ArArgs {
   char* slot[kMaxRanks];       // slot-0 base of every rank (peer mapped; own at [rank])

@@ -1,0 +1,304 @@
+// fused.cuh -- one kernel per merge group: K1 pack -> K2/K3 all-reduce -> K4 unpack.
+//
+// The separate kernels cost three launches per group and a round trip of the whole
+// bucket through the result buffer.  Here every CTA packs exactly the bucket chunk its
+// peers' matching CTA will read (so the per-CTA barrier still suffices), folds the
+// chunk from all ranks in the reference order, and writes the reduced values straight
+// back into the layer tensors.  Same bits as pack + all-reduce + unpack.
+//
+//   one-shot: CTA b packs chunk b of its own slot, barrier, folds chunk b from the N
+//             slots into the tensors.
+//   two-shot: CTA b packs chunk b of every rank's part, barrier, folds chunk b of its
+//             own part into its slot (in place) and the tensors, barrier, copies chunk
+//             b of every peer's reduced part into the tensors.
+#pragma once
+
+#include "allreduce.cuh"
+#include "rows.cuh"
+
+namespace mgw {
+
+struct FusedArgs {
+  ArArgs ar;
+  Row inline_rows[kInlineRows];
+  const Row* rows;
+  int n_rows;
+  int use_inline;
+  float scale;
+};
+
+__device__ __forceinline__ Row fused_row(const FusedArgs& f, int k) {
+  return f.use_inline ? f.inline_rows[k] : f.rows[k];
+}
+
+__device__ __forceinline__ int fused_row_covering(const FusedArgs& f, int64_t e) {
+  int lo = 0, hi = f.n_rows;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    const Row r = fused_row(f, mid);
+    if (r.offset + r.count > e)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  return lo;
+}
+
+// Tensor address of bucket element e; `k` is a monotone per-thread row cursor.
+// fast4: the 16-B slot at e is inside one row at a 16-B aligned tensor address.
+__device__ __forceinline__ float* fused_tensor(const FusedArgs& f, int& k, int64_t e, bool& fast4) {
+  Row r = fused_row(f, k);
+  while (e >= r.offset + r.count) r = fused_row(f, ++k);
+  float* p = r.ptr + (e - r.offset);
+  fast4 = e + 4 <= r.offset + r.count && (reinterpret_cast<uintptr_t>(p) & 15) == 0;
+  return p;
+}
+
+__device__ __forceinline__ float* fused_tensor1(const FusedArgs& f, int k, int64_t e) {
+  Row r = fused_row(f, k);
+  while (e >= r.offset + r.count) r = fused_row(f, ++k);
+  return r.ptr + (e - r.offset);
+}
+
+// Pack bucket vectors [v0, v1) (16-B slots) plus scalar elements [t0, t1) into `slot`.
+__device__ void fused_pack_range(const FusedArgs& f, float* slot, int64_t v0, int64_t v1, int64_t t0, int64_t t1) {
+  const float scale = f.scale;
+  const bool scaled = scale != 1.0f;
+  if (v0 < v1) {
+    int k = fused_row_covering(f, (v0 + threadIdx.x) << 2 < (v1 << 2) ? (v0 + threadIdx.x) << 2 : v0 << 2);
+    for (int64_t v = v0 + threadIdx.x; v < v1; v += kThreads) {
+      const int64_t e = v << 2;
+      bool fast;
+      float* tp = fused_tensor(f, k, e, fast);
+      if (fast) {
+        float4 x = *reinterpret_cast<const float4*>(tp);
+        *reinterpret_cast<float4*>(slot + e) = scaled ? fmul4(x, scale) : x;
+      } else {
+        for (int j = 0; j < 4; ++j) {
+          const float x = *fused_tensor1(f, k, e + j);
+          slot[e + j] = scaled ? __fmul_rn(x, scale) : x;
+        }
+      }
+    }
+  }
+  for (int64_t e = t0 + threadIdx.x; e < t1; e += kThreads) {
+    const float x = *fused_tensor1(f, fused_row_covering(f, e), e);
+    slot[e] = scaled ? __fmul_rn(x, scale) : x;
+  }
+}
+
+// Fold bucket vectors [v0, v1) from the N slots (reference order); write to the
+// tensors and, when `own` is non-null, to own[] as well.
+template <int N, int U>
+__device__ void fused_reduce_range(const FusedArgs& f, const float* const* in, const int64_t* seg_end, int64_t v0,
+                                   int64_t v1, float* own) {
+  if (v0 >= v1) return;
+  int seg = advance_segment(0, (v0 + threadIdx.x) << 2 < (v1 << 2) ? (v0 + threadIdx.x) << 2 : v0 << 2, seg_end);
+  int k = fused_row_covering(f, (v0 + threadIdx.x) << 2 < (v1 << 2) ? (v0 + threadIdx.x) << 2 : v0 << 2);
+  for (int64_t base = v0 + threadIdx.x; base < v1; base += (int64_t)U * kThreads) {
+    float4 x[U][N];
+    int su[U];
+    bool ok[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t vv = base + (int64_t)u * kThreads;
+      ok[u] = false;
+      su[u] = seg;
+      if (vv < v1) {
+        const int64_t e = vv << 2;
+        seg = advance_segment(seg, e, seg_end);
+        su[u] = seg;
+        ok[u] = e + 3 < seg_end[seg];
+        if (ok[u]) {
+#pragma unroll
+          for (int kk = 0; kk < N; ++kk) {
+            const int src = seg + kk >= N ? seg + kk - N : seg + kk;
+            x[u][kk] = __ldcg(reinterpret_cast<const float4*>(in[src] + e));
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t vv = base + (int64_t)u * kThreads;
+      if (vv >= v1) continue;
+      const int64_t e = vv << 2;
+      bool fast;
+      float* tp = fused_tensor(f, k, e, fast);
+      if (ok[u]) {
+        float4 acc = x[u][0];
+#pragma unroll
+        for (int kk = 1; kk < N; ++kk) acc = fadd4(acc, x[u][kk]);
+        if (own) *reinterpret_cast<float4*>(own + e) = acc;
+        if (fast) {
+          *reinterpret_cast<float4*>(tp) = acc;
+        } else {
+          const float y[4] = {acc.x, acc.y, acc.z, acc.w};
+          for (int j = 0; j < 4; ++j) *fused_tensor1(f, k, e + j) = y[j];
+        }
+      } else {
+        int s = su[u];
+        for (int j = 0; j < 4; ++j) {
+          s = advance_segment(s, e + j, seg_end);
+          const float y = fold1<N>(in, s, e + j);
+          if (own) own[e + j] = y;
+          *fused_tensor1(f, k, e + j) = y;
+        }
+      }
+    }
+  }
+}
+
+template <int N>
+__device__ void fused_reduce_tail(const FusedArgs& f, const float* const* in, const int64_t* seg_end, int64_t e0,
+                                  int64_t e1, float* own) {
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += kThreads) {
+    const int s = advance_segment(0, e, seg_end);
+    const float y = fold1<N>(in, s, e);
+    if (own) own[e] = y;
+    *fused_tensor1(f, fused_row_covering(f, e), e) = y;
+  }
+}
+
+// copy reduced bucket vectors [v0, v1) (and scalars [t0, t1)) of `src` into the tensors
+__device__ void fused_scatter_range(const FusedArgs& f, const float* src, int64_t v0, int64_t v1, int64_t t0,
+                                    int64_t t1) {
+  constexpr int UC = 4;
+  if (v0 < v1) {
+    int k = fused_row_covering(f, (v0 + threadIdx.x) << 2 < (v1 << 2) ? (v0 + threadIdx.x) << 2 : v0 << 2);
+    for (int64_t base = v0 + threadIdx.x; base < v1; base += (int64_t)UC * kThreads) {
+      float4 x[UC];
+#pragma unroll
+      for (int u = 0; u < UC; ++u) {
+        const int64_t vv = base + (int64_t)u * kThreads;
+        if (vv < v1) x[u] = __ldcg(reinterpret_cast<const float4*>(src) + vv);
+      }
+#pragma unroll
+      for (int u = 0; u < UC; ++u) {
+        const int64_t vv = base + (int64_t)u * kThreads;
+        if (vv >= v1) continue;
+        const int64_t e = vv << 2;
+        bool fast;
+        float* tp = fused_tensor(f, k, e, fast);
+        if (fast) {
+          *reinterpret_cast<float4*>(tp) = x[u];
+        } else {
+          const float y[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+          for (int j = 0; j < 4; ++j) *fused_tensor1(f, k, e + j) = y[j];
+        }
+      }
+    }
+  }
+  for (int64_t e = t0 + threadIdx.x; e < t1; e += kThreads)
+    *fused_tensor1(f, fused_row_covering(f, e), e) = __ldcg(src + e);
+}
+
+template <int N>
+__global__ void __launch_bounds__(kThreads, 2) fused_oneshot_kernel(const __grid_constant__ FusedArgs f) {
+  constexpr int U = Unroll<N>::value;
+  const ArArgs& a = f.ar;
+  __shared__ const float* s_in[kMaxRanks];
+  __shared__ int64_t s_end[kMaxRanks];
+  uint32_t epoch;
+  int parity;
+  kernel_prologue<N>(a, epoch, parity, s_in, s_end);
+  const int64_t nv = a.n >> 2;
+  const int64_t per = (nv + gridDim.x - 1) / gridDim.x;
+  const int64_t v0 = (int64_t)blockIdx.x * per;
+  const int64_t v1 = v0 + per < nv ? v0 + per : nv;
+  const bool last = blockIdx.x == gridDim.x - 1;
+  float* mine = const_cast<float*>(s_in[a.rank]);
+  if (!(a.flags & kSkipPack)) fused_pack_range(f, mine, v0, v1, last ? nv << 2 : 0, last ? a.n : 0);
+  int status = MGW_DEV_OK;
+  if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, (uint32_t)a.n, a);
+  if (status == MGW_DEV_OK) {
+    fused_reduce_range<N, U>(f, s_in, s_end, v0, v1, nullptr);
+    if (last) fused_reduce_tail<N>(f, s_in, s_end, nv << 2, a.n, nullptr);
+  }
+  finish_call(a);
+}
+
+template <int N>
+__global__ void __launch_bounds__(kThreads, 2) fused_twoshot_kernel(const __grid_constant__ FusedArgs f) {
+  constexpr int U = Unroll<N>::value;
+  const ArArgs& a = f.ar;
+  __shared__ const float* s_in[kMaxRanks];
+  __shared__ int64_t s_end[kMaxRanks];
+  uint32_t epoch;
+  int parity;
+  kernel_prologue<N>(a, epoch, parity, s_in, s_end);
+  const int me = a.rank;
+  const int b = blockIdx.x, G = gridDim.x;
+  const int64_t nv = a.n >> 2;
+  const bool last = b == G - 1;
+  float* mine = const_cast<float*>(s_in[me]);
+  // chunk b of every part p: [c0(p), c1(p))
+  auto chunk = [&](int p, int64_t& c0, int64_t& c1) {
+    const int64_t q0 = part_begin(p, nv, N), q1 = part_begin(p + 1, nv, N);
+    const int64_t per = (q1 - q0 + G - 1) / G;
+    c0 = q0 + (int64_t)b * per;
+    c1 = c0 + per < q1 ? c0 + per : q1;
+    if (c1 < c0) c1 = c0;
+  };
+  if (!(a.flags & (kSkipPhase1 | kSkipPack))) {
+    for (int p = 0; p < N; ++p) {
+      int64_t c0, c1;
+      chunk(p, c0, c1);
+      const bool tail = last && p == N - 1;
+      fused_pack_range(f, mine, c0, c1, tail ? nv << 2 : 0, tail ? a.n : 0);
+    }
+  }
+  int status = MGW_DEV_OK;
+  if (!(a.flags & kSkipPhase1)) {
+    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, (uint32_t)a.n, a);
+    if (status == MGW_DEV_OK) {
+      int64_t c0, c1;
+      chunk(me, c0, c1);
+      fused_reduce_range<N, U>(f, s_in, s_end, c0, c1, mine);
+      if (last && me == N - 1) fused_reduce_tail<N>(f, s_in, s_end, nv << 2, a.n, mine);
+    }
+  }
+  if (status == MGW_DEV_OK && !(a.flags & kSkipPhase2)) {
+    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.mid, parity, epoch, (uint32_t)a.n, a);
+    if (status == MGW_DEV_OK) {
+      for (int kk = 1; kk < N; ++kk) {
+        const int p = me + kk >= N ? me + kk - N : me + kk;
+        int64_t c0, c1;
+        chunk(p, c0, c1);
+        const bool tail = last && p == N - 1;
+        fused_scatter_range(f, s_in[p], c0, c1, tail ? nv << 2 : 0, tail ? a.n : 0);
+      }
+    }
+  }
+  finish_call(a);
+}
+
+template <int N>
+int launch_fused_n(const FusedArgs& f, int algo, int max_ctas, cudaStream_t stream) {
+  constexpr int U = Unroll<N>::value;
+  const int64_t nv = f.ar.n >> 2;
+  if (algo == MGW_ALGO_ONESHOT) {
+    fused_oneshot_kernel<N><<<grid_for(nv, (int64_t)kThreads * U, max_ctas), kThreads, 0, stream>>>(f);
+  } else {
+    fused_twoshot_kernel<N><<<grid_for(nv / N, (int64_t)kThreads * U, max_ctas), kThreads, 0, stream>>>(f);
+  }
+  MGW_CHECK_LAUNCH();
+  return MGW_OK;
+}
+
+inline int launch_fused(const FusedArgs& f, int algo, int max_ctas, cudaStream_t stream) {
+  max_ctas = max_ctas < kMaxBlocks ? max_ctas : kMaxBlocks;
+  switch (f.ar.world) {
+    case 1: return launch_fused_n<1>(f, algo, max_ctas, stream);
+    case 2: return launch_fused_n<2>(f, algo, max_ctas, stream);
+    case 3: return launch_fused_n<3>(f, algo, max_ctas, stream);
+    case 4: return launch_fused_n<4>(f, algo, max_ctas, stream);
+    case 5: return launch_fused_n<5>(f, algo, max_ctas, stream);
+    case 6: return launch_fused_n<6>(f, algo, max_ctas, stream);
+    case 7: return launch_fused_n<7>(f, algo, max_ctas, stream);
+    case 8: return launch_fused_n<8>(f, algo, max_ctas, stream);
+    default: return set_error(MGW_EINVAL, "world %d outside 1..%d", f.ar.world, kMaxRanks);
+  }
+}
+
+}  // namespace mgw

@@ -26,6 +26,7 @@
 
 #include "allreduce.cuh"
 #include "common.cuh"
+#include "fused.cuh"
 #include "rows.cuh"
 
 using namespace mgw;
@@ -161,6 +162,27 @@ int comm_pack(mgw_comm* c, const Row* host_rows, const Row* dev_rows, int n_rows
   const uint32_t* calls = c->world > 1 ? c->state : nullptr;
   return launch_rows<RowOp::kPack>(host_rows, dev_rows, n_rows, slot0, n, scale, nullptr, calls, c->slot_bytes / 4,
                                    nullptr, stream, stamp);
+}
+
+// pack -> all-reduce -> unpack of one group in a single kernel (fused.cuh)
+int comm_allreduce_fused(mgw_comm* c, const Row* host_rows, const Row* dev_rows, int n_rows, int64_t n, float scale,
+                         int algo, cudaStream_t stream, uint64_t* stamp = nullptr) {
+  if (n < 0 || n * 4 > c->slot_bytes)
+    return set_error(MGW_EINVAL, "bucket of %lld elements exceeds slot capacity %lld B", (long long)n,
+                     (long long)c->slot_bytes);
+  if (c->world > 1 && !c->peers_open) return set_error(MGW_EINVAL, "peers not opened (call mgw_comm_open_peers)");
+  if (n == 0 || n_rows == 0) return MGW_OK;
+  FusedArgs f;
+  memset(&f, 0, sizeof(f));
+  f.ar = make_args(c, n);
+  f.ar.stamp = stamp;
+  f.use_inline = n_rows <= kInlineRows && host_rows != nullptr;
+  if (f.use_inline)
+    for (int k = 0; k < n_rows; ++k) f.inline_rows[k] = host_rows[k];
+  f.rows = dev_rows;
+  f.n_rows = n_rows;
+  f.scale = scale;
+  return launch_fused(f, pick_algo(c, n, algo), c->max_ctas, stream);
 }
 
 const mgw_table_t* as_table(const void* t) { return static_cast<const mgw_table_t*>(t); }
@@ -415,6 +437,24 @@ int mgw_allreduce(mgw_comm* c, int64_t n_elem, int algo, void* stream) {
   return comm_allreduce(c, n_elem, algo, static_cast<cudaStream_t>(stream));
 }
 
+int mgw_allreduce_fused(mgw_comm* c, const void* table, int n_rows, int64_t n_elem, float scale, int algo,
+                        void* stream) {
+  if (!c) return set_error(MGW_EINVAL, "comm is null");
+  if (algo < MGW_ALGO_AUTO || algo > MGW_ALGO_TWOSHOT) return set_error(MGW_EINVAL, "unknown algorithm %d", algo);
+  int rc = check_table(table, n_rows, n_elem);
+  if (rc) return rc;
+  const mgw_table_t* t = as_table(table);
+  if (c->world == 1) {
+    // nothing to exchange: the reduced value is the (scaled) local gradient
+    if (scale == 1.0f) return MGW_OK;
+    rc = comm_pack(c, t->host.data(), t->dev, n_rows, n_elem, scale, static_cast<cudaStream_t>(stream));
+    if (rc) return rc;
+    return launch_rows<RowOp::kUnpack>(t->host.data(), t->dev, n_rows, reinterpret_cast<float*>(c->region + kCtrlBytes),
+                                       n_elem, 1.f, nullptr, nullptr, 0, nullptr, static_cast<cudaStream_t>(stream));
+  }
+  return comm_allreduce_fused(c, t->host.data(), t->dev, n_rows, n_elem, scale, algo, static_cast<cudaStream_t>(stream));
+}
+
 int mgw_comm_error(mgw_comm* c, int* code) {
   if (!c || !code) return set_error(MGW_EINVAL, "bad arguments");
   MGW_CUDA(cudaSetDevice(c->device));
@@ -471,23 +511,71 @@ int mgw_allreduce_emulated(float* const* ins, float* const* outs, int world, int
   return MGW_OK;
 }
 
+// Emulated ranks on one device: every rank packs its own layer tensors into its
+// slot, then the fused kernel (no barriers) folds and writes back, phase by phase.
+int mgw_allreduce_fused_emulated(void* const* tables, float* const* slots, int world, int64_t n, float scale, int algo,
+                                 void* stream) {
+  if (!tables || !slots || world < 1 || world > kMaxRanks || n < 0)
+    return set_error(MGW_EINVAL, "bad emulated fused arguments");
+  if (algo != MGW_ALGO_ONESHOT && algo != MGW_ALGO_TWOSHOT)
+    return set_error(MGW_EINVAL, "emulated all-reduce needs an explicit algorithm");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (int r = 0; r < world; ++r) {
+    const mgw_table_t* t = as_table(tables[r]);
+    int rc = check_table(tables[r], t ? (int)t->host.size() : 0, n);
+    if (rc) return rc;
+  }
+  if (n == 0) return MGW_OK;
+  for (int r = 0; r < world; ++r) {
+    const mgw_table_t* t = as_table(tables[r]);
+    int rc = launch_rows<RowOp::kPack>(t->host.data(), t->dev, (int)t->host.size(), slots[r], n, scale, nullptr, nullptr,
+                                       0, nullptr, s);
+    if (rc) return rc;
+  }
+  FusedArgs f;
+  memset(&f, 0, sizeof(f));
+  for (int r = 0; r < world; ++r) f.ar.slot[r] = reinterpret_cast<char*>(slots[r]);
+  f.ar.n = n;
+  f.ar.world = world;
+  f.scale = scale;
+  const int phases = algo == MGW_ALGO_ONESHOT ? 1 : 2;
+  for (int phase = 0; phase < phases; ++phase) {
+    for (int r = 0; r < world; ++r) {
+      const mgw_table_t* t = as_table(tables[r]);
+      const int n_rows = (int)t->host.size();
+      f.use_inline = n_rows <= kInlineRows;
+      if (f.use_inline)
+        for (int k = 0; k < n_rows; ++k) f.inline_rows[k] = t->host[k];
+      f.rows = t->dev;
+      f.n_rows = n_rows;
+      f.ar.rank = r;
+      f.ar.flags = kNoBarrier | kSkipPack | (phases == 1 ? 0 : (phase == 0 ? kSkipPhase2 : kSkipPhase1));
+      int rc = launch_fused(f, algo, 2 * kSMs, s);
+      if (rc) return rc;
+    }
+  }
+  return MGW_OK;
+}
+
 // Device time of back-to-back group-exchange steps, timed as one event pair around
 // `reps` repetitions (after `warmups` untimed ones) so no per-launch event cost
 // enters the figure.  kind: 0 = pack -> all-reduce -> unpack (single rank: pack ->
 // unpack into `local_bucket`), 1 = all-reduce kernel only, 2 = pack only, 3 = unpack only.
 int mgw_time_exchange(mgw_comm* c, const void* table, int n_rows, int64_t n_elem, float* local_bucket, int algo,
                       int kind, int reps, int warmups, double* seconds_per_rep, void* stream) {
-  if (reps < 1 || warmups < 0 || !seconds_per_rep || n_elem <= 0 || kind < 0 || kind > 3)
+  if (reps < 1 || warmups < 0 || !seconds_per_rep || n_elem <= 0 || kind < 0 || kind > 4)
     return set_error(MGW_EINVAL, "bad timing arguments");
   int rc = check_table(table, n_rows, n_elem);
   if (rc) return rc;
   const mgw_table_t* t = as_table(table);
   const bool multi = c && c->world > 1;
   if (!multi && !local_bucket) return set_error(MGW_EINVAL, "single-rank timing needs a local bucket");
-  if (kind == 1 && !multi) return set_error(MGW_EINVAL, "all-reduce timing needs a multi-rank communicator");
+  if ((kind == 1 || kind == 4) && !multi)
+    return set_error(MGW_EINVAL, "all-reduce timing needs a multi-rank communicator");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   auto step = [&]() -> int {
     int r = MGW_OK;
+    if (kind == 4) return comm_allreduce_fused(c, t->host.data(), t->dev, n_rows, n_elem, 1.f, algo, s);
     if (multi) {
       if (kind == 0 || kind == 2) r = comm_pack(c, t->host.data(), t->dev, n_rows, n_elem, 1.f, s);
       if (r == MGW_OK && (kind == 0 || kind == 1)) r = comm_allreduce(c, n_elem, algo, s);
@@ -618,8 +706,10 @@ int mgw_sched_create(mgw_comm* comm, const mgw_tensor_desc* rows, int n_rows, co
     launches += 1;  // spin
     if (groups[g].n_elem == 0) continue;
     launches += (flags & MGW_SCHED_FILL) ? 1 : 0;  // gradient production
-    launches += 2;                                 // pack + unpack
-    launches += world > 1 ? 1 : 0;                 // all-reduce
+    if (world > 1 && (flags & MGW_SCHED_FUSED))
+      launches += 1;                               // fused pack + all-reduce + unpack
+    else
+      launches += world > 1 ? 3 : 2;               // pack (+ all-reduce) + unpack
   }
   s->launches = launches;
   *out = s;
@@ -680,6 +770,9 @@ static int sched_enqueue(mgw_sched* s, cudaStream_t cs, cudaStream_t ms) {
       if (rc) return rc;
       rc = launch_rows<RowOp::kUnpack>(hrows, grows, gr.desc_count, s->local_bucket, gr.n_elem, 1.f, nullptr, nullptr, 0,
                                        nullptr, ms, st + 4);
+      if (rc) return rc;
+    } else if (s->flags & MGW_SCHED_FUSED) {
+      rc = comm_allreduce_fused(s->comm, hrows, grows, gr.desc_count, gr.n_elem, s->scale, gr.algo, ms, st + 2);
       if (rc) return rc;
     } else {
       rc = comm_pack(s->comm, hrows, grows, gr.desc_count, gr.n_elem, s->scale, ms, st);

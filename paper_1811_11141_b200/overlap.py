@@ -94,6 +94,7 @@ class OverlappedIteration:
         host_io: bool = False,
         algo: int = _native.ALGO_AUTO,
         tensors: dict | None = None,
+        fused: bool = False,
     ) -> None:
         import torch
 
@@ -145,6 +146,9 @@ class OverlappedIteration:
         garr = (_native.Group * len(groups))(*groups)
         fill_arr = (ctypes.c_float * max(1, len(fills)))(*fills) if fill else None
         flags = (_native.SCHED_FILL if fill else 0) | (_native.SCHED_GRAPH if graph else 0)
+        if fused:
+            flags |= _native.SCHED_FUSED
+        self.fused = fused
         src_arr = dst_arr = None
         if host_io:
             flags |= _native.SCHED_HOSTIO

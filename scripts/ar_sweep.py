@@ -19,7 +19,7 @@ import bench  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--ctas", default="148,296")
+    ap.add_argument("--ctas", default="296")
     ap.add_argument("--sizes", default=",".join(str(1 << k) for k in range(12, 28)))
     ap.add_argument("--reps", type=int, default=20)
     args = ap.parse_args()
@@ -44,6 +44,7 @@ def main():
         for algo, name in ((_native.ALGO_ONESHOT, "oneshot"), (_native.ALGO_TWOSHOT, "twoshot")):
             res[f"{name}_{ctas}"] = bench._exchange_times(comm, world, device, sizes, kind=1, algo=algo, repeats=args.reps)
         res[f"exchange_{ctas}"] = bench._exchange_times(comm, world, device, sizes, kind=0, repeats=args.reps)
+        res[f"fused_{ctas}"] = bench._exchange_times(comm, world, device, sizes, kind=4, repeats=args.reps)
     res["nccl"] = bench._nccl_times(world, device, sizes, repeats=args.reps)
     session.raise_if_failed()
     for i, nbytes in enumerate(sizes):

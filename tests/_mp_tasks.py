@@ -53,3 +53,9 @@ def random_task(config, session, *, arrays):
         ring_allreduce(GradientBuffer(1, 1, t), config, session)
         out[key + "_tensor"] = t.cpu().numpy()
     return out
+
+
+def emulate_task(config, session, *, profile, plan, fused, graph):
+    from paper_1811_11141_b200 import run_emulation
+
+    return run_emulation(profile, plan, config, session, 3, warmup=1, fused=fused, graph=graph)

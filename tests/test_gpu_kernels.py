@@ -167,3 +167,70 @@ def test_integer_payloads_exact(torch_cuda):
         ones = [torch.full((1_000_000,), float(r + 1), device="cuda") for r in range(world)]
         for out in _emulated(torch, ones, _native.ALGO_TWOSHOT):
             assert bool((out == world * (world + 1) / 2).all())
+
+
+def _fused_emulated(torch, per_rank_tensors, counts, algo, scale=1.0):
+    """Emulated fused kernel: every rank packs its own layer tensors, folds, writes back."""
+    world = len(per_rank_tensors)
+    tables, slots = [], []
+    total = sum(counts)
+    for tensors in per_rank_tensors:
+        rows, off = [], 0
+        for x, p in zip(tensors, counts):
+            rows.append((x.data_ptr(), p, off))
+            off += p
+        tables.append(_native.DeviceTable(rows))
+        slots.append(torch.full((total,), float("nan"), device="cuda"))
+    tp = (ctypes.c_void_p * world)(*[t.ptr for t in tables])
+    sp = (ctypes.c_void_p * world)(*[x.data_ptr() for x in slots])
+    _native.call("mgw_allreduce_fused_emulated", tp, sp, world, total, ctypes.c_float(scale), algo,
+                 torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    for t in tables:
+        t.close()
+
+
+@pytest.mark.parametrize("algo", [_native.ALGO_ONESHOT, _native.ALGO_TWOSHOT])
+@pytest.mark.parametrize("n_ranks", [2, 3, 4, 8])
+@pytest.mark.parametrize("shift", [0, 1])
+def test_fused_exchange_bit_exact(torch_cuda, algo, n_ranks, shift):
+    """Fused pack -> fold -> write-back equals oracle pack + reference ring + unpack, bit for bit,
+    for a layer mix with odd sizes, misaligned tensors and a tail."""
+    torch = torch_cuda
+    counts = [9408, 4096, 1001, 3, 36864, 17, 2049]  # layer high first
+    rng = np.random.default_rng(100 + n_ranks)
+    host = [[(rng.standard_normal(p) * 10.0 ** rng.integers(-2, 3, p)).astype("<f4") for p in counts]
+            for _ in range(n_ranks)]
+    tensors = []
+    for r in range(n_ranks):
+        ts = []
+        for h in host[r]:
+            base = torch.empty(h.size + shift, device="cuda")
+            t = base[shift:]
+            t.copy_(torch.from_numpy(h))
+            ts.append(t)
+        tensors.append(ts)
+    _fused_emulated(torch, tensors, counts, algo)
+    buckets = [np.concatenate(host[r]) for r in range(n_ranks)]
+    want = ring_oracle.ring_allreduce(buckets)[0]
+    off = 0
+    for k, p in enumerate(counts):
+        for r in range(n_ranks):
+            got = tensors[r][k].cpu().numpy()
+            assert np.array_equal(got.view("<u4"), want[off:off + p].view("<u4")), (r, k)
+        off += p
+
+
+def test_fused_exchange_many_rows_from_device_table(torch_cuda):
+    """More layers than fit in the kernel parameters (BERT-like: 124 tiny + big rows)."""
+    torch = torch_cuda
+    counts = [768] * 60 + [3072, 589824] + [768] * 60
+    n_ranks = 4
+    rng = np.random.default_rng(5)
+    host = [[rng.standard_normal(p).astype("<f4") for p in counts] for _ in range(n_ranks)]
+    tensors = [[torch.from_numpy(h).cuda() for h in host[r]] for r in range(n_ranks)]
+    _fused_emulated(torch, tensors, counts, _native.ALGO_TWOSHOT, scale=0.25)
+    buckets = [np.concatenate(host[r]) * np.float32(0.25) for r in range(n_ranks)]
+    want = ring_oracle.ring_allreduce(buckets)[0]
+    got = np.concatenate([t.cpu().numpy() for t in tensors[2]])
+    assert np.array_equal(got.view("<u4"), want.view("<u4"))

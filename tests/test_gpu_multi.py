@@ -92,6 +92,16 @@ def test_emulate_local_verified_report():
         assert r.mean_seconds >= profile.forward_time + profile.total_backward_time - 1e-4
 
 
+def test_emulate_fused_and_unfused_agree():
+    profile = synth_profile(30, param_range=(1e3, 3e5), time_scale=2e-3, seed=4)
+    plan = MergePlan(frozenset({3, 4, 5, 10, 11, 20, 30}), 30)
+    n = max(_worlds())
+    for fused in (False, True):
+        for graph in (False, True):
+            reports = run_workers(n, partial(_mp_tasks.emulate_task, profile=profile, plan=plan, fused=fused, graph=graph))
+            assert all(r.verified for r in reports.values()), (fused, graph)
+
+
 def test_criterion_8_calibrate_then_predict():
     n = max(_worlds())
     sizes = [32768, 131072, 262144, 524288, 1048576, 2097152, 4194304, 8388608]

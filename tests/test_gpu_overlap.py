@@ -35,7 +35,7 @@ def test_single_gpu_iteration_matches_profile(torch_cuda, graph):
     profile = resnet50_like(backward_seconds=4e-3, forward_seconds=2e-3)
     compute = profile.forward_time + profile.total_backward_time
     for name, plan in _plans(profile).items():
-        it = OverlappedIteration(profile, plan, comm=None, rank=0, world=1, device="cuda:0", graph=graph)
+        it = OverlappedIteration(profile, plan, comm=None, rank=0, world=1, device="cuda:0", graph=graph, fused=graph)
         try:
             for _ in range(3):
                 t = it.run()
