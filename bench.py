@@ -257,7 +257,8 @@ def run_ours(args) -> dict | None:
         comm = session.comm
 
     # 1. fit the startup/bandwidth model of one group exchange on this box
-    exch = _exchange_times(comm, world, device, FIT_SIZES, kind=4 if (world > 1 and not args.unfused) else 0)
+    exch = _exchange_times(comm, world, device, FIT_SIZES, kind=4 if (world > 1 and not args.unfused) else 0,
+                           repeats=3 if args.quick else 20, warmups=1 if args.quick else 3)
     if session is not None:
         session.raise_if_failed()
     model, fit_ok = _fit(FIT_SIZES, exch, world)
@@ -381,6 +382,8 @@ def run_ours(args) -> dict | None:
 
     # e2e: the same MG-WFBP iteration with host buffers (H2D of every layer's gradient,
     # D2H of every reduced gradient) inside the timed region
+    if args.quick:
+        args.no_sweep = args.no_cpu_baseline = True
     e2e_it = OverlappedIteration(profile, plans["mgwfbp"], comm=comm, rank=rank, world=world, device=device,
                                  host_io=True, graph=not args.no_graph, fused=not args.unfused)
     try:
@@ -547,6 +550,8 @@ def main(argv=None) -> int:
     ap.add_argument("--no-sweep", action="store_true", help="skip the all-reduce bus-bandwidth sweep (N > 1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--quick", action="store_true",
+                    help="profiling aid: 3 fit repetitions, no e2e / sweep / CPU baseline")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
