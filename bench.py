@@ -313,6 +313,8 @@ def run_ours(args) -> dict | None:
             gbytes = it.group_bytes()
             res = {
                 "t_iter_ms": round(statistics.fmean(t_iter_max) * 1e3, 4),
+                "t_iter_ms_median": round(statistics.median(t_iter_max) * 1e3, 4),
+                "t_c_no_us_median": round(statistics.median(exposed_max) * 1e6, 2),
                 "t_iter_ms_min": round(min(t_iter_max) * 1e3, 4),
                 "compute_ms": round(statistics.fmean(compute_max) * 1e3, 4),
                 "t_c_no_us": round(statistics.fmean(exposed_max) * 1e6, 2),
@@ -413,6 +415,7 @@ def run_ours(args) -> dict | None:
         return None
 
     mg = results["mgwfbp"]
+    same_as_wfbp = plans["mgwfbp"].merged_layers == plans["wfbp"].merged_layers
     line = {
         "metric": METRIC,
         "value": mg["t_iter_ms"],
@@ -444,6 +447,7 @@ def run_ours(args) -> dict | None:
             "fused_group_kernel": world > 1 and not args.unfused,
         },
         "strategies": results,
+        "mgwfbp_plan_equals_wfbp": same_as_wfbp,
         "roofline": roofline,
         "e2e": {"value": round(statistics.fmean(e2e_max) * 1e3, 4), "unit": "ms",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "verified": e2e_ok},

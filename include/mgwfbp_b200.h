@@ -58,6 +58,7 @@ extern "C" {
 #define MGW_ALGO_AUTO 0
 #define MGW_ALGO_ONESHOT 1
 #define MGW_ALGO_TWOSHOT 2
+#define MGW_ALGO_LL 3 /* push-based low-latency one-shot (fused path only, <= 65,536 elements) */
 
 /* schedule flags */
 #define MGW_SCHED_FILL 1u  /* "backward" writes fill_values into each layer before its deadline */
@@ -114,6 +115,7 @@ int mgw_comm_destroy(mgw_comm* comm);
 int mgw_comm_set_timeout_ms(mgw_comm* comm, int64_t ms);
 int mgw_comm_set_oneshot_max(mgw_comm* comm, int64_t bytes);
 int mgw_comm_set_max_ctas(mgw_comm* comm, int ctas);
+int mgw_comm_set_ll_max(mgw_comm* comm, int64_t bytes);
 int mgw_comm_input(mgw_comm* comm, float** slot); /* slot the next collective reads (syncs) */
 int mgw_comm_result(mgw_comm* comm, float** result);
 int mgw_comm_pack(mgw_comm* comm, const void* dev_table, int n, int64_t n_elem, float scale, void* stream);

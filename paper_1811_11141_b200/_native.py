@@ -18,7 +18,7 @@ LIB_DIR = pathlib.Path(__file__).resolve().parent / "_lib"
 LIB_PATH = LIB_DIR / "libmgwfbp_b200.so"
 
 MGW_OK, MGW_EINVAL, MGW_EPROTO, MGW_ECUDA = 0, 1, 2, 3
-ALGO_AUTO, ALGO_ONESHOT, ALGO_TWOSHOT = 0, 1, 2
+ALGO_AUTO, ALGO_ONESHOT, ALGO_TWOSHOT, ALGO_LL = 0, 1, 2, 3
 SCHED_FILL, SCHED_GRAPH, SCHED_HOSTIO, SCHED_FUSED = 1, 2, 4, 8
 DEV_OK, DEV_LENGTH_MISMATCH, DEV_TIMEOUT, DEV_PEER_ABORT = 0, 1, 2, 3
 IPC_HANDLE_BYTES = 64
@@ -65,6 +65,7 @@ _SIGNATURES = {
     "mgw_comm_set_timeout_ms": ([_P, _I64], _I),
     "mgw_comm_set_oneshot_max": ([_P, _I64], _I),
     "mgw_comm_set_max_ctas": ([_P, _I], _I),
+    "mgw_comm_set_ll_max": ([_P, _I64], _I),
     "mgw_comm_input": ([_P, ctypes.POINTER(_P)], _I),
     "mgw_comm_result": ([_P, ctypes.POINTER(_P)], _I),
     "mgw_comm_pack": ([_P, _P, _I, _I64, ctypes.c_float, _P], _I),

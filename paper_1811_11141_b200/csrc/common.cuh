@@ -59,8 +59,15 @@ constexpr size_t kFlagsPerParity = (size_t)kMaxBlocks * kMaxRanks;
 constexpr size_t kArriveOff = 0;
 constexpr size_t kMidOff = kArriveOff + 2 * kFlagsPerParity * sizeof(uint64_t);
 constexpr size_t kAbortOff = kMidOff + 2 * kFlagsPerParity * sizeof(uint64_t);
+constexpr size_t kHdrOff = kAbortOff + 1024;  // LL headers u64 [2 parity][kMaxRanks src]
 constexpr size_t kCtrlBytes = 262144;
-static_assert(kAbortOff + 256 <= kCtrlBytes, "control area overflow");
+static_assert(kHdrOff + 2 * kMaxRanks * sizeof(uint64_t) <= kCtrlBytes, "control area overflow");
+// LL receive area u64 [2 parity][kMaxRanks src][kLLElems] follows the control area,
+// then the two bucket slots.
+constexpr int64_t kLLElems = 65536;
+constexpr size_t kLLOff = kCtrlBytes;
+constexpr size_t kLLBytes = 2 * (size_t)kMaxRanks * (size_t)kLLElems * sizeof(uint64_t);
+constexpr size_t kSlotOff = kLLOff + kLLBytes;
 
 struct Row {  // identical layout to mgw_tensor_desc
   float* ptr;

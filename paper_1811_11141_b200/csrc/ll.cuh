@@ -1,0 +1,209 @@
+// ll.cuh -- push-based low-latency one-shot for small, startup-dominated groups.
+//
+// The messages MG-WFBP creates by merging are small: their cost is the startup `a`
+// (paper Eq. 8), not bandwidth.  The pull one-shot pays a flag round trip (signal +
+// poll) and then a remote-read round trip.  Here every rank *pushes* its packed
+// values into every peer's LL receive area as 8-byte words (epoch << 32 | fp32 bits):
+// a word is data and flag at once (single-copy atomic 64-bit store), so a receiver
+// only polls its own local memory and folds as soon as all N words of an element
+// carry the current epoch.  One NVLink crossing, no separate barrier.  Twice the bytes
+// on the wire, which is irrelevant at these sizes.
+//
+// Fold order is the reference's (start at the element's `_segments` segment), so the
+// result is bit-identical to K2/K3.  Length disagreement: CTA 0 of every rank also
+// pushes a header (epoch << 32 | n) and checks every peer's header before folding;
+// a mismatch raises the sticky abort flag that every poll loop watches.
+#pragma once
+
+#include "fused.cuh"
+
+namespace mgw {
+
+constexpr int64_t kLLMaxElems = kLLElems;  // per rank per parity (256 KB of fp32 payload)
+
+struct LLArgs {
+  FusedArgs f;                   // rows (layer tensors), scale, comm pointers, epochs
+  uint64_t* ll[kMaxRanks];       // per-rank LL receive area base: [2 parity][kMaxRanks src][kLLMaxElems]
+  uint64_t* hdr[kMaxRanks];      // per-rank header words: [2 parity][kMaxRanks src]
+};
+
+__device__ __forceinline__ void st_relaxed_sys_v2(uint64_t* p, uint64_t a, uint64_t b) {
+  asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+
+__device__ __forceinline__ void st_relaxed_sys_u64(uint64_t* p, uint64_t a) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(a) : "memory");
+}
+
+__device__ __forceinline__ uint64_t ld_relaxed_sys_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ uint64_t ll_word(uint32_t epoch, float x) {
+  return ((uint64_t)epoch << 32) | (uint64_t)__float_as_uint(x);
+}
+
+// Wait until word p carries `epoch`; returns the value.  Bounded; watches the abort flag.
+__device__ __forceinline__ float ll_wait(const uint64_t* p, uint32_t epoch, const ArArgs& a, int& status) {
+  uint64_t v = ld_relaxed_sys_u64(p);
+  if ((uint32_t)(v >> 32) == epoch) return __uint_as_float((uint32_t)v);
+  const uint64_t start = global_ns();
+  for (uint32_t spin = 0;; ++spin) {
+    v = ld_relaxed_sys_u64(p);
+    if ((uint32_t)(v >> 32) == epoch) return __uint_as_float((uint32_t)v);
+    if ((spin & 31) == 31) {
+      if (load_relaxed_sys32(a.abort_flag[a.rank]) != 0u) {
+        status = MGW_DEV_PEER_ABORT;
+        return 0.f;
+      }
+      if (global_ns() - start > a.timeout_ns) {
+        status = MGW_DEV_TIMEOUT;
+        return 0.f;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ float* ll_tensor(const FusedArgs& f, int& k, int64_t e) {
+  Row r = fused_row(f, k);
+  while (e >= r.offset + r.count) r = fused_row(f, ++k);
+  return r.ptr + (e - r.offset);
+}
+
+template <int N>
+__global__ void __launch_bounds__(kThreads, 2) ll_oneshot_kernel(const __grid_constant__ LLArgs l) {
+  const FusedArgs& f = l.f;
+  const ArArgs& a = f.ar;
+  stamp_enter(a.stamp);
+  __shared__ int64_t s_end[kMaxRanks];
+  __shared__ int s_status;
+  const uint32_t epoch = load_volatile32(a.state) + 1u;
+  const int parity = (int)(epoch & 1u);
+  const int me = a.rank;
+  const int64_t n = a.n;
+  if (threadIdx.x < N) {
+    const int t = threadIdx.x;
+    const int64_t q = n / N, r = n % N;
+    s_end[t] = (int64_t)(t + 1) * q + (t + 1 < r ? t + 1 : r);
+  }
+  if (threadIdx.x == 0) s_status = MGW_DEV_OK;
+  // header: (epoch, n) to every rank (CTA 0)
+  if (blockIdx.x == 0 && threadIdx.x < N)
+    st_relaxed_sys_u64(l.hdr[threadIdx.x] + parity * kMaxRanks + me, ((uint64_t)epoch << 32) | (uint32_t)n);
+  __syncthreads();
+
+  // element pairs of this CTA: [p0, p1) (pair j = elements 2j, 2j+1)
+  const int64_t pairs = (n + 1) >> 1;
+  const int64_t per = (pairs + gridDim.x - 1) / gridDim.x;
+  const int64_t p0 = (int64_t)blockIdx.x * per;
+  const int64_t p1 = p0 + per < pairs ? p0 + per : pairs;
+  const float scale = f.scale;
+  const size_t my_off = ((size_t)parity * kMaxRanks + me) * kLLMaxElems;
+
+  // 1. pack and push: my two elements of each pair to every rank's LL area
+  int k = 0;
+  if (p0 < p1) k = fused_row_covering(f, (p0 + threadIdx.x) * 2 < n ? (p0 + threadIdx.x) * 2 : 0);
+  for (int64_t j = p0 + threadIdx.x; j < p1; j += kThreads) {
+    const int64_t e = 2 * j;
+    float x0 = *ll_tensor(f, k, e);
+    float x1 = e + 1 < n ? *ll_tensor(f, k, e + 1) : 0.f;
+    if (scale != 1.0f) {
+      x0 = __fmul_rn(x0, scale);
+      x1 = __fmul_rn(x1, scale);
+    }
+    const uint64_t w0 = ll_word(epoch, x0), w1 = ll_word(epoch, x1);
+#pragma unroll
+    for (int r = 0; r < N; ++r) st_relaxed_sys_v2(l.ll[r] + my_off + e, w0, w1);
+  }
+
+  // 2. CTA 0 checks every peer's header (length agreement)
+  int status = MGW_DEV_OK;
+  if (blockIdx.x == 0 && threadIdx.x < N) {
+    const uint64_t h = [&] {
+      const uint64_t* p = l.hdr[me] + parity * kMaxRanks + threadIdx.x;
+      uint64_t v = ld_relaxed_sys_u64(p);
+      const uint64_t start = global_ns();
+      for (uint32_t spin = 0; (uint32_t)(v >> 32) != epoch; ++spin) {
+        if ((spin & 31) == 31) {
+          if (load_relaxed_sys32(a.abort_flag[me]) != 0u) {
+            status = MGW_DEV_PEER_ABORT;
+            break;
+          }
+          if (global_ns() - start > a.timeout_ns) {
+            status = MGW_DEV_TIMEOUT;
+            break;
+          }
+        }
+        v = ld_relaxed_sys_u64(p);
+      }
+      return v;
+    }();
+    if (status == MGW_DEV_OK && (uint32_t)h != (uint32_t)n) status = MGW_DEV_LENGTH_MISMATCH;
+    if (status != MGW_DEV_OK) atomicCAS(&s_status, 0, status);
+  }
+  __syncthreads();
+  if (s_status != MGW_DEV_OK && threadIdx.x == 0) {
+    atomicCAS(a.err, 0, s_status);
+    if (s_status != MGW_DEV_PEER_ABORT)
+      for (int r = 0; r < N; ++r) store_release_sys32(a.abort_flag[r], 1u);
+  }
+  status = s_status;
+
+  // 3. fold every element of my pairs from the N local LL areas, write the tensors
+  if (status == MGW_DEV_OK) {
+    const uint64_t* base = l.ll[me] + (size_t)parity * kMaxRanks * kLLMaxElems;
+    int seg = 0;
+    k = 0;
+    if (p0 < p1) k = fused_row_covering(f, (p0 + threadIdx.x) * 2 < n ? (p0 + threadIdx.x) * 2 : 0);
+    for (int64_t j = p0 + threadIdx.x; j < p1 && status == MGW_DEV_OK; j += kThreads) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t e = 2 * j + h;
+        if (e >= n) break;
+        seg = advance_segment(seg, e, s_end);
+        float x[N];
+#pragma unroll
+        for (int kk = 0; kk < N; ++kk) {
+          const int src = seg + kk >= N ? seg + kk - N : seg + kk;
+          x[kk] = ll_wait(base + (size_t)src * kLLMaxElems + e, epoch, a, status);
+        }
+        float acc = x[0];
+#pragma unroll
+        for (int kk = 1; kk < N; ++kk) acc = __fadd_rn(acc, x[kk]);
+        if (status == MGW_DEV_OK) *ll_tensor(f, k, e) = acc;
+      }
+    }
+    if (status != MGW_DEV_OK) {
+      atomicCAS(a.err, 0, status);
+      if (status != MGW_DEV_PEER_ABORT)
+        for (int r = 0; r < N; ++r) store_release_sys32(a.abort_flag[r], 1u);
+    }
+  }
+  finish_call(a);
+}
+
+template <int N>
+int launch_ll_n(const LLArgs& l, int max_ctas, cudaStream_t stream) {
+  const int64_t pairs = (l.f.ar.n + 1) >> 1;
+  ll_oneshot_kernel<N><<<grid_for(pairs, kThreads, max_ctas < 128 ? max_ctas : 128), kThreads, 0, stream>>>(l);
+  MGW_CHECK_LAUNCH();
+  return MGW_OK;
+}
+
+inline int launch_ll(const LLArgs& l, int max_ctas, cudaStream_t stream) {
+  if (l.f.ar.n > kLLMaxElems) return set_error(MGW_EINVAL, "LL path takes at most %lld elements", (long long)kLLMaxElems);
+  switch (l.f.ar.world) {
+    case 2: return launch_ll_n<2>(l, max_ctas, stream);
+    case 3: return launch_ll_n<3>(l, max_ctas, stream);
+    case 4: return launch_ll_n<4>(l, max_ctas, stream);
+    case 5: return launch_ll_n<5>(l, max_ctas, stream);
+    case 6: return launch_ll_n<6>(l, max_ctas, stream);
+    case 7: return launch_ll_n<7>(l, max_ctas, stream);
+    case 8: return launch_ll_n<8>(l, max_ctas, stream);
+    default: return set_error(MGW_EINVAL, "LL path needs 2..%d ranks, got %d", kMaxRanks, l.f.ar.world);
+  }
+}
+
+}  // namespace mgw

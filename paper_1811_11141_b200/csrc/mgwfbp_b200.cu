@@ -27,6 +27,7 @@
 #include "allreduce.cuh"
 #include "common.cuh"
 #include "fused.cuh"
+#include "ll.cuh"
 #include "rows.cuh"
 
 using namespace mgw;
@@ -84,6 +85,7 @@ struct mgw_comm {
   float* result = nullptr;
   uint64_t timeout_ns = 30ull * 1000000000ull;
   int64_t oneshot_max_bytes = 1 << 20;
+  int64_t ll_max_bytes = 64 << 10;
   int max_ctas = 2 * kSMs;
 };
 
@@ -118,7 +120,7 @@ ArArgs make_args(const mgw_comm* c, int64_t n) {
   memset(&a, 0, sizeof(a));
   for (int s = 0; s < c->world; ++s) {
     char* base = c->peer[s];
-    a.slot[s] = base + kCtrlBytes;
+    a.slot[s] = base + kSlotOff;
     a.arrive[s] = reinterpret_cast<uint64_t*>(base + kArriveOff);
     a.mid[s] = reinterpret_cast<uint64_t*>(base + kMidOff);
     a.abort_flag[s] = reinterpret_cast<uint32_t*>(base + kAbortOff);
@@ -139,12 +141,19 @@ int pick_algo(const mgw_comm* c, int64_t n, int algo) {
   return n * 4 <= c->oneshot_max_bytes ? MGW_ALGO_ONESHOT : MGW_ALGO_TWOSHOT;
 }
 
+// fused group exchange: LL push for small buckets, else pull one-shot / two-shot
+int pick_fused_algo(const mgw_comm* c, int64_t n, int algo) {
+  if (algo != MGW_ALGO_AUTO) return algo;
+  if (c->world > 1 && n * 4 <= c->ll_max_bytes && n <= kLLElems) return MGW_ALGO_LL;
+  return pick_algo(c, n, algo);
+}
+
 int comm_allreduce(mgw_comm* c, int64_t n, int algo, cudaStream_t stream, uint64_t* stamp = nullptr) {
   if (n < 0 || n * 4 > c->slot_bytes)
     return set_error(MGW_EINVAL, "bucket of %lld elements exceeds slot capacity %lld B", (long long)n,
                      (long long)c->slot_bytes);
   if (c->world == 1) {
-    if (n > 0) MGW_CUDA(cudaMemcpyAsync(c->result, c->region + kCtrlBytes, n * 4, cudaMemcpyDeviceToDevice, stream));
+    if (n > 0) MGW_CUDA(cudaMemcpyAsync(c->result, c->region + kSlotOff, n * 4, cudaMemcpyDeviceToDevice, stream));
     return MGW_OK;
   }
   if (!c->peers_open) return set_error(MGW_EINVAL, "peers not opened (call mgw_comm_open_peers)");
@@ -158,7 +167,7 @@ int comm_pack(mgw_comm* c, const Row* host_rows, const Row* dev_rows, int n_rows
   if (n * 4 > c->slot_bytes)
     return set_error(MGW_EINVAL, "bucket of %lld elements exceeds slot capacity %lld B", (long long)n,
                      (long long)c->slot_bytes);
-  float* slot0 = reinterpret_cast<float*>(c->region + kCtrlBytes);
+  float* slot0 = reinterpret_cast<float*>(c->region + kSlotOff);
   const uint32_t* calls = c->world > 1 ? c->state : nullptr;
   return launch_rows<RowOp::kPack>(host_rows, dev_rows, n_rows, slot0, n, scale, nullptr, calls, c->slot_bytes / 4,
                                    nullptr, stream, stamp);
@@ -182,7 +191,18 @@ int comm_allreduce_fused(mgw_comm* c, const Row* host_rows, const Row* dev_rows,
   f.rows = dev_rows;
   f.n_rows = n_rows;
   f.scale = scale;
-  return launch_fused(f, pick_algo(c, n, algo), c->max_ctas, stream);
+  const int chosen = pick_fused_algo(c, n, algo);
+  if (chosen == MGW_ALGO_LL) {
+    LLArgs l;
+    memset(&l, 0, sizeof(l));
+    l.f = f;
+    for (int s = 0; s < c->world; ++s) {
+      l.ll[s] = reinterpret_cast<uint64_t*>(c->peer[s] + kLLOff);
+      l.hdr[s] = reinterpret_cast<uint64_t*>(c->peer[s] + kHdrOff);
+    }
+    return launch_ll(l, c->max_ctas, stream);
+  }
+  return launch_fused(f, chosen, c->max_ctas, stream);
 }
 
 const mgw_table_t* as_table(const void* t) { return static_cast<const mgw_table_t*>(t); }
@@ -329,9 +349,9 @@ int mgw_comm_create(int rank, int world, int device, int64_t capacity_bytes, mgw
   c->device = device;
   c->capacity = capacity_bytes;
   c->slot_bytes = round_up(std::max<int64_t>(capacity_bytes, 256), 256);
-  const size_t region_bytes = kCtrlBytes + 2 * (size_t)c->slot_bytes;
+  const size_t region_bytes = kSlotOff + 2 * (size_t)c->slot_bytes;
   cudaError_t e = cudaMalloc(&c->region, region_bytes);
-  if (e == cudaSuccess) e = cudaMemset(c->region, 0, kCtrlBytes);
+  if (e == cudaSuccess) e = cudaMemset(c->region, 0, kSlotOff);  // flags, headers, LL area
   if (e == cudaSuccess) e = cudaMalloc(&c->state, 2 * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMemset(c->state, 0, 2 * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMalloc(&c->err, sizeof(int));
@@ -398,6 +418,12 @@ int mgw_comm_set_oneshot_max(mgw_comm* c, int64_t bytes) {
   return MGW_OK;
 }
 
+int mgw_comm_set_ll_max(mgw_comm* c, int64_t bytes) {
+  if (!c || bytes < 0 || bytes > kLLElems * 4) return set_error(MGW_EINVAL, "LL threshold must lie in 0..%lld B", (long long)(kLLElems * 4));
+  c->ll_max_bytes = bytes;
+  return MGW_OK;
+}
+
 int mgw_comm_set_max_ctas(mgw_comm* c, int ctas) {
   if (!c || ctas < 1 || ctas > kMaxBlocks) return set_error(MGW_EINVAL, "CTA cap must lie in 1..%d", kMaxBlocks);
   c->max_ctas = ctas;
@@ -413,7 +439,7 @@ int mgw_comm_input(mgw_comm* c, float** slot) {
     MGW_CUDA(cudaMemcpy(&calls, c->state, sizeof(calls), cudaMemcpyDeviceToHost));
   }
   const int64_t parity = c->world > 1 ? (int64_t)((calls + 1u) & 1u) : 0;
-  *slot = reinterpret_cast<float*>(c->region + kCtrlBytes + parity * c->slot_bytes);
+  *slot = reinterpret_cast<float*>(c->region + kSlotOff + parity * c->slot_bytes);
   return MGW_OK;
 }
 
@@ -440,7 +466,7 @@ int mgw_allreduce(mgw_comm* c, int64_t n_elem, int algo, void* stream) {
 int mgw_allreduce_fused(mgw_comm* c, const void* table, int n_rows, int64_t n_elem, float scale, int algo,
                         void* stream) {
   if (!c) return set_error(MGW_EINVAL, "comm is null");
-  if (algo < MGW_ALGO_AUTO || algo > MGW_ALGO_TWOSHOT) return set_error(MGW_EINVAL, "unknown algorithm %d", algo);
+  if (algo < MGW_ALGO_AUTO || algo > MGW_ALGO_LL) return set_error(MGW_EINVAL, "unknown algorithm %d", algo);
   int rc = check_table(table, n_rows, n_elem);
   if (rc) return rc;
   const mgw_table_t* t = as_table(table);
@@ -449,7 +475,7 @@ int mgw_allreduce_fused(mgw_comm* c, const void* table, int n_rows, int64_t n_el
     if (scale == 1.0f) return MGW_OK;
     rc = comm_pack(c, t->host.data(), t->dev, n_rows, n_elem, scale, static_cast<cudaStream_t>(stream));
     if (rc) return rc;
-    return launch_rows<RowOp::kUnpack>(t->host.data(), t->dev, n_rows, reinterpret_cast<float*>(c->region + kCtrlBytes),
+    return launch_rows<RowOp::kUnpack>(t->host.data(), t->dev, n_rows, reinterpret_cast<float*>(c->region + kSlotOff),
                                        n_elem, 1.f, nullptr, nullptr, 0, nullptr, static_cast<cudaStream_t>(stream));
   }
   return comm_allreduce_fused(c, t->host.data(), t->dev, n_rows, n_elem, scale, algo, static_cast<cudaStream_t>(stream));

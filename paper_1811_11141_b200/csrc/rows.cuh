@@ -147,8 +147,10 @@ __global__ void __launch_bounds__(kThreads) rows_kernel(const __grid_constant__ 
 }
 
 inline int rows_grid(int64_t total) {
+  // one resident wave: 512-thread CTAs at <= 40 registers -> 3 per SM (ncu r01:
+  // launch__occupancy_limit_registers = 3; a 592-CTA grid left a 1/3 tail wave)
   const int64_t tiles = (total + kTile - 1) / kTile;
-  const int64_t cap = (int64_t)kSMs * 4;
+  const int64_t cap = (int64_t)kSMs * 3;
   return (int)(tiles < 1 ? 1 : (tiles < cap ? tiles : cap));
 }
 

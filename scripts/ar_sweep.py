@@ -45,6 +45,11 @@ def main():
             res[f"{name}_{ctas}"] = bench._exchange_times(comm, world, device, sizes, kind=1, algo=algo, repeats=args.reps)
         res[f"exchange_{ctas}"] = bench._exchange_times(comm, world, device, sizes, kind=0, repeats=args.reps)
         res[f"fused_{ctas}"] = bench._exchange_times(comm, world, device, sizes, kind=4, repeats=args.reps)
+        _native.call("mgw_comm_set_ll_max", comm, 0)
+        res[f"fused_noll_{ctas}"] = bench._exchange_times(comm, world, device, sizes, kind=4, repeats=args.reps)
+        _native.call("mgw_comm_set_ll_max", comm, 256 << 10)
+        res[f"fused_ll256k_{ctas}"] = bench._exchange_times(comm, world, device, [s for s in sizes], kind=4, repeats=args.reps)
+        _native.call("mgw_comm_set_ll_max", comm, 64 << 10)
     res["nccl"] = bench._nccl_times(world, device, sizes, repeats=args.reps)
     session.raise_if_failed()
     for i, nbytes in enumerate(sizes):
