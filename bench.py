@@ -231,6 +231,76 @@ def _fit(sizes, times, world):
         return CommModel(a=min(times), b=0.0), False
 
 
+class RankContext:
+    """This rank's view of the run: ids, device, communicator and the L2-flush buffer."""
+
+    def __init__(self, rank, world, local, device, comm, session, flush):
+        self.rank, self.world, self.local, self.device = rank, world, local, device
+        self.comm, self.session, self.flush = comm, session, flush
+
+
+def run_strategy(ctx, profile, plan, predicted, steps, warmup, *, graph=True, fused=True, keep=False):
+    """Warm up, then time `steps` Algorithm-2 iterations of `plan` (max over ranks per
+    iteration); every iteration is preceded by an L2 flush outside its events and the
+    reduced gradients are verified before and after the timed region."""
+    import torch
+
+    from paper_1811_11141_b200.overlap import OverlappedIteration
+
+    world, device = ctx.world, ctx.device
+    it = OverlappedIteration(profile, plan, comm=ctx.comm, rank=ctx.rank, world=world, device=device,
+                             fill=True, graph=graph, fused=fused)
+    try:
+        for _ in range(warmup):
+            with torch.cuda.stream(it.compute_stream):
+                ctx.flush.zero_()
+            it.run()
+        if not it.verify():
+            raise RuntimeError(f"{profile.name}: reduced gradients differ from the expected sums")
+        _barrier(world)
+        torch.cuda.synchronize()
+        wall0 = time.perf_counter()
+        t_iter, compute, exposed, kern = [], [], [], []
+        for _ in range(steps):
+            with torch.cuda.stream(it.compute_stream):
+                ctx.flush.zero_()  # L2 flush between iterations, outside the iteration's events
+            times = it.run()
+            t_iter.append(times.t_iter)
+            compute.append(times.compute_time)
+            exposed.append(times.t_c_no)
+            kern.append(it.kernel_times())
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - wall0
+        _barrier(world)
+        if ctx.session is not None:
+            ctx.session.raise_if_failed()
+        ok = it.verify()
+        t_iter_max = _max_over_ranks(t_iter, world, device)
+        compute_max = _max_over_ranks(compute, world, device)
+        exposed_max = _max_over_ranks(exposed, world, device)
+        res = {
+            "t_iter_ms": round(statistics.fmean(t_iter_max) * 1e3, 4),
+            "t_iter_ms_median": round(statistics.median(t_iter_max) * 1e3, 4),
+            "t_iter_ms_min": round(min(t_iter_max) * 1e3, 4),
+            "compute_ms": round(statistics.fmean(compute_max) * 1e3, 4),
+            "t_c_no_us": round(statistics.fmean(exposed_max) * 1e6, 2),
+            "t_c_no_us_median": round(statistics.median(exposed_max) * 1e6, 2),
+            "scaling_eff": round(statistics.fmean(compute_max) / statistics.fmean(t_iter_max), 5),
+            "predicted_t_iter_ms": round(predicted.t_iter * 1e3, 4),
+            "predicted_t_c_no_us": round(predicted.t_c_no * 1e6, 2),
+            "groups": len(plan.groups()),
+            "verified": ok,
+            "wall_s": round(wall, 4),
+        }
+    except BaseException:
+        it.close()
+        raise
+    if not keep:
+        it.close()
+        it = None
+    return res, it, kern, t_iter_max, wall
+
+
 def run_ours(args) -> dict | None:
     import torch
 
@@ -274,64 +344,20 @@ def run_ours(args) -> dict | None:
     }
 
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=device)
+    ctx = RankContext(rank, world, local, device, comm, session, flush)
     results = {}
     headline = None
     for name in ("wfbp", "synceasgd", "mgwfbp"):
-        it = OverlappedIteration(profile, plans[name], comm=comm, rank=rank, world=world, device=device,
-                                 fill=True, graph=not args.no_graph, fused=not args.unfused)
         sampler = ClockSampler(local) if (rank == 0 and name == "mgwfbp") else None
         if sampler:
             sampler.__enter__()
-        try:
-            for _ in range(args.warmup):
-                with torch.cuda.stream(it.compute_stream):
-                    flush.zero_()
-                it.run()
-            if not it.verify():
-                raise RuntimeError(f"{name}: reduced gradients differ from the expected sums")
-            _barrier(world)
-            torch.cuda.synchronize()
-            wall0 = time.perf_counter()
-            t_iter, compute, exposed, kern = [], [], [], []
-            for _ in range(args.steps):
-                with torch.cuda.stream(it.compute_stream):
-                    flush.zero_()  # L2 flush between iterations, outside the iteration's events
-                times = it.run()
-                t_iter.append(times.t_iter)
-                compute.append(times.compute_time)
-                exposed.append(times.t_c_no)
-                kern.append(it.kernel_times())
-            torch.cuda.synchronize()
-            wall = time.perf_counter() - wall0
-            _barrier(world)
-            if session is not None:
-                session.raise_if_failed()
-            ok = it.verify()
-            t_iter_max = _max_over_ranks(t_iter, world, device)
-            compute_max = _max_over_ranks(compute, world, device)
-            exposed_max = _max_over_ranks(exposed, world, device)
-            gbytes = it.group_bytes()
-            res = {
-                "t_iter_ms": round(statistics.fmean(t_iter_max) * 1e3, 4),
-                "t_iter_ms_median": round(statistics.median(t_iter_max) * 1e3, 4),
-                "t_c_no_us_median": round(statistics.median(exposed_max) * 1e6, 2),
-                "t_iter_ms_min": round(min(t_iter_max) * 1e3, 4),
-                "compute_ms": round(statistics.fmean(compute_max) * 1e3, 4),
-                "t_c_no_us": round(statistics.fmean(exposed_max) * 1e6, 2),
-                "scaling_eff": round(statistics.fmean(compute_max) / statistics.fmean(t_iter_max), 5),
-                "predicted_t_iter_ms": round(predicted[name].t_iter * 1e3, 4),
-                "predicted_t_c_no_us": round(predicted[name].t_c_no * 1e6, 2),
-                "groups": len(gbytes),
-                "verified": ok,
-                "wall_s": round(wall, 4),
-            }
-            results[name] = res
-            if name == "mgwfbp":
-                headline = (it, kern, gbytes, sampler, t_iter_max, wall)
-                launches = it.launches_per_iteration
-        finally:
-            if name != "mgwfbp":
-                it.close()
+        res, it, kern, t_iter_max, wall = run_strategy(ctx, profile, plans[name], predicted[name], args.steps,
+                                                        args.warmup, graph=not args.no_graph,
+                                                        fused=not args.unfused, keep=name == "mgwfbp")
+        results[name] = res
+        if name == "mgwfbp":
+            headline = (it, kern, it.group_bytes(), sampler, t_iter_max, wall)
+            launches = it.launches_per_iteration
 
     it, kern, gbytes, sampler, t_iter_max, wall = headline
     # roofline of the dominant kernel inside the MG-WFBP timed region; kernel spans are

@@ -389,7 +389,11 @@ class RingSession:
         c = self.counters
         c.frames_sent += 1
         c.frames_received += 1
-        if algo == _native.ALGO_ONESHOT:
+        if algo == _native.ALGO_LL:  # pushed as 8-byte (epoch, value) words
+            c.rounds += 1
+            c.payload_bytes_received += 8 * n * (world - 1)
+            c.payload_bytes_sent += 8 * n * (world - 1)
+        elif algo == _native.ALGO_ONESHOT:
             c.rounds += 1
             c.payload_bytes_received += 4 * n * (world - 1)
             c.payload_bytes_sent += 4 * n * (world - 1)
@@ -411,12 +415,18 @@ def _segments(n_elements: int, n_parts: int) -> tuple[list[int], list[int]]:
     return sizes, offsets
 
 
-def _algo_for(session: RingSession, n: int) -> int:
+LL_MAX_BYTES = 256 << 10  # push-based low-latency path (fused exchanges only)
+
+
+def _algo_for(session: RingSession, n: int, fused: bool = False) -> int:
+    if fused and 4 * n <= LL_MAX_BYTES:
+        return _native.ALGO_LL
     return _native.ALGO_ONESHOT if 4 * n <= session_oneshot_max(session) else _native.ALGO_TWOSHOT
 
 
 def session_oneshot_max(session: RingSession) -> int:
-    return getattr(session, "oneshot_max_bytes", 1 << 20)
+    world = session.config.n_workers
+    return getattr(session, "oneshot_max_bytes", (8 << 20) // max(1, world - 1))
 
 
 def set_oneshot_max(session: RingSession, nbytes: int) -> None:
@@ -458,12 +468,13 @@ def ring_allreduce(
                 raise ValueError(f"tensor on {values.device}, session on {session.device}")
             stream.wait_stream(torch.cuda.current_stream(session.device))
             ptr = values.data_ptr()
-        algo = _algo_for(session, n)
+        algo = _algo_for(session, n, fused=True)
         handle = stream.cuda_stream
         if n:
             # one kernel: pack -> all-reduce -> unpack, in place on the payload
             table = session.table(ptr, n)
-            _native.call("mgw_allreduce_fused", session.comm, table.ptr, 1, n, ctypes.c_float(1.0), algo, handle)
+            _native.call("mgw_allreduce_fused", session.comm, table.ptr, 1, n, ctypes.c_float(1.0),
+                         _native.ALGO_AUTO, handle)
         else:
             _native.call("mgw_allreduce", session.comm, 0, algo, handle)  # still collective
         stream.synchronize()
@@ -594,7 +605,8 @@ def run_emulation(
                 count += it.sending_groups
                 for (low, _, rows), t in zip(it.layout, times.group_comm):
                     if rows:
-                        session.account(sum(p for _, p, _ in rows), _algo_for(session, sum(p for _, p, _ in rows)))
+                        size = sum(p for _, p, _ in rows)
+                        session.account(size, _algo_for(session, size, fused=fused))
                         if k >= warmup:
                             per_group[low].append(t)
                 if k >= warmup:

@@ -84,8 +84,8 @@ struct mgw_comm {
   int* err = nullptr;
   float* result = nullptr;
   uint64_t timeout_ns = 30ull * 1000000000ull;
-  int64_t oneshot_max_bytes = 1 << 20;
-  int64_t ll_max_bytes = 64 << 10;
+  int64_t oneshot_max_bytes = 1 << 20;  // set per world in mgw_comm_create
+  int64_t ll_max_bytes = kLLElems * 4;  // 256 KB: the whole LL area
   int max_ctas = 2 * kSMs;
 };
 
@@ -349,6 +349,9 @@ int mgw_comm_create(int rank, int world, int device, int64_t capacity_bytes, mgw
   c->device = device;
   c->capacity = capacity_bytes;
   c->slot_bytes = round_up(std::max<int64_t>(capacity_bytes, 256), 256);
+  // one-shot pulls (N-1) M per rank, two-shot 2 (N-1)/N M in two phases: measured
+  // crossover on B200 ~ 8 MB / (N - 1) (profiles/ar_sweep_n*_r01_*.json)
+  c->oneshot_max_bytes = world > 1 ? (8ll << 20) / (world - 1) : (1ll << 20);
   const size_t region_bytes = kSlotOff + 2 * (size_t)c->slot_bytes;
   cudaError_t e = cudaMalloc(&c->region, region_bytes);
   if (e == cudaSuccess) e = cudaMemset(c->region, 0, kSlotOff);  // flags, headers, LL area
