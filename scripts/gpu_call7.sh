@@ -1,0 +1,8 @@
+#!/bin/bash
+NG=${NG:-4}
+mkdir -p gpurun_out; rm -f gpurun_out/status.txt
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $NG --master-addr 127.0.0.1 --master-port 29535 bench.py --gpus $NG --steps 20 --warmup 5 > gpurun_out/bench_n$NG.json 2> gpurun_out/bench_n$NG.err; echo "bench$NG rc=$?" >> gpurun_out/status.txt
+timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node $NG --master-addr 127.0.0.1 --master-port 29536 scripts/run_profiles.py --steps 10 > gpurun_out/profiles_n$NG.json 2> gpurun_out/profiles_n$NG.err; echo "profiles$NG rc=$?" >> gpurun_out/status.txt
+timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_n1.json 2> gpurun_out/bench_n1.err; echo "bench1 rc=$?" >> gpurun_out/status.txt
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29537 bench.py --gpus 2 --steps 20 --warmup 5 > gpurun_out/bench_n2.json 2> gpurun_out/bench_n2.err; echo "bench2 rc=$?" >> gpurun_out/status.txt
+cat gpurun_out/status.txt

@@ -92,6 +92,16 @@ def main():
                   file=sys.stderr, flush=True)
     if session is not None:
         session.close()
+    if rank == 0 and world > 1:
+        # BASELINE config 0: the reference CPU path on the same GoogLeNet profile and N
+        from oracle import emulation
+
+        key, prof = profiles()[0]
+        plan, cpu_model = bench._cpu_plan(prof, world)
+        walls, ok = emulation.emulate(prof, plan, world, 10, warmup=1, time_budget_s=15.0)
+        out["cpu_reference_" + key] = {"ranks": world, "t_iter_ms": sum(walls) / len(walls) * 1e3,
+                                        "iterations": len(walls), "verified": ok, "plan_groups": len(plan.groups()),
+                                        "fitted_a_us": None if cpu_model is None else cpu_model.a * 1e6}
     if rank == 0:
         print(json.dumps(out))
     if world > 1:
