@@ -116,6 +116,8 @@ int mgw_comm_set_timeout_ms(mgw_comm* comm, int64_t ms);
 int mgw_comm_set_oneshot_max(mgw_comm* comm, int64_t bytes);
 int mgw_comm_set_max_ctas(mgw_comm* comm, int ctas);
 int mgw_comm_set_ll_max(mgw_comm* comm, int64_t bytes);
+/* tuning: key 0 = one-shot 16-B slots per CTA, key 1 = two-shot slots per CTA (0 = default) */
+int mgw_comm_set_tuning(mgw_comm* comm, int key, int64_t value);
 int mgw_comm_input(mgw_comm* comm, float** slot); /* slot the next collective reads (syncs) */
 int mgw_comm_result(mgw_comm* comm, float** result);
 int mgw_comm_pack(mgw_comm* comm, const void* dev_table, int n, int64_t n_elem, float scale, void* stream);

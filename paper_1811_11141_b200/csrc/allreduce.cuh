@@ -314,32 +314,37 @@ inline int grid_for(int64_t vectors, int64_t per_cta, int max_ctas) {
   return (int)g;
 }
 
+// CTAs for a collective over `vectors` 16-B slots (whole bucket for one-shot, one part
+// for two-shot): one batch of U slots per thread by default, or `per_cta` when tuned.
 template <int N>
-int launch_allreduce_n(const ArArgs& a, int algo, int max_ctas, cudaStream_t stream) {
-  constexpr int U = Unroll<N>::value;
+inline int collective_grid(int64_t vectors, int64_t per_cta, int max_ctas) {
+  return grid_for(vectors, per_cta > 0 ? per_cta : (int64_t)kThreads * Unroll<N>::value, max_ctas);
+}
+
+template <int N>
+int launch_allreduce_n(const ArArgs& a, int algo, int max_ctas, cudaStream_t stream, const int64_t* per_cta) {
   const int64_t nv = a.n >> 2;
   if (algo == MGW_ALGO_ONESHOT) {
-    const int grid = grid_for(nv, (int64_t)kThreads * U, max_ctas);
-    oneshot_kernel<N><<<grid, kThreads, 0, stream>>>(a);
+    oneshot_kernel<N><<<collective_grid<N>(nv, per_cta ? per_cta[0] : 0, max_ctas), kThreads, 0, stream>>>(a);
   } else {
-    const int grid = grid_for(nv / N, (int64_t)kThreads * U, max_ctas);
-    twoshot_kernel<N><<<grid, kThreads, 0, stream>>>(a);
+    twoshot_kernel<N><<<collective_grid<N>(nv / N, per_cta ? per_cta[1] : 0, max_ctas), kThreads, 0, stream>>>(a);
   }
   MGW_CHECK_LAUNCH();
   return MGW_OK;
 }
 
-inline int launch_allreduce(const ArArgs& a, int algo, int max_ctas, cudaStream_t stream) {
+inline int launch_allreduce(const ArArgs& a, int algo, int max_ctas, cudaStream_t stream,
+                            const int64_t* per_cta = nullptr) {
   max_ctas = max_ctas < kMaxBlocks ? max_ctas : kMaxBlocks;  // one barrier flag slot per CTA
   switch (a.world) {
-    case 1: return launch_allreduce_n<1>(a, algo, max_ctas, stream);
-    case 2: return launch_allreduce_n<2>(a, algo, max_ctas, stream);
-    case 3: return launch_allreduce_n<3>(a, algo, max_ctas, stream);
-    case 4: return launch_allreduce_n<4>(a, algo, max_ctas, stream);
-    case 5: return launch_allreduce_n<5>(a, algo, max_ctas, stream);
-    case 6: return launch_allreduce_n<6>(a, algo, max_ctas, stream);
-    case 7: return launch_allreduce_n<7>(a, algo, max_ctas, stream);
-    case 8: return launch_allreduce_n<8>(a, algo, max_ctas, stream);
+    case 1: return launch_allreduce_n<1>(a, algo, max_ctas, stream, per_cta);
+    case 2: return launch_allreduce_n<2>(a, algo, max_ctas, stream, per_cta);
+    case 3: return launch_allreduce_n<3>(a, algo, max_ctas, stream, per_cta);
+    case 4: return launch_allreduce_n<4>(a, algo, max_ctas, stream, per_cta);
+    case 5: return launch_allreduce_n<5>(a, algo, max_ctas, stream, per_cta);
+    case 6: return launch_allreduce_n<6>(a, algo, max_ctas, stream, per_cta);
+    case 7: return launch_allreduce_n<7>(a, algo, max_ctas, stream, per_cta);
+    case 8: return launch_allreduce_n<8>(a, algo, max_ctas, stream, per_cta);
     default: return set_error(MGW_EINVAL, "world %d outside 1..%d", a.world, kMaxRanks);
   }
 }

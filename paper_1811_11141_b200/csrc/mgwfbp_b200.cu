@@ -87,6 +87,7 @@ struct mgw_comm {
   int64_t oneshot_max_bytes = 1 << 20;  // set per world in mgw_comm_create
   int64_t ll_max_bytes = kLLElems * 4;  // 256 KB: the whole LL area
   int max_ctas = 2 * kSMs;
+  int64_t vec_per_cta[2] = {0, 0};      // tuning: 16-B slots per CTA (one-shot, two-shot); 0 = default
 };
 
 struct mgw_sched {
@@ -136,6 +137,10 @@ ArArgs make_args(const mgw_comm* c, int64_t n) {
   return a;
 }
 
+int comm_launch_allreduce(const mgw_comm* c, const ArArgs& a, int algo, cudaStream_t stream) {
+  return launch_allreduce(a, algo, c->max_ctas, stream, c->vec_per_cta);
+}
+
 int pick_algo(const mgw_comm* c, int64_t n, int algo) {
   if (algo != MGW_ALGO_AUTO) return algo;
   return n * 4 <= c->oneshot_max_bytes ? MGW_ALGO_ONESHOT : MGW_ALGO_TWOSHOT;
@@ -159,7 +164,7 @@ int comm_allreduce(mgw_comm* c, int64_t n, int algo, cudaStream_t stream, uint64
   if (!c->peers_open) return set_error(MGW_EINVAL, "peers not opened (call mgw_comm_open_peers)");
   ArArgs a = make_args(c, n);
   a.stamp = stamp;
-  return launch_allreduce(a, pick_algo(c, n, algo), c->max_ctas, stream);
+  return comm_launch_allreduce(c, a, pick_algo(c, n, algo), stream);
 }
 
 int comm_pack(mgw_comm* c, const Row* host_rows, const Row* dev_rows, int n_rows, int64_t n, float scale,
@@ -202,7 +207,7 @@ int comm_allreduce_fused(mgw_comm* c, const Row* host_rows, const Row* dev_rows,
     }
     return launch_ll(l, c->max_ctas, stream);
   }
-  return launch_fused(f, chosen, c->max_ctas, stream);
+  return launch_fused(f, chosen, c->max_ctas, stream, c->vec_per_cta);
 }
 
 const mgw_table_t* as_table(const void* t) { return static_cast<const mgw_table_t*>(t); }
@@ -424,6 +429,12 @@ int mgw_comm_set_oneshot_max(mgw_comm* c, int64_t bytes) {
 int mgw_comm_set_ll_max(mgw_comm* c, int64_t bytes) {
   if (!c || bytes < 0 || bytes > kLLElems * 4) return set_error(MGW_EINVAL, "LL threshold must lie in 0..%lld B", (long long)(kLLElems * 4));
   c->ll_max_bytes = bytes;
+  return MGW_OK;
+}
+
+int mgw_comm_set_tuning(mgw_comm* c, int key, int64_t value) {
+  if (!c || key < 0 || key > 1 || value < 0) return set_error(MGW_EINVAL, "bad tuning key/value");
+  c->vec_per_cta[key] = value;
   return MGW_OK;
 }
 
