@@ -218,6 +218,95 @@ __global__ void __launch_bounds__(kThreads, 2) fused_oneshot_kernel(const __grid
   finish_call(a);
 }
 
+// Interleaved walk over chunk b of several parts: slot i of every part is handled in the
+// same loop trip, so the parts' memory streams are in flight together (one round trip
+// per trip instead of one per part).  `cur` are per-part monotone row cursors.
+template <int N>
+struct PartChunks {
+  int64_t lo[N];   // first 16-B slot of chunk b in part p
+  int64_t len[N];  // slots of chunk b in part p
+  int64_t longest;
+};
+
+template <int N>
+__device__ __forceinline__ void part_chunks(int64_t nv, int b, int G, PartChunks<N>& pc) {
+  pc.longest = 0;
+#pragma unroll
+  for (int p = 0; p < N; ++p) {
+    const int64_t q0 = part_begin(p, nv, N), q1 = part_begin(p + 1, nv, N);
+    const int64_t per = (q1 - q0 + G - 1) / G;
+    const int64_t c0 = q0 + (int64_t)b * per;
+    const int64_t c1 = c0 + per < q1 ? c0 + per : q1;
+    pc.lo[p] = c0;
+    pc.len[p] = c1 > c0 ? c1 - c0 : 0;
+    pc.longest = pc.len[p] > pc.longest ? pc.len[p] : pc.longest;
+  }
+}
+
+// pack chunk b of every part into my slot, parts interleaved
+template <int N>
+__device__ void fused_pack_parts(const FusedArgs& f, float* slot, const PartChunks<N>& pc) {
+  const float scale = f.scale;
+  const bool scaled = scale != 1.0f;
+  int cur[N];
+#pragma unroll
+  for (int p = 0; p < N; ++p) cur[p] = fused_row_covering(f, (pc.lo[p] + (threadIdx.x < pc.len[p] ? threadIdx.x : 0)) << 2);
+  for (int64_t i = threadIdx.x; i < pc.longest; i += kThreads) {
+    float4 x[N];
+    float* tp[N];
+    bool fast[N];
+#pragma unroll
+    for (int p = 0; p < N; ++p) {
+      fast[p] = false;
+      if (i < pc.len[p]) {
+        const int64_t e = (pc.lo[p] + i) << 2;
+        tp[p] = fused_tensor(f, cur[p], e, fast[p]);
+        if (fast[p]) x[p] = *reinterpret_cast<const float4*>(tp[p]);
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < N; ++p) {
+      if (i >= pc.len[p]) continue;
+      const int64_t e = (pc.lo[p] + i) << 2;
+      if (fast[p]) {
+        *reinterpret_cast<float4*>(slot + e) = scaled ? fmul4(x[p], scale) : x[p];
+      } else {
+        for (int j = 0; j < 4; ++j) {
+          const float y = *fused_tensor1(f, cur[p], e + j);
+          slot[e + j] = scaled ? __fmul_rn(y, scale) : y;
+        }
+      }
+    }
+  }
+}
+
+// copy chunk b of every peer's reduced part from its slot into my tensors, interleaved
+template <int N>
+__device__ void fused_scatter_parts(const FusedArgs& f, const float* const* in, int me, const PartChunks<N>& pc) {
+  int cur[N];
+#pragma unroll
+  for (int p = 0; p < N; ++p) cur[p] = fused_row_covering(f, (pc.lo[p] + (threadIdx.x < pc.len[p] ? threadIdx.x : 0)) << 2);
+  for (int64_t i = threadIdx.x; i < pc.longest; i += kThreads) {
+    float4 x[N];
+#pragma unroll
+    for (int p = 0; p < N; ++p)
+      if (p != me && i < pc.len[p]) x[p] = __ldcg(reinterpret_cast<const float4*>(in[p]) + pc.lo[p] + i);
+#pragma unroll
+    for (int p = 0; p < N; ++p) {
+      if (p == me || i >= pc.len[p]) continue;
+      const int64_t e = (pc.lo[p] + i) << 2;
+      bool fast;
+      float* tp = fused_tensor(f, cur[p], e, fast);
+      if (fast) {
+        *reinterpret_cast<float4*>(tp) = x[p];
+      } else {
+        const float y[4] = {x[p].x, x[p].y, x[p].z, x[p].w};
+        for (int j = 0; j < 4; ++j) *fused_tensor1(f, cur[p], e + j) = y[j];
+      }
+    }
+  }
+}
+
 template <int N>
 __global__ void __launch_bounds__(kThreads, 2) fused_twoshot_kernel(const __grid_constant__ FusedArgs f) {
   constexpr int U = Unroll<N>::value;
@@ -231,43 +320,28 @@ __global__ void __launch_bounds__(kThreads, 2) fused_twoshot_kernel(const __grid
   const int b = blockIdx.x, G = gridDim.x;
   const int64_t nv = a.n >> 2;
   const bool last = b == G - 1;
+  const int64_t tail0 = nv << 2;
   float* mine = const_cast<float*>(s_in[me]);
-  // chunk b of every part p: [c0(p), c1(p))
-  auto chunk = [&](int p, int64_t& c0, int64_t& c1) {
-    const int64_t q0 = part_begin(p, nv, N), q1 = part_begin(p + 1, nv, N);
-    const int64_t per = (q1 - q0 + G - 1) / G;
-    c0 = q0 + (int64_t)b * per;
-    c1 = c0 + per < q1 ? c0 + per : q1;
-    if (c1 < c0) c1 = c0;
-  };
+  __shared__ PartChunks<N> pc;  // CTA-uniform: keep it out of the registers
+  if (threadIdx.x == 0) part_chunks<N>(nv, b, G, pc);
+  __syncthreads();
   if (!(a.flags & (kSkipPhase1 | kSkipPack))) {
-    for (int p = 0; p < N; ++p) {
-      int64_t c0, c1;
-      chunk(p, c0, c1);
-      const bool tail = last && p == N - 1;
-      fused_pack_range(f, mine, c0, c1, tail ? nv << 2 : 0, tail ? a.n : 0);
-    }
+    fused_pack_parts<N>(f, mine, pc);
+    if (last) fused_pack_range(f, mine, 0, 0, tail0, a.n);  // the n % 4 tail (part N-1)
   }
   int status = MGW_DEV_OK;
   if (!(a.flags & kSkipPhase1)) {
     if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, (uint32_t)a.n, a);
     if (status == MGW_DEV_OK) {
-      int64_t c0, c1;
-      chunk(me, c0, c1);
-      fused_reduce_range<N, U>(f, s_in, s_end, c0, c1, mine);
-      if (last && me == N - 1) fused_reduce_tail<N>(f, s_in, s_end, nv << 2, a.n, mine);
+      fused_reduce_range<N, U>(f, s_in, s_end, pc.lo[me], pc.lo[me] + pc.len[me], mine);
+      if (last && me == N - 1) fused_reduce_tail<N>(f, s_in, s_end, tail0, a.n, mine);
     }
   }
   if (status == MGW_DEV_OK && !(a.flags & kSkipPhase2)) {
     if (!(a.flags & kNoBarrier)) status = cta_barrier(a.mid, parity, epoch, (uint32_t)a.n, a);
     if (status == MGW_DEV_OK) {
-      for (int kk = 1; kk < N; ++kk) {
-        const int p = me + kk >= N ? me + kk - N : me + kk;
-        int64_t c0, c1;
-        chunk(p, c0, c1);
-        const bool tail = last && p == N - 1;
-        fused_scatter_range(f, s_in[p], c0, c1, tail ? nv << 2 : 0, tail ? a.n : 0);
-      }
+      fused_scatter_parts<N>(f, s_in, me, pc);
+      if (last && me != N - 1) fused_scatter_range(f, s_in[N - 1], 0, 0, tail0, a.n);
     }
   }
   finish_call(a);
