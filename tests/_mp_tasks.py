@@ -59,3 +59,38 @@ def emulate_task(config, session, *, profile, plan, fused, graph):
     from paper_1811_11141_b200 import run_emulation
 
     return run_emulation(profile, plan, config, session, 3, warmup=1, fused=fused, graph=graph)
+
+
+def every_algorithm_task(config, session, *, arrays):
+    """Each algorithm (fused LL / one-shot / two-shot, unfused one-shot / two-shot) on the
+    golden inputs through the real IPC path; returns the reduced bits per (size, algo)."""
+    import ctypes
+
+    import torch
+
+    from paper_1811_11141_b200 import _native
+
+    out = {}
+    h = session.stream.cuda_stream
+    with torch.cuda.device(session.device), torch.cuda.stream(session.stream):
+        for key, vals in arrays[config.rank].items():
+            n = vals.size
+            for name, algo in (("ll", _native.ALGO_LL), ("one", _native.ALGO_ONESHOT), ("two", _native.ALGO_TWOSHOT)):
+                t = torch.from_numpy(vals.copy()).to(session.device)
+                table = _native.DeviceTable([(t.data_ptr(), n, 0)])
+                _native.call("mgw_allreduce_fused", session.comm, table.ptr, 1, n, ctypes.c_float(1.0), algo, h)
+                session.stream.synchronize()
+                session.raise_if_failed()
+                out[f"{key}_fused_{name}"] = t.cpu().numpy()
+                table.close()
+            for name, algo in (("one", _native.ALGO_ONESHOT), ("two", _native.ALGO_TWOSHOT)):
+                t = torch.from_numpy(vals.copy()).to(session.device)
+                table = _native.DeviceTable([(t.data_ptr(), n, 0)])
+                _native.call("mgw_comm_pack", session.comm, table.ptr, 1, n, ctypes.c_float(1.0), h)
+                _native.call("mgw_allreduce", session.comm, n, algo, h)
+                _native.call("mgw_unpack", table.ptr, 1, session.result_ptr(), n, h)
+                session.stream.synchronize()
+                session.raise_if_failed()
+                out[f"{key}_plain_{name}"] = t.cpu().numpy()
+                table.close()
+    return out

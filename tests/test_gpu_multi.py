@@ -71,6 +71,20 @@ def test_random_payloads_bit_exact_vs_reference_ring():
                 assert np.array_equal(results[r][f"n{size}_tensor"].view("<u4"), want)
 
 
+def test_every_algorithm_bit_exact_over_ipc():
+    """LL, one-shot and two-shot (fused and unfused) all reproduce the reference ring's bits."""
+    g = golden_ring()
+    for n in _worlds():
+        arrays = [{f"n{size}": g[f"in_N{n}_n{size}_r{r}"] for size in (1, 17, 1001, 4099)} for r in range(n)]
+        results = run_workers(n, partial(_mp_tasks.every_algorithm_task, arrays=arrays))
+        for size in (1, 17, 1001, 4099):
+            want = g[f"out_N{n}_n{size}"].view("<u4")
+            for r in range(n):
+                for variant in ("fused_ll", "fused_one", "fused_two", "plain_one", "plain_two"):
+                    got = results[r][f"n{size}_{variant}"].view("<u4")
+                    assert np.array_equal(got, want), (n, size, r, variant)
+
+
 def test_bench_local_measurement_shape():
     ms = bench_local(2, [4096, 65536, 1 << 22], repeats=3, warmups=2)
     assert [m.nbytes for m in ms] == [4096, 65536, 1 << 22]
