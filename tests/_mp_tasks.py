@@ -94,3 +94,31 @@ def every_algorithm_task(config, session, *, arrays):
                 out[f"{key}_plain_{name}"] = t.cpu().numpy()
                 table.close()
     return out
+
+
+def autograd_task(config, session):
+    """Two ranks with different data: merged-gradient sync leaves bit-identical averaged
+    gradients that equal the oracle-ordered sum of the per-rank gradients."""
+    import numpy as np
+    import torch
+
+    from oracle import ring_oracle
+    from paper_1811_11141_b200 import MergePlan
+    from paper_1811_11141_b200.autograd import MergedGradientSync, trainable_parameters
+
+    torch.manual_seed(0)
+    net = torch.nn.Sequential(torch.nn.Linear(64, 257), torch.nn.Tanh(), torch.nn.Linear(257, 10)).to(session.device)
+    g = torch.Generator(device=session.device).manual_seed(1000 + config.rank)
+    x = torch.randn(16, 64, device=session.device, generator=g)
+    params = trainable_parameters(net)
+    net.zero_grad(set_to_none=False)
+    net(x).square().mean().backward()
+    local = [p.grad.detach().cpu().numpy().copy() for p in params]
+    sync = MergedGradientSync(params, MergePlan(frozenset({3, 4}), 4), comm=session.comm, world=config.n_workers)
+    net.zero_grad(set_to_none=False)
+    net(x).square().mean().backward()
+    sync.finish()
+    torch.cuda.synchronize()
+    session.raise_if_failed()
+    sync.close()
+    return local, [p.grad.detach().cpu().numpy() for p in params]

@@ -85,6 +85,22 @@ def test_every_algorithm_bit_exact_over_ipc():
                     assert np.array_equal(got, want), (n, size, r, variant)
 
 
+def test_autograd_merged_sync_matches_reference_fold():
+    import numpy as np
+    from oracle import ring_oracle
+
+    n = max(_worlds())
+    results = run_workers(n, _mp_tasks.autograd_task)
+    groups = [(1, 2), (3, 4)]  # plan {3, 4} over 4 tensors: [1..2] [3..4]
+    for low, high in groups:
+        buckets = [np.concatenate([results[r][0][layer - 1].reshape(-1) for layer in range(high, low - 1, -1)])
+                   for r in range(n)]
+        want = ring_oracle.ring_allreduce(buckets)[0]
+        for r in range(n):
+            got = np.concatenate([results[r][1][layer - 1].reshape(-1) for layer in range(high, low - 1, -1)])
+            assert np.array_equal(got.view("<u4"), want.view("<u4"))
+
+
 def test_bench_local_measurement_shape():
     ms = bench_local(2, [4096, 65536, 1 << 22], repeats=3, warmups=2)
     assert [m.nbytes for m in ms] == [4096, 65536, 1 << 22]

@@ -4,7 +4,7 @@ matches eager execution."""
 
 import pytest
 
-from paper_1811_11141_b200 import CommModel, MergePlan, find_merge_plan, resnet50_like, simulate_mgwfbp, synth_profile
+from paper_1811_11141_b200 import CommModel, MergePlan, find_merge_plan, resnet50_like, simulate_mgwfbp, synth_profile  # noqa: F401
 from paper_1811_11141_b200.overlap import OverlappedIteration
 
 pytestmark = pytest.mark.gpu
@@ -80,3 +80,30 @@ def test_launch_count_reported(torch_cuda):
         assert it.launches_per_iteration == 2 + 4 * profile.num_layers
     finally:
         it.close()
+
+
+def test_autograd_sync_single_gpu(torch_cuda):
+    """Hooks fire for every parameter, groups complete, and the scale is applied once."""
+    torch = torch_cuda
+    from paper_1811_11141_b200.autograd import MergedGradientSync, measure_profile, trainable_parameters
+
+    torch.manual_seed(0)
+    net = torch.nn.Sequential(torch.nn.Linear(64, 128), torch.nn.ReLU(), torch.nn.Linear(128, 10)).cuda()
+    x = torch.randn(32, 64, device="cuda")
+    step = lambda: net(x).square().mean()  # noqa: E731
+    params = trainable_parameters(net)
+    prof = measure_profile(net, step, repeats=2)
+    assert prof.num_layers == 4 and prof.total_params == sum(p.numel() for p in params)
+    net.zero_grad(set_to_none=False)
+    step().backward()
+    want = [p.grad.clone() * 0.5 for p in params]
+    sync = MergedGradientSync(params, MergePlan(frozenset({2, 4}), 4), scale=0.5)
+    try:
+        net.zero_grad(set_to_none=False)
+        step().backward()
+        sync.finish()
+        assert sync.launched == 2
+        for p, w in zip(params, want):
+            assert torch.equal(p.grad, w)
+    finally:
+        sync.close()
