@@ -46,7 +46,7 @@ class MergedGradientSync:
     """
 
     def __init__(self, params, plan: MergePlan, *, comm=None, world: int = 1, scale: float = 1.0,
-                 algo: int = _native.ALGO_AUTO, sync_after_backward: bool = False):
+                 algo: int = _native.ALGO_AUTO, sync_after_backward: bool = False, max_ctas: int | None = None):
         import torch
 
         self.torch = torch
@@ -59,6 +59,9 @@ class MergedGradientSync:
         self.plan = plan
         self.comm, self.world, self.scale, self.algo = comm, world, float(scale), algo
         self.sync_after_backward = sync_after_backward
+        if max_ctas is not None and comm is not None:
+            # overlapped collectives share the SMs with backward: bound their CTA budget
+            _native.call("mgw_comm_set_max_ctas", comm, int(max_ctas))
         self.groups = plan.groups()  # ascending (low, high)
         self.group_of = {}
         for gid, (low, high) in enumerate(self.groups):

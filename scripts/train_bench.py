@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--model", default="resnet50")
+    ap.add_argument("--ctas", default="296,64,32,16", help="CTA caps to try for the overlapped collectives")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -104,28 +105,33 @@ def main():
         opt.step()
 
     results["compute_only"] = timed(local_step, "compute_only")
-    for name in ("wfbp", "mgwfbp", "synceasgd"):
-        sync = MergedGradientSync(params, plans[name], comm=comm, world=world, scale=1.0 / world,
-                                  sync_after_backward=name == "synceasgd")
+    for cap in [int(c) for c in args.ctas.split(",")]:
+        for name in ("wfbp", "mgwfbp", "synceasgd"):
+            sync = MergedGradientSync(params, plans[name], comm=comm, world=world, scale=1.0 / world,
+                                      sync_after_backward=name == "synceasgd", max_ctas=cap)
 
-        def synced_step():
-            opt.zero_grad(set_to_none=False)
-            step().backward()
-            sync.finish()
-            opt.step()
+            def synced_step():
+                opt.zero_grad(set_to_none=False)
+                step().backward()
+                sync.finish()
+                opt.step()
 
-        results[name] = timed(synced_step, name)
-        results[name].update({"groups": len(plans[name].groups()), "launched_per_step": sync.launched // (args.warmup + args.steps),
-                              "predicted_t_iter_ms": round(predicted[name].t_iter * 1e3, 4),
-                              "predicted_t_c_no_us": round(predicted[name].t_c_no * 1e6, 2)})
-        # consistency: every rank holds bit-identical reduced gradients
-        if world > 1:
-            flat = torch.cat([p.grad.reshape(-1) for p in params])
-            lo, hi = flat.clone(), flat.clone()
-            dist.all_reduce(lo, op=dist.ReduceOp.MIN)
-            dist.all_reduce(hi, op=dist.ReduceOp.MAX)
-            results[name]["ranks_bit_identical"] = bool(torch.equal(lo, hi))
-        sync.close()
+            key = f"{name}_ctas{cap}"
+            results[key] = timed(synced_step, key)
+            results[key].update({"groups": len(plans[name].groups()),
+                                 "launched_per_step": sync.launched // (args.warmup + args.steps),
+                                 "predicted_t_iter_ms": round(predicted[name].t_iter * 1e3, 4),
+                                 "predicted_t_c_no_us": round(predicted[name].t_c_no * 1e6, 2)})
+            # consistency: every rank holds bit-identical reduced gradients
+            if world > 1:
+                flat = torch.cat([p.grad.reshape(-1) for p in params])
+                lo, hi = flat.clone(), flat.clone()
+                dist.all_reduce(lo, op=dist.ReduceOp.MIN)
+                dist.all_reduce(hi, op=dist.ReduceOp.MAX)
+                results[key]["ranks_bit_identical"] = bool(torch.equal(lo, hi))
+            sync.close()
+        if world == 1:
+            break
     if world > 1:
         ddp = torch.nn.parallel.DistributedDataParallel(net, device_ids=[local], gradient_as_bucket_view=True,
                                                       broadcast_buffers=False)

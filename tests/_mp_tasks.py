@@ -97,26 +97,34 @@ def every_algorithm_task(config, session, *, arrays):
 
 
 def autograd_task(config, session):
-    """Two ranks with different data: merged-gradient sync leaves bit-identical averaged
-    gradients that equal the oracle-ordered sum of the per-rank gradients."""
-    import numpy as np
+    """Two+ ranks with different data: merged-gradient sync leaves averaged gradients equal,
+    bit for bit, to the oracle ring over the per-rank gradients.  The model is elementwise so
+    its backward is deterministic (cuBLAS split-K GEMMs are not, run to run)."""
     import torch
 
-    from oracle import ring_oracle
     from paper_1811_11141_b200 import MergePlan
     from paper_1811_11141_b200.autograd import MergedGradientSync, trainable_parameters
 
-    torch.manual_seed(0)
-    net = torch.nn.Sequential(torch.nn.Linear(64, 257), torch.nn.Tanh(), torch.nn.Linear(257, 10)).to(session.device)
+    class Elementwise(torch.nn.Module):
+        def __init__(self):
+            super().__init__()
+            g = torch.Generator().manual_seed(0)
+            self.w = torch.nn.ParameterList(
+                [torch.nn.Parameter(torch.randn(n, generator=g)) for n in (16448, 257, 2570, 10)])
+
+        def forward(self, xs):
+            return sum((w * x).sin().square().sum() for w, x in zip(self.w, xs))
+
+    net = Elementwise().to(session.device)
     g = torch.Generator(device=session.device).manual_seed(1000 + config.rank)
-    x = torch.randn(16, 64, device=session.device, generator=g)
+    xs = [torch.randn(w.numel(), device=session.device, generator=g) for w in net.w]
     params = trainable_parameters(net)
     net.zero_grad(set_to_none=False)
-    net(x).square().mean().backward()
+    net(xs).backward()
     local = [p.grad.detach().cpu().numpy().copy() for p in params]
     sync = MergedGradientSync(params, MergePlan(frozenset({3, 4}), 4), comm=session.comm, world=config.n_workers)
     net.zero_grad(set_to_none=False)
-    net(x).square().mean().backward()
+    net(xs).backward()
     sync.finish()
     torch.cuda.synchronize()
     session.raise_if_failed()
