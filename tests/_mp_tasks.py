@@ -96,7 +96,7 @@ def every_algorithm_task(config, session, *, arrays):
     return out
 
 
-def autograd_task(config, session):
+def autograd_task(config, session, *, algo=0, deferred=False):
     """Two+ ranks with different data: merged-gradient sync leaves averaged gradients equal,
     bit for bit, to the oracle ring over the per-rank gradients.  The model is elementwise so
     its backward is deterministic (cuBLAS split-K GEMMs are not, run to run)."""
@@ -122,11 +122,48 @@ def autograd_task(config, session):
     net.zero_grad(set_to_none=False)
     net(xs).backward()
     local = [p.grad.detach().cpu().numpy().copy() for p in params]
-    sync = MergedGradientSync(params, MergePlan(frozenset({3, 4}), 4), comm=session.comm, world=config.n_workers)
     net.zero_grad(set_to_none=False)
     net(xs).backward()
+    again = [p.grad.detach().cpu().numpy().copy() for p in params]
+    sync = MergedGradientSync(params, MergePlan(frozenset({2, 4}), 4), comm=session.comm, world=config.n_workers,
+                              algo=algo, sync_after_backward=deferred)
+    net.zero_grad(set_to_none=False)
+    net(xs).backward()
+    if deferred:  # groups not launched yet: the synced backward's own gradients
+        torch.cuda.synchronize()
+        third = [p.grad.detach().cpu().numpy().copy() for p in params]
+        local = third
     sync.finish()
     torch.cuda.synchronize()
     session.raise_if_failed()
     sync.close()
-    return local, [p.grad.detach().cpu().numpy() for p in params]
+    deterministic = all((a.view("<u4") == b.view("<u4")).all() for a, b in zip(local, again))
+    return local, [p.grad.detach().cpu().numpy() for p in params], deterministic
+
+
+def sizes_task(config, session, *, sizes, algos):
+    """Seeded random payloads of several sizes split into two rows, through each fused
+    algorithm; returns inputs and outputs for a host-side oracle comparison."""
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    from paper_1811_11141_b200 import _native
+
+    out = {}
+    h = session.stream.cuda_stream
+    with torch.cuda.device(session.device), torch.cuda.stream(session.stream):
+        for n in sizes:
+            vals = np.random.default_rng(7 * n + config.rank).standard_normal(n).astype("<f4")
+            out[("in", n)] = vals
+            for algo in algos:
+                a = torch.from_numpy(vals[:257].copy()).to(session.device)
+                b = torch.from_numpy(vals[257:].copy()).to(session.device)
+                table = _native.DeviceTable([(a.data_ptr(), 257, 0), (b.data_ptr(), n - 257, 257)])
+                _native.call("mgw_allreduce_fused", session.comm, table.ptr, 2, n, ctypes.c_float(1.0), algo, h)
+                session.stream.synchronize()
+                session.raise_if_failed()
+                out[(algo, n)] = np.concatenate([a.cpu().numpy(), b.cpu().numpy()])
+                table.close()
+    return out
