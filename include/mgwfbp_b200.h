@@ -138,6 +138,12 @@ int mgw_time_exchange(mgw_comm* comm, const void* dev_table, int n_rows, int64_t
 int mgw_allreduce_emulated(float* const* ins, float* const* outs, int world, int64_t n_elem, int algo,
                            void* stream);
 
+/* autograd hook path: record `event` on compute_stream, make comm_stream wait on it, then
+ * mgw_allreduce_fused on comm_stream -- one call per ready merge group */
+int mgw_group_launch(mgw_comm* comm, const void* table, int n_rows, int64_t n_elem, float scale, int algo,
+                     void* compute_stream, void* comm_stream, void* event);
+int mgw_event_create(void** event);
+int mgw_event_destroy(void* event);
 int mgw_allreduce_fused_emulated(void* const* tables, float* const* slots, int world, int64_t n_elem, float scale,
                                  int algo, void* stream);
 

@@ -72,6 +72,9 @@ _SIGNATURES = {
     "mgw_comm_pack": ([_P, _P, _I, _I64, ctypes.c_float, _P], _I),
     "mgw_allreduce": ([_P, _I64, _I, _P], _I),
     "mgw_allreduce_fused": ([_P, _P, _I, _I64, ctypes.c_float, _I, _P], _I),
+    "mgw_group_launch": ([_P, _P, _I, _I64, ctypes.c_float, _I, _P, _P, _P], _I),
+    "mgw_event_create": ([ctypes.POINTER(_P)], _I),
+    "mgw_event_destroy": ([_P], _I),
     "mgw_allreduce_fused_emulated": ([ctypes.POINTER(_P), ctypes.POINTER(_P), _I, _I64, ctypes.c_float, _I, _P], _I),
     "mgw_comm_error": ([_P, ctypes.POINTER(_I)], _I),
     "mgw_comm_calls": ([_P, ctypes.POINTER(_I64)], _I),

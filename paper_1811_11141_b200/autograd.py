@@ -70,6 +70,7 @@ class MergedGradientSync:
         self.size = [high - low + 1 for low, high in self.groups]
         self.count = [0] * len(self.groups)
         self.tables: dict[int, tuple] = {}
+        self.events: dict[int, int] = {}
         self.stream = torch.cuda.Stream()
         self.launched = 0
         self.pending: list[int] = []
@@ -94,16 +95,26 @@ class MergedGradientSync:
             self.tables[gid] = cached
         return cached[1], cached[2]
 
+    def _event(self, gid):
+        ev = self.events.get(gid)
+        if ev is None:
+            handle = ctypes.c_void_p()
+            _native.call("mgw_event_create", ctypes.byref(handle))
+            ev = self.events[gid] = handle.value
+        return ev
+
     def _launch(self, gid):
         torch = self.torch
         table, n = self._table(gid)
-        ev = torch.cuda.Event()
-        ev.record()  # the backward (current) stream: the group's gradients are written
-        self.stream.wait_event(ev)
         if self.comm is not None and self.world > 1:
-            _native.call("mgw_allreduce_fused", self.comm, table.ptr, table.n, n, ctypes.c_float(self.scale),
-                         self.algo, self.stream.cuda_stream)
+            # one native call: event on the backward (current) stream -> comm stream waits
+            # -> fused pack / all-reduce / unpack of the group
+            _native.call("mgw_group_launch", self.comm, table.ptr, table.n, n, ctypes.c_float(self.scale), self.algo,
+                         torch.cuda.current_stream().cuda_stream, self.stream.cuda_stream, self._event(gid))
         elif self.scale != 1.0:
+            ev = torch.cuda.Event()
+            ev.record()
+            self.stream.wait_event(ev)
             with torch.cuda.stream(self.stream):
                 for layer in range(self.groups[gid][0], self.groups[gid][1] + 1):
                     self.params[layer - 1].grad.mul_(self.scale)
@@ -135,6 +146,9 @@ class MergedGradientSync:
         for _, table, _ in self.tables.values():
             table.close()
         self.tables.clear()
+        for ev in self.events.values():
+            _native.lib().mgw_event_destroy(ev)
+        self.events.clear()
 
 
 def measure_profile(model, step, *, name="measured", repeats=5) -> ModelProfile:

@@ -495,6 +495,31 @@ int mgw_allreduce_fused(mgw_comm* c, const void* table, int n_rows, int64_t n_el
   return comm_allreduce_fused(c, t->host.data(), t->dev, n_rows, n_elem, scale, algo, static_cast<cudaStream_t>(stream));
 }
 
+int mgw_event_create(void** event) {
+  if (!event) return set_error(MGW_EINVAL, "event is null");
+  cudaEvent_t e = nullptr;
+  MGW_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  *event = e;
+  return MGW_OK;
+}
+
+int mgw_event_destroy(void* event) {
+  if (event) MGW_CUDA(cudaEventDestroy(static_cast<cudaEvent_t>(event)));
+  return MGW_OK;
+}
+
+// One call per ready merge group (autograd hook path): the comm stream waits for
+// everything enqueued so far on the compute stream, then runs the fused exchange.
+int mgw_group_launch(mgw_comm* c, const void* table, int n_rows, int64_t n_elem, float scale, int algo,
+                     void* compute_stream, void* comm_stream, void* event) {
+  if (!event) return set_error(MGW_EINVAL, "event is null");
+  cudaStream_t cs = static_cast<cudaStream_t>(compute_stream);
+  cudaStream_t ms = static_cast<cudaStream_t>(comm_stream);
+  MGW_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(event), cs));
+  MGW_CUDA(cudaStreamWaitEvent(ms, static_cast<cudaEvent_t>(event), 0));
+  return mgw_allreduce_fused(c, table, n_rows, n_elem, scale, algo, ms);
+}
+
 int mgw_comm_error(mgw_comm* c, int* code) {
   if (!c || !code) return set_error(MGW_EINVAL, "bad arguments");
   MGW_CUDA(cudaSetDevice(c->device));
