@@ -59,6 +59,7 @@ extern "C" {
 #define MGW_ALGO_ONESHOT 1
 #define MGW_ALGO_TWOSHOT 2
 #define MGW_ALGO_LL 3 /* push-based low-latency one-shot (fused path only, <= 65,536 elements) */
+#define MGW_ALGO_NVLS 4 /* NVSwitch in-switch reduction (opt-in; fp32 sum, NOT the reference fold order) */
 
 /* schedule flags */
 #define MGW_SCHED_FILL 1u  /* "backward" writes fill_values into each layer before its deadline */
@@ -137,6 +138,16 @@ int mgw_time_exchange(mgw_comm* comm, const void* dev_table, int n_rows, int64_t
 /* ---- emulated ranks on one device (test path; no barriers) ------------ */
 int mgw_allreduce_emulated(float* const* ins, float* const* outs, int world, int64_t n_elem, int algo,
                            void* stream);
+
+/* ---- NVLS (opt-in): one multicast object per communicator --------------
+ * rank 0 mgw_nvls_create -> pass the fd (SCM_RIGHTS) -> others mgw_nvls_import ->
+ * all mgw_nvls_add_device -> barrier -> all mgw_nvls_bind -> barrier */
+int mgw_nvls_supported(int device, int* ok);
+int mgw_nvls_create(mgw_comm* comm, int64_t bytes, int* fd_out);
+int mgw_nvls_import(mgw_comm* comm, int fd, int64_t bytes);
+int mgw_nvls_add_device(mgw_comm* comm);
+int mgw_nvls_bind(mgw_comm* comm);
+int mgw_comm_set_nvls_min(mgw_comm* comm, int64_t bytes);
 
 /* autograd hook path: record `event` on compute_stream, make comm_stream wait on it, then
  * mgw_allreduce_fused on comm_stream -- one call per ready merge group */

@@ -18,7 +18,7 @@ LIB_DIR = pathlib.Path(__file__).resolve().parent / "_lib"
 LIB_PATH = LIB_DIR / "libmgwfbp_b200.so"
 
 MGW_OK, MGW_EINVAL, MGW_EPROTO, MGW_ECUDA = 0, 1, 2, 3
-ALGO_AUTO, ALGO_ONESHOT, ALGO_TWOSHOT, ALGO_LL = 0, 1, 2, 3
+ALGO_AUTO, ALGO_ONESHOT, ALGO_TWOSHOT, ALGO_LL, ALGO_NVLS = 0, 1, 2, 3, 4
 SCHED_FILL, SCHED_GRAPH, SCHED_HOSTIO, SCHED_FUSED = 1, 2, 4, 8
 DEV_OK, DEV_LENGTH_MISMATCH, DEV_TIMEOUT, DEV_PEER_ABORT = 0, 1, 2, 3
 IPC_HANDLE_BYTES = 64
@@ -72,6 +72,12 @@ _SIGNATURES = {
     "mgw_comm_pack": ([_P, _P, _I, _I64, ctypes.c_float, _P], _I),
     "mgw_allreduce": ([_P, _I64, _I, _P], _I),
     "mgw_allreduce_fused": ([_P, _P, _I, _I64, ctypes.c_float, _I, _P], _I),
+    "mgw_nvls_supported": ([_I, ctypes.POINTER(_I)], _I),
+    "mgw_nvls_create": ([_P, _I64, ctypes.POINTER(_I)], _I),
+    "mgw_nvls_import": ([_P, _I, _I64], _I),
+    "mgw_nvls_add_device": ([_P], _I),
+    "mgw_nvls_bind": ([_P], _I),
+    "mgw_comm_set_nvls_min": ([_P, _I64], _I),
     "mgw_group_launch": ([_P, _P, _I, _I64, ctypes.c_float, _I, _P, _P, _P], _I),
     "mgw_event_create": ([ctypes.POINTER(_P)], _I),
     "mgw_event_destroy": ([_P], _I),

@@ -68,6 +68,7 @@ __all__ = [
     "emulate_local",
     "open_ring",
     "open_session_dist",
+    "enable_nvls",
     "rendezvous",
     "ring_allreduce",
     "run_emulation",
@@ -721,6 +722,65 @@ def open_session_dist(
         _native.lib().mgw_comm_destroy(comm)
         raise
     return config, session
+
+
+def enable_nvls(session: RingSession, nbytes: int, *, min_bytes: int = 0, group=None) -> None:
+    """Opt-in NVSwitch multicast (NVLS) exchange on a torchrun-launched session.
+
+    Rank 0 creates a multicast object of ``nbytes`` and hands its POSIX fd to every
+    other rank over an abstract Unix socket (SCM_RIGHTS); every rank adds its device,
+    then binds and maps its copy.  Afterwards ``MGW_ALGO_NVLS`` (or AUTO for buckets
+    >= ``min_bytes`` when non-zero) reduces in the switch.  NVLS sums in the switch's
+    order: identical on every rank and within fp32 rounding of the exact sum, but not
+    bit-identical to the reference ring -- so it is never on by default.
+    """
+    import os
+    import secrets
+
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    ok = ctypes.c_int()
+    _native.call("mgw_nvls_supported", session.config.device_index, ctypes.byref(ok))
+    flags: list = [None] * world
+    dist.all_gather_object(flags, bool(ok.value), group=group)
+    if not all(flags):
+        raise RuntimeError("NVLS (CUDA multicast) is not supported on every device of the group")
+    box = [secrets.token_hex(8) if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0, group=group)
+    name = "\0mgwfbp-nvls-" + box[0]
+    comm = session.comm
+    if rank == 0:
+        fd = ctypes.c_int(-1)
+        _native.call("mgw_nvls_create", comm, int(nbytes), ctypes.byref(fd))
+        srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+        srv.bind(name)
+        srv.listen(world)
+        dist.barrier(group=group)
+        try:
+            for _ in range(world - 1):
+                conn, _ = srv.accept()
+                with conn:
+                    socket.send_fds(conn, [b"f"], [fd.value])
+        finally:
+            srv.close()
+            os.close(fd.value)
+    else:
+        dist.barrier(group=group)
+        with socket.socket(socket.AF_UNIX, socket.SOCK_STREAM) as s:
+            s.connect(name)
+            _, fds, _, _ = socket.recv_fds(s, 1, 1)
+        try:
+            _native.call("mgw_nvls_import", comm, fds[0], int(nbytes))
+        finally:
+            os.close(fds[0])
+    _native.call("mgw_nvls_add_device", comm)
+    dist.barrier(group=group)
+    _native.call("mgw_nvls_bind", comm)
+    dist.barrier(group=group)
+    if min_bytes:
+        _native.call("mgw_comm_set_nvls_min", comm, int(min_bytes))
+    session.nvls_bytes = int(nbytes)
 
 
 def _worker_main(result_q, rank, n_workers, host, base_port, chunk_elements, timeout, capacity_bytes, task) -> None:

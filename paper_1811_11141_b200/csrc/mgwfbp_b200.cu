@@ -15,6 +15,8 @@
 
 #include "mgwfbp_b200.h"
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -28,6 +30,7 @@
 #include "common.cuh"
 #include "fused.cuh"
 #include "ll.cuh"
+#include "nvls.cuh"
 #include "rows.cuh"
 
 using namespace mgw;
@@ -88,6 +91,12 @@ struct mgw_comm {
   int64_t ll_max_bytes = kLLElems * 4;  // 256 KB: the whole LL area
   int max_ctas = 2 * kSMs;
   int64_t vec_per_cta[2] = {0, 0};      // tuning: 16-B slots per CTA (one-shot, two-shot); 0 = default
+  // NVLS (opt-in): multicast object bound to a per-rank bucket
+  CUmemGenericAllocationHandle nvls_mc = 0, nvls_mem = 0;
+  CUdeviceptr nvls_uc = 0, nvls_mcva = 0;
+  size_t nvls_bytes = 0;
+  bool nvls_mc_valid = false, nvls_bound = false;
+  int64_t nvls_min_bytes = 0;  // AUTO picks NVLS at >= this size when set (0 = never)
 };
 
 struct mgw_sched {
@@ -141,14 +150,75 @@ int comm_launch_allreduce(const mgw_comm* c, const ArArgs& a, int algo, cudaStre
   return launch_allreduce(a, algo, c->max_ctas, stream, c->vec_per_cta);
 }
 
+// ------------------------------------------------------------- NVLS plumbing
+// Driver entry points through the runtime (no link-time dependency on libcuda).
+struct DriverFns {
+  PFN_cuMulticastCreate mc_create = nullptr;
+  PFN_cuMulticastAddDevice mc_add = nullptr;
+  PFN_cuMulticastBindMem mc_bind = nullptr;
+  PFN_cuMulticastUnbind mc_unbind = nullptr;
+  PFN_cuMulticastGetGranularity mc_gran = nullptr;
+  PFN_cuMemCreate mem_create = nullptr;
+  PFN_cuMemRelease mem_release = nullptr;
+  PFN_cuMemAddressReserve addr_reserve = nullptr;
+  PFN_cuMemAddressFree addr_free = nullptr;
+  PFN_cuMemMap mem_map = nullptr;
+  PFN_cuMemUnmap mem_unmap = nullptr;
+  PFN_cuMemSetAccess set_access = nullptr;
+  PFN_cuMemExportToShareableHandle export_handle = nullptr;
+  PFN_cuMemImportFromShareableHandle import_handle = nullptr;
+  PFN_cuDeviceGetAttribute get_attr = nullptr;
+  bool ok = false;
+};
+
+const DriverFns& driver() {
+  static DriverFns fns = [] {
+    DriverFns d;
+    auto get = [](const char* name, void** fn) {
+      cudaDriverEntryPointQueryResult q;
+      return cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess;
+    };
+    d.ok = get("cuMulticastCreate", (void**)&d.mc_create) && get("cuMulticastAddDevice", (void**)&d.mc_add) &&
+           get("cuMulticastBindMem", (void**)&d.mc_bind) && get("cuMulticastUnbind", (void**)&d.mc_unbind) &&
+           get("cuMulticastGetGranularity", (void**)&d.mc_gran) && get("cuMemCreate", (void**)&d.mem_create) &&
+           get("cuMemRelease", (void**)&d.mem_release) && get("cuMemAddressReserve", (void**)&d.addr_reserve) &&
+           get("cuMemAddressFree", (void**)&d.addr_free) && get("cuMemMap", (void**)&d.mem_map) &&
+           get("cuMemUnmap", (void**)&d.mem_unmap) && get("cuMemSetAccess", (void**)&d.set_access) &&
+           get("cuMemExportToShareableHandle", (void**)&d.export_handle) &&
+           get("cuMemImportFromShareableHandle", (void**)&d.import_handle) &&
+           get("cuDeviceGetAttribute", (void**)&d.get_attr);
+    return d;
+  }();
+  return fns;
+}
+
+#define MGW_CU(call)                                                                                \
+  do {                                                                                              \
+    CUresult r_ = (call);                                                                           \
+    if (r_ != CUDA_SUCCESS) return set_error(MGW_ECUDA, "%s failed: CUresult %d", #call, (int)r_); \
+  } while (0)
+
+size_t nvls_granularity(int world) {
+  CUmulticastObjectProp p = {};
+  p.numDevices = (unsigned)world;
+  p.size = 2ull << 20;
+  p.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  size_t g = 0;
+  if (driver().mc_gran(&g, &p, CU_MULTICAST_GRANULARITY_MINIMUM) != CUDA_SUCCESS || g == 0) g = 2ull << 20;
+  return g;
+}
+
 int pick_algo(const mgw_comm* c, int64_t n, int algo) {
   if (algo != MGW_ALGO_AUTO) return algo;
   return n * 4 <= c->oneshot_max_bytes ? MGW_ALGO_ONESHOT : MGW_ALGO_TWOSHOT;
 }
 
-// fused group exchange: LL push for small buckets, else pull one-shot / two-shot
+// fused group exchange: LL push for small buckets, else pull one-shot / two-shot;
+// NVLS only when enabled (not bit-exact with the reference order)
 int pick_fused_algo(const mgw_comm* c, int64_t n, int algo) {
   if (algo != MGW_ALGO_AUTO) return algo;
+  if (c->nvls_bound && c->nvls_min_bytes > 0 && n * 4 >= c->nvls_min_bytes && (size_t)n * 4 <= c->nvls_bytes)
+    return MGW_ALGO_NVLS;
   if (c->world > 1 && n * 4 <= c->ll_max_bytes && n <= kLLElems) return MGW_ALGO_LL;
   return pick_algo(c, n, algo);
 }
@@ -197,6 +267,17 @@ int comm_allreduce_fused(mgw_comm* c, const Row* host_rows, const Row* dev_rows,
   f.n_rows = n_rows;
   f.scale = scale;
   const int chosen = pick_fused_algo(c, n, algo);
+  if (chosen == MGW_ALGO_NVLS) {
+    if (!c->nvls_bound) return set_error(MGW_EINVAL, "NVLS not set up on this communicator");
+    if ((size_t)n * 4 > c->nvls_bytes)
+      return set_error(MGW_EINVAL, "bucket of %lld B exceeds the NVLS buffer (%zu B)", (long long)(n * 4), c->nvls_bytes);
+    NvlsArgs x;
+    memset(&x, 0, sizeof(x));
+    x.f = f;
+    x.uc = reinterpret_cast<float*>(c->nvls_uc);
+    x.mc = reinterpret_cast<float*>(c->nvls_mcva);
+    return launch_nvls(x, c->max_ctas, stream, c->vec_per_cta);
+  }
   if (chosen == MGW_ALGO_LL) {
     LLArgs l;
     memset(&l, 0, sizeof(l));
@@ -404,6 +485,20 @@ int mgw_comm_destroy(mgw_comm* c) {
   if (!c) return MGW_OK;
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
+  if (driver().ok) {
+    const DriverFns& d = driver();
+    if (c->nvls_mcva) {
+      d.mem_unmap(c->nvls_mcva, c->nvls_bytes);
+      d.addr_free(c->nvls_mcva, c->nvls_bytes);
+    }
+    if (c->nvls_uc) {
+      d.mem_unmap(c->nvls_uc, c->nvls_bytes);
+      d.addr_free(c->nvls_uc, c->nvls_bytes);
+    }
+    if (c->nvls_bound) d.mc_unbind(c->nvls_mc, (CUdevice)c->device, 0, c->nvls_bytes);
+    if (c->nvls_mem) d.mem_release(c->nvls_mem);
+    if (c->nvls_mc_valid) d.mem_release(c->nvls_mc);
+  }
   for (int s = 0; s < kMaxRanks; ++s)
     if (s != c->rank && c->peer[s]) cudaIpcCloseMemHandle(c->peer[s]);
   if (c->region) cudaFree(c->region);
@@ -480,7 +575,7 @@ int mgw_allreduce(mgw_comm* c, int64_t n_elem, int algo, void* stream) {
 int mgw_allreduce_fused(mgw_comm* c, const void* table, int n_rows, int64_t n_elem, float scale, int algo,
                         void* stream) {
   if (!c) return set_error(MGW_EINVAL, "comm is null");
-  if (algo < MGW_ALGO_AUTO || algo > MGW_ALGO_LL) return set_error(MGW_EINVAL, "unknown algorithm %d", algo);
+  if (algo < MGW_ALGO_AUTO || algo > MGW_ALGO_NVLS) return set_error(MGW_EINVAL, "unknown algorithm %d", algo);
   int rc = check_table(table, n_rows, n_elem);
   if (rc) return rc;
   const mgw_table_t* t = as_table(table);
@@ -493,6 +588,86 @@ int mgw_allreduce_fused(mgw_comm* c, const void* table, int n_rows, int64_t n_el
                                        n_elem, 1.f, nullptr, nullptr, 0, nullptr, static_cast<cudaStream_t>(stream));
   }
   return comm_allreduce_fused(c, t->host.data(), t->dev, n_rows, n_elem, scale, algo, static_cast<cudaStream_t>(stream));
+}
+
+int mgw_nvls_supported(int device, int* ok) {
+  if (!ok) return set_error(MGW_EINVAL, "ok is null");
+  *ok = 0;
+  if (!driver().ok) return MGW_OK;
+  int v = 0;
+  if (driver().get_attr(&v, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, (CUdevice)device) == CUDA_SUCCESS) *ok = v;
+  return MGW_OK;
+}
+
+// rank 0: create the multicast object for `bytes` (rounded up) and export a POSIX fd
+int mgw_nvls_create(mgw_comm* c, int64_t bytes, int* fd_out) {
+  if (!c || !fd_out || bytes <= 0 || c->world < 2) return set_error(MGW_EINVAL, "bad NVLS arguments");
+  if (!driver().ok) return set_error(MGW_ECUDA, "driver multicast entry points unavailable");
+  MGW_CUDA(cudaSetDevice(c->device));
+  const size_t g = nvls_granularity(c->world);
+  c->nvls_bytes = (size_t)round_up(bytes, (int64_t)g);
+  CUmulticastObjectProp p = {};
+  p.numDevices = (unsigned)c->world;
+  p.size = c->nvls_bytes;
+  p.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  MGW_CU(driver().mc_create(&c->nvls_mc, &p));
+  c->nvls_mc_valid = true;
+  int fd = -1;
+  MGW_CU(driver().export_handle(&fd, c->nvls_mc, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0));
+  *fd_out = fd;
+  return MGW_OK;
+}
+
+// ranks != 0: import the multicast object from the fd rank 0 exported
+int mgw_nvls_import(mgw_comm* c, int fd, int64_t bytes) {
+  if (!c || fd < 0 || bytes <= 0) return set_error(MGW_EINVAL, "bad NVLS arguments");
+  if (!driver().ok) return set_error(MGW_ECUDA, "driver multicast entry points unavailable");
+  MGW_CUDA(cudaSetDevice(c->device));
+  c->nvls_bytes = (size_t)round_up(bytes, (int64_t)nvls_granularity(c->world));
+  MGW_CU(driver().import_handle(&c->nvls_mc, (void*)(uintptr_t)fd, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR));
+  c->nvls_mc_valid = true;
+  return MGW_OK;
+}
+
+// every rank adds its device; all ranks must finish this before any binds memory
+int mgw_nvls_add_device(mgw_comm* c) {
+  if (!c || !c->nvls_mc_valid) return set_error(MGW_EINVAL, "no multicast object");
+  MGW_CU(driver().mc_add(c->nvls_mc, (CUdevice)c->device));
+  return MGW_OK;
+}
+
+// every rank: allocate its copy, bind it to the multicast object, map unicast + multicast
+int mgw_nvls_bind(mgw_comm* c) {
+  if (!c || !c->nvls_mc_valid) return set_error(MGW_EINVAL, "no multicast object");
+  const DriverFns& d = driver();
+  MGW_CUDA(cudaSetDevice(c->device));
+  CUmemAllocationProp prop = {};
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = c->device;
+  MGW_CU(d.mem_create(&c->nvls_mem, c->nvls_bytes, &prop, 0));
+  MGW_CU(d.mc_bind(c->nvls_mc, 0, c->nvls_mem, 0, c->nvls_bytes, 0));
+  c->nvls_bound = true;
+  CUmemAccessDesc acc = {};
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = c->device;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  const size_t g = nvls_granularity(c->world);
+  MGW_CU(d.addr_reserve(&c->nvls_uc, c->nvls_bytes, g, 0, 0));
+  MGW_CU(d.mem_map(c->nvls_uc, c->nvls_bytes, 0, c->nvls_mem, 0));
+  MGW_CU(d.set_access(c->nvls_uc, c->nvls_bytes, &acc, 1));
+  MGW_CU(d.addr_reserve(&c->nvls_mcva, c->nvls_bytes, g, 0, 0));
+  MGW_CU(d.mem_map(c->nvls_mcva, c->nvls_bytes, 0, c->nvls_mc, 0));
+  MGW_CU(d.set_access(c->nvls_mcva, c->nvls_bytes, &acc, 1));
+  MGW_CUDA(cudaMemset(reinterpret_cast<void*>(c->nvls_uc), 0, c->nvls_bytes));
+  MGW_CUDA(cudaDeviceSynchronize());
+  return MGW_OK;
+}
+
+int mgw_comm_set_nvls_min(mgw_comm* c, int64_t bytes) {
+  if (!c || bytes < 0) return set_error(MGW_EINVAL, "bad NVLS threshold");
+  c->nvls_min_bytes = bytes;
+  return MGW_OK;
 }
 
 int mgw_event_create(void** event) {
