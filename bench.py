@@ -211,13 +211,28 @@ def _allreduce_sweep(session, comm, world, device, sizes):
     two = _exchange_times(comm, world, device, sizes, kind=1, algo=_native.ALGO_TWOSHOT)
     nccl = _nccl_times(world, device, sizes)
     session.raise_if_failed()
+    nvls = None
+    try:  # opt-in NVSwitch reduction, measured for comparison only (not bit-exact)
+        from paper_1811_11141_b200.allreduce_net import enable_nvls
+
+        if not getattr(session, "nvls_bytes", 0):
+            enable_nvls(session, max(sizes))
+        nvls = _exchange_times(comm, world, device, sizes, kind=4, algo=_native.ALGO_NVLS)
+    except Exception as exc:  # unsupported fabric: leave the column out
+        print(f"NVLS unavailable: {exc}", file=sys.stderr)
+    fused = _exchange_times(comm, world, device, sizes, kind=4)
     rows = []
-    for nbytes, t1, t2, tn in zip(sizes, one, two, nccl):
+    for i, (nbytes, t1, t2, tn) in enumerate(zip(sizes, one, two, nccl)):
         bus = 2 * (world - 1) / world * nbytes
         rows.append({"bytes": nbytes,
                      "oneshot_us": round(t1 * 1e6, 2), "oneshot_busbw_gbs": round(bus / t1 / 1e9, 1),
                      "twoshot_us": round(t2 * 1e6, 2), "twoshot_busbw_gbs": round(bus / t2 / 1e9, 1),
-                     "nccl_us": round(tn * 1e6, 2), "nccl_busbw_gbs": round(bus / tn / 1e9, 1)})
+                     "nccl_us": round(tn * 1e6, 2), "nccl_busbw_gbs": round(bus / tn / 1e9, 1),
+                     "fused_exchange_us": round(fused[i] * 1e6, 2),
+                     "fused_exchange_busbw_gbs": round(bus / fused[i] / 1e9, 1)})
+        if nvls is not None:
+            rows[-1]["nvls_fused_us"] = round(nvls[i] * 1e6, 2)
+            rows[-1]["nvls_fused_busbw_gbs"] = round(bus / nvls[i] / 1e9, 1)
     return rows
 
 

@@ -645,6 +645,7 @@ int mgw_nvls_bind(mgw_comm* c) {
   prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
   prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
   prop.location.id = c->device;
+  prop.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;  // as the multicast object's
   MGW_CU(d.mem_create(&c->nvls_mem, c->nvls_bytes, &prop, 0));
   MGW_CU(d.mc_bind(c->nvls_mc, 0, c->nvls_mem, 0, c->nvls_bytes, 0));
   c->nvls_bound = true;

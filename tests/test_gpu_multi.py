@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 import _mp_tasks
-from conftest import cuda_devices, golden_ring, make_profile
+from conftest import ROOT, cuda_devices, golden_ring, make_profile
 from paper_1811_11141_b200 import (
     EmulationReport,
     MergePlan,
@@ -129,6 +129,20 @@ def test_autograd_merged_sync_matches_reference_fold(algo, deferred):
                     rot[s] = bool(acc == got[i])
                 raise AssertionError(f"group {(low, high)} rank {r}: {bad.size} mismatches, first {i} "
                                      f"(of {got.size}); got {got[i]!r} want {want[i]!r}; rotations matching got: {rot}")
+
+
+def test_nvls_opt_in_within_tolerance():
+    """Opt-in NVLS (in-switch fp32 reduction): within N ulps of the exact sum, identical on
+    every rank (scripts/nvls_check.py exits non-zero otherwise)."""
+    import subprocess
+    import sys
+
+    n = max(_worlds())
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", "29571", "scripts/nvls_check.py"]
+    proc = subprocess.run(cmd, cwd=str(ROOT), capture_output=True, text=True, timeout=600)
+    assert proc.returncode == 0, proc.stderr[-3000:]
+    assert '"ok": true' in proc.stdout
 
 
 def test_bench_local_measurement_shape():
