@@ -202,7 +202,7 @@ def _nccl_times(world, device, sizes, repeats=20, warmups=3):
     return _max_over_ranks(out, world, device)
 
 
-def _allreduce_sweep(session, comm, world, device, sizes):
+def _allreduce_sweep(session, comm, world, device, sizes, with_nvls=False):
     """Bus GB/s vs size: our one-shot and two-shot kernels alone, the full group
     exchange (pack + all-reduce + unpack), and ncclAllReduce."""
     from paper_1811_11141_b200 import _native
@@ -213,6 +213,8 @@ def _allreduce_sweep(session, comm, world, device, sizes):
     session.raise_if_failed()
     nvls = None
     try:  # opt-in NVSwitch reduction, measured for comparison only (not bit-exact)
+        if not with_nvls:
+            raise RuntimeError("not requested (--nvls)")
         from paper_1811_11141_b200.allreduce_net import enable_nvls
 
         if not getattr(session, "nvls_bytes", 0):
@@ -448,7 +450,7 @@ def run_ours(args) -> dict | None:
 
     sweep = None
     if world > 1 and not args.no_sweep:
-        sweep = _allreduce_sweep(session, comm, world, device, FIT_SIZES)
+        sweep = _allreduce_sweep(session, comm, world, device, FIT_SIZES, with_nvls=args.nvls)
     it.close()
     if session is not None:
         session.close()
@@ -592,6 +594,7 @@ def main(argv=None) -> int:
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-graph", action="store_true", help="eager stream schedule instead of CUDA-graph replay")
     ap.add_argument("--unfused", action="store_true", help="separate pack / all-reduce / unpack kernels per group")
+    ap.add_argument("--nvls", action="store_true", help="also time the opt-in NVLS exchange in the sweep (N > 1)")
     ap.add_argument("--no-sweep", action="store_true", help="skip the all-reduce bus-bandwidth sweep (N > 1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
