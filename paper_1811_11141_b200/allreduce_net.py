@@ -693,6 +693,20 @@ def open_ring(
     return config, session
 
 
+def exchange_handles_dist(handle: bytes, *, group=None) -> bytes:
+    """All-gather every rank's 64-byte IPC handle through torch.distributed; returns the
+    rank-ordered concatenation ``mgw_comm_open_peers`` expects."""
+    import torch.distributed as dist
+
+    if len(handle) != _native.IPC_HANDLE_BYTES:
+        raise ValueError(f"IPC handles are {_native.IPC_HANDLE_BYTES} bytes, got {len(handle)}")
+    handles: list = [None] * dist.get_world_size(group)
+    dist.all_gather_object(handles, bytes(handle), group=group)
+    if any(h is None or len(h) != _native.IPC_HANDLE_BYTES for h in handles):
+        raise ProtocolError("a rank contributed a malformed IPC handle")
+    return b"".join(handles)
+
+
 def open_session_dist(
     *,
     capacity_bytes: int = DEFAULT_CAPACITY_BYTES,
@@ -712,9 +726,7 @@ def open_session_dist(
     torch.cuda.set_device(dev)
     comm, ipc = _create_comm(rank, world, dev, capacity_bytes)
     try:
-        handles: list = [None] * world
-        dist.all_gather_object(handles, ipc, group=group)
-        _native.call("mgw_comm_open_peers", comm, b"".join(handles))
+        _native.call("mgw_comm_open_peers", comm, exchange_handles_dist(ipc, group=group))
         addresses = tuple(("torch.distributed", r) for r in range(world))
         config = WorkerConfig(rank, world, addresses, device=dev)
         session = RingSession(config, comm, capacity_bytes=capacity_bytes, timeout=timeout)

@@ -42,11 +42,13 @@ class MergedGradientSync:
     ``comm`` is a native communicator (``RingSession.comm``) or None for a single GPU
     (then only the optional ``scale`` is applied).  ``plan`` groups the parameter list
     (layer k = params[k-1]); the group's bucket layout is the reference's (highest
-    layer first).  ``scale=1/N`` averages.
+    layer first).  ``scale=1/N`` averages.  ``priority`` is the comm stream's CUDA
+    priority (-1 = high).
     """
 
     def __init__(self, params, plan: MergePlan, *, comm=None, world: int = 1, scale: float = 1.0,
-                 algo: int = _native.ALGO_AUTO, sync_after_backward: bool = False, max_ctas: int | None = None):
+                 algo: int = _native.ALGO_AUTO, sync_after_backward: bool = False, max_ctas: int | None = None,
+                 priority: int = 0):
         import torch
 
         self.torch = torch
@@ -71,7 +73,9 @@ class MergedGradientSync:
         self.count = [0] * len(self.groups)
         self.tables: dict[int, tuple] = {}
         self.events: dict[int, int] = {}
-        self.stream = torch.cuda.Stream()
+        # priority < 0 puts the comm stream ahead of backward in the CTA scheduler, so a
+        # ready group's collective is not queued behind a wave of backward blocks
+        self.stream = torch.cuda.Stream(priority=priority)
         self.launched = 0
         self.pending: list[int] = []
         self.handles = [p.register_post_accumulate_grad_hook(partial(self._ready, k))
