@@ -117,6 +117,11 @@ int mgw_comm_set_timeout_ms(mgw_comm* comm, int64_t ms);
 int mgw_comm_set_oneshot_max(mgw_comm* comm, int64_t bytes);
 int mgw_comm_set_max_ctas(mgw_comm* comm, int ctas);
 int mgw_comm_set_ll_max(mgw_comm* comm, int64_t bytes);
+/* gate: precede every collective with a one-warp kernel that waits until all peers
+ * have reached the same collective (the reference ring's blocking receive,
+ * allreduce_net.py:277-307), so overlapped bulk kernels never hold SMs in a barrier
+ * while a peer is still computing.  Off by default. */
+int mgw_comm_set_gate(mgw_comm* comm, int enable);
 /* tuning: key 0 = one-shot 16-B slots per CTA, key 1 = two-shot slots per CTA (0 = default) */
 int mgw_comm_set_tuning(mgw_comm* comm, int key, int64_t value);
 int mgw_comm_input(mgw_comm* comm, float** slot); /* slot the next collective reads (syncs) */

@@ -66,6 +66,7 @@ _SIGNATURES = {
     "mgw_comm_set_oneshot_max": ([_P, _I64], _I),
     "mgw_comm_set_max_ctas": ([_P, _I], _I),
     "mgw_comm_set_ll_max": ([_P, _I64], _I),
+    "mgw_comm_set_gate": ([_P, _I], _I),
     "mgw_comm_set_tuning": ([_P, _I, _I64], _I),
     "mgw_comm_input": ([_P, ctypes.POINTER(_P)], _I),
     "mgw_comm_result": ([_P, ctypes.POINTER(_P)], _I),

@@ -43,12 +43,13 @@ class MergedGradientSync:
     (then only the optional ``scale`` is applied).  ``plan`` groups the parameter list
     (layer k = params[k-1]); the group's bucket layout is the reference's (highest
     layer first).  ``scale=1/N`` averages.  ``priority`` is the comm stream's CUDA
-    priority (-1 = high).
+    priority (-1 = high); ``gate`` launches each collective only once every peer has
+    reached it (``mgw_comm_set_gate``).
     """
 
     def __init__(self, params, plan: MergePlan, *, comm=None, world: int = 1, scale: float = 1.0,
                  algo: int = _native.ALGO_AUTO, sync_after_backward: bool = False, max_ctas: int | None = None,
-                 priority: int = 0):
+                 priority: int = 0, gate: bool = False):
         import torch
 
         self.torch = torch
@@ -64,6 +65,9 @@ class MergedGradientSync:
         if max_ctas is not None and comm is not None:
             # overlapped collectives share the SMs with backward: bound their CTA budget
             _native.call("mgw_comm_set_max_ctas", comm, int(max_ctas))
+        if comm is not None:
+            # gate: every bulk kernel waits (one warp) until all peers reached it
+            _native.call("mgw_comm_set_gate", comm, int(gate))
         self.groups = plan.groups()  # ascending (low, high)
         self.group_of = {}
         for gid, (low, high) in enumerate(self.groups):

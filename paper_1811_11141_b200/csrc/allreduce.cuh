@@ -89,6 +89,49 @@ __device__ __noinline__ int cta_barrier(uint64_t* const* flags, int parity, uint
   return status;
 }
 
+// Peer gate (opt-in, mgw_comm_set_gate): one warp announces "collective `epoch` is
+// next on my comm stream" to every peer and waits until every peer has announced the
+// same, so the bulk kernel that follows is launched only when all ranks have reached
+// it.  Under a real backward pass ranks drift by tens of microseconds; without the
+// gate the first rank's CTAs would sit in the entry barrier holding SM slots that the
+// backward kernels need.  Door words are monotonic epochs -- no parity, no reset.
+__global__ void gate_kernel(const __grid_constant__ ArArgs a) {
+  const int t = threadIdx.x;
+  const uint32_t epoch = load_volatile32(a.state) + 1u;
+  int status = MGW_DEV_OK;
+  if (t < a.world) {
+    uint64_t* door_t = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(a.arrive[t]) - kArriveOff + kDoorOff);
+    const uint64_t* mine =
+        reinterpret_cast<const uint64_t*>(reinterpret_cast<char*>(a.arrive[a.rank]) - kArriveOff + kDoorOff) + t;
+    store_release_sys(door_t + a.rank, epoch);
+    const uint64_t start = global_ns();
+    for (uint32_t spin = 0;; ++spin) {
+      if ((int32_t)((uint32_t)load_acquire_sys(mine) - epoch) >= 0) break;
+      if ((spin & 63) == 63) {
+        if (load_relaxed_sys32(a.abort_flag[a.rank]) != 0u) {
+          status = MGW_DEV_PEER_ABORT;
+          break;
+        }
+        if (global_ns() - start > a.timeout_ns) {
+          status = MGW_DEV_TIMEOUT;
+          break;
+        }
+      }
+    }
+  }
+  if (status != MGW_DEV_OK) {
+    atomicCAS(a.err, 0, status);
+    if (status != MGW_DEV_PEER_ABORT)
+      for (int r = 0; r < a.world; ++r) store_release_sys32(a.abort_flag[r], 1u);
+  }
+}
+
+inline int launch_gate(const ArArgs& a, cudaStream_t stream) {
+  gate_kernel<<<1, 32, 0, stream>>>(a);
+  MGW_CHECK_LAUNCH();
+  return MGW_OK;
+}
+
 // Last CTA out advances the call counter (epochs and slot parity come from it).
 // Kernel completion publishes the counter to the next kernel on the stream.
 __device__ __forceinline__ void finish_call(const ArArgs& a) {

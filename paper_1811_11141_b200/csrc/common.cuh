@@ -60,8 +60,9 @@ constexpr size_t kArriveOff = 0;
 constexpr size_t kMidOff = kArriveOff + 2 * kFlagsPerParity * sizeof(uint64_t);
 constexpr size_t kAbortOff = kMidOff + 2 * kFlagsPerParity * sizeof(uint64_t);
 constexpr size_t kHdrOff = kAbortOff + 1024;  // LL headers u64 [2 parity][kMaxRanks src]
+constexpr size_t kDoorOff = kHdrOff + 2 * kMaxRanks * sizeof(uint64_t);  // gate u64 [kMaxRanks src]
 constexpr size_t kCtrlBytes = 262144;
-static_assert(kHdrOff + 2 * kMaxRanks * sizeof(uint64_t) <= kCtrlBytes, "control area overflow");
+static_assert(kDoorOff + kMaxRanks * sizeof(uint64_t) <= kCtrlBytes, "control area overflow");
 // LL receive area u64 [2 parity][kMaxRanks src][kLLElems] follows the control area,
 // then the two bucket slots.
 constexpr int64_t kLLElems = 65536;

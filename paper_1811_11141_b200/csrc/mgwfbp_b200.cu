@@ -97,6 +97,7 @@ struct mgw_comm {
   size_t nvls_bytes = 0;
   bool nvls_mc_valid = false, nvls_bound = false;
   int64_t nvls_min_bytes = 0;  // AUTO picks NVLS at >= this size when set (0 = never)
+  bool gate = false;           // launch gate_kernel ahead of every collective (mgw_comm_set_gate)
 };
 
 struct mgw_sched {
@@ -233,6 +234,10 @@ int comm_allreduce(mgw_comm* c, int64_t n, int algo, cudaStream_t stream, uint64
   }
   if (!c->peers_open) return set_error(MGW_EINVAL, "peers not opened (call mgw_comm_open_peers)");
   ArArgs a = make_args(c, n);
+  if (c->gate) {
+    int rc = launch_gate(a, stream);
+    if (rc) return rc;
+  }
   a.stamp = stamp;
   return comm_launch_allreduce(c, a, pick_algo(c, n, algo), stream);
 }
@@ -259,6 +264,10 @@ int comm_allreduce_fused(mgw_comm* c, const Row* host_rows, const Row* dev_rows,
   FusedArgs f;
   memset(&f, 0, sizeof(f));
   f.ar = make_args(c, n);
+  if (c->world > 1 && c->gate) {
+    int rc = launch_gate(f.ar, stream);
+    if (rc) return rc;
+  }
   f.ar.stamp = stamp;
   f.use_inline = n_rows <= kInlineRows && host_rows != nullptr;
   if (f.use_inline)
@@ -536,6 +545,12 @@ int mgw_comm_set_tuning(mgw_comm* c, int key, int64_t value) {
 int mgw_comm_set_max_ctas(mgw_comm* c, int ctas) {
   if (!c || ctas < 1 || ctas > kMaxBlocks) return set_error(MGW_EINVAL, "CTA cap must lie in 1..%d", kMaxBlocks);
   c->max_ctas = ctas;
+  return MGW_OK;
+}
+
+int mgw_comm_set_gate(mgw_comm* c, int enable) {
+  if (!c) return set_error(MGW_EINVAL, "communicator is null");
+  c->gate = enable != 0;
   return MGW_OK;
 }
 
@@ -984,13 +999,16 @@ static int sched_enqueue(mgw_sched* s, cudaStream_t cs, cudaStream_t ms) {
         if (s->rows[k].count)
           MGW_CUDA(cudaMemcpyAsync(s->rows[k].ptr, s->host_src[k], s->rows[k].count * 4, cudaMemcpyHostToDevice, cs));
     }
+    spin_until_kernel<<<1, 32, 0, cs>>>(s->d_clock, gr.ready_ns);
+    MGW_CHECK_LAUNCH();
     if ((s->flags & MGW_SCHED_FILL) && gr.n_elem > 0) {
+      // the layer's gradient is written at the END of its backward window (as a real
+      // weight-gradient kernel would), so it does not contend with the previous group's
+      // exchange for SMs and HBM
       int rc = launch_rows<RowOp::kFill>(s->rows.data() + gr.desc_begin, d_rows + gr.desc_begin, gr.desc_count, nullptr,
                                          gr.n_elem, 1.f, s->d_fill + gr.desc_begin, nullptr, 0, nullptr, cs);
       if (rc) return rc;
     }
-    spin_until_kernel<<<1, 32, 0, cs>>>(s->d_clock, gr.ready_ns);
-    MGW_CHECK_LAUNCH();
     MGW_CUDA(cudaEventRecord(s->dep_ready[g], cs));
   }
   MGW_CUDA(record_timing(s, s->t_compute, cs));
@@ -1056,7 +1074,7 @@ int mgw_sched_run(mgw_sched* s, void* compute_stream, void* comm_stream) {
     }
     if (e != cudaSuccess) return set_error(MGW_ECUDA, "graph capture: %s", cudaGetErrorString(e));
     s->graph = graph;
-    MGW_CUDA(cudaGraphInstantiate(&s->graph_exec, graph, 0));
+    MGW_CUDA(cudaGraphInstantiate(&s->graph_exec, graph, cudaGraphInstantiateFlagUseNodePriority));  // keep the comm stream's priority
   }
   MGW_CUDA(cudaGraphLaunch(s->graph_exec, cs));
   return MGW_OK;

@@ -1,7 +1,7 @@
 // rows.cuh -- K1 pack(+scale), K4 unpack, and the fill / check helpers.
 //
 // A merge group's bucket is the concatenation of its layer gradients, layer `high`
-// first (allreduce_net.py:499-509).  The kernels walk the *bucket* in 64 KB tiles,
+// first (allreduce_net.py:499-509).  The kernels walk the *bucket* in 8-64 KB tiles,
 // one tile per CTA step; every thread owns fixed 16-B slots of the tile and finds the
 // layer row holding each slot by a forward scan (rows are sorted by bucket offset, so
 // the scan is monotone per thread).  A slot that lies inside one row at a 16-B aligned
@@ -28,6 +28,7 @@ struct RowsParam {
   int use_inline;
   float* bucket;
   int64_t total;  // bucket elements
+  int64_t tile;   // bucket elements per CTA step (multiple of 4 * kThreads)
   float scale;
   const float* values;      // kFill / kCheck: one value per row
   const uint32_t* calls;    // comm pack: slot parity = (completed calls + 1) & 1
@@ -75,8 +76,9 @@ __global__ void __launch_bounds__(kThreads) rows_kernel(const __grid_constant__ 
   if (p.calls != nullptr) bucket += (int64_t)((load_volatile32(p.calls) + 1u) & 1u) * p.slot_stride_elems;
   const float scale = p.scale;
   unsigned long long bad = 0;
-  for (int64_t t0 = (int64_t)blockIdx.x * kTile; t0 < p.total; t0 += (int64_t)gridDim.x * kTile) {
-    const int64_t t1 = t0 + kTile < p.total ? t0 + kTile : p.total;
+  const int64_t tile = p.tile;
+  for (int64_t t0 = (int64_t)blockIdx.x * tile; t0 < p.total; t0 += (int64_t)gridDim.x * tile) {
+    const int64_t t1 = t0 + tile < p.total ? t0 + tile : p.total;
     int k = row_covering(p, t0 + 4 * threadIdx.x < t1 ? t0 + 4 * threadIdx.x : t0);
     for (int64_t base = t0 + 4 * threadIdx.x; base < t1; base += 4 * kThreads * kRowsUnroll) {
       float* tp[kRowsUnroll];
@@ -146,11 +148,19 @@ __global__ void __launch_bounds__(kThreads) rows_kernel(const __grid_constant__ 
   stamp_exit(p.stamp);
 }
 
-inline int rows_grid(int64_t total) {
-  // one resident wave: 512-thread CTAs at <= 40 registers -> 3 per SM (ncu r01:
-  // launch__occupancy_limit_registers = 3; a 592-CTA grid left a 1/3 tail wave)
-  const int64_t tiles = (total + kTile - 1) / kTile;
+// Tile and grid for a bucket of `total` elements.  At most one resident wave
+// (512-thread CTAs at <= 40 registers -> 3 per SM; ncu r01:
+// launch__occupancy_limit_registers = 3, a 592-CTA grid left a 1/3 tail wave).  A
+// mid-sized group (a 9.4 MB ResNet layer) is spread over the whole wave with smaller
+// tiles instead of parking on 144 CTAs of 64 KB: more SMs, more bytes in flight.
+inline int rows_grid(int64_t total, int64_t* tile_out) {
+  constexpr int64_t kStep = 4 * kThreads;  // one 16-B slot per thread
   const int64_t cap = (int64_t)kSMs * 3;
+  int64_t tile = (total + cap - 1) / cap;
+  tile = (tile + kStep - 1) / kStep * kStep;
+  tile = tile < kStep ? kStep : (tile > kTile ? kTile : tile);
+  *tile_out = tile;
+  const int64_t tiles = (total + tile - 1) / tile;
   return (int)(tiles < 1 ? 1 : (tiles < cap ? tiles : cap));
 }
 
@@ -176,7 +186,7 @@ int launch_rows(const Row* host_rows, const Row* dev_rows, int n_rows, float* bu
   p.mismatches = mismatches;
   p.stamp = stamp;
   if (!p.use_inline && dev_rows == nullptr) return set_error(MGW_EINVAL, "row table missing");
-  const int grid = rows_grid(total);
+  const int grid = rows_grid(total, &p.tile);
   if (kOp == RowOp::kPack && scale != 1.0f)
     rows_kernel<kOp, true><<<grid, kThreads, 0, stream>>>(p);
   else

@@ -182,7 +182,8 @@ class OverlappedIteration:
         self._sched = handle.value
         self.n_rows = len(rows)
         self.compute_stream = torch.cuda.Stream(device=self.device)
-        self.comm_stream = torch.cuda.Stream(device=self.device)
+        # high priority: a ready group's exchange is scheduled ahead of queued compute CTAs
+        self.comm_stream = torch.cuda.Stream(device=self.device, priority=-1)
         n = ctypes.c_int()
         _native.call("mgw_sched_launches", self._sched, ctypes.byref(n))
         self.launches_per_iteration = n.value

@@ -30,6 +30,20 @@ KEYS = [
 ]
 
 
+def _base(name):
+    """Kernel name without its parameter list, keeping template arguments
+    (``rows_kernel<(mgw::RowOp)0, true>(...)`` -> ``rows_kernel<(mgw::RowOp)0, true>``)."""
+    depth = 0
+    for i, ch in enumerate(name):
+        if ch == "<":
+            depth += 1
+        elif ch == ">":
+            depth -= 1
+        elif ch == "(" and depth == 0:
+            return name[:i]
+    return name
+
+
 def launches(path):
     lines = open(path).read().splitlines()
     start = next(i for i, l in enumerate(lines) if l.startswith('"ID"'))
@@ -37,7 +51,7 @@ def launches(path):
     agg = collections.defaultdict(lambda: [0, 0.0])
     scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
     for r in rows:
-        name = r["Kernel Name"].split("(")[0]
+        name = _base(r["Kernel Name"])
         agg[name][0] += 1
         agg[name][1] += float(r["Metric Value"].replace(",", "")) * scale[r["Metric Unit"]]
     total = sum(t for _, t in agg.values())

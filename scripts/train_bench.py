@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--model", default="resnet50")
     ap.add_argument("--ctas", default="296,64,32,16", help="CTA caps to try for the overlapped collectives")
     ap.add_argument("--priorities", default="0,-1", help="comm stream priorities to try")
+    ap.add_argument("--gates", default="0,1", help="peer gate off/on variants to try")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -106,11 +107,13 @@ def main():
         opt.step()
 
     results["compute_only"] = timed(local_step, "compute_only")
-    variants = [(int(c), int(p)) for c in args.ctas.split(",") for p in args.priorities.split(",")]
-    for cap, prio in variants:
+    variants = [(int(c), int(p), int(g)) for c in args.ctas.split(",") for p in args.priorities.split(",")
+                for g in args.gates.split(",")]
+    for cap, prio, gate in variants:
         for name in ("wfbp", "mgwfbp", "synceasgd"):
             sync = MergedGradientSync(params, plans[name], comm=comm, world=world, scale=1.0 / world,
-                                      sync_after_backward=name == "synceasgd", max_ctas=cap, priority=prio)
+                                      sync_after_backward=name == "synceasgd", max_ctas=cap, priority=prio,
+                                      gate=bool(gate))
 
             def synced_step():
                 opt.zero_grad(set_to_none=False)
@@ -118,7 +121,7 @@ def main():
                 sync.finish()
                 opt.step()
 
-            key = f"{name}_ctas{cap}" + ("_hiprio" if prio < 0 else "")
+            key = f"{name}_ctas{cap}" + ("_hiprio" if prio < 0 else "") + ("_gate" if gate else "")
             results[key] = timed(synced_step, key)
             results[key].update({"groups": len(plans[name].groups()),
                                  "launched_per_step": sync.launched // (args.warmup + args.steps),

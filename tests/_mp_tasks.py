@@ -93,10 +93,21 @@ def every_algorithm_task(config, session, *, arrays):
                 session.raise_if_failed()
                 out[f"{key}_plain_{name}"] = t.cpu().numpy()
                 table.close()
+            # peer gate on: the same bits, one extra one-warp kernel per collective
+            _native.call("mgw_comm_set_gate", session.comm, 1)
+            for name, algo in (("ll", _native.ALGO_LL), ("two", _native.ALGO_TWOSHOT)):
+                t = torch.from_numpy(vals.copy()).to(session.device)
+                table = _native.DeviceTable([(t.data_ptr(), n, 0)])
+                _native.call("mgw_allreduce_fused", session.comm, table.ptr, 1, n, ctypes.c_float(1.0), algo, h)
+                session.stream.synchronize()
+                session.raise_if_failed()
+                out[f"{key}_gate_{name}"] = t.cpu().numpy()
+                table.close()
+            _native.call("mgw_comm_set_gate", session.comm, 0)
     return out
 
 
-def autograd_task(config, session, *, algo=0, deferred=False):
+def autograd_task(config, session, *, algo=0, deferred=False, gate=False):
     """Two+ ranks with different data: merged-gradient sync leaves averaged gradients equal,
     bit for bit, to the oracle ring over the per-rank gradients.  The model is elementwise so
     its backward is deterministic (cuBLAS split-K GEMMs are not, run to run)."""
@@ -126,7 +137,7 @@ def autograd_task(config, session, *, algo=0, deferred=False):
     net(xs).backward()
     again = [p.grad.detach().cpu().numpy().copy() for p in params]
     sync = MergedGradientSync(params, MergePlan(frozenset({2, 4}), 4), comm=session.comm, world=config.n_workers,
-                              algo=algo, sync_after_backward=deferred)
+                              algo=algo, sync_after_backward=deferred, gate=gate, priority=-1 if gate else 0)
     net.zero_grad(set_to_none=False)
     net(xs).backward()
     if deferred:  # groups not launched yet: the synced backward's own gradients

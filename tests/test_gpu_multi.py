@@ -80,7 +80,7 @@ def test_every_algorithm_bit_exact_over_ipc():
         for size in (1, 17, 1001, 4099):
             want = g[f"out_N{n}_n{size}"].view("<u4")
             for r in range(n):
-                for variant in ("fused_ll", "fused_one", "fused_two", "plain_one", "plain_two"):
+                for variant in ("fused_ll", "fused_one", "fused_two", "plain_one", "plain_two", "gate_ll", "gate_two"):
                     got = results[r][f"n{size}_{variant}"].view("<u4")
                     assert np.array_equal(got, want), (n, size, r, variant)
 
@@ -102,12 +102,13 @@ def test_fused_algorithms_large_multirow_vs_oracle():
                     assert bad.size == 0, (n, size, algo, r, bad.size, int(bad[0]))
 
 
-@pytest.mark.parametrize("algo,deferred", [(0, False), (3, False), (1, False), (2, False), (0, True)])
-def test_autograd_merged_sync_matches_reference_fold(algo, deferred):
+@pytest.mark.parametrize("algo,deferred,gate", [(0, False, False), (3, False, False), (1, False, False),
+                                               (2, False, False), (0, True, False), (0, False, True)])
+def test_autograd_merged_sync_matches_reference_fold(algo, deferred, gate):
     from oracle import ring_oracle
 
     n = max(_worlds())
-    results = run_workers(n, partial(_mp_tasks.autograd_task, algo=algo, deferred=deferred))
+    results = run_workers(n, partial(_mp_tasks.autograd_task, algo=algo, deferred=deferred, gate=gate))
     assert all(results[r][2] for r in range(n)), "the test model's backward is not deterministic"
     groups = MergePlan(frozenset({2, 4}), 4).groups()
     assert groups == [(1, 2), (3, 4)]
