@@ -178,3 +178,31 @@ def sizes_task(config, session, *, sizes, algos):
                 out[(algo, n)] = np.concatenate([a.cpu().numpy(), b.cpu().numpy()])
                 table.close()
     return out
+
+
+def replan_task(config, session, *, iterations=4):
+    """Live group-exchange spans of real overlapped iterations feed the online planner."""
+    import torch
+
+    from paper_1811_11141_b200 import MergePlan, find_merge_plan, resnet50_like
+    from paper_1811_11141_b200.overlap import OverlappedIteration
+    from paper_1811_11141_b200.replan import OnlinePlanner, observe_iteration
+
+    profile = resnet50_like(backward_seconds=0.00972, forward_seconds=0.00464)
+    plan = MergePlan(frozenset(), profile.num_layers)
+    planner = OnlinePlanner(profile, config.n_workers, plan=plan, min_samples=16)
+    with torch.cuda.device(session.device):
+        it = OverlappedIteration(profile, plan, comm=session.comm, rank=config.rank, world=config.n_workers,
+                                 device=session.device, fused=True)
+        try:
+            for _ in range(iterations):
+                it.run()
+                observe_iteration(planner, it)
+            ok = it.verify()
+        finally:
+            it.close()
+    session.raise_if_failed()
+    new = planner.update()
+    m = planner.model
+    return {"verified": ok, "samples": len(planner.samples), "a": m.a, "b": m.b,
+            "consistent": (new or planner.plan) == find_merge_plan(profile, m)}

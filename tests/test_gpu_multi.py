@@ -189,3 +189,12 @@ def test_criterion_8_calibrate_then_predict():
             assert all(r.verified for r in reports.values())
             measured = max(r.mean_seconds for r in reports.values())
             assert abs(measured - predicted) / predicted <= 0.05, (measured, predicted)
+
+
+def test_online_replanning_from_live_spans():
+    """the fused kernels' own spans refit (a, b) and re-run Algorithm 1."""
+    res = run_workers(2, partial(_mp_tasks.replan_task, iterations=4))
+    for r in res.values():
+        assert r["verified"] and r["consistent"]
+        assert r["samples"] == 4 * 54
+        assert 0 <= r["a"] < 1e-3 and 0 < r["b"] < 1e-9  # µs-class startup, > 1 GB/s
