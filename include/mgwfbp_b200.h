@@ -163,6 +163,21 @@ int mgw_event_destroy(void* event);
 int mgw_allreduce_fused_emulated(void* const* tables, float* const* slots, int world, int64_t n_elem, float scale,
                                  int algo, void* stream);
 
+/* ---- bf16 gradients, fp32 accumulation ------------------
+ * Same tables (rows' ptr point at bf16 data; count / offset in bf16 elements), bf16
+ * bucket and wire format.  Element e of reference segment s (allreduce_net.py:360-367)
+ * becomes bf16_rn((((f32(x_s) + f32(x_s+1)) + ...) + f32(x_s+N-1)) * scale), the
+ * multiply only when scale != 1: the reference ring's fold order (allreduce_net.py:401)
+ * in fp32 over exactly-upcast inputs, rounded once.  Algorithms: AUTO, one-shot,
+ * two-shot.  Replaces ring_allreduce (allreduce_net.py:370-411) for element_bytes = 2
+ * profiles (model_profile.py:24). */
+int mgw_allreduce_fused_bf16(mgw_comm* comm, const void* table, int n_rows, int64_t n_elem, float scale, int algo,
+                             void* stream);
+int mgw_group_launch_bf16(mgw_comm* comm, const void* table, int n_rows, int64_t n_elem, float scale, int algo,
+                          void* compute_stream, void* comm_stream, void* event);
+int mgw_allreduce_fused_bf16_emulated(void* const* tables, void* const* slots, int world, int64_t n_elem,
+                                      float scale, int algo, void* stream);
+
 /* ---- Algorithm 2 on streams ------------------------------------------- */
 int mgw_sched_create(mgw_comm* comm /* NULL: single rank */, const mgw_tensor_desc* rows, int n_rows,
                      const mgw_group* groups, int n_groups, float scale, uint32_t flags,

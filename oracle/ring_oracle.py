@@ -13,6 +13,11 @@ Restates, step for step:
 * ``pack_group``         <- allreduce_net.py:499-509 (layer ``high`` at offset 0,
                             walking down to ``low``) and :546 (per-layer slice fill)
 * ``emulation_expected`` <- allreduce_net.py:507
+* ``ring_allreduce_bf16`` (extension; no reference counterpart): bf16
+                            inputs upcast exactly to fp32, the reference ring above
+                            (same fold order), times ``scale`` when != 1, rounded once
+                            to bf16 (round-to-nearest-even; ``bf16_round`` is pinned
+                            against torch's fp32 -> bf16 cast in tests/test_oracle.py)
 
 A C build of the same ring (``ring_oracle.c`` -> ``_build/libring_oracle.so``,
 one thread per simulated rank) is used when present; ``tests/test_oracle.py``
@@ -130,3 +135,27 @@ def unpack_group(bucket: np.ndarray, counts, low: int, high: int) -> dict:
 
 def emulation_expected(n_workers: int, layer: int) -> float:
     return float(n_workers * (n_workers + 1) // 2 + n_workers * (layer % 5))
+
+
+def bf16_to_f32(u16: np.ndarray) -> np.ndarray:
+    """bf16 bit patterns (uint16) -> float32, exact."""
+    return (np.asarray(u16, dtype=np.uint16).astype(np.uint32) << 16).view(np.float32)
+
+
+def bf16_round(x: np.ndarray) -> np.ndarray:
+    """float32 -> bf16 bit patterns, round to nearest even (NaN stays a quiet NaN)."""
+    u = np.asarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+    nan = np.isnan(np.asarray(x, dtype=np.float32))
+    if nan.any():
+        r[nan] = ((u[nan] >> 16) | 0x40).astype(np.uint16)
+    return r
+
+
+def ring_allreduce_bf16(rank_values_u16, scale: float = 1.0) -> np.ndarray:
+    """bf16 gradients with fp32 accumulation: the reference fold over upcast inputs,
+    scaled (fp32, only when ``scale != 1``) and rounded once.  Same bits on every rank."""
+    acc = ring_allreduce([bf16_to_f32(v) for v in rank_values_u16])[0]
+    if scale != 1.0:
+        acc = (acc * np.float32(scale)).astype(np.float32)
+    return bf16_round(acc)

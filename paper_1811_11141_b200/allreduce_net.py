@@ -131,7 +131,8 @@ class GradientBuffer:
     """Flat fp32 payload of the layer span ``[layer_low, layer_high]``.
 
     ``values`` is a contiguous little-endian float32 numpy copy (reference
-    semantics) or, zero-copy, a contiguous CUDA float32 torch tensor.
+    semantics) or, zero-copy, a contiguous CUDA float32 torch tensor -- or a bf16 one
+    (bf16 on the wire, fp32 accumulation, ``mgw_allreduce_fused_bf16``).
     """
 
     __slots__ = ("layer_low", "layer_high", "values")
@@ -144,8 +145,8 @@ class GradientBuffer:
         if _is_torch_tensor(values):
             import torch
 
-            if values.dtype != torch.float32 or values.dim() != 1 or not values.is_contiguous():
-                raise ValueError("tensor payloads must be contiguous 1-D float32")
+            if values.dtype not in (torch.float32, torch.bfloat16) or values.dim() != 1 or not values.is_contiguous():
+                raise ValueError("tensor payloads must be contiguous 1-D float32 or bfloat16")
             self.values = values
         else:
             self.values = np.ascontiguousarray(values, dtype=_F32)
@@ -383,9 +384,10 @@ class RingSession:
             raise ProtocolError(f"{who}: a peer never reached the collective within {self._timeout}s")
         raise ProtocolError(f"{who}: a peer aborted the collective")
 
-    def account(self, n: int, algo: int) -> None:
+    def account(self, n: int, algo: int, elem_bytes: int = 4) -> None:
         """NVLink payload accounting for one collective of n elements."""
         world, rank = self.config.n_workers, self.config.rank
+        w = elem_bytes
         sizes, _ = _segments(n, world)
         c = self.counters
         c.frames_sent += 1
@@ -396,13 +398,13 @@ class RingSession:
             c.payload_bytes_sent += 8 * n * (world - 1)
         elif algo == _native.ALGO_ONESHOT:
             c.rounds += 1
-            c.payload_bytes_received += 4 * n * (world - 1)
-            c.payload_bytes_sent += 4 * n * (world - 1)
+            c.payload_bytes_received += w * n * (world - 1)
+            c.payload_bytes_sent += w * n * (world - 1)
         else:
             c.rounds += 2
             mine = sizes[rank]
-            c.payload_bytes_received += 4 * ((world - 1) * mine + n - mine)
-            c.payload_bytes_sent += 4 * ((n - mine) + (world - 1) * mine)
+            c.payload_bytes_received += w * ((world - 1) * mine + n - mine)
+            c.payload_bytes_sent += w * ((n - mine) + (world - 1) * mine)
 
 
 def _segments(n_elements: int, n_parts: int) -> tuple[list[int], list[int]]:
@@ -453,8 +455,10 @@ def ring_allreduce(
     torch = session.torch
     values = buffer.values
     n = len(buffer)
-    if 4 * n > session.capacity_bytes:
-        raise ValueError(f"buffer of {4 * n} B exceeds the session capacity of {session.capacity_bytes} B")
+    bf16 = _is_torch_tensor(values) and values.dtype == torch.bfloat16
+    width = 2 if bf16 else 4
+    if width * n > session.capacity_bytes:
+        raise ValueError(f"buffer of {width * n} B exceeds the session capacity of {session.capacity_bytes} B")
     stream = session.stream
     numpy_payload = not _is_torch_tensor(values)
     with torch.cuda.device(session.device):
@@ -471,7 +475,12 @@ def ring_allreduce(
             ptr = values.data_ptr()
         algo = _algo_for(session, n, fused=True)
         handle = stream.cuda_stream
-        if n:
+        if n and bf16:
+            algo = _native.ALGO_ONESHOT if 2 * n <= session_oneshot_max(session) else _native.ALGO_TWOSHOT
+            table = session.table(ptr, n)
+            _native.call("mgw_allreduce_fused_bf16", session.comm, table.ptr, 1, n, ctypes.c_float(1.0),
+                         _native.ALGO_AUTO, handle)
+        elif n:
             # one kernel: pack -> all-reduce -> unpack, in place on the payload
             table = session.table(ptr, n)
             _native.call("mgw_allreduce_fused", session.comm, table.ptr, 1, n, ctypes.c_float(1.0),
@@ -482,7 +491,7 @@ def ring_allreduce(
         session.raise_if_failed()
         if numpy_payload and n:
             values[:] = session.staging(n)[:n].cpu().numpy()
-    session.account(n, algo)
+    session.account(n, algo, width)
     return buffer
 
 

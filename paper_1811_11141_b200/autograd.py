@@ -57,8 +57,8 @@ class MergedGradientSync:
         if plan.num_layers != len(self.params):
             raise ValueError(f"plan covers {plan.num_layers} layers, model has {len(self.params)} trainable tensors")
         for p in self.params:
-            if p.dtype != torch.float32:
-                raise ValueError("the B200 data path reduces fp32 gradients")
+            if p.dtype not in (torch.float32, torch.bfloat16):
+                raise ValueError("the B200 data path reduces fp32 or bf16 gradients")
         self.plan = plan
         self.comm, self.world, self.scale, self.algo = comm, world, float(scale), algo
         self.sync_after_backward = sync_after_backward
@@ -74,6 +74,13 @@ class MergedGradientSync:
             for layer in range(low, high + 1):
                 self.group_of[layer] = gid
         self.size = [high - low + 1 for low, high in self.groups]
+        # bf16 groups: bf16 on the wire, fp32 accumulation (mgw_group_launch_bf16)
+        self.bf16 = []
+        for low, high in self.groups:
+            kinds = {self.params[layer - 1].dtype for layer in range(low, high + 1)}
+            if len(kinds) != 1:
+                raise ValueError(f"group {(low, high)} mixes gradient dtypes {sorted(map(str, kinds))}")
+            self.bf16.append(kinds == {torch.bfloat16})
         self.count = [0] * len(self.groups)
         self.tables: dict[int, tuple] = {}
         self.events: dict[int, int] = {}
@@ -117,7 +124,8 @@ class MergedGradientSync:
         if self.comm is not None and self.world > 1:
             # one native call: event on the backward (current) stream -> comm stream waits
             # -> fused pack / all-reduce / unpack of the group
-            _native.call("mgw_group_launch", self.comm, table.ptr, table.n, n, ctypes.c_float(self.scale), self.algo,
+            fn = "mgw_group_launch_bf16" if self.bf16[gid] else "mgw_group_launch"
+            _native.call(fn, self.comm, table.ptr, table.n, n, ctypes.c_float(self.scale), self.algo,
                          torch.cuda.current_stream().cuda_stream, self.stream.cuda_stream, self._event(gid))
         elif self.scale != 1.0:
             ev = torch.cuda.Event()

@@ -27,6 +27,7 @@
 #include <vector>
 
 #include "allreduce.cuh"
+#include "bf16.cuh"
 #include "common.cuh"
 #include "fused.cuh"
 #include "ll.cuh"
@@ -298,6 +299,34 @@ int comm_allreduce_fused(mgw_comm* c, const Row* host_rows, const Row* dev_rows,
     return launch_ll(l, c->max_ctas, stream);
   }
   return launch_fused(f, chosen, c->max_ctas, stream, c->vec_per_cta);
+}
+
+// bf16 group exchange with fp32 accumulation (bf16.cuh): one-shot / two-shot only
+int comm_allreduce_fused_bf16(mgw_comm* c, const Row* host_rows, const Row* dev_rows, int n_rows, int64_t n,
+                              float scale, int algo, cudaStream_t stream, uint64_t* stamp = nullptr) {
+  if (n < 0 || n * 2 > c->slot_bytes)
+    return set_error(MGW_EINVAL, "bf16 bucket of %lld elements exceeds slot capacity %lld B", (long long)n,
+                     (long long)c->slot_bytes);
+  if (c->world > 1 && !c->peers_open) return set_error(MGW_EINVAL, "peers not opened (call mgw_comm_open_peers)");
+  if (n == 0 || n_rows == 0) return MGW_OK;
+  if (c->world == 1 && scale == 1.0f) return MGW_OK;  // nothing to exchange or scale
+  if (algo == MGW_ALGO_AUTO) algo = n * 2 <= c->oneshot_max_bytes ? MGW_ALGO_ONESHOT : MGW_ALGO_TWOSHOT;
+  FusedArgs f;
+  memset(&f, 0, sizeof(f));
+  f.ar = make_args(c, n);
+  if (c->world > 1 && c->gate) {
+    int rc = launch_gate(f.ar, stream);
+    if (rc) return rc;
+  }
+  f.ar.stamp = stamp;
+  if (c->world == 1) f.ar.flags = kNoBarrier;
+  f.use_inline = n_rows <= kInlineRows && host_rows != nullptr;
+  if (f.use_inline)
+    for (int k = 0; k < n_rows; ++k) f.inline_rows[k] = host_rows[k];
+  f.rows = dev_rows;
+  f.n_rows = n_rows;
+  f.scale = scale;
+  return launch_b16(f, algo, c->max_ctas, stream);
 }
 
 const mgw_table_t* as_table(const void* t) { return static_cast<const mgw_table_t*>(t); }
@@ -605,6 +634,18 @@ int mgw_allreduce_fused(mgw_comm* c, const void* table, int n_rows, int64_t n_el
   return comm_allreduce_fused(c, t->host.data(), t->dev, n_rows, n_elem, scale, algo, static_cast<cudaStream_t>(stream));
 }
 
+int mgw_allreduce_fused_bf16(mgw_comm* c, const void* table, int n_rows, int64_t n_elem, float scale, int algo,
+                             void* stream) {
+  if (!c) return set_error(MGW_EINVAL, "comm is null");
+  if (algo != MGW_ALGO_AUTO && algo != MGW_ALGO_ONESHOT && algo != MGW_ALGO_TWOSHOT)
+    return set_error(MGW_EINVAL, "bf16 buckets support AUTO, one-shot and two-shot (got %d)", algo);
+  int rc = check_table(table, n_rows, n_elem);
+  if (rc) return rc;
+  const mgw_table_t* t = as_table(table);
+  return comm_allreduce_fused_bf16(c, t->host.data(), t->dev, n_rows, n_elem, scale, algo,
+                                   static_cast<cudaStream_t>(stream));
+}
+
 int mgw_nvls_supported(int device, int* ok) {
   if (!ok) return set_error(MGW_EINVAL, "ok is null");
   *ok = 0;
@@ -711,6 +752,16 @@ int mgw_group_launch(mgw_comm* c, const void* table, int n_rows, int64_t n_elem,
   return mgw_allreduce_fused(c, table, n_rows, n_elem, scale, algo, ms);
 }
 
+int mgw_group_launch_bf16(mgw_comm* c, const void* table, int n_rows, int64_t n_elem, float scale, int algo,
+                          void* compute_stream, void* comm_stream, void* event) {
+  if (!event) return set_error(MGW_EINVAL, "event is null");
+  cudaStream_t cs = static_cast<cudaStream_t>(compute_stream);
+  cudaStream_t ms = static_cast<cudaStream_t>(comm_stream);
+  MGW_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(event), cs));
+  MGW_CUDA(cudaStreamWaitEvent(ms, static_cast<cudaEvent_t>(event), 0));
+  return mgw_allreduce_fused_bf16(c, table, n_rows, n_elem, scale, algo, ms);
+}
+
 int mgw_comm_error(mgw_comm* c, int* code) {
   if (!c || !code) return set_error(MGW_EINVAL, "bad arguments");
   MGW_CUDA(cudaSetDevice(c->device));
@@ -807,6 +858,46 @@ int mgw_allreduce_fused_emulated(void* const* tables, float* const* slots, int w
       f.ar.rank = r;
       f.ar.flags = kNoBarrier | kSkipPack | (phases == 1 ? 0 : (phase == 0 ? kSkipPhase2 : kSkipPhase1));
       int rc = launch_fused(f, algo, 2 * kSMs, s);
+      if (rc) return rc;
+    }
+  }
+  return MGW_OK;
+}
+
+int mgw_allreduce_fused_bf16_emulated(void* const* tables, void* const* slots, int world, int64_t n, float scale,
+                                      int algo, void* stream) {
+  if (!tables || !slots || world < 1 || world > kMaxRanks || n < 0)
+    return set_error(MGW_EINVAL, "bad emulated bf16 arguments");
+  if (algo != MGW_ALGO_ONESHOT && algo != MGW_ALGO_TWOSHOT)
+    return set_error(MGW_EINVAL, "emulated all-reduce needs an explicit algorithm");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (int r = 0; r < world; ++r) {
+    const mgw_table_t* t = as_table(tables[r]);
+    int rc = check_table(tables[r], t ? (int)t->host.size() : 0, n);
+    if (rc) return rc;
+  }
+  if (n == 0) return MGW_OK;
+  FusedArgs f;
+  memset(&f, 0, sizeof(f));
+  for (int r = 0; r < world; ++r) f.ar.slot[r] = static_cast<char*>(slots[r]);
+  f.ar.n = n;
+  f.ar.world = world;
+  f.scale = scale;
+  // step 0 packs every rank, then the one-shot fold, or the two-shot's two phases
+  const int steps = algo == MGW_ALGO_ONESHOT ? 2 : 3;
+  for (int step = 0; step < steps; ++step) {
+    for (int r = 0; r < world; ++r) {
+      const mgw_table_t* t = as_table(tables[r]);
+      const int n_rows = (int)t->host.size();
+      f.use_inline = n_rows <= kInlineRows;
+      if (f.use_inline)
+        for (int k = 0; k < n_rows; ++k) f.inline_rows[k] = t->host[k];
+      f.rows = t->dev;
+      f.n_rows = n_rows;
+      f.ar.rank = r;
+      f.ar.flags = kNoBarrier | (step == 0 ? kSkipPhase1 | kSkipPhase2
+                                           : kSkipPack | (step == 1 ? kSkipPhase2 : kSkipPhase1));
+      int rc = launch_b16(f, algo, 2 * kSMs, s);
       if (rc) return rc;
     }
   }

@@ -206,3 +206,69 @@ def replan_task(config, session, *, iterations=4):
     m = planner.model
     return {"verified": ok, "samples": len(planner.samples), "a": m.a, "b": m.b,
             "consistent": (new or planner.plan) == find_merge_plan(profile, m)}
+
+
+def bf16_task(config, session, *, sizes):
+    """bf16 payloads (seeded per rank) through ring_allreduce (AUTO) and each explicit
+    algorithm of mgw_allreduce_fused_bf16; inputs and outputs as uint16 bit patterns."""
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    from paper_1811_11141_b200 import GradientBuffer, _native
+
+    out = {}
+    h = session.stream.cuda_stream
+    for n in sizes:
+        g = torch.Generator().manual_seed(11 * n + config.rank)
+        vals = (torch.randn(n, generator=g) * 4).to(torch.bfloat16)
+        out[("in", n)] = vals.view(torch.int16).numpy().view(np.uint16).copy()
+        t = vals.to(session.device)
+        ring_allreduce(GradientBuffer(1, 1, t), config, session)
+        out[("auto", n)] = t.view(torch.int16).cpu().numpy().view(np.uint16)
+        for name, algo in (("one", _native.ALGO_ONESHOT), ("two", _native.ALGO_TWOSHOT)):
+            t = vals.to(session.device)
+            table = _native.DeviceTable([(t.data_ptr(), n, 0)])
+            with torch.cuda.device(session.device):
+                session.stream.wait_stream(torch.cuda.current_stream(session.device))
+                _native.call("mgw_allreduce_fused_bf16", session.comm, table.ptr, 1, n, ctypes.c_float(0.5), algo, h)
+                session.stream.synchronize()
+            session.raise_if_failed()
+            out[(name, n)] = t.view(torch.int16).cpu().numpy().view(np.uint16)
+            table.close()
+    out["bytes_received"] = session.counters.payload_bytes_received
+    return out
+
+
+def autograd_bf16_task(config, session):
+    """bf16 parameters: merged-gradient sync moves bf16, folds in fp32, averages."""
+    import numpy as np
+    import torch
+
+    from paper_1811_11141_b200 import MergePlan
+    from paper_1811_11141_b200.autograd import MergedGradientSync, trainable_parameters
+
+    g = torch.Generator().manual_seed(0)
+    ws = [torch.nn.Parameter(torch.randn(n, generator=g).to(torch.bfloat16).to(session.device))
+          for n in (16448, 257, 2570, 10)]
+    g2 = torch.Generator(device=session.device).manual_seed(1000 + config.rank)
+    xs = [torch.randn(w.numel(), device=session.device, generator=g2).to(torch.bfloat16) for w in ws]
+
+    def loss():
+        return sum((w * x).float().sin().square().sum() for w, x in zip(ws, xs))
+
+    for w in ws:
+        w.grad = None
+    loss().backward()
+    local = [w.grad.view(torch.int16).cpu().numpy().view(np.uint16).copy() for w in ws]
+    for w in ws:
+        w.grad = None
+    sync = MergedGradientSync(ws, MergePlan(frozenset({2, 4}), 4), comm=session.comm, world=config.n_workers,
+                              scale=1.0 / config.n_workers)
+    loss().backward()
+    sync.finish()
+    torch.cuda.synchronize()
+    session.raise_if_failed()
+    sync.close()
+    return local, [w.grad.view(torch.int16).cpu().numpy().view(np.uint16).copy() for w in ws]

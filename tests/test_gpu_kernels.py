@@ -234,3 +234,58 @@ def test_fused_exchange_many_rows_from_device_table(torch_cuda):
     want = ring_oracle.ring_allreduce(buckets)[0]
     got = np.concatenate([t.cpu().numpy() for t in tensors[2]])
     assert np.array_equal(got.view("<u4"), want.view("<u4"))
+
+
+@pytest.mark.parametrize("algo", [_native.ALGO_ONESHOT, _native.ALGO_TWOSHOT])
+@pytest.mark.parametrize("n_ranks", [1, 2, 3, 4, 5, 8])
+@pytest.mark.parametrize("shift,scale", [(0, 1.0), (1, 1.0), (3, 0.125)])
+def test_bf16_exchange_bit_exact(torch_cuda, algo, n_ranks, shift, scale):
+    """bf16 gradients, fp32 accumulation: fused pack -> fold -> write-back
+    equals the oracle (reference fold over upcast inputs, rounded once), bit for bit, for odd
+    row sizes, misaligned tensors, segment-straddling slots and an n % 8 tail."""
+    torch = torch_cuda
+    counts = [9408, 4096, 1001, 3, 36864, 17, 2049, 8, 7]  # layer high first
+    total = sum(counts)
+    rng = np.random.default_rng(300 + n_ranks)
+    host = [[ring_oracle.bf16_round((rng.standard_normal(p) * 10.0 ** rng.integers(-3, 4, p)).astype("<f4"))
+             for p in counts] for _ in range(n_ranks)]
+    tensors, tables, slots = [], [], []
+    for r in range(n_ranks):
+        ts, rows, off = [], [], 0
+        for h, p in zip(host[r], counts):
+            base = torch.empty(p + shift, dtype=torch.bfloat16, device="cuda")
+            t = base[shift:]
+            t.copy_(torch.from_numpy(h.view(np.int16)).view(torch.bfloat16))
+            ts.append(t)
+            rows.append((t.data_ptr(), p, off))
+            off += p
+        tensors.append(ts)
+        tables.append(_native.DeviceTable(rows))
+        slots.append(torch.full((total,), float("nan"), dtype=torch.bfloat16, device="cuda"))
+    tp = (ctypes.c_void_p * n_ranks)(*[t.ptr for t in tables])
+    sp = (ctypes.c_void_p * n_ranks)(*[x.data_ptr() for x in slots])
+    _native.call("mgw_allreduce_fused_bf16_emulated", tp, sp, n_ranks, total, ctypes.c_float(scale), algo,
+                 torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    for t in tables:
+        t.close()
+    want = ring_oracle.ring_allreduce_bf16([np.concatenate(host[r]) for r in range(n_ranks)], scale=scale)
+    off = 0
+    for k, p in enumerate(counts):
+        for r in range(n_ranks):
+            got = tensors[r][k].view(torch.int16).cpu().numpy().view(np.uint16)
+            bad = np.flatnonzero(got != want[off:off + p])
+            assert bad.size == 0, (r, k, bad.size, int(bad[0]))
+        off += p
+
+
+def test_bf16_rejects_unsupported_algorithms(torch_cuda):
+    torch = torch_cuda
+    t = torch.zeros(64, dtype=torch.bfloat16, device="cuda")
+    table = _native.DeviceTable([(t.data_ptr(), 64, 0)])
+    tp = (ctypes.c_void_p * 2)(table.ptr, table.ptr)
+    sp = (ctypes.c_void_p * 2)(t.data_ptr(), t.data_ptr())
+    with pytest.raises(ValueError):
+        _native.call("mgw_allreduce_fused_bf16_emulated", tp, sp, 2, 64, ctypes.c_float(1.0), _native.ALGO_LL,
+                     torch.cuda.current_stream().cuda_stream)
+    table.close()

@@ -198,3 +198,34 @@ def test_online_replanning_from_live_spans():
         assert r["verified"] and r["consistent"]
         assert r["samples"] == 4 * 54
         assert 0 <= r["a"] < 1e-3 and 0 < r["b"] < 1e-9  # µs-class startup, > 1 GB/s
+
+
+def test_bf16_exchange_over_ipc_vs_oracle():
+    """bf16 on the wire, fp32 accumulation, one rounding: bit-exact vs the oracle for the
+    AUTO path (scale 1) and both explicit algorithms (scale 1/2); half the fp32 bytes."""
+    from oracle import ring_oracle
+
+    sizes = (1, 17, 1001, 4099, 65543, 1 << 20)
+    for n in _worlds():
+        res = run_workers(n, partial(_mp_tasks.bf16_task, sizes=sizes))
+        for size in sizes:
+            ins = [res[r][("in", size)] for r in range(n)]
+            want1 = ring_oracle.ring_allreduce_bf16(ins)
+            want_half = ring_oracle.ring_allreduce_bf16(ins, scale=0.5)
+            for r in range(n):
+                assert np.array_equal(res[r][("auto", size)], want1), (n, size, r)
+                assert np.array_equal(res[r][("one", size)], want_half), (n, size, r, "one")
+                assert np.array_equal(res[r][("two", size)], want_half), (n, size, r, "two")
+
+
+def test_autograd_bf16_parameters():
+    from oracle import ring_oracle
+
+    n = max(_worlds())
+    res = run_workers(n, _mp_tasks.autograd_bf16_task)
+    for low, high in MergePlan(frozenset({2, 4}), 4).groups():
+        buckets = [np.concatenate([res[r][0][layer - 1] for layer in range(high, low - 1, -1)]) for r in range(n)]
+        want = ring_oracle.ring_allreduce_bf16(buckets, scale=1.0 / n)
+        for r in range(n):
+            got = np.concatenate([res[r][1][layer - 1] for layer in range(high, low - 1, -1)])
+            assert np.array_equal(got, want), (low, high, r, int(np.count_nonzero(got != want)))

@@ -73,3 +73,33 @@ def test_pack_layout_high_layer_first():
     back = ring_oracle.unpack_group(bucket, counts, 1, 4)
     assert set(back) == {1, 3, 4} and all(np.array_equal(back[k], vals[k]) for k in back)
     assert ring_oracle.emulation_expected(4, 7) == 10 + 4 * 2
+
+
+def test_bf16_rounding_matches_torch_cast():
+    import torch
+
+    from oracle import ring_oracle
+
+    rng = np.random.default_rng(5)
+    x = np.concatenate([rng.standard_normal(20000).astype(np.float32) * 10.0 ** rng.integers(-30, 30, 20000),
+                        np.array([0.0, -0.0, 1.0 + 2.0 ** -8, 1.0 + 3 * 2.0 ** -8, 3.3895314e38, 1e-40, -1e-40],
+                                 dtype=np.float32)]).astype(np.float32)
+    want = torch.from_numpy(x).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    assert np.array_equal(ring_oracle.bf16_round(x), want)
+    assert np.array_equal(ring_oracle.bf16_to_f32(want), torch.from_numpy(want.view(np.int16)).view(torch.bfloat16).float().numpy())
+
+
+def test_bf16_ring_is_fp32_fold_rounded_once():
+    from oracle import ring_oracle
+
+    rng = np.random.default_rng(9)
+    for n_ranks in (2, 3, 8):
+        ins = [ring_oracle.bf16_round(rng.standard_normal(1001).astype(np.float32)) for _ in range(n_ranks)]
+        got = ring_oracle.ring_allreduce_bf16(ins)
+        folded = ring_oracle.ring_allreduce([ring_oracle.bf16_to_f32(v) for v in ins])[0]
+        assert np.array_equal(got, ring_oracle.bf16_round(folded))
+        # integers are exact in both formats: the reference's exact-sum pattern survives
+        ones = [ring_oracle.bf16_round(np.full(17, r + 1, np.float32)) for r in range(n_ranks)]
+        assert np.all(ring_oracle.bf16_to_f32(ring_oracle.ring_allreduce_bf16(ones)) == n_ranks * (n_ranks + 1) / 2)
+        half = ring_oracle.ring_allreduce_bf16(ones, scale=0.5)
+        assert np.all(ring_oracle.bf16_to_f32(half) == n_ranks * (n_ranks + 1) / 4)
