@@ -165,7 +165,7 @@ def _exchange_times(comm, world, device, sizes, kind=0, algo=0, repeats=20, warm
     scratch = torch.ones(max(sizes) // 4, dtype=torch.float32, device=device)
     local_bucket = torch.empty_like(scratch) if world == 1 else None
     for nbytes in sizes:
-        n = nbytes // 4
+        n = nbytes // (2 if kind == 5 else 4)  # kind 5: bf16 elements
         table = _native.DeviceTable([(scratch.data_ptr(), n, 0)])
         sec = ctypes.c_double()
         _native.call("mgw_time_exchange", comm, table.ptr, 1, n,
@@ -176,7 +176,7 @@ def _exchange_times(comm, world, device, sizes, kind=0, algo=0, repeats=20, warm
     return _max_over_ranks(out, world, device)
 
 
-def _nccl_times(world, device, sizes, repeats=20, warmups=3):
+def _nccl_times(world, device, sizes, repeats=20, warmups=3, bf16=False):
     """ncclAllReduce (torch.distributed, comparison only), same loop timing."""
     import torch
     import torch.distributed as dist
@@ -184,11 +184,12 @@ def _nccl_times(world, device, sizes, repeats=20, warmups=3):
     from paper_1811_11141_b200 import _native
 
     stream = torch.cuda.Stream(device=device)
-    buf = torch.ones(max(sizes) // 4, dtype=torch.float32, device=device)
+    width = 2 if bf16 else 4
+    buf = torch.ones(max(sizes) // width, dtype=torch.bfloat16 if bf16 else torch.float32, device=device)
     out = []
     with torch.cuda.stream(stream):
         for nbytes in sizes:
-            x = buf[: nbytes // 4]
+            x = buf[: nbytes // width]
             for _ in range(warmups):
                 dist.all_reduce(x)
             _native.call("mgw_spin_ns", 1_000_000 + 20_000 * repeats, stream.cuda_stream)
@@ -204,7 +205,8 @@ def _nccl_times(world, device, sizes, repeats=20, warmups=3):
 
 def _allreduce_sweep(session, comm, world, device, sizes, with_nvls=False):
     """Bus GB/s vs size: our one-shot and two-shot kernels alone, the full group
-    exchange (pack + all-reduce + unpack), and ncclAllReduce."""
+    exchange (pack + all-reduce + unpack), and ncclAllReduce; the bf16 group exchange
+    (bf16 wire, fp32 accumulation) vs NCCL bf16 at the same payload bytes."""
     from paper_1811_11141_b200 import _native
 
     one = _exchange_times(comm, world, device, sizes, kind=1, algo=_native.ALGO_ONESHOT)
@@ -223,6 +225,10 @@ def _allreduce_sweep(session, comm, world, device, sizes, with_nvls=False):
     except Exception as exc:  # unsupported fabric: leave the column out
         print(f"NVLS unavailable: {exc}", file=sys.stderr)
     fused = _exchange_times(comm, world, device, sizes, kind=4)
+    # bf16 gradients (fp32 accumulation) at the same payload bytes, vs NCCL bf16
+    fused_bf16 = _exchange_times(comm, world, device, sizes, kind=5)
+    nccl_bf16 = _nccl_times(world, device, sizes, bf16=True)
+    session.raise_if_failed()
     rows = []
     for i, (nbytes, t1, t2, tn) in enumerate(zip(sizes, one, two, nccl)):
         bus = 2 * (world - 1) / world * nbytes
@@ -231,7 +237,11 @@ def _allreduce_sweep(session, comm, world, device, sizes, with_nvls=False):
                      "twoshot_us": round(t2 * 1e6, 2), "twoshot_busbw_gbs": round(bus / t2 / 1e9, 1),
                      "nccl_us": round(tn * 1e6, 2), "nccl_busbw_gbs": round(bus / tn / 1e9, 1),
                      "fused_exchange_us": round(fused[i] * 1e6, 2),
-                     "fused_exchange_busbw_gbs": round(bus / fused[i] / 1e9, 1)})
+                     "fused_exchange_busbw_gbs": round(bus / fused[i] / 1e9, 1),
+                     "fused_bf16_us": round(fused_bf16[i] * 1e6, 2),
+                     "fused_bf16_busbw_gbs": round(bus / fused_bf16[i] / 1e9, 1),
+                     "nccl_bf16_us": round(nccl_bf16[i] * 1e6, 2),
+                     "nccl_bf16_busbw_gbs": round(bus / nccl_bf16[i] / 1e9, 1)})
         if nvls is not None:
             rows[-1]["nvls_fused_us"] = round(nvls[i] * 1e6, 2)
             rows[-1]["nvls_fused_busbw_gbs"] = round(bus / nvls[i] / 1e9, 1)

@@ -910,19 +910,20 @@ int mgw_allreduce_fused_bf16_emulated(void* const* tables, void* const* slots, i
 // unpack into `local_bucket`), 1 = all-reduce kernel only, 2 = pack only, 3 = unpack only.
 int mgw_time_exchange(mgw_comm* c, const void* table, int n_rows, int64_t n_elem, float* local_bucket, int algo,
                       int kind, int reps, int warmups, double* seconds_per_rep, void* stream) {
-  if (reps < 1 || warmups < 0 || !seconds_per_rep || n_elem <= 0 || kind < 0 || kind > 4)
+  if (reps < 1 || warmups < 0 || !seconds_per_rep || n_elem <= 0 || kind < 0 || kind > 5)
     return set_error(MGW_EINVAL, "bad timing arguments");
   int rc = check_table(table, n_rows, n_elem);
   if (rc) return rc;
   const mgw_table_t* t = as_table(table);
   const bool multi = c && c->world > 1;
   if (!multi && !local_bucket) return set_error(MGW_EINVAL, "single-rank timing needs a local bucket");
-  if ((kind == 1 || kind == 4) && !multi)
+  if ((kind == 1 || kind == 4 || kind == 5) && !multi)
     return set_error(MGW_EINVAL, "all-reduce timing needs a multi-rank communicator");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   auto step = [&]() -> int {
     int r = MGW_OK;
     if (kind == 4) return comm_allreduce_fused(c, t->host.data(), t->dev, n_rows, n_elem, 1.f, algo, s);
+    if (kind == 5) return comm_allreduce_fused_bf16(c, t->host.data(), t->dev, n_rows, n_elem, 1.f, algo, s);
     if (multi) {
       if (kind == 0 || kind == 2) r = comm_pack(c, t->host.data(), t->dev, n_rows, n_elem, 1.f, s);
       if (r == MGW_OK && (kind == 0 || kind == 1)) r = comm_allreduce(c, n_elem, algo, s);
