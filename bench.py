@@ -354,7 +354,7 @@ def run_ours(args) -> dict | None:
         comm = session.comm
 
     # 1. fit the startup/bandwidth model of one group exchange on this box
-    exch = _exchange_times(comm, world, device, FIT_SIZES, kind=4 if (world > 1 and not args.unfused) else 0,
+    exch = _exchange_times(comm, world, device, FIT_SIZES, kind=0 if args.unfused else 4,
                            repeats=3 if args.quick else 20, warmups=1 if args.quick else 3)
     if session is not None:
         session.raise_if_failed()
@@ -390,27 +390,37 @@ def run_ours(args) -> dict | None:
     # roofline of the dominant kernel inside the MG-WFBP timed region; kernel spans are
     # %globaltimer stamps written by the kernels (first CTA entry .. last CTA exit)
     steps = len(kern)
-    spans = {"pack": sum(sum(k[0]) for k in kern), "unpack": sum(sum(k[2]) for k in kern)}
-    if world > 1:
-        spans["allreduce"] = sum(sum(k[1]) for k in kern)
+    fused = not args.unfused
+    if fused:  # one kernel per group (N = 1: pack -> one-input fold -> write-back)
+        spans = {"fused": sum(sum(k[1]) for k in kern)}
+    else:
+        spans = {"pack": sum(sum(k[0]) for k in kern), "unpack": sum(sum(k[2]) for k in kern)}
+        if world > 1:
+            spans["allreduce"] = sum(sum(k[1]) for k in kern)
     dominant = max(spans, key=spans.get)
     total_bytes = sum(gbytes)
     sending = sum(1 for b in gbytes if b)
     hbm_peak, hbm_src = peaks()
-    if dominant in ("pack", "unpack"):
-        per_step = 2 * total_bytes  # read + write of every bucket byte
+    names = {"pack": "K1 pack", "unpack": "K4 unpack", "allreduce": "K2/K3 all-reduce",
+             "fused": "fused K1+K4 (N=1)" if world == 1 else "fused K1+K2/K3+K4"}
+    if world == 1 or dominant in ("pack", "unpack"):
+        # HBM: pack / unpack read + write every bucket byte once; the N=1 fused kernel does both
+        per_unit = 4 if dominant == "fused" else 2
+        per_step = per_unit * total_bytes
         achieved = per_step * steps / spans[dominant] / 1e9
-        roofline = {"bound": "hbm", "kernel": "K1 pack" if dominant == "pack" else "K4 unpack",
+        roofline = {"bound": "hbm", "kernel": names[dominant],
                     "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-                    "frac": round(achieved / hbm_peak, 4), "peak_source": hbm_src}
+                    "frac": round(achieved / hbm_peak, 4), "peak_source": hbm_src,
+                    "algorithmic_bytes": f"{per_unit} x group bucket bytes per launch"}
     else:
-        per_step = int(2 * (world - 1) / world * total_bytes)  # nccl-tests bus bytes
-        achieved = per_step * steps / spans["allreduce"] / 1e9
-        roofline = {"bound": "nvlink",
-                    "kernel": "fused K1+K2/K3+K4" if (not args.unfused) else "K2/K3 all-reduce",
+        per_unit = 2 * (world - 1) / world
+        per_step = int(per_unit * total_bytes)  # nccl-tests bus bytes
+        achieved = per_step * steps / spans[dominant] / 1e9
+        roofline = {"bound": "nvlink", "kernel": names[dominant],
                     "achieved": round(achieved, 1),
                     "peak": NVLINK_PEAK_GBS, "unit": "GB/s", "frac": round(achieved / NVLINK_PEAK_GBS, 4),
-                    "peak_source": "measured peer copy per direction, B200_PROFILING.md (900 nominal)"}
+                    "peak_source": "measured peer copy per direction, B200_PROFILING.md (900 nominal)",
+                    "algorithmic_bytes": "2(N-1)/N x group bucket bytes per launch (bus bytes)"}
     roofline.update({
         "bytes_per_step": per_step,
         "launches_per_step": sending,
@@ -424,12 +434,9 @@ def run_ours(args) -> dict | None:
     if traffic_file.exists():
         roofline["traffic"] = json.loads(traffic_file.read_text()).get(f"{roofline['kernel']}@N{world}")
     # the same kernel on the whole-model bucket, back to back under one event pair
-    big_kind = {"pack": 2, "allreduce": 1 if args.unfused else 4, "unpack": 3}[dominant] if world > 1 else 2
+    big_kind = {"pack": 2, "allreduce": 1, "unpack": 3, "fused": 4}[dominant]
     big = _exchange_times(comm, world, device, [4 * profile.total_params], kind=big_kind)[0]
-    if dominant in ("pack", "unpack") or world == 1:
-        big_bw = 2 * 4 * profile.total_params / big / 1e9
-    else:
-        big_bw = 2 * (world - 1) / world * 4 * profile.total_params / big / 1e9
+    big_bw = per_unit * 4 * profile.total_params / big / 1e9
     roofline["whole_model_bucket"] = {"bytes": 4 * profile.total_params, "us": round(big * 1e6, 2),
                                       "achieved": round(big_bw, 1),
                                       "frac": round(big_bw / (hbm_peak if roofline["bound"] == "hbm" else NVLINK_PEAK_GBS), 4),
@@ -497,7 +504,7 @@ def run_ours(args) -> dict | None:
             "parallelism": f"dp{world}",
             "l2": "flushed between iterations (256 MiB write on the compute stream, outside the timed events)",
             "cuda_graph": not args.no_graph,
-            "fused_group_kernel": world > 1 and not args.unfused,
+            "fused_group_kernel": not args.unfused,
         },
         "strategies": results,
         "mgwfbp_plan_equals_wfbp": same_as_wfbp,

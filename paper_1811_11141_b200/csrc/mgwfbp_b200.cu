@@ -301,6 +301,28 @@ int comm_allreduce_fused(mgw_comm* c, const Row* host_rows, const Row* dev_rows,
   return launch_fused(f, chosen, c->max_ctas, stream, c->vec_per_cta);
 }
 
+// Single rank: the group's fused kernel with N = 1 -- pack into the local bucket, the
+// one-input fold, write back -- one launch per group like the multi-rank path.  Every
+// thread re-reads only the bucket slots it packed itself, so no barrier is needed.
+int local_fused(float* bucket, const Row* host_rows, const Row* dev_rows, int n_rows, int64_t n, float scale,
+                cudaStream_t stream, uint64_t* stamp = nullptr) {
+  if (n == 0 || n_rows == 0) return MGW_OK;
+  FusedArgs f;
+  memset(&f, 0, sizeof(f));
+  f.ar.slot[0] = reinterpret_cast<char*>(bucket);
+  f.ar.n = n;
+  f.ar.world = 1;
+  f.ar.flags = kNoBarrier;
+  f.ar.stamp = stamp;
+  f.use_inline = n_rows <= kInlineRows && host_rows != nullptr;
+  if (f.use_inline)
+    for (int k = 0; k < n_rows; ++k) f.inline_rows[k] = host_rows[k];
+  f.rows = dev_rows;
+  f.n_rows = n_rows;
+  f.scale = scale;
+  return launch_fused(f, MGW_ALGO_ONESHOT, 2 * kSMs, stream);
+}
+
 // bf16 group exchange with fp32 accumulation (bf16.cuh): one-shot / two-shot only
 int comm_allreduce_fused_bf16(mgw_comm* c, const Row* host_rows, const Row* dev_rows, int n_rows, int64_t n,
                               float scale, int algo, cudaStream_t stream, uint64_t* stamp = nullptr) {
@@ -626,10 +648,11 @@ int mgw_allreduce_fused(mgw_comm* c, const void* table, int n_rows, int64_t n_el
   if (c->world == 1) {
     // nothing to exchange: the reduced value is the (scaled) local gradient
     if (scale == 1.0f) return MGW_OK;
-    rc = comm_pack(c, t->host.data(), t->dev, n_rows, n_elem, scale, static_cast<cudaStream_t>(stream));
-    if (rc) return rc;
-    return launch_rows<RowOp::kUnpack>(t->host.data(), t->dev, n_rows, reinterpret_cast<float*>(c->region + kSlotOff),
-                                       n_elem, 1.f, nullptr, nullptr, 0, nullptr, static_cast<cudaStream_t>(stream));
+    if (n_elem * 4 > c->slot_bytes)
+      return set_error(MGW_EINVAL, "bucket of %lld elements exceeds slot capacity %lld B", (long long)n_elem,
+                       (long long)c->slot_bytes);
+    return local_fused(reinterpret_cast<float*>(c->region + kSlotOff), t->host.data(), t->dev, n_rows, n_elem, scale,
+                       static_cast<cudaStream_t>(stream));
   }
   return comm_allreduce_fused(c, t->host.data(), t->dev, n_rows, n_elem, scale, algo, static_cast<cudaStream_t>(stream));
 }
@@ -917,12 +940,14 @@ int mgw_time_exchange(mgw_comm* c, const void* table, int n_rows, int64_t n_elem
   const mgw_table_t* t = as_table(table);
   const bool multi = c && c->world > 1;
   if (!multi && !local_bucket) return set_error(MGW_EINVAL, "single-rank timing needs a local bucket");
-  if ((kind == 1 || kind == 4 || kind == 5) && !multi)
+  if ((kind == 1 || kind == 5) && !multi)
     return set_error(MGW_EINVAL, "all-reduce timing needs a multi-rank communicator");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   auto step = [&]() -> int {
     int r = MGW_OK;
-    if (kind == 4) return comm_allreduce_fused(c, t->host.data(), t->dev, n_rows, n_elem, 1.f, algo, s);
+    if (kind == 4)
+      return multi ? comm_allreduce_fused(c, t->host.data(), t->dev, n_rows, n_elem, 1.f, algo, s)
+                   : local_fused(local_bucket, t->host.data(), t->dev, n_rows, n_elem, 1.f, s);
     if (kind == 5) return comm_allreduce_fused_bf16(c, t->host.data(), t->dev, n_rows, n_elem, 1.f, algo, s);
     if (multi) {
       if (kind == 0 || kind == 2) r = comm_pack(c, t->host.data(), t->dev, n_rows, n_elem, 1.f, s);
@@ -1054,8 +1079,8 @@ int mgw_sched_create(mgw_comm* comm, const mgw_tensor_desc* rows, int n_rows, co
     launches += 1;  // spin
     if (groups[g].n_elem == 0) continue;
     launches += (flags & MGW_SCHED_FILL) ? 1 : 0;  // gradient production
-    if (world > 1 && (flags & MGW_SCHED_FUSED))
-      launches += 1;                               // fused pack + all-reduce + unpack
+    if (flags & MGW_SCHED_FUSED)
+      launches += 1 + (world > 1 && comm->gate ? 1 : 0);  // (gate +) fused pack + all-reduce + unpack
     else
       launches += world > 1 ? 3 : 2;               // pack (+ all-reduce) + unpack
   }
@@ -1115,7 +1140,10 @@ static int sched_enqueue(mgw_sched* s, cudaStream_t cs, cudaStream_t ms) {
     MGW_CUDA(cudaStreamWaitEvent(ms, s->dep_ready[g], 0));
     if (gr.n_elem == 0) continue;  // silent group: nothing to send (allreduce_net.py:549)
     int rc;
-    if (s->world == 1) {
+    if (s->world == 1 && (s->flags & MGW_SCHED_FUSED)) {
+      rc = local_fused(s->local_bucket, hrows, grows, gr.desc_count, gr.n_elem, s->scale, ms, st + 2);
+      if (rc) return rc;
+    } else if (s->world == 1) {
       rc = launch_rows<RowOp::kPack>(hrows, grows, gr.desc_count, s->local_bucket, gr.n_elem, s->scale, nullptr, nullptr,
                                      0, nullptr, ms, st);
       if (rc) return rc;

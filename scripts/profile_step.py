@@ -1,11 +1,12 @@
 """ncu workload: exactly the bench's N=1 MG-WFBP iteration (B200 ResNet-50 profile, the
-plan bench.py derives, CUDA graph, per-group fill + pack + unpack), run ITERS times.
+plan bench.py derives, CUDA graph, per-group fill + one fused group kernel), run ITERS times.
 
-    ncu --set full --kernel-name-base demangled -k regex:'rows_kernel<\\(mgw::RowOp\\)0' \\
+    ncu --set full --kernel-name-base demangled -k regex:'fused_oneshot_kernel<1>' \\
         python scripts/profile_step.py --iters 1
 
-prints the per-group algorithmic pack bytes (2 x group bytes: read layers + write bucket)
-as JSON so scripts/summarize_step.py can pair them with ncu's per-launch dram bytes.
+writes the per-group algorithmic bytes of the fused N=1 kernel (4 x group bytes: read
+layers, write bucket, read bucket, write layers) as JSON so scripts/summarize_step.py can
+pair them with ncu's per-launch dram bytes.
 """
 
 from __future__ import annotations
@@ -36,7 +37,7 @@ def main():
     exch = bench._exchange_times(None, 1, device, bench.FIT_SIZES, kind=0, repeats=3, warmups=1)
     model, _ = bench._fit(bench.FIT_SIZES, exch, 1)
     plan = find_merge_plan(profile, model)
-    it = OverlappedIteration(profile, plan, comm=None, rank=0, world=1, device=device, graph=True)
+    it = OverlappedIteration(profile, plan, comm=None, rank=0, world=1, device=device, graph=True, fused=True)
     try:
         for _ in range(args.iters):
             it.run()
@@ -45,7 +46,8 @@ def main():
         groups = [b for b in it.group_bytes() if b]
     finally:
         it.close()
-    out = {"groups": len(groups), "pack_algorithmic_bytes": [2 * b for b in groups], "verified": bool(ok)}
+    out = {"groups": len(groups), "algorithmic_bytes": [4 * b for b in groups], "verified": bool(ok),
+           "kernel": "fused K1+K4 (N=1)"}
     pathlib.Path(args.out).parent.mkdir(parents=True, exist_ok=True)
     pathlib.Path(args.out).write_text(json.dumps(out))
     print(json.dumps({k: out[k] for k in ("groups", "verified")}))

@@ -1,9 +1,10 @@
 """Pair an ncu --set full capture of the bench's N=1 step (scripts/profile_step.py) with
-the per-group algorithmic bytes: DRAM traffic per K1 pack launch vs algorithmic bytes.
+the per-group algorithmic bytes: DRAM traffic per launch of the dominant kernel (the
+fused N=1 group kernel) vs algorithmic bytes.
 
     python scripts/summarize_step.py step.ncu-rep profile_step_groups.json out.json
 
-Writes the summary and merges ``"K1 pack@N1"`` (mean dram read+write bytes per launch)
+Writes the summary and merges ``"<kernel>@N1"`` (mean dram read+write bytes per launch)
 into profiles/roofline_traffic.json, which bench.py reports as ``roofline.traffic``.
 """
 
@@ -35,23 +36,24 @@ def main():
              "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "ns": 1e-9, "us": 1e-6, "ms": 1e-3}
     launches = []
     for r in rows[2:]:
-        if "RowOp)0" not in r[col["Kernel Name"]]:
+        if "fused_oneshot_kernel<1>" not in r[col["Kernel Name"]]:
             continue
         get = lambda k: _num(r[col[k]]) * scale.get(units[col[k]], 1)  # noqa: E731
         launches.append({"us": get("gpu__time_duration.sum") * 1e6,
                          "dram_bytes": get("dram__bytes_read.sum") + get("dram__bytes_write.sum"),
                          "dram_pct": _num(r[col["gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"]]),
                          "grid": int(_num(r[col["launch__grid_size"]]))})
-    alg = json.loads(pathlib.Path(groups_path).read_text())["pack_algorithmic_bytes"]
+    meta = json.loads(pathlib.Path(groups_path).read_text())
+    alg = meta["algorithmic_bytes"]
     n = min(len(alg), len(launches))
     if n == 0:
-        raise SystemExit("no pack launches in the capture")
+        raise SystemExit("no fused N=1 launches in the capture")
     launches, alg = launches[:n], alg[:n]
     mean_traffic = sum(l["dram_bytes"] for l in launches) / n
     mean_alg = sum(alg) / n
     summary = {
         "what": "ncu --set full --clock-control none of the bench's N=1 MG-WFBP step (scripts/profile_step.py), "
-                "K1 pack launches in send order; ncu serialises and cold-starts every launch",
+                "fused N=1 group kernel launches in send order; ncu serialises and cold-starts every launch",
         "launches": n,
         "mean_algorithmic_bytes": round(mean_alg),
         "mean_dram_bytes": round(mean_traffic),
@@ -62,7 +64,7 @@ def main():
     pathlib.Path(out_path).write_text(json.dumps(summary, indent=1))
     tf = ROOT / "profiles" / "roofline_traffic.json"
     merged = json.loads(tf.read_text()) if tf.exists() else {}
-    merged["K1 pack@N1"] = round(mean_traffic)
+    merged[f"{meta['kernel']}@N1"] = round(mean_traffic)
     merged["_note"] = ("mean dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel "
                        "from one ncu --set full capture (scripts/summarize_step.py); multi-rank kernels "
                        "cannot be replayed by ncu, so N>1 stays null")

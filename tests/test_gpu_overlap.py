@@ -80,6 +80,14 @@ def test_launch_count_reported(torch_cuda):
         assert it.launches_per_iteration == 2 + 4 * profile.num_layers
     finally:
         it.close()
+    it = OverlappedIteration(profile, None, comm=None, rank=0, world=1, device="cuda:0", fused=True)
+    try:
+        # per group: spin, fill, one fused kernel
+        assert it.launches_per_iteration == 2 + 3 * profile.num_layers
+        it.run()
+        assert it.verify()
+    finally:
+        it.close()
 
 
 def test_autograd_sync_single_gpu(torch_cuda):
