@@ -26,6 +26,7 @@ def _num(v):
 
 def main():
     rep, groups_path, out_path = sys.argv[1:4]
+    traffic_path = pathlib.Path(sys.argv[4]) if len(sys.argv) > 4 else ROOT / "profiles" / "roofline_traffic.json"
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
@@ -62,7 +63,7 @@ def main():
         "per_launch": [dict(l, algorithmic_bytes=a) for l, a in zip(launches, alg)],
     }
     pathlib.Path(out_path).write_text(json.dumps(summary, indent=1))
-    tf = ROOT / "profiles" / "roofline_traffic.json"
+    tf = traffic_path
     merged = json.loads(tf.read_text()) if tf.exists() else {}
     merged[f"{meta['kernel']}@N1"] = round(mean_traffic)
     merged["_note"] = ("mean dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel "
