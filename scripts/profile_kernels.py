@@ -5,6 +5,8 @@
   K2 one-shot           4 emulated ranks x 1 MiB   (local memory: same code as the IPC path
   K3 two-shot           4 emulated ranks x 64 MiB   minus the barriers and NVLink)
   fused two-shot        4 emulated ranks, ResNet-50 layer table
+  fused N=1             the single-rank group kernel on the whole ResNet-50 table
+  bf16 two-shot         4 emulated ranks, ResNet-50 layer table in bf16
 """
 
 from __future__ import annotations
@@ -62,6 +64,23 @@ def main():
     tp = (ctypes.c_void_p * world)(*[t.ptr for t, _ in tables])
     sp = (ctypes.c_void_p * world)(*[x.data_ptr() for x in slots])
     _native.call("mgw_allreduce_fused_emulated", tp, sp, world, off, ctypes.c_float(1.0), _native.ALGO_TWOSHOT, s)
+    # single-rank fused group kernel (bench N=1 dominant kernel), whole-model table
+    sec = ctypes.c_double()
+    _native.call("mgw_time_exchange", None, table.ptr, table.n, off, bucket.data_ptr(), 0, 4, 1, 0,
+                 ctypes.byref(sec), s)
+    # bf16 gradients, fp32 accumulation: 4 emulated ranks
+    btables, bslots = [], []
+    for r in range(world):
+        ls = [torch.randn(p, device="cuda").to(torch.bfloat16) for p in counts]
+        rr, o = [], 0
+        for x, p in zip(ls, counts):
+            rr.append((x.data_ptr(), p, o))
+            o += p
+        btables.append((_native.DeviceTable(rr), ls))
+        bslots.append(torch.empty(o, dtype=torch.bfloat16, device="cuda"))
+    tp = (ctypes.c_void_p * world)(*[t.ptr for t, _ in btables])
+    sp = (ctypes.c_void_p * world)(*[x.data_ptr() for x in bslots])
+    _native.call("mgw_allreduce_fused_bf16_emulated", tp, sp, world, off, ctypes.c_float(1.0), _native.ALGO_TWOSHOT, s)
     torch.cuda.synchronize()
     print("profile workload done")
 

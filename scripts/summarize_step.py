@@ -37,7 +37,7 @@ def main():
              "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "ns": 1e-9, "us": 1e-6, "ms": 1e-3}
     launches = []
     for r in rows[2:]:
-        if "fused_oneshot_kernel<1>" not in r[col["Kernel Name"]]:
+        if "fused_oneshot_kernel" not in r[col["Kernel Name"]]:
             continue
         get = lambda k: _num(r[col[k]]) * scale.get(units[col[k]], 1)  # noqa: E731
         launches.append({"us": get("gpu__time_duration.sum") * 1e6,
