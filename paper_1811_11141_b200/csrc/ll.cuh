@@ -41,29 +41,32 @@ __device__ __forceinline__ uint64_t ld_relaxed_sys_u64(const uint64_t* p) {
   return v;
 }
 
-__device__ __forceinline__ uint64_t ll_word(uint32_t epoch, float x) {
-  return ((uint64_t)epoch << 32) | (uint64_t)__float_as_uint(x);
+__device__ __forceinline__ void ld_relaxed_sys_v2(const uint64_t* p, uint64_t& a, uint64_t& b) {
+  asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
 }
 
-// Wait until word p carries `epoch`; returns the value.  Bounded; watches the abort flag.
-__device__ __forceinline__ float ll_wait(const uint64_t* p, uint32_t epoch, const ArArgs& a, int& status) {
-  uint64_t v = ld_relaxed_sys_u64(p);
-  if ((uint32_t)(v >> 32) == epoch) return __uint_as_float((uint32_t)v);
+// Re-poll a pair of words until both carry `epoch`.  Bounded; watches the abort flag.
+__device__ __forceinline__ void ll_wait2(const uint64_t* p, uint32_t epoch, const ArArgs& a, int& status, uint64_t& w0,
+                                      uint64_t& w1) {
   const uint64_t start = global_ns();
   for (uint32_t spin = 0;; ++spin) {
-    v = ld_relaxed_sys_u64(p);
-    if ((uint32_t)(v >> 32) == epoch) return __uint_as_float((uint32_t)v);
+    ld_relaxed_sys_v2(p, w0, w1);
+    if ((uint32_t)(w0 >> 32) == epoch && (uint32_t)(w1 >> 32) == epoch) return;
     if ((spin & 31) == 31) {
       if (load_relaxed_sys32(a.abort_flag[a.rank]) != 0u) {
         status = MGW_DEV_PEER_ABORT;
-        return 0.f;
+        return;
       }
       if (global_ns() - start > a.timeout_ns) {
         status = MGW_DEV_TIMEOUT;
-        return 0.f;
+        return;
       }
     }
   }
+}
+
+__device__ __forceinline__ uint64_t ll_word(uint32_t epoch, float x) {
+  return ((uint64_t)epoch << 32) | (uint64_t)__float_as_uint(x);
 }
 
 __device__ __forceinline__ float* ll_tensor(const FusedArgs& f, int& k, int64_t e) {
@@ -151,28 +154,44 @@ __global__ void __launch_bounds__(kThreads, 2) ll_oneshot_kernel(const __grid_co
   }
   status = s_status;
 
-  // 3. fold every element of my pairs from the N local LL areas, write the tensors
+  // 3. fold every element of my pairs from the N local LL areas, write the tensors.
+  //    The N sources' words of a pair are fetched as N independent 16-B loads issued
+  //    back to back (one memory latency, not 2N serial ones); only words that do not yet
+  //    carry this epoch are polled again.
   if (status == MGW_DEV_OK) {
     const uint64_t* base = l.ll[me] + (size_t)parity * kMaxRanks * kLLMaxElems;
     int seg = 0;
     k = 0;
     if (p0 < p1) k = fused_row_covering(f, (p0 + threadIdx.x) * 2 < n ? (p0 + threadIdx.x) * 2 : 0);
     for (int64_t j = p0 + threadIdx.x; j < p1 && status == MGW_DEV_OK; j += kThreads) {
+      const int64_t e = 2 * j;
+      uint64_t w0[N], w1[N];
+#pragma unroll
+      for (int src = 0; src < N; ++src) ld_relaxed_sys_v2(base + (size_t)src * kLLMaxElems + e, w0[src], w1[src]);
+#pragma unroll
+      for (int src = 0; src < N; ++src) {
+        if ((uint32_t)(w0[src] >> 32) != epoch || (uint32_t)(w1[src] >> 32) != epoch)
+          ll_wait2(base + (size_t)src * kLLMaxElems + e, epoch, a, status, w0[src], w1[src]);
+      }
+      if (status != MGW_DEV_OK) break;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int64_t e = 2 * j + h;
-        if (e >= n) break;
-        seg = advance_segment(seg, e, s_end);
-        float x[N];
+        const int64_t eh = e + h;
+        if (eh >= n) break;
+        seg = advance_segment(seg, eh, s_end);
+        float acc = 0.f;
 #pragma unroll
         for (int kk = 0; kk < N; ++kk) {
-          const int src = seg + kk >= N ? seg + kk - N : seg + kk;
-          x[kk] = ll_wait(base + (size_t)src * kLLMaxElems + e, epoch, a, status);
-        }
-        float acc = x[0];
+          int src = seg + kk;
+          src = src >= N ? src - N : src;
+          // select the word of source `src` without dynamic register indexing
+          uint64_t w = 0;
 #pragma unroll
-        for (int kk = 1; kk < N; ++kk) acc = __fadd_rn(acc, x[kk]);
-        if (status == MGW_DEV_OK) *ll_tensor(f, k, e) = acc;
+          for (int q = 0; q < N; ++q) w = q == src ? (h ? w1[q] : w0[q]) : w;
+          const float x = __uint_as_float((uint32_t)w);
+          acc = kk == 0 ? x : __fadd_rn(acc, x);
+        }
+        *ll_tensor(f, k, eh) = acc;
       }
     }
     if (status != MGW_DEV_OK) {

@@ -57,6 +57,11 @@ __global__ void clock_mark_kernel(uint64_t* clock) {
   if (threadIdx.x == 0) *clock = global_ns();
 }
 
+// advances the device call counter by one (timing of the gate alone, kind 6)
+__global__ void finish_kernel(uint32_t* state) {
+  if (threadIdx.x == 0) state[0] += 1u;
+}
+
 __global__ void spin_until_kernel(const uint64_t* clock, int64_t deadline_ns) {
   if (threadIdx.x != 0) return;
   const uint64_t until = *reinterpret_cast<const volatile uint64_t*>(clock) + (uint64_t)deadline_ns;
@@ -933,14 +938,14 @@ int mgw_allreduce_fused_bf16_emulated(void* const* tables, void* const* slots, i
 // unpack into `local_bucket`), 1 = all-reduce kernel only, 2 = pack only, 3 = unpack only.
 int mgw_time_exchange(mgw_comm* c, const void* table, int n_rows, int64_t n_elem, float* local_bucket, int algo,
                       int kind, int reps, int warmups, double* seconds_per_rep, void* stream) {
-  if (reps < 1 || warmups < 0 || !seconds_per_rep || n_elem <= 0 || kind < 0 || kind > 5)
+  if (reps < 1 || warmups < 0 || !seconds_per_rep || n_elem <= 0 || kind < 0 || kind > 6)
     return set_error(MGW_EINVAL, "bad timing arguments");
   int rc = check_table(table, n_rows, n_elem);
   if (rc) return rc;
   const mgw_table_t* t = as_table(table);
   const bool multi = c && c->world > 1;
   if (!multi && !local_bucket) return set_error(MGW_EINVAL, "single-rank timing needs a local bucket");
-  if ((kind == 1 || kind == 5) && !multi)
+  if ((kind == 1 || kind == 5 || kind == 6) && !multi)
     return set_error(MGW_EINVAL, "all-reduce timing needs a multi-rank communicator");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   auto step = [&]() -> int {
@@ -949,6 +954,15 @@ int mgw_time_exchange(mgw_comm* c, const void* table, int n_rows, int64_t n_elem
       return multi ? comm_allreduce_fused(c, t->host.data(), t->dev, n_rows, n_elem, 1.f, algo, s)
                    : local_fused(local_bucket, t->host.data(), t->dev, n_rows, n_elem, 1.f, s);
     if (kind == 5) return comm_allreduce_fused_bf16(c, t->host.data(), t->dev, n_rows, n_elem, 1.f, algo, s);
+    if (kind == 6) {  // rendezvous only: the one-warp gate kernel (launch + one fabric round trip)
+      ArArgs a = make_args(c, n_elem);
+      int g = launch_gate(a, s);
+      if (g) return g;
+      // advance the call counter so the next gate waits for a new epoch
+      finish_kernel<<<1, 32, 0, s>>>(c->state);
+      MGW_CHECK_LAUNCH();
+      return MGW_OK;
+    }
     if (multi) {
       if (kind == 0 || kind == 2) r = comm_pack(c, t->host.data(), t->dev, n_rows, n_elem, 1.f, s);
       if (r == MGW_OK && (kind == 0 || kind == 1)) r = comm_allreduce(c, n_elem, algo, s);

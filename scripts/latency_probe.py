@@ -1,0 +1,58 @@
+"""Small-message latency breakdown over the real IPC path (torchrun, one rank per GPU).
+
+    torchrun --nproc-per-node N scripts/latency_probe.py
+
+Loop-timed (mgw_time_exchange: 50 back-to-back steps under one CUDA event pair, max over
+ranks) for 4 KiB .. 1 MiB: the gate rendezvous alone (kind 6: one-warp fabric round trip
++ a counter kernel), the fused exchange per algorithm (LL / one-shot / two-shot), the
+bare all-reduce kernels, the bf16 exchange, and a local pack (launch floor).
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import pathlib
+import sys
+
+sys.path.insert(0, str(pathlib.Path(__file__).resolve().parents[1]))
+
+import bench  # noqa: E402
+
+
+def main():
+    import torch
+
+    from paper_1811_11141_b200 import _native
+    from paper_1811_11141_b200.allreduce_net import open_session_dist
+
+    class A:
+        gpus = int(os.environ.get("WORLD_SIZE", "1"))
+
+    rank, world, local = bench._dist_setup(A())
+    device = torch.device("cuda", local)
+    _, session = open_session_dist(capacity_bytes=64 << 20)
+    comm = session.comm
+    sizes = [4096, 16384, 65536, 262144, 1 << 20]
+    T = lambda **kw: [round(t * 1e6, 2) for t in bench._exchange_times(comm, world, device, sizes, repeats=50, **kw)]  # noqa: E731
+    out = {"world": world, "sizes": sizes, "us": {
+        "gate_plus_counter": T(kind=6),
+        "fused_ll": T(kind=4, algo=_native.ALGO_LL),
+        "fused_oneshot": T(kind=4, algo=_native.ALGO_ONESHOT),
+        "fused_twoshot": T(kind=4, algo=_native.ALGO_TWOSHOT),
+        "allreduce_oneshot": T(kind=1, algo=_native.ALGO_ONESHOT),
+        "allreduce_twoshot": T(kind=1, algo=_native.ALGO_TWOSHOT),
+        "fused_bf16_auto": T(kind=5),
+        "local_pack": [round(t * 1e6, 2) for t in bench._exchange_times(None, 1, device, sizes, kind=2, repeats=50)],
+    }}
+    session.raise_if_failed()
+    session.close()
+    if rank == 0:
+        print(json.dumps(out))
+    import torch.distributed as dist
+
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
