@@ -61,22 +61,42 @@ __device__ __forceinline__ float* fused_tensor1(const FusedArgs& f, int k, int64
 }
 
 // Pack bucket vectors [v0, v1) (16-B slots) plus scalar elements [t0, t1) into `slot`.
+// UP slots per thread are loaded before any is stored (ncu r01: one outstanding 16-B load
+// per thread left the pack phase latency-bound on long-scoreboard stalls).
 __device__ void fused_pack_range(const FusedArgs& f, float* slot, int64_t v0, int64_t v1, int64_t t0, int64_t t1) {
+  constexpr int UP = 4;
   const float scale = f.scale;
   const bool scaled = scale != 1.0f;
   if (v0 < v1) {
     int k = fused_row_covering(f, (v0 + threadIdx.x) << 2 < (v1 << 2) ? (v0 + threadIdx.x) << 2 : v0 << 2);
-    for (int64_t v = v0 + threadIdx.x; v < v1; v += kThreads) {
-      const int64_t e = v << 2;
-      bool fast;
-      float* tp = fused_tensor(f, k, e, fast);
-      if (fast) {
-        float4 x = *reinterpret_cast<const float4*>(tp);
-        *reinterpret_cast<float4*>(slot + e) = scaled ? fmul4(x, scale) : x;
-      } else {
-        for (int j = 0; j < 4; ++j) {
-          const float x = *fused_tensor1(f, k, e + j);
-          slot[e + j] = scaled ? __fmul_rn(x, scale) : x;
+    for (int64_t base = v0 + threadIdx.x; base < v1; base += (int64_t)UP * kThreads) {
+      float4 x[UP];
+      float* tp[UP];
+      bool fast[UP];
+      int ku[UP];
+#pragma unroll
+      for (int u = 0; u < UP; ++u) {
+        const int64_t vv = base + (int64_t)u * kThreads;
+        fast[u] = false;
+        ku[u] = k;
+        if (vv < v1) {
+          tp[u] = fused_tensor(f, k, vv << 2, fast[u]);
+          ku[u] = k;
+          if (fast[u]) x[u] = *reinterpret_cast<const float4*>(tp[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < UP; ++u) {
+        const int64_t vv = base + (int64_t)u * kThreads;
+        if (vv >= v1) continue;
+        const int64_t e = vv << 2;
+        if (fast[u]) {
+          *reinterpret_cast<float4*>(slot + e) = scaled ? fmul4(x[u], scale) : x[u];
+        } else {
+          for (int j = 0; j < 4; ++j) {
+            const float y = *fused_tensor1(f, ku[u], e + j);
+            slot[e + j] = scaled ? __fmul_rn(y, scale) : y;
+          }
         }
       }
     }
