@@ -34,10 +34,14 @@ def main():
     _, session = open_session_dist(capacity_bytes=64 << 20)
     comm = session.comm
     sizes = [4096, 16384, 65536, 262144, 1 << 20]
-    T = lambda **kw: [round(t * 1e6, 2) for t in bench._exchange_times(comm, world, device, sizes, repeats=50, **kw)]  # noqa: E731
+    def T(limit=None, **kw):
+        ok = [m for m in sizes if limit is None or m <= limit]
+        got = [round(t * 1e6, 2) for t in bench._exchange_times(comm, world, device, ok, repeats=50, **kw)]
+        return got + [None] * (len(sizes) - len(ok))
+
     out = {"world": world, "sizes": sizes, "us": {
         "gate_plus_counter": T(kind=6),
-        "fused_ll": T(kind=4, algo=_native.ALGO_LL),
+        "fused_ll": T(kind=4, algo=_native.ALGO_LL, limit=262144),
         "fused_oneshot": T(kind=4, algo=_native.ALGO_ONESHOT),
         "fused_twoshot": T(kind=4, algo=_native.ALGO_TWOSHOT),
         "allreduce_oneshot": T(kind=1, algo=_native.ALGO_ONESHOT),
@@ -45,6 +49,15 @@ def main():
         "fused_bf16_auto": T(kind=5),
         "local_pack": [round(t * 1e6, 2) for t in bench._exchange_times(None, 1, device, sizes, kind=2, repeats=50)],
     }}
+    # CTA-count sensitivity of the fused one-shot (16-B slots per CTA; default 512 x Unroll)
+    for per in (128, 256, 512):
+        _native.call("mgw_comm_set_tuning", comm, 0, per)
+        out["us"][f"fused_oneshot_per{per}"] = T(kind=4, algo=_native.ALGO_ONESHOT)
+    _native.call("mgw_comm_set_tuning", comm, 0, 0)
+    for per in (256, 512):
+        _native.call("mgw_comm_set_tuning", comm, 1, per)
+        out["us"][f"fused_twoshot_per{per}"] = T(kind=4, algo=_native.ALGO_TWOSHOT)
+    _native.call("mgw_comm_set_tuning", comm, 1, 0)
     session.raise_if_failed()
     session.close()
     if rank == 0:
