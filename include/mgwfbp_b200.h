@@ -169,8 +169,8 @@ int mgw_allreduce_fused_emulated(void* const* tables, float* const* slots, int w
  * bucket and wire format.  Element e of reference segment s (allreduce_net.py:360-367)
  * becomes bf16_rn((((f32(x_s) + f32(x_s+1)) + ...) + f32(x_s+N-1)) * scale), the
  * multiply only when scale != 1: the reference ring's fold order (allreduce_net.py:401)
- * in fp32 over exactly-upcast inputs, rounded once.  Algorithms: AUTO, one-shot,
- * two-shot.  Replaces ring_allreduce (allreduce_net.py:370-411) for element_bytes = 2
+ * in fp32 over exactly-upcast inputs, rounded once.  Algorithms: AUTO, LL (<= 256 KB,
+ * two bf16 per pushed word), one-shot, two-shot.  Replaces ring_allreduce (allreduce_net.py:370-411) for element_bytes = 2
  * profiles (model_profile.py:24). */
 int mgw_allreduce_fused_bf16(mgw_comm* comm, const void* table, int n_rows, int64_t n_elem, float scale, int algo,
                              void* stream);

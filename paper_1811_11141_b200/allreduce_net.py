@@ -392,10 +392,10 @@ class RingSession:
         c = self.counters
         c.frames_sent += 1
         c.frames_received += 1
-        if algo == _native.ALGO_LL:  # pushed as 8-byte (epoch, value) words
+        if algo == _native.ALGO_LL:  # pushed as 8-byte (epoch, payload) words: 2x the payload bytes
             c.rounds += 1
-            c.payload_bytes_received += 8 * n * (world - 1)
-            c.payload_bytes_sent += 8 * n * (world - 1)
+            c.payload_bytes_received += 2 * w * n * (world - 1)
+            c.payload_bytes_sent += 2 * w * n * (world - 1)
         elif algo == _native.ALGO_ONESHOT:
             c.rounds += 1
             c.payload_bytes_received += w * n * (world - 1)
@@ -476,7 +476,10 @@ def ring_allreduce(
         algo = _algo_for(session, n, fused=True)
         handle = stream.cuda_stream
         if n and bf16:
-            algo = _native.ALGO_ONESHOT if 2 * n <= session_oneshot_max(session) else _native.ALGO_TWOSHOT
+            if 2 * n <= LL_MAX_BYTES:
+                algo = _native.ALGO_LL
+            else:
+                algo = _native.ALGO_ONESHOT if 2 * n <= session_oneshot_max(session) else _native.ALGO_TWOSHOT
             table = session.table(ptr, n)
             _native.call("mgw_allreduce_fused_bf16", session.comm, table.ptr, 1, n, ctypes.c_float(1.0),
                          _native.ALGO_AUTO, handle)

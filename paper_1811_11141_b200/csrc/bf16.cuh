@@ -20,7 +20,7 @@
 
 #include <cuda_bf16.h>
 
-#include "fused.cuh"
+#include "ll.cuh"
 
 namespace mgw {
 
@@ -217,6 +217,63 @@ __device__ void b16_scatter_range(const FusedArgs& f, const uint16_t* src, int64
     *b16_tensor1(f, fused_row_covering(f, e), e) = __ldcg(src + e);
 }
 
+// pack chunk b of every part into my slot, parts interleaved (N loads in flight)
+template <int N>
+__device__ void b16_pack_parts(const FusedArgs& f, uint16_t* slot, const PartChunks<N>& pc) {
+  int cur[N];
+#pragma unroll
+  for (int p = 0; p < N; ++p) cur[p] = fused_row_covering(f, (pc.lo[p] + (threadIdx.x < pc.len[p] ? threadIdx.x : 0)) * kB16);
+  for (int64_t i = threadIdx.x; i < pc.longest; i += kThreads) {
+    uint4 x[N];
+    bool fast[N];
+#pragma unroll
+    for (int p = 0; p < N; ++p) {
+      fast[p] = false;
+      if (i < pc.len[p]) {
+        const uint16_t* tp = b16_tensor(f, cur[p], (pc.lo[p] + i) * kB16, fast[p]);
+        if (fast[p]) x[p] = *reinterpret_cast<const uint4*>(tp);
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < N; ++p) {
+      if (i >= pc.len[p]) continue;
+      const int64_t e = (pc.lo[p] + i) * kB16;
+      if (fast[p]) {
+        *reinterpret_cast<uint4*>(slot + e) = x[p];
+      } else {
+        for (int j = 0; j < kB16; ++j) slot[e + j] = *b16_tensor1(f, cur[p], e + j);
+      }
+    }
+  }
+}
+
+// copy chunk b of every peer's reduced part into my tensors, parts interleaved
+template <int N>
+__device__ void b16_scatter_parts(const FusedArgs& f, const uint16_t* const* in, int me, const PartChunks<N>& pc) {
+  int cur[N];
+#pragma unroll
+  for (int p = 0; p < N; ++p) cur[p] = fused_row_covering(f, (pc.lo[p] + (threadIdx.x < pc.len[p] ? threadIdx.x : 0)) * kB16);
+  for (int64_t i = threadIdx.x; i < pc.longest; i += kThreads) {
+    uint4 x[N];
+#pragma unroll
+    for (int p = 0; p < N; ++p)
+      if (p != me && i < pc.len[p]) x[p] = __ldcg(reinterpret_cast<const uint4*>(in[p]) + pc.lo[p] + i);
+#pragma unroll
+    for (int p = 0; p < N; ++p) {
+      if (p == me || i >= pc.len[p]) continue;
+      const int64_t e = (pc.lo[p] + i) * kB16;
+      bool fast;
+      uint16_t* tp = b16_tensor(f, cur[p], e, fast);
+      if (fast) {
+        *reinterpret_cast<uint4*>(tp) = x[p];
+      } else {
+        const uint16_t* h = reinterpret_cast<const uint16_t*>(&x[p]);
+        for (int j = 0; j < kB16; ++j) *b16_tensor1(f, cur[p], e + j) = h[j];
+      }
+    }
+  }
+}
+
 template <int N>
 __global__ void __launch_bounds__(kThreads, 2) b16_oneshot_kernel(const __grid_constant__ FusedArgs f) {
   constexpr int U = Unroll<N>::value;
@@ -265,7 +322,7 @@ __global__ void __launch_bounds__(kThreads, 2) b16_twoshot_kernel(const __grid_c
   if (threadIdx.x == 0) part_chunks<N>(nv, b, G, pc);
   __syncthreads();
   if (!(a.flags & kSkipPack)) {
-    for (int p = 0; p < N; ++p) b16_pack_range(f, mine, pc.lo[p], pc.lo[p] + pc.len[p], 0, 0);
+    b16_pack_parts<N>(f, mine, pc);
     if (last) b16_pack_range(f, mine, 0, 0, tail0, a.n);
   }
   int status = MGW_DEV_OK;
@@ -279,12 +336,166 @@ __global__ void __launch_bounds__(kThreads, 2) b16_twoshot_kernel(const __grid_c
   if (status == MGW_DEV_OK && !(a.flags & kSkipPhase2)) {
     if (!(a.flags & kNoBarrier)) status = cta_barrier(a.mid, parity, epoch, b16_tag(a.n), a);
     if (status == MGW_DEV_OK) {
-      for (int p = 0; p < N; ++p)
-        if (p != me) b16_scatter_range(f, in[p], pc.lo[p], pc.lo[p] + pc.len[p], 0, 0);
+      b16_scatter_parts<N>(f, in, me, pc);
       if (last && me != N - 1) b16_scatter_range(f, in[N - 1], 0, 0, tail0, a.n);
     }
   }
   finish_call(a);
+}
+
+// LL push one-shot for small bf16 buckets: a word carries (epoch << 32 | two bf16), a
+// 16-B push carries four elements.  Same protocol as ll_oneshot_kernel (ll.cuh): header
+// length check by CTA 0, batched polls of the N sources, fold in the reference order in
+// fp32, one rounding.  At most 2 * kLLMaxElems elements (256 KB).
+__device__ __forceinline__ uint64_t ll_b16_word(uint32_t epoch, uint16_t lo, uint16_t hi) {
+  return ((uint64_t)epoch << 32) | ((uint32_t)hi << 16) | lo;
+}
+
+template <int N>
+__global__ void __launch_bounds__(kThreads, 2) ll_b16_kernel(const __grid_constant__ LLArgs l) {
+  const FusedArgs& f = l.f;
+  const ArArgs& a = f.ar;
+  stamp_enter(a.stamp);
+  __shared__ int64_t s_end[kMaxRanks];
+  __shared__ int s_status;
+  const uint32_t epoch = load_volatile32(a.state) + 1u;
+  const int parity = (int)(epoch & 1u);
+  const int me = a.rank;
+  const int64_t n = a.n;
+  if (threadIdx.x < N) {
+    const int t = threadIdx.x;
+    const int64_t q = n / N, r = n % N;
+    s_end[t] = (int64_t)(t + 1) * q + (t + 1 < r ? t + 1 : r);
+  }
+  if (threadIdx.x == 0) s_status = MGW_DEV_OK;
+  if (blockIdx.x == 0 && threadIdx.x < N)
+    st_relaxed_sys_u64(l.hdr[threadIdx.x] + parity * kMaxRanks + me, ((uint64_t)epoch << 32) | b16_tag(n));
+  __syncthreads();
+
+  // element quads of this CTA: [q0, q1) (quad j = elements 4j .. 4j+3 = words 2j, 2j+1)
+  const int64_t quads = (n + 3) >> 2;
+  const int64_t per = (quads + gridDim.x - 1) / gridDim.x;
+  const int64_t q0 = (int64_t)blockIdx.x * per;
+  const int64_t q1 = q0 + per < quads ? q0 + per : quads;
+  const size_t my_off = ((size_t)parity * kMaxRanks + me) * kLLMaxElems;
+
+  // 1. pack and push my four elements of each quad to every rank
+  int k = 0;
+  if (q0 < q1) k = fused_row_covering(f, (q0 + threadIdx.x) * 4 < n ? (q0 + threadIdx.x) * 4 : 0);
+  for (int64_t j = q0 + threadIdx.x; j < q1; j += kThreads) {
+    const int64_t e = 4 * j;
+    uint16_t x[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      x[h] = 0;
+      if (e + h < n) {
+        Row r = fused_row(f, k);
+        while (e + h >= r.offset + r.count) r = fused_row(f, ++k);
+        x[h] = reinterpret_cast<const uint16_t*>(r.ptr)[e + h - r.offset];
+      }
+    }
+    const uint64_t w0 = ll_b16_word(epoch, x[0], x[1]), w1 = ll_b16_word(epoch, x[2], x[3]);
+#pragma unroll
+    for (int r = 0; r < N; ++r) st_relaxed_sys_v2(l.ll[r] + my_off + 2 * j, w0, w1);
+  }
+
+  // 2. CTA 0 checks every peer's header (length and dtype agreement)
+  int status = MGW_DEV_OK;
+  if (blockIdx.x == 0 && threadIdx.x < N) {
+    const uint64_t* p = l.hdr[me] + parity * kMaxRanks + threadIdx.x;
+    uint64_t v = ld_relaxed_sys_u64(p);
+    const uint64_t start = global_ns();
+    for (uint32_t spin = 0; (uint32_t)(v >> 32) != epoch; ++spin) {
+      if ((spin & 31) == 31) {
+        if (load_relaxed_sys32(a.abort_flag[me]) != 0u) {
+          status = MGW_DEV_PEER_ABORT;
+          break;
+        }
+        if (global_ns() - start > a.timeout_ns) {
+          status = MGW_DEV_TIMEOUT;
+          break;
+        }
+      }
+      v = ld_relaxed_sys_u64(p);
+    }
+    if (status == MGW_DEV_OK && (uint32_t)v != b16_tag(n)) status = MGW_DEV_LENGTH_MISMATCH;
+    if (status != MGW_DEV_OK) atomicCAS(&s_status, 0, status);
+  }
+  __syncthreads();
+  if (s_status != MGW_DEV_OK && threadIdx.x == 0) {
+    atomicCAS(a.err, 0, s_status);
+    if (s_status != MGW_DEV_PEER_ABORT)
+      for (int r = 0; r < N; ++r) store_release_sys32(a.abort_flag[r], 1u);
+  }
+  status = s_status;
+
+  // 3. fold: batched 16-B polls of the N sources, fp32 fold in the reference order
+  if (status == MGW_DEV_OK) {
+    const float scale = f.scale;
+    const bool scaled = scale != 1.0f;
+    const uint64_t* base = l.ll[me] + (size_t)parity * kMaxRanks * kLLMaxElems;
+    int seg = 0;
+    k = 0;
+    if (q0 < q1) k = fused_row_covering(f, (q0 + threadIdx.x) * 4 < n ? (q0 + threadIdx.x) * 4 : 0);
+    for (int64_t j = q0 + threadIdx.x; j < q1 && status == MGW_DEV_OK; j += kThreads) {
+      const int64_t e = 4 * j;
+      uint64_t w0[N], w1[N];
+#pragma unroll
+      for (int src = 0; src < N; ++src) ld_relaxed_sys_v2(base + (size_t)src * kLLMaxElems + 2 * j, w0[src], w1[src]);
+#pragma unroll
+      for (int src = 0; src < N; ++src) {
+        if ((uint32_t)(w0[src] >> 32) != epoch || (uint32_t)(w1[src] >> 32) != epoch)
+          ll_wait2(base + (size_t)src * kLLMaxElems + 2 * j, epoch, a, status, w0[src], w1[src]);
+      }
+      if (status != MGW_DEV_OK) break;
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const int64_t eh = e + h;
+        if (eh >= n) break;
+        seg = advance_segment(seg, eh, s_end);
+        float acc = 0.f;
+#pragma unroll
+        for (int kk = 0; kk < N; ++kk) {
+          int src = seg + kk;
+          src = src >= N ? src - N : src;
+          uint64_t w = 0;
+#pragma unroll
+          for (int q = 0; q < N; ++q) w = q == src ? (h < 2 ? w0[q] : w1[q]) : w;
+          const float x = (h & 1) ? b16_word_hi((uint32_t)w) : b16_word_lo((uint32_t)w);
+          acc = kk == 0 ? x : __fadd_rn(acc, x);
+        }
+        const uint16_t y = f32_to_b16(scaled ? __fmul_rn(acc, scale) : acc);
+        Row r = fused_row(f, k);
+        while (eh >= r.offset + r.count) r = fused_row(f, ++k);
+        reinterpret_cast<uint16_t*>(r.ptr)[eh - r.offset] = y;
+      }
+    }
+    if (status != MGW_DEV_OK) {
+      atomicCAS(a.err, 0, status);
+      if (status != MGW_DEV_PEER_ABORT)
+        for (int r = 0; r < N; ++r) store_release_sys32(a.abort_flag[r], 1u);
+    }
+  }
+  finish_call(a);
+}
+
+inline int launch_ll_b16(const LLArgs& l, int max_ctas, cudaStream_t stream) {
+  if (l.f.ar.n > 2 * kLLMaxElems)
+    return set_error(MGW_EINVAL, "bf16 LL path takes at most %lld elements", (long long)(2 * kLLMaxElems));
+  const int64_t quads = (l.f.ar.n + 3) >> 2;
+  const int grid = grid_for(quads, kThreads, max_ctas < 128 ? max_ctas : 128);
+  switch (l.f.ar.world) {
+    case 2: ll_b16_kernel<2><<<grid, kThreads, 0, stream>>>(l); break;
+    case 3: ll_b16_kernel<3><<<grid, kThreads, 0, stream>>>(l); break;
+    case 4: ll_b16_kernel<4><<<grid, kThreads, 0, stream>>>(l); break;
+    case 5: ll_b16_kernel<5><<<grid, kThreads, 0, stream>>>(l); break;
+    case 6: ll_b16_kernel<6><<<grid, kThreads, 0, stream>>>(l); break;
+    case 7: ll_b16_kernel<7><<<grid, kThreads, 0, stream>>>(l); break;
+    case 8: ll_b16_kernel<8><<<grid, kThreads, 0, stream>>>(l); break;
+    default: return set_error(MGW_EINVAL, "LL path needs 2..%d ranks, got %d", kMaxRanks, l.f.ar.world);
+  }
+  MGW_CHECK_LAUNCH();
+  return MGW_OK;
 }
 
 template <int N>

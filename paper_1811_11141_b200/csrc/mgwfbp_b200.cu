@@ -337,7 +337,13 @@ int comm_allreduce_fused_bf16(mgw_comm* c, const Row* host_rows, const Row* dev_
   if (c->world > 1 && !c->peers_open) return set_error(MGW_EINVAL, "peers not opened (call mgw_comm_open_peers)");
   if (n == 0 || n_rows == 0) return MGW_OK;
   if (c->world == 1 && scale == 1.0f) return MGW_OK;  // nothing to exchange or scale
-  if (algo == MGW_ALGO_AUTO) algo = n * 2 <= c->oneshot_max_bytes ? MGW_ALGO_ONESHOT : MGW_ALGO_TWOSHOT;
+  if (algo == MGW_ALGO_AUTO) {
+    if (c->world > 1 && n * 2 <= c->ll_max_bytes && n <= 2 * kLLElems)
+      algo = MGW_ALGO_LL;
+    else
+      algo = n * 2 <= c->oneshot_max_bytes ? MGW_ALGO_ONESHOT : MGW_ALGO_TWOSHOT;
+  }
+  if (algo == MGW_ALGO_LL && c->world == 1) algo = MGW_ALGO_ONESHOT;
   FusedArgs f;
   memset(&f, 0, sizeof(f));
   f.ar = make_args(c, n);
@@ -353,6 +359,16 @@ int comm_allreduce_fused_bf16(mgw_comm* c, const Row* host_rows, const Row* dev_
   f.rows = dev_rows;
   f.n_rows = n_rows;
   f.scale = scale;
+  if (algo == MGW_ALGO_LL) {
+    LLArgs l;
+    memset(&l, 0, sizeof(l));
+    l.f = f;
+    for (int s = 0; s < c->world; ++s) {
+      l.ll[s] = reinterpret_cast<uint64_t*>(c->peer[s] + kLLOff);
+      l.hdr[s] = reinterpret_cast<uint64_t*>(c->peer[s] + kHdrOff);
+    }
+    return launch_ll_b16(l, c->max_ctas, stream);
+  }
   return launch_b16(f, algo, c->max_ctas, stream);
 }
 
@@ -665,8 +681,8 @@ int mgw_allreduce_fused(mgw_comm* c, const void* table, int n_rows, int64_t n_el
 int mgw_allreduce_fused_bf16(mgw_comm* c, const void* table, int n_rows, int64_t n_elem, float scale, int algo,
                              void* stream) {
   if (!c) return set_error(MGW_EINVAL, "comm is null");
-  if (algo != MGW_ALGO_AUTO && algo != MGW_ALGO_ONESHOT && algo != MGW_ALGO_TWOSHOT)
-    return set_error(MGW_EINVAL, "bf16 buckets support AUTO, one-shot and two-shot (got %d)", algo);
+  if (algo != MGW_ALGO_AUTO && algo != MGW_ALGO_ONESHOT && algo != MGW_ALGO_TWOSHOT && algo != MGW_ALGO_LL)
+    return set_error(MGW_EINVAL, "bf16 buckets support AUTO, LL, one-shot and two-shot (got %d)", algo);
   int rc = check_table(table, n_rows, n_elem);
   if (rc) return rc;
   const mgw_table_t* t = as_table(table);

@@ -227,7 +227,10 @@ def bf16_task(config, session, *, sizes):
         t = vals.to(session.device)
         ring_allreduce(GradientBuffer(1, 1, t), config, session)
         out[("auto", n)] = t.view(torch.int16).cpu().numpy().view(np.uint16)
-        for name, algo in (("one", _native.ALGO_ONESHOT), ("two", _native.ALGO_TWOSHOT)):
+        algos = [("one", _native.ALGO_ONESHOT), ("two", _native.ALGO_TWOSHOT)]
+        if n <= 131072:
+            algos.append(("ll", _native.ALGO_LL))
+        for name, algo in algos:
             t = vals.to(session.device)
             table = _native.DeviceTable([(t.data_ptr(), n, 0)])
             with torch.cuda.device(session.device):
@@ -272,3 +275,15 @@ def autograd_bf16_task(config, session):
     session.raise_if_failed()
     sync.close()
     return local, [w.grad.view(torch.int16).cpu().numpy().view(np.uint16).copy() for w in ws]
+
+
+def dtype_mismatch_task(config, session):
+    """Rank 0 reduces bf16, the others fp32, same element count: a protocol error."""
+    import torch
+
+    from paper_1811_11141_b200 import GradientBuffer
+
+    dtype = torch.bfloat16 if config.rank == 0 else torch.float32
+    t = torch.ones(1000, dtype=dtype, device=session.device)
+    ring_allreduce(GradientBuffer(1, 1, t), config, session)
+    return True

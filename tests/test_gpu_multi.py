@@ -53,6 +53,13 @@ def test_length_mismatch_is_a_protocol_error():
     assert "buffer lengths" in str(err.value) or "ProtocolError" in str(err.value)
 
 
+def test_dtype_mismatch_is_a_protocol_error():
+    """bf16 on one rank, fp32 on another (same length): caught by the barrier / LL header tag."""
+    with pytest.raises(RuntimeError) as err:
+        run_workers(2, _mp_tasks.dtype_mismatch_task, timeout=60)
+    assert "buffer lengths" in str(err.value) or "ProtocolError" in str(err.value)
+
+
 def test_criterion_7_collective_correctness():
     for n in _worlds():
         for verdicts in run_workers(n, _mp_tasks.collective_task).values():
@@ -202,7 +209,7 @@ def test_online_replanning_from_live_spans():
 
 def test_bf16_exchange_over_ipc_vs_oracle():
     """bf16 on the wire, fp32 accumulation, one rounding: bit-exact vs the oracle for the
-    AUTO path (scale 1) and both explicit algorithms (scale 1/2); half the fp32 bytes."""
+    AUTO path (scale 1) and every explicit algorithm -- LL, one-shot, two-shot (scale 1/2)."""
     from oracle import ring_oracle
 
     sizes = (1, 17, 1001, 4099, 65543, 1 << 20)
@@ -216,6 +223,8 @@ def test_bf16_exchange_over_ipc_vs_oracle():
                 assert np.array_equal(res[r][("auto", size)], want1), (n, size, r)
                 assert np.array_equal(res[r][("one", size)], want_half), (n, size, r, "one")
                 assert np.array_equal(res[r][("two", size)], want_half), (n, size, r, "two")
+                if size <= 131072:
+                    assert np.array_equal(res[r][("ll", size)], want_half), (n, size, r, "ll")
 
 
 def test_autograd_bf16_parameters():
