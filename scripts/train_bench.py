@@ -32,6 +32,8 @@ def main():
     ap.add_argument("--ctas", default="296,64,32,16", help="CTA caps to try for the overlapped collectives")
     ap.add_argument("--priorities", default="0,-1", help="comm stream priorities to try")
     ap.add_argument("--gates", default="0,1", help="peer gate off/on variants to try")
+    ap.add_argument("--a-scales", default="", help="extra MG-WFBP plans under an inflated startup a (e.g. 4,16): "
+                    "probes whether merging more pays once interference with backward is priced in")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -78,6 +80,13 @@ def main():
              "synceasgd": MergePlan(frozenset(range(2, n + 1)), n)}
     predicted = {"wfbp": simulate_wfbp(prof, model_ab), "mgwfbp": simulate_mgwfbp(prof, model_ab, plans["mgwfbp"]),
                  "synceasgd": simulate_sync_easgd(prof, model_ab)}
+    from paper_1811_11141_b200 import CommModel
+
+    for k in [float(x) for x in args.a_scales.split(",") if x]:
+        inflated = CommModel(model_ab.a * k, model_ab.b)
+        name = f"mgwfbp_a{k:g}x"
+        plans[name] = find_merge_plan(prof, inflated)
+        predicted[name] = simulate_mgwfbp(prof, inflated, plans[name])
 
     def timed(run_one, label):
         s = torch.cuda.current_stream()
@@ -110,7 +119,7 @@ def main():
     variants = [(int(c), int(p), int(g)) for c in args.ctas.split(",") for p in args.priorities.split(",")
                 for g in args.gates.split(",")]
     for cap, prio, gate in variants:
-        for name in ("wfbp", "mgwfbp", "synceasgd"):
+        for name in plans:
             sync = MergedGradientSync(params, plans[name], comm=comm, world=world, scale=1.0 / world,
                                       sync_after_backward=name == "synceasgd", max_ctas=cap, priority=prio,
                                       gate=bool(gate))
