@@ -25,7 +25,7 @@ from .comm_model import CommModel, Measurement, fit_ab
 from .merge_planner import MergePlan, find_merge_plan
 from .model_profile import ModelProfile
 
-__all__ = ["OnlinePlanner", "dist_agree", "observe_iteration"]
+__all__ = ["OnlinePlanner", "calibrate_startup", "dist_agree", "dist_max", "observe_iteration"]
 
 
 def dist_agree(group=None) -> Callable[[CommModel], CommModel]:
@@ -42,6 +42,47 @@ def dist_agree(group=None) -> Callable[[CommModel], CommModel]:
         return CommModel(float(t[0]), float(t[1]))
 
     return agree
+
+
+def dist_max(group=None) -> Callable[[float], float]:
+    """A float max-reduced over the ranks of a torch.distributed group."""
+
+    def agree(x: float) -> float:
+        import torch
+        import torch.distributed as dist
+
+        backend = dist.get_backend(group)
+        dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+        t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        return float(t[0])
+
+    return agree
+
+
+def calibrate_startup(profile: ModelProfile, model: CommModel, measure: Callable[[MergePlan], float], *,
+                      scales=(1, 2, 4, 8, 16, 32, 64), agree: Callable[[float], float] | None = None):
+    """Interference-aware startup for real overlap.
+
+    The alpha/beta model prices an exchange alone; overlapped with a real backward pass
+    every collective also takes SMs and HBM from the backward kernels, a per-collective
+    cost the model does not see.  Pricing it as a larger startup ``k * a`` lets Algorithm 1
+    trade it off (fewer, larger messages).  ``measure(plan)`` returns the seconds of a real
+    training step under ``plan`` (collective across ranks when ``agree`` is set: it is
+    called with the same plans in the same order on every rank); plans that coincide are
+    measured once.  Returns ``(k, plan, {k: seconds})`` for the fastest ``k``.
+    """
+    times: dict[float, float] = {}
+    by_plan: dict[frozenset, float] = {}
+    for k in scales:
+        plan = find_merge_plan(profile, CommModel(model.a * k, model.b))
+        key = plan.merged_layers
+        if key not in by_plan:
+            t = float(measure(plan))
+            by_plan[key] = agree(t) if agree is not None else t
+        times[k] = by_plan[key]
+    best = min(scales, key=lambda k: (times[k], k))
+    return best, find_merge_plan(profile, CommModel(model.a * best, model.b)), times
 
 
 class OnlinePlanner:

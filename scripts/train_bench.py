@@ -32,6 +32,9 @@ def main():
     ap.add_argument("--ctas", default="296,64,32,16", help="CTA caps to try for the overlapped collectives")
     ap.add_argument("--priorities", default="0,-1", help="comm stream priorities to try")
     ap.add_argument("--gates", default="0,1", help="peer gate off/on variants to try")
+    ap.add_argument("--tune", action="store_true",
+                    help="interference-aware MG-WFBP: pick the startup scale k by measured step time "
+                         "(replan.calibrate_startup) at each CTA cap, then time the chosen plan")
     ap.add_argument("--a-scales", default="", help="extra MG-WFBP plans under an inflated startup a (e.g. 4,16): "
                     "probes whether merging more pays once interference with backward is priced in")
     args = ap.parse_args()
@@ -146,6 +149,36 @@ def main():
             sync.close()
         if world == 1:
             break
+    if args.tune and world > 1:
+        from paper_1811_11141_b200.replan import calibrate_startup
+
+        for cap in [int(c) for c in args.ctas.split(",")]:
+            def synced(plan, steps, warm):
+                sync = MergedGradientSync(params, plan, comm=comm, world=world, scale=1.0 / world, max_ctas=cap,
+                                          priority=-1)
+
+                def synced_step():
+                    opt.zero_grad(set_to_none=False)
+                    step().backward()
+                    sync.finish()
+                    opt.step()
+
+                saved = args.steps, args.warmup
+                args.steps, args.warmup = steps, warm
+                try:
+                    res = timed(synced_step, "tune")
+                finally:
+                    args.steps, args.warmup = saved
+                    sync.close()
+                return res
+
+            # timed() already takes the max over ranks, so every rank sees the same numbers
+            k, plan, times = calibrate_startup(prof, model_ab, lambda p: synced(p, 10, 3)["ms_mean"],
+                                               scales=(1, 2, 4, 8, 16, 32, 64))
+            key = f"mgwfbp_tuned_ctas{cap}_hiprio"
+            results[key] = synced(plan, args.steps, args.warmup)
+            results[key].update({"groups": len(plan.groups()), "startup_scale": k,
+                                 "calibration_ms": {str(kk): round(v, 4) for kk, v in times.items()}})
     if world > 1:
         ddp = torch.nn.parallel.DistributedDataParallel(net, device_ids=[local], gradient_as_bucket_view=True,
                                                       broadcast_buffers=False)

@@ -96,3 +96,21 @@ def test_ranks_agree_on_one_plan_over_gloo():
     (a, b), merged = res[0]
     assert a == pytest.approx(300e-6, rel=1e-6) and b == pytest.approx(1 / 100e9, rel=1e-6)
     assert merged == sorted(find_merge_plan(PROFILE, CommModel(a, b)).merged_layers)
+
+
+def test_calibrate_startup_picks_the_fastest_measured_scale():
+    from paper_1811_11141_b200.replan import calibrate_startup
+
+    model = CommModel(12e-6, 1 / 500e9)
+    calls = []
+
+    def measure(plan):  # a synthetic "real step": every collective costs 20 µs of interference
+        calls.append(plan.merged_layers)
+        groups = len(plan.groups())
+        return 15e-3 + groups * 20e-6 + (300e-6 if groups == 1 else 0.0)
+
+    k, plan, times = calibrate_startup(PROFILE, model, measure, scales=(1, 4, 16, 64, 256))
+    assert len(calls) == len(set(calls))  # identical plans are measured once
+    assert times[k] == min(times.values())
+    assert plan == find_merge_plan(PROFILE, CommModel(model.a * k, model.b))
+    assert len(plan.groups()) < len(find_merge_plan(PROFILE, model).groups())
