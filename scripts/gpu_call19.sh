@@ -1,0 +1,5 @@
+#!/bin/bash
+mkdir -p gpurun_out; rm -f gpurun_out/status19.txt
+timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29593 scripts/train_bench.py --steps 30 --ctas 64,296 --priorities -1 --gates 0 --tune > gpurun_out/train_n4.json 2> gpurun_out/train_n4.err; echo "train4 rc=$?" >> gpurun_out/status19.txt
+timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29594 scripts/train_bench.py --steps 30 --ctas 64 --priorities -1 --gates 0 --tune > gpurun_out/train_n2.json 2> gpurun_out/train_n2.err; echo "train2 rc=$?" >> gpurun_out/status19.txt
+cat gpurun_out/status19.txt
