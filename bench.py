@@ -356,9 +356,15 @@ def run_ours(args) -> dict | None:
     # 1. fit the startup/bandwidth model of one group exchange on this box
     exch = _exchange_times(comm, world, device, FIT_SIZES, kind=0 if args.unfused else 4,
                            repeats=3 if args.quick else 20, warmups=1 if args.quick else 3)
+    # the same exchange steps replayed as one CUDA graph: the per-launch cost inside the
+    # engine's graph (reported next to the stream-timed fit the planner uses)
+    exch_graph = _exchange_times(comm, world, device, FIT_SIZES,
+                                 kind=(0 if args.unfused else 4) | 256, repeats=3 if args.quick else 20,
+                                 warmups=1 if args.quick else 3)
     if session is not None:
         session.raise_if_failed()
     model, fit_ok = _fit(FIT_SIZES, exch, world)
+    model_graph, _ = _fit(FIT_SIZES, exch_graph, world)
     plans = {
         "wfbp": MergePlan(frozenset(), n),
         "synceasgd": MergePlan(frozenset(range(2, n + 1)), n),
@@ -501,6 +507,8 @@ def run_ours(args) -> dict | None:
             "fitted_a_us": round(model.a * 1e6, 3),
             "fitted_b_ns_per_byte": model.b * 1e9,
             "fit_ok": fit_ok,
+            "fitted_a_graph_us": round(model_graph.a * 1e6, 3),
+            "fitted_b_graph_ns_per_byte": model_graph.b * 1e9,
             "parallelism": f"dp{world}",
             "l2": "flushed between iterations (256 MiB write on the compute stream, outside the timed events)",
             "cuda_graph": not args.no_graph,
@@ -513,6 +521,7 @@ def run_ours(args) -> dict | None:
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "verified": e2e_ok},
         "gpu_launches": launches * args.steps,
         "group_exchange_us": {str(s): round(t * 1e6, 2) for s, t in zip(FIT_SIZES, exch)},
+        "group_exchange_graph_us": {str(s): round(t * 1e6, 2) for s, t in zip(FIT_SIZES, exch_graph)},
         "timed_wall_s": round(wall, 4),
     }
     if sweep is not None:

@@ -137,7 +137,10 @@ int mgw_comm_calls(mgw_comm* comm, int64_t* calls);
 /* Device seconds per step of `reps` back-to-back exchange steps under one event pair
  * (the (a, b) fit's input and the bus-bandwidth sweep).  kind: 0 pack+all-reduce+unpack,
  * 1 all-reduce only, 2 pack only, 3 unpack only, 4 fused kernel, 5 fused bf16 kernel
- * (n_elem bf16 elements), 6 peer rendezvous only (gate kernel).  comm NULL: single rank. */
+ * (n_elem bf16 elements), 6 peer rendezvous only (gate kernel).  comm NULL: single rank.
+ * kind | MGW_TIME_GRAPH: the reps are captured into one CUDA graph and replayed (the
+ * per-launch cost inside the Algorithm-2 engine's graph). */
+#define MGW_TIME_GRAPH 256
 int mgw_time_exchange(mgw_comm* comm, const void* dev_table, int n_rows, int64_t n_elem, float* local_bucket,
                       int algo, int kind, int reps, int warmups, double* seconds_per_rep, void* stream);
 

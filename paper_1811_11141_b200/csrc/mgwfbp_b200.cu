@@ -954,6 +954,8 @@ int mgw_allreduce_fused_bf16_emulated(void* const* tables, void* const* slots, i
 // unpack into `local_bucket`), 1 = all-reduce kernel only, 2 = pack only, 3 = unpack only.
 int mgw_time_exchange(mgw_comm* c, const void* table, int n_rows, int64_t n_elem, float* local_bucket, int algo,
                       int kind, int reps, int warmups, double* seconds_per_rep, void* stream) {
+  const bool as_graph = (kind & MGW_TIME_GRAPH) != 0;  // replay the reps as one CUDA graph
+  kind &= ~MGW_TIME_GRAPH;
   if (reps < 1 || warmups < 0 || !seconds_per_rep || n_elem <= 0 || kind < 0 || kind > 6)
     return set_error(MGW_EINVAL, "bad timing arguments");
   int rc = check_table(table, n_rows, n_elem);
@@ -1003,10 +1005,37 @@ int mgw_time_exchange(mgw_comm* c, const void* table, int n_rows, int64_t n_elem
     return set_error(MGW_ECUDA, "cudaEventCreate: %s", cudaGetErrorString(e));
   }
   for (int r = 0; r < warmups && rc == MGW_OK; ++r) rc = step();
-  // hold the stream while the host enqueues the timed reps
-  if (rc == MGW_OK) spin_relative_kernel<<<1, 32, 0, s>>>(1000000 + 20000LL * reps);
+  cudaGraphExec_t exec = nullptr;
+  if (as_graph && rc == MGW_OK) {
+    // the reps as kernel nodes of one graph: the per-launch cost of the Algorithm-2
+    // engine (which replays its iteration as a graph), not of eager stream launches
+    cudaGraph_t graph = nullptr;
+    e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) rc = set_error(MGW_ECUDA, "capture: %s", cudaGetErrorString(e));
+    for (int r = 0; r < reps && rc == MGW_OK; ++r) rc = step();
+    e = cudaStreamEndCapture(s, &graph);
+    if (rc == MGW_OK && e != cudaSuccess) rc = set_error(MGW_ECUDA, "capture: %s", cudaGetErrorString(e));
+    if (rc == MGW_OK) {
+      e = cudaGraphInstantiate(&exec, graph, 0);
+      if (e != cudaSuccess) rc = set_error(MGW_ECUDA, "instantiate: %s", cudaGetErrorString(e));
+    }
+    if (graph) cudaGraphDestroy(graph);
+    if (rc == MGW_OK) {  // one untimed replay (upload), then the timed one
+      e = cudaGraphLaunch(exec, s);
+      if (e != cudaSuccess) rc = set_error(MGW_ECUDA, "graph launch: %s", cudaGetErrorString(e));
+    }
+  }
+  if (rc == MGW_OK && !as_graph) spin_relative_kernel<<<1, 32, 0, s>>>(1000000 + 20000LL * reps);  // hold the
+  // stream while the host enqueues the timed reps
   if (rc == MGW_OK) cudaEventRecord(ev0, s);
-  for (int r = 0; r < reps && rc == MGW_OK; ++r) rc = step();
+  if (as_graph) {
+    if (rc == MGW_OK) {
+      e = cudaGraphLaunch(exec, s);
+      if (e != cudaSuccess) rc = set_error(MGW_ECUDA, "graph launch: %s", cudaGetErrorString(e));
+    }
+  } else {
+    for (int r = 0; r < reps && rc == MGW_OK; ++r) rc = step();
+  }
   if (rc == MGW_OK) {
     cudaEventRecord(ev1, s);
     e = cudaEventSynchronize(ev1);
@@ -1017,6 +1046,7 @@ int mgw_time_exchange(mgw_comm* c, const void* table, int n_rows, int64_t n_elem
     else
       *seconds_per_rep = ms * 1e-3 / reps;
   }
+  if (exec) cudaGraphExecDestroy(exec);
   cudaEventDestroy(ev0);
   cudaEventDestroy(ev1);
   return rc;

@@ -48,6 +48,12 @@ def main():
         "allreduce_twoshot": T(kind=1, algo=_native.ALGO_TWOSHOT),
         "fused_bf16_auto": T(kind=5),
         "local_pack": [round(t * 1e6, 2) for t in bench._exchange_times(None, 1, device, sizes, kind=2, repeats=50)],
+        # the same steps replayed as one CUDA graph (kind | MGW_TIME_GRAPH): engine-like launch cost
+        "graph_fused_ll": T(kind=4 | 256, algo=_native.ALGO_LL, limit=262144),
+        "graph_fused_auto": T(kind=4 | 256),
+        "graph_gate_plus_counter": T(kind=6 | 256),
+        "graph_local_pack": [round(t * 1e6, 2) for t in
+                             bench._exchange_times(None, 1, device, sizes, kind=2 | 256, repeats=50)],
     }}
     # CTA-count sensitivity of the fused one-shot (16-B slots per CTA; default 512 x Unroll)
     for per in (128, 256, 512):
