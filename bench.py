@@ -165,7 +165,7 @@ def _exchange_times(comm, world, device, sizes, kind=0, algo=0, repeats=20, warm
     scratch = torch.ones(max(sizes) // 4, dtype=torch.float32, device=device)
     local_bucket = torch.empty_like(scratch) if world == 1 else None
     for nbytes in sizes:
-        n = nbytes // (2 if kind == 5 else 4)  # kind 5: bf16 elements
+        n = nbytes // (2 if (kind & 255) == 5 else 4)  # kind 5: bf16 elements
         table = _native.DeviceTable([(scratch.data_ptr(), n, 0)])
         sec = ctypes.c_double()
         _native.call("mgw_time_exchange", comm, table.ptr, 1, n,
