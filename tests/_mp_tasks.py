@@ -287,3 +287,18 @@ def dtype_mismatch_task(config, session):
     t = torch.ones(1000, dtype=dtype, device=session.device)
     ring_allreduce(GradientBuffer(1, 1, t), config, session)
     return True
+
+
+def absent_peer_task(config, session):
+    """Rank 0 enters a collective that rank 1 never joins: a bounded device wait ends in a
+    ProtocolError (no hang); rank 1 outlives the 2 s device timeout, then leaves."""
+    import time
+
+    from paper_1811_11141_b200 import _native
+
+    _native.call("mgw_comm_set_timeout_ms", session.comm, 2000)
+    if config.rank != 0:
+        time.sleep(5.0)
+        return "absent"
+    ring_allreduce(GradientBuffer(1, 1, np.ones(4096, dtype="<f4")), config, session)
+    return "completed"

@@ -60,6 +60,17 @@ def test_dtype_mismatch_is_a_protocol_error():
     assert "buffer lengths" in str(err.value) or "ProtocolError" in str(err.value)
 
 
+def test_absent_peer_times_out_as_protocol_error():
+    """A peer that never reaches the collective: bounded spin -> ProtocolError, not a hang."""
+    import time
+
+    t0 = time.monotonic()
+    with pytest.raises(RuntimeError) as err:
+        run_workers(2, _mp_tasks.absent_peer_task, timeout=120)
+    assert "never reached the collective" in str(err.value)
+    assert time.monotonic() - t0 < 100
+
+
 def test_criterion_7_collective_correctness():
     for n in _worlds():
         for verdicts in run_workers(n, _mp_tasks.collective_task).values():
