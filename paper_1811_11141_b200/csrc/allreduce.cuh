@@ -358,10 +358,21 @@ inline int grid_for(int64_t vectors, int64_t per_cta, int max_ctas) {
 }
 
 // CTAs for a collective over `vectors` 16-B slots (whole bucket for one-shot, one part
-// for two-shot): one batch of U slots per thread by default, or `per_cta` when tuned.
+// for two-shot), or `per_cta` slots per CTA when tuned.  Default: spread a mid-size
+// bucket over up to one CTA per SM (slots per CTA a multiple of 128, at most one batch of
+// U slots per thread) -- engine-mode sweeps (profiles/grid_n{2,4}_r01.json) show one CTA
+// per SM beats both fewer, fatter CTAs (load issue per SM) and two per SM (per-CTA flag
+// traffic, shared SM issue) for 0.25-8 MB; beyond 148 full batches the grid grows to the
+// CTA cap.
 template <int N>
 inline int collective_grid(int64_t vectors, int64_t per_cta, int max_ctas) {
-  return grid_for(vectors, per_cta > 0 ? per_cta : (int64_t)kThreads * Unroll<N>::value, max_ctas);
+  if (per_cta <= 0) {
+    const int64_t full = (int64_t)kThreads * Unroll<N>::value;
+    per_cta = (vectors + kSMs - 1) / kSMs;
+    per_cta = (per_cta + 127) / 128 * 128;
+    per_cta = per_cta < 128 ? 128 : (per_cta > full ? full : per_cta);
+  }
+  return grid_for(vectors, per_cta, max_ctas);
 }
 
 template <int N>
