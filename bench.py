@@ -82,6 +82,8 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
+        if self.proc is not None:
+            time.sleep(1.0)  # NVML start-up stays out of the timed region
         return self
 
     def __exit__(self, *exc):
