@@ -32,6 +32,7 @@
 #include "fused.cuh"
 #include "ll.cuh"
 #include "nvls.cuh"
+#include "push.cuh"
 #include "rows.cuh"
 
 using namespace mgw;
@@ -281,7 +282,7 @@ int comm_allreduce_fused(mgw_comm* c, const Row* host_rows, const Row* dev_rows,
   f.rows = dev_rows;
   f.n_rows = n_rows;
   f.scale = scale;
-  const int chosen = pick_fused_algo(c, n, algo);
+  int chosen = pick_fused_algo(c, n, algo);
   if (chosen == MGW_ALGO_NVLS) {
     if (!c->nvls_bound) return set_error(MGW_EINVAL, "NVLS not set up on this communicator");
     if ((size_t)n * 4 > c->nvls_bytes)
@@ -302,6 +303,18 @@ int comm_allreduce_fused(mgw_comm* c, const Row* host_rows, const Row* dev_rows,
       l.hdr[s] = reinterpret_cast<uint64_t*>(c->peer[s] + kHdrOff);
     }
     return launch_ll(l, c->max_ctas, stream);
+  }
+  if (chosen == MGW_ALGO_PUSH) {
+    const int64_t stride = ((n / 4 + c->world - 1) / c->world + 1) * 4;  // push_stride()
+    if (c->world * stride * 4 <= c->slot_bytes) {
+      PushArgs x;
+      memset(&x, 0, sizeof(x));
+      x.f = f;
+      x.stride = stride;
+      for (int s = 0; s < c->world; ++s) x.gather[s] = c->peer[s] + kSlotOff + 2 * c->slot_bytes;
+      return launch_push(x, c->max_ctas, stream, c->vec_per_cta);
+    }
+    chosen = MGW_ALGO_TWOSHOT;  // the incoming rows do not fit the slot: pull two-shot
   }
   return launch_fused(f, chosen, c->max_ctas, stream, c->vec_per_cta);
 }
@@ -519,7 +532,8 @@ int mgw_comm_create(int rank, int world, int device, int64_t capacity_bytes, mgw
   // one-shot pulls (N-1) M per rank, two-shot 2 (N-1)/N M in two phases: measured
   // crossover on B200 ~ 8 MB / (N - 1) (profiles/ar_sweep_n*_r01_*.json)
   c->oneshot_max_bytes = world > 1 ? (8ll << 20) / (world - 1) : (1ll << 20);
-  const size_t region_bytes = kSlotOff + 2 * (size_t)c->slot_bytes;
+  // [control | LL | slot 0 | slot 1 | gather 0 | gather 1] (gather: push two-shot)
+  const size_t region_bytes = kSlotOff + 4 * (size_t)c->slot_bytes;
   cudaError_t e = cudaMalloc(&c->region, region_bytes);
   if (e == cudaSuccess) e = cudaMemset(c->region, 0, kSlotOff);  // flags, headers, LL area
   if (e == cudaSuccess) e = cudaMalloc(&c->state, 2 * sizeof(uint32_t));
@@ -662,7 +676,7 @@ int mgw_allreduce(mgw_comm* c, int64_t n_elem, int algo, void* stream) {
 int mgw_allreduce_fused(mgw_comm* c, const void* table, int n_rows, int64_t n_elem, float scale, int algo,
                         void* stream) {
   if (!c) return set_error(MGW_EINVAL, "comm is null");
-  if (algo < MGW_ALGO_AUTO || algo > MGW_ALGO_NVLS) return set_error(MGW_EINVAL, "unknown algorithm %d", algo);
+  if (algo < MGW_ALGO_AUTO || algo > MGW_ALGO_PUSH) return set_error(MGW_EINVAL, "unknown algorithm %d", algo);
   int rc = check_table(table, n_rows, n_elem);
   if (rc) return rc;
   const mgw_table_t* t = as_table(table);
@@ -864,10 +878,56 @@ int mgw_allreduce_emulated(float* const* ins, float* const* outs, int world, int
 
 // Emulated ranks on one device: every rank packs its own layer tensors into its
 // slot, then the fused kernel (no barriers) folds and writes back, phase by phase.
+// emulated push two-shot: incoming rows and gather areas allocated here (test path)
+static int push_emulated(void* const* tables, int world, int64_t n, float scale, cudaStream_t s) {
+  if (world < 2) return set_error(MGW_EINVAL, "push two-shot needs >= 2 ranks");
+  const int64_t stride = ((n / 4 + world - 1) / world + 1) * 4;
+  char* mem = nullptr;
+  const size_t in_bytes = (size_t)world * stride * 4, g_bytes = (size_t)n * 4 + 16;
+  MGW_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&mem), (size_t)world * (in_bytes + g_bytes), s));
+  PushArgs x;
+  memset(&x, 0, sizeof(x));
+  for (int r = 0; r < world; ++r) {
+    x.f.ar.slot[r] = mem + (size_t)r * in_bytes;
+    x.gather[r] = mem + (size_t)world * in_bytes + (size_t)r * g_bytes;
+  }
+  x.f.ar.n = n;
+  x.f.ar.world = world;
+  x.f.scale = scale;
+  x.stride = stride;
+  int rc = MGW_OK;
+  for (int step = 0; step < 3 && rc == MGW_OK; ++step) {
+    for (int r = 0; r < world && rc == MGW_OK; ++r) {
+      const mgw_table_t* t = as_table(tables[r]);
+      const int n_rows = (int)t->host.size();
+      x.f.use_inline = n_rows <= kInlineRows;
+      if (x.f.use_inline)
+        for (int k = 0; k < n_rows; ++k) x.f.inline_rows[k] = t->host[k];
+      x.f.rows = t->dev;
+      x.f.n_rows = n_rows;
+      x.f.ar.rank = r;
+      x.f.ar.flags = kNoBarrier | (step == 0 ? kSkipPhase1 | kSkipPhase2
+                                             : kSkipPack | (step == 1 ? kSkipPhase2 : kSkipPhase1));
+      rc = launch_push(x, 2 * kSMs, s, nullptr);
+    }
+  }
+  cudaError_t e = cudaFreeAsync(mem, s);
+  if (rc == MGW_OK && e != cudaSuccess) rc = set_error(MGW_ECUDA, "cudaFreeAsync: %s", cudaGetErrorString(e));
+  return rc;
+}
+
 int mgw_allreduce_fused_emulated(void* const* tables, float* const* slots, int world, int64_t n, float scale, int algo,
                                  void* stream) {
   if (!tables || !slots || world < 1 || world > kMaxRanks || n < 0)
     return set_error(MGW_EINVAL, "bad emulated fused arguments");
+  if (algo == MGW_ALGO_PUSH) {
+    for (int r = 0; r < world; ++r) {
+      const mgw_table_t* t = as_table(tables[r]);
+      int rc = check_table(tables[r], t ? (int)t->host.size() : 0, n);
+      if (rc) return rc;
+    }
+    return n == 0 ? MGW_OK : push_emulated(tables, world, n, scale, static_cast<cudaStream_t>(stream));
+  }
   if (algo != MGW_ALGO_ONESHOT && algo != MGW_ALGO_TWOSHOT)
     return set_error(MGW_EINVAL, "emulated all-reduce needs an explicit algorithm");
   cudaStream_t s = static_cast<cudaStream_t>(stream);

@@ -1,0 +1,202 @@
+// push.cuh -- push-based two-shot group exchange (pack -> reduce-scatter -> all-gather ->
+// unpack in one kernel) for mid-size buckets.
+//
+// The pull two-shot (fused.cuh) pays a remote-read round trip in each of its phases:
+// every load from a peer slot waits ~2 us for NVLink.  Here every byte crosses NVLink
+// as a *store* (fire-and-forget, pipelined by the fabric) and every load is local:
+//
+//   phase 1  CTA b reads chunk b of every part p from the layer tensors (scaled) and
+//            stores it into rank p's incoming area, row `me`             -> barrier
+//   phase 2  CTA b folds chunk b of its own part from the N local incoming rows in the
+//            reference order (fold start = the element's `_segments` segment), writes
+//            the result to its own tensors and stores it into every peer's gather
+//            area at the bucket offset                                      -> barrier
+//   phase 3  CTA b copies chunk b of every peer part from its local gather area into
+//            its tensors.
+//
+// Same bits as the pull kernels (same fp32 adds in the same order).  Incoming area =
+// slot[parity] of each rank viewed as [N src][stride] (stride = one part + tail), gather
+// area = a second pair of capacity-sized buffers in the IPC region.  Reuse distance 2 by
+// parity, as for the slots: a peer can only store into my area of call k + 2 after its
+// CTA b passed the call k + 1 barrier with my CTA b, i.e. after my call k finished.
+#pragma once
+
+#include "fused.cuh"
+
+namespace mgw {
+
+struct PushArgs {
+  FusedArgs f;                 // f.ar.slot[r] = rank r's slot 0 (incoming area for parity 0)
+  char* gather[kMaxRanks];     // rank r's gather area 0 (parity 1 follows at f.ar.slot_stride)
+  int64_t stride;              // incoming row stride in elements (multiple of 4)
+};
+
+__device__ __forceinline__ int64_t push_stride(int64_t nv, int world) {
+  return ((nv + world - 1) / world + 1) * 4;  // one part of 16-B slots + the n % 4 tail
+}
+
+template <int N>
+__global__ void __launch_bounds__(kThreads, 2) push_twoshot_kernel(const __grid_constant__ PushArgs x) {
+  const FusedArgs& f = x.f;
+  const ArArgs& a = f.ar;
+  __shared__ const float* s_in[kMaxRanks];  // incoming area of every rank (this parity)
+  __shared__ int64_t s_end[kMaxRanks];
+  __shared__ float* s_gat[kMaxRanks];
+  uint32_t epoch;
+  int parity;
+  kernel_prologue<N>(a, epoch, parity, s_in, s_end);
+  if (threadIdx.x < N) s_gat[threadIdx.x] = reinterpret_cast<float*>(x.gather[threadIdx.x] + (int64_t)parity * a.slot_stride);
+  const int me = a.rank;
+  const int b = blockIdx.x, G = gridDim.x;
+  const int64_t nv = a.n >> 2;
+  const bool last = b == G - 1;
+  const int64_t tail0 = nv << 2;
+  const int64_t stride = x.stride;
+  const float scale = f.scale;
+  const bool scaled = scale != 1.0f;
+  __shared__ PartChunks<N> pc;
+  __shared__ int64_t s_part0[kMaxRanks + 1];  // first element of every part
+  if (threadIdx.x == 0) part_chunks<N>(nv, b, G, pc);
+  if (threadIdx.x <= N) s_part0[threadIdx.x] = part_begin(threadIdx.x, nv, N) << 2;
+  __syncthreads();
+
+  // ---- phase 1: push chunk b of every part p into rank p's incoming row `me`
+  if (!(a.flags & kSkipPack)) {
+    int cur[N];
+#pragma unroll
+    for (int p = 0; p < N; ++p)
+      cur[p] = fused_row_covering(f, (pc.lo[p] + (threadIdx.x < pc.len[p] ? threadIdx.x : 0)) << 2);
+    for (int64_t i = threadIdx.x; i < pc.longest; i += kThreads) {
+      float4 v[N];
+      bool fast[N];
+#pragma unroll
+      for (int p = 0; p < N; ++p) {
+        fast[p] = false;
+        if (i < pc.len[p]) {
+          const float* tp = fused_tensor(f, cur[p], (pc.lo[p] + i) << 2, fast[p]);
+          if (fast[p]) v[p] = *reinterpret_cast<const float4*>(tp);
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < N; ++p) {
+        if (i >= pc.len[p]) continue;
+        const int64_t e = (pc.lo[p] + i) << 2;
+        float* dst = const_cast<float*>(s_in[p]) + (int64_t)me * stride + (e - s_part0[p]);
+        if (fast[p]) {
+          *reinterpret_cast<float4*>(dst) = scaled ? fmul4(v[p], scale) : v[p];
+        } else {
+          for (int j = 0; j < 4; ++j) {
+            const float y = *fused_tensor1(f, cur[p], e + j);
+            dst[j] = scaled ? __fmul_rn(y, scale) : y;
+          }
+        }
+      }
+    }
+    if (last) {  // the n % 4 tail belongs to part N-1
+      float* dst = const_cast<float*>(s_in[N - 1]) + (int64_t)me * stride - s_part0[N - 1];
+      for (int64_t e = tail0 + threadIdx.x; e < a.n; e += kThreads) {
+        const float y = *fused_tensor1(f, fused_row_covering(f, e), e);
+        dst[e] = scaled ? __fmul_rn(y, scale) : y;
+      }
+    }
+  }
+  int status = MGW_DEV_OK;
+  // ---- phase 2: fold my part's chunk b from the N local rows, write my tensors, push
+  //      the result into every peer's gather area
+  if (!(a.flags & kSkipPhase1)) {
+    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, (uint32_t)a.n, a);
+    if (status == MGW_DEV_OK) {
+      const float* in = s_in[me];
+      const int64_t p0 = s_part0[me];
+      const int64_t v0 = pc.lo[me], v1 = pc.lo[me] + pc.len[me];
+      int seg = advance_segment(0, (v0 + threadIdx.x < v1 ? v0 + threadIdx.x : v0) << 2, s_end);
+      int k = fused_row_covering(f, (v0 + threadIdx.x < v1 ? v0 + threadIdx.x : v0) << 2);
+      for (int64_t v = v0 + threadIdx.x; v < v1; v += kThreads) {
+        const int64_t e = v << 2;
+        const int64_t o = e - p0;
+        seg = advance_segment(seg, e, s_end);
+        float4 y;
+        if (e + 3 < s_end[seg]) {
+          float4 xs[N];
+#pragma unroll
+          for (int kk = 0; kk < N; ++kk) {
+            const int src = seg + kk >= N ? seg + kk - N : seg + kk;
+            xs[kk] = __ldcg(reinterpret_cast<const float4*>(in + (int64_t)src * stride + o));
+          }
+          y = xs[0];
+#pragma unroll
+          for (int kk = 1; kk < N; ++kk) y = fadd4(y, xs[kk]);
+        } else {  // the slot straddles a segment boundary
+          float r[4];
+          int s = seg;
+          for (int j = 0; j < 4; ++j) {
+            s = advance_segment(s, e + j, s_end);
+            float acc = __ldcg(in + (int64_t)s * stride + o + j);
+            for (int kk = 1; kk < N; ++kk) {
+              const int src = s + kk >= N ? s + kk - N : s + kk;
+              acc = __fadd_rn(acc, __ldcg(in + (int64_t)src * stride + o + j));
+            }
+            r[j] = acc;
+          }
+          y = make_float4(r[0], r[1], r[2], r[3]);
+        }
+#pragma unroll
+        for (int q = 0; q < N; ++q)
+          if (q != me) *reinterpret_cast<float4*>(s_gat[q] + e) = y;
+        bool fast;
+        float* tp = fused_tensor(f, k, e, fast);
+        if (fast) {
+          *reinterpret_cast<float4*>(tp) = y;
+        } else {
+          const float r[4] = {y.x, y.y, y.z, y.w};
+          for (int j = 0; j < 4; ++j) *fused_tensor1(f, k, e + j) = r[j];
+        }
+      }
+      if (last && me == N - 1) {
+        for (int64_t e = tail0 + threadIdx.x; e < a.n; e += kThreads) {
+          const int64_t o = e - p0;
+          const int s = advance_segment(0, e, s_end);
+          float acc = __ldcg(in + (int64_t)s * stride + o);
+          for (int kk = 1; kk < N; ++kk) {
+            const int src = s + kk >= N ? s + kk - N : s + kk;
+            acc = __fadd_rn(acc, __ldcg(in + (int64_t)src * stride + o));
+          }
+          for (int q = 0; q < N; ++q)
+            if (q != me) s_gat[q][e] = acc;
+          *fused_tensor1(f, fused_row_covering(f, e), e) = acc;
+        }
+      }
+    }
+  }
+  // ---- phase 3: copy chunk b of every peer part from my gather area into my tensors
+  if (status == MGW_DEV_OK && !(a.flags & kSkipPhase2)) {
+    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.mid, parity, epoch, (uint32_t)a.n, a);
+    if (status == MGW_DEV_OK) {
+      const float* g = s_gat[me];
+      for (int p = 0; p < N; ++p)
+        if (p != me) fused_scatter_range(f, g, pc.lo[p], pc.lo[p] + pc.len[p], 0, 0);
+      if (last && me != N - 1) fused_scatter_range(f, g, 0, 0, tail0, a.n);
+    }
+  }
+  finish_call(a);
+}
+
+inline int launch_push(const PushArgs& x, int max_ctas, cudaStream_t stream, const int64_t* per_cta) {
+  max_ctas = max_ctas < kMaxBlocks ? max_ctas : kMaxBlocks;
+  const int64_t nv = x.f.ar.n >> 2;
+  const int64_t per = per_cta ? per_cta[1] : 0;
+  switch (x.f.ar.world) {
+    case 2: push_twoshot_kernel<2><<<collective_grid<2>(nv / 2, per, max_ctas), kThreads, 0, stream>>>(x); break;
+    case 3: push_twoshot_kernel<3><<<collective_grid<3>(nv / 3, per, max_ctas), kThreads, 0, stream>>>(x); break;
+    case 4: push_twoshot_kernel<4><<<collective_grid<4>(nv / 4, per, max_ctas), kThreads, 0, stream>>>(x); break;
+    case 5: push_twoshot_kernel<5><<<collective_grid<5>(nv / 5, per, max_ctas), kThreads, 0, stream>>>(x); break;
+    case 6: push_twoshot_kernel<6><<<collective_grid<6>(nv / 6, per, max_ctas), kThreads, 0, stream>>>(x); break;
+    case 7: push_twoshot_kernel<7><<<collective_grid<7>(nv / 7, per, max_ctas), kThreads, 0, stream>>>(x); break;
+    case 8: push_twoshot_kernel<8><<<collective_grid<8>(nv / 8, per, max_ctas), kThreads, 0, stream>>>(x); break;
+    default: return set_error(MGW_EINVAL, "push two-shot needs 2..%d ranks, got %d", kMaxRanks, x.f.ar.world);
+  }
+  MGW_CHECK_LAUNCH();
+  return MGW_OK;
+}
+
+}  // namespace mgw

@@ -31,7 +31,17 @@ def main():
     comm = session.comm
     sizes = [262144, 524288, 1 << 20, 2 << 20, 4 << 20, 8 << 20, 16 << 20]
     out = {"world": world, "sizes": sizes, "us": {}}
-    for algo, key, name in ((_native.ALGO_ONESHOT, 0, "one"), (_native.ALGO_TWOSHOT, 1, "two")):
+    # defaults of every fused algorithm, engine mode (graph replay) and stream mode
+    for name, algo in (("one", _native.ALGO_ONESHOT), ("two", _native.ALGO_TWOSHOT), ("push", _native.ALGO_PUSH),
+                       ("auto", _native.ALGO_AUTO)):
+        for mode, flag in (("graph", 256), ("stream", 0)):
+            t = bench._exchange_times(comm, world, device, sizes, kind=4 | flag, algo=algo, repeats=20)
+            out["us"][f"{name}_default_{mode}"] = [round(x * 1e6, 2) for x in t]
+    if os.environ.get("GRID_DEFAULTS_ONLY"):
+        sweep = ()
+    else:
+        sweep = ((_native.ALGO_ONESHOT, 0, "one"), (_native.ALGO_TWOSHOT, 1, "two"))
+    for algo, key, name in sweep:
         for cap in (148, 296, 512):
             _native.call("mgw_comm_set_max_ctas", comm, cap)
             for per in (128, 256, 512, 0):
