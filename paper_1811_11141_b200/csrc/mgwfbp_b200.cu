@@ -883,7 +883,8 @@ static int push_emulated(void* const* tables, int world, int64_t n, float scale,
   if (world < 2) return set_error(MGW_EINVAL, "push two-shot needs >= 2 ranks");
   const int64_t stride = ((n / 4 + world - 1) / world + 1) * 4;
   char* mem = nullptr;
-  const size_t in_bytes = (size_t)world * stride * 4, g_bytes = (size_t)n * 4 + 16;
+  const size_t in_bytes = (size_t)round_up((int64_t)world * stride * 4, 256);
+  const size_t g_bytes = (size_t)round_up(n * 4, 256);
   MGW_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&mem), (size_t)world * (in_bytes + g_bytes), s));
   PushArgs x;
   memset(&x, 0, sizeof(x));

@@ -27,9 +27,11 @@ def main():
 
     rank, world, local = bench._dist_setup(A())
     device = torch.device("cuda", local)
-    _, session = open_session_dist(capacity_bytes=64 << 20)
+    _, session = open_session_dist(capacity_bytes=(128 << 20) + (1 << 20))
     comm = session.comm
     sizes = [262144, 524288, 1 << 20, 2 << 20, 4 << 20, 8 << 20, 16 << 20]
+    if os.environ.get("GRID_LARGE"):
+        sizes = [8 << 20, 16 << 20, 32 << 20, 64 << 20, 128 << 20]
     out = {"world": world, "sizes": sizes, "us": {}}
     # defaults of every fused algorithm, engine mode (graph replay) and stream mode
     for name, algo in (("one", _native.ALGO_ONESHOT), ("two", _native.ALGO_TWOSHOT), ("push", _native.ALGO_PUSH),
