@@ -422,8 +422,15 @@ LL_MAX_BYTES = 256 << 10  # push-based low-latency path (fused exchanges only)
 
 
 def _algo_for(session: RingSession, n: int, fused: bool = False) -> int:
+    """The algorithm the native AUTO choice takes (mirrors pick_fused_algo / pick_algo)."""
     if fused and 4 * n <= LL_MAX_BYTES:
         return _native.ALGO_LL
+    if fused:
+        if session.config.n_workers == 2:
+            return _native.ALGO_ONESHOT if 4 * n <= (16 << 20) else _native.ALGO_PUSH
+        if 4 * n <= session_oneshot_max(session):
+            return _native.ALGO_ONESHOT
+        return _native.ALGO_PUSH if 4 * n >= (8 << 20) else _native.ALGO_TWOSHOT
     return _native.ALGO_ONESHOT if 4 * n <= session_oneshot_max(session) else _native.ALGO_TWOSHOT
 
 

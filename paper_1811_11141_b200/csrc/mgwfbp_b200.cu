@@ -228,7 +228,13 @@ int pick_fused_algo(const mgw_comm* c, int64_t n, int algo) {
   if (c->nvls_bound && c->nvls_min_bytes > 0 && n * 4 >= c->nvls_min_bytes && (size_t)n * 4 <= c->nvls_bytes)
     return MGW_ALGO_NVLS;
   if (c->world > 1 && n * 4 <= c->ll_max_bytes && n <= kLLElems) return MGW_ALGO_LL;
-  return pick_algo(c, n, algo);
+  // engine-mode sweeps (profiles/grid_push_n*_r01.json, profiles/grid_large_n*_r01.json): at
+  // N = 2 the pull one-shot wins up to 16 MB; above it, and from 8 MB at N >= 3, the push
+  // two-shot beats the pull two-shot (546 vs 509 GB/s bus at N = 4, 128 MB)
+  const int64_t bytes = n * 4;
+  if (c->world == 2) return bytes <= (16ll << 20) ? MGW_ALGO_ONESHOT : MGW_ALGO_PUSH;
+  if (bytes <= c->oneshot_max_bytes) return MGW_ALGO_ONESHOT;
+  return bytes >= (8ll << 20) ? MGW_ALGO_PUSH : MGW_ALGO_TWOSHOT;
 }
 
 int comm_allreduce(mgw_comm* c, int64_t n, int algo, cudaStream_t stream, uint64_t* stamp = nullptr) {
