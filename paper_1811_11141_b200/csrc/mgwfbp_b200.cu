@@ -534,7 +534,8 @@ int mgw_comm_create(int rank, int world, int device, int64_t capacity_bytes, mgw
   c->world = world;
   c->device = device;
   c->capacity = capacity_bytes;
-  c->slot_bytes = round_up(std::max<int64_t>(capacity_bytes, 256), 256);
+  // + one 16-B slot per rank of slack: the push two-shot's incoming rows are part-rounded
+  c->slot_bytes = round_up(std::max<int64_t>(capacity_bytes, 256) + 2 * kMaxRanks * 16, 256);
   // one-shot pulls (N-1) M per rank, two-shot 2 (N-1)/N M in two phases: measured
   // crossover on B200 ~ 8 MB / (N - 1) (profiles/ar_sweep_n*_r01_*.json)
   c->oneshot_max_bytes = world > 1 ? (8ll << 20) / (world - 1) : (1ll << 20);
