@@ -215,4 +215,6 @@ def measure_profile(model, step, *, name="measured", repeats=5) -> ModelProfile:
         for k in range(n):
             samples_tb[k].append(times[k])
     layers = tuple(LayerProfile(k + 1, params[k].numel(), statistics.median(samples_tb[k][1:])) for k in range(n))
-    return ModelProfile(name=name, layers=layers, forward_time=statistics.median(samples_tf[1:]))
+    widths = {p.element_size() for p in params}
+    return ModelProfile(name=name, layers=layers, forward_time=statistics.median(samples_tf[1:]),
+                        element_bytes=widths.pop() if len(widths) == 1 else 4)

@@ -32,6 +32,8 @@ def main():
     ap.add_argument("--ctas", default="296,64,32,16", help="CTA caps to try for the overlapped collectives")
     ap.add_argument("--priorities", default="0,-1", help="comm stream priorities to try")
     ap.add_argument("--gates", default="0,1", help="peer gate off/on variants to try")
+    ap.add_argument("--bf16", action="store_true",
+                    help="bf16 parameters and gradients (bf16 wire, fp32 accumulation in the exchange)")
     ap.add_argument("--tune", action="store_true",
                     help="interference-aware MG-WFBP: pick the startup scale k by measured step time "
                          "(replan.calibrate_startup) at each CTA cap, then time the chosen plan")
@@ -55,11 +57,12 @@ def main():
         dist.init_process_group("nccl", device_id=device)
 
     torch.manual_seed(0)
-    net = getattr(torchvision.models, args.model)().to(device)
+    dtype = torch.bfloat16 if args.bf16 else torch.float32
+    net = getattr(torchvision.models, args.model)().to(device=device, dtype=dtype)
     params = trainable_parameters(net)
     total = sum(p.numel() for p in params)
     gen = torch.Generator(device=device).manual_seed(1000 + rank)
-    x = torch.randn(args.batch, 3, 224, 224, device=device, generator=gen)
+    x = torch.randn(args.batch, 3, 224, 224, device=device, generator=gen).to(dtype)
     y = torch.randint(0, 1000, (args.batch,), device=device, generator=gen)
     loss_fn = torch.nn.CrossEntropyLoss()
 
@@ -74,9 +77,11 @@ def main():
         prof = box[0]
     session = comm = None
     if world > 1:
-        _, session = open_session_dist(capacity_bytes=4 * total)
+        _, session = open_session_dist(capacity_bytes=4 * total)  # fp32-sized: also holds bf16 buckets
         comm = session.comm
-    exch = bench._exchange_times(comm, world, device, bench.FIT_SIZES, kind=4 if world > 1 else 0)
+    # (a, b) of the exchange the run will use: bf16 group exchange (kind 5) for bf16 gradients
+    exch = bench._exchange_times(comm, world, device, bench.FIT_SIZES,
+                                 kind=(5 if args.bf16 else 4) if world > 1 else 0)
     model_ab, _ = bench._fit(bench.FIT_SIZES, exch, world)
     n = prof.num_layers
     plans = {"wfbp": MergePlan(frozenset(), n), "mgwfbp": find_merge_plan(prof, model_ab),
@@ -194,7 +199,8 @@ def main():
         session.raise_if_failed()
         session.close()
     out = {
-        "workload": f"torchvision {args.model}, batch {args.batch} per GPU, fp32, SGD momentum, synthetic data",
+        "workload": f"torchvision {args.model}, batch {args.batch} per GPU, {'bf16' if args.bf16 else 'fp32'}, "
+                    f"SGD momentum, synthetic data",
         "world": world, "params": total, "layers": n,
         "measured_forward_ms": round(prof.forward_time * 1e3, 3),
         "measured_backward_ms": round(prof.total_backward_time * 1e3, 3),
