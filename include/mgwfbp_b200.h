@@ -61,6 +61,7 @@ extern "C" {
 #define MGW_ALGO_LL 3 /* push-based low-latency one-shot (fused path only, <= 65,536 elements) */
 #define MGW_ALGO_NVLS 4 /* NVSwitch in-switch reduction (opt-in; fp32 sum, NOT the reference fold order) */
 #define MGW_ALGO_PUSH 5 /* push-based two-shot (fused path only): every NVLink byte is a store */
+#define MGW_ALGO_PUSH_ONESHOT 6 /* push-based one-shot (fused path only): stores out, local fold */
 
 /* schedule flags */
 #define MGW_SCHED_FILL 1u  /* "backward" writes fill_values into each layer before its deadline */

@@ -310,6 +310,18 @@ int comm_allreduce_fused(mgw_comm* c, const Row* host_rows, const Row* dev_rows,
     }
     return launch_ll(l, c->max_ctas, stream);
   }
+  if (chosen == MGW_ALGO_PUSH_ONESHOT) {
+    const int64_t stride = round_up(n, 16);  // one 64-B aligned row per source
+    if (c->world * stride * 4 <= c->slot_bytes) {
+      PushArgs x;
+      memset(&x, 0, sizeof(x));
+      x.f = f;
+      x.stride = stride;
+      for (int s = 0; s < c->world; ++s) x.gather[s] = c->peer[s] + kSlotOff + 2 * c->slot_bytes;
+      return launch_push1(x, c->max_ctas, stream, c->vec_per_cta);
+    }
+    chosen = MGW_ALGO_ONESHOT;  // the rows do not fit: pull one-shot
+  }
   if (chosen == MGW_ALGO_PUSH) {
     const int64_t stride = ((n / 4 + c->world - 1) / c->world + 1) * 4;  // push_stride()
     if (c->world * stride * 4 <= c->slot_bytes) {
@@ -683,7 +695,7 @@ int mgw_allreduce(mgw_comm* c, int64_t n_elem, int algo, void* stream) {
 int mgw_allreduce_fused(mgw_comm* c, const void* table, int n_rows, int64_t n_elem, float scale, int algo,
                         void* stream) {
   if (!c) return set_error(MGW_EINVAL, "comm is null");
-  if (algo < MGW_ALGO_AUTO || algo > MGW_ALGO_PUSH) return set_error(MGW_EINVAL, "unknown algorithm %d", algo);
+  if (algo < MGW_ALGO_AUTO || algo > MGW_ALGO_PUSH_ONESHOT) return set_error(MGW_EINVAL, "unknown algorithm %d", algo);
   int rc = check_table(table, n_rows, n_elem);
   if (rc) return rc;
   const mgw_table_t* t = as_table(table);
@@ -885,13 +897,13 @@ int mgw_allreduce_emulated(float* const* ins, float* const* outs, int world, int
 
 // Emulated ranks on one device: every rank packs its own layer tensors into its
 // slot, then the fused kernel (no barriers) folds and writes back, phase by phase.
-// emulated push two-shot: incoming rows and gather areas allocated here (test path)
-static int push_emulated(void* const* tables, int world, int64_t n, float scale, cudaStream_t s) {
-  if (world < 2) return set_error(MGW_EINVAL, "push two-shot needs >= 2 ranks");
-  const int64_t stride = ((n / 4 + world - 1) / world + 1) * 4;
+// emulated push exchanges: incoming rows and gather areas allocated here (test path)
+static int push_emulated(void* const* tables, int world, int64_t n, float scale, cudaStream_t s, bool oneshot) {
+  if (world < 2) return set_error(MGW_EINVAL, "push exchanges need >= 2 ranks");
+  const int64_t stride = oneshot ? round_up(n, 16) : ((n / 4 + world - 1) / world + 1) * 4;
   char* mem = nullptr;
   const size_t in_bytes = (size_t)round_up((int64_t)world * stride * 4, 256);
-  const size_t g_bytes = (size_t)round_up(n * 4, 256);
+  const size_t g_bytes = oneshot ? in_bytes : (size_t)round_up(n * 4, 256);
   MGW_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&mem), (size_t)world * (in_bytes + g_bytes), s));
   PushArgs x;
   memset(&x, 0, sizeof(x));
@@ -904,7 +916,7 @@ static int push_emulated(void* const* tables, int world, int64_t n, float scale,
   x.f.scale = scale;
   x.stride = stride;
   int rc = MGW_OK;
-  for (int step = 0; step < 3 && rc == MGW_OK; ++step) {
+  for (int step = 0; step < (oneshot ? 2 : 3) && rc == MGW_OK; ++step) {
     for (int r = 0; r < world && rc == MGW_OK; ++r) {
       const mgw_table_t* t = as_table(tables[r]);
       const int n_rows = (int)t->host.size();
@@ -916,7 +928,7 @@ static int push_emulated(void* const* tables, int world, int64_t n, float scale,
       x.f.ar.rank = r;
       x.f.ar.flags = kNoBarrier | (step == 0 ? kSkipPhase1 | kSkipPhase2
                                              : kSkipPack | (step == 1 ? kSkipPhase2 : kSkipPhase1));
-      rc = launch_push(x, 2 * kSMs, s, nullptr);
+      rc = oneshot ? launch_push1(x, 2 * kSMs, s, nullptr) : launch_push(x, 2 * kSMs, s, nullptr);
     }
   }
   cudaError_t e = cudaFreeAsync(mem, s);
@@ -928,13 +940,15 @@ int mgw_allreduce_fused_emulated(void* const* tables, float* const* slots, int w
                                  void* stream) {
   if (!tables || !slots || world < 1 || world > kMaxRanks || n < 0)
     return set_error(MGW_EINVAL, "bad emulated fused arguments");
-  if (algo == MGW_ALGO_PUSH) {
+  if (algo == MGW_ALGO_PUSH || algo == MGW_ALGO_PUSH_ONESHOT) {
     for (int r = 0; r < world; ++r) {
       const mgw_table_t* t = as_table(tables[r]);
       int rc = check_table(tables[r], t ? (int)t->host.size() : 0, n);
       if (rc) return rc;
     }
-    return n == 0 ? MGW_OK : push_emulated(tables, world, n, scale, static_cast<cudaStream_t>(stream));
+    return n == 0 ? MGW_OK
+                  : push_emulated(tables, world, n, scale, static_cast<cudaStream_t>(stream),
+                                  algo == MGW_ALGO_PUSH_ONESHOT);
   }
   if (algo != MGW_ALGO_ONESHOT && algo != MGW_ALGO_TWOSHOT)
     return set_error(MGW_EINVAL, "emulated all-reduce needs an explicit algorithm");

@@ -1,5 +1,5 @@
-// push.cuh -- push-based two-shot group exchange (pack -> reduce-scatter -> all-gather ->
-// unpack in one kernel) for mid-size buckets.
+// push.cuh -- push-based group exchanges: two-shot (pack -> reduce-scatter -> all-gather
+// -> unpack in one kernel) for large buckets, one-shot for mid-size ones.
 //
 // The pull two-shot (fused.cuh) pays a remote-read round trip in each of its phases:
 // every load from a peer slot waits ~2 us for NVLink.  Here every byte crosses NVLink
@@ -179,6 +179,115 @@ __global__ void __launch_bounds__(kThreads, 2) push_twoshot_kernel(const __grid_
     }
   }
   finish_call(a);
+}
+
+// Push one-shot: CTA b stores chunk b of its (scaled) bucket into row `me` of every
+// rank's incoming area (x.gather[r], rows of `stride` = n rounded to 16 B), one barrier,
+// then folds chunk b from the N local rows in the reference order into its tensors.
+// (N-1)·M NVLink bytes out per rank, all as stores; no remote loads.
+template <int N>
+__global__ void __launch_bounds__(kThreads, 2) push_oneshot_kernel(const __grid_constant__ PushArgs x) {
+  constexpr int U = Unroll<N>::value;
+  const FusedArgs& f = x.f;
+  const ArArgs& a = f.ar;
+  __shared__ const float* s_in[kMaxRanks];  // unused slots (prologue computes them)
+  __shared__ int64_t s_end[kMaxRanks];
+  __shared__ float* s_row[kMaxRanks];       // rank r's incoming area (this parity)
+  __shared__ const float* s_mine[kMaxRanks];  // my incoming rows, one per source
+  uint32_t epoch;
+  int parity;
+  kernel_prologue<N>(a, epoch, parity, s_in, s_end);
+  const int me = a.rank;
+  const int64_t stride = x.stride;
+  if (threadIdx.x < N) {
+    s_row[threadIdx.x] = reinterpret_cast<float*>(x.gather[threadIdx.x] + (int64_t)parity * a.slot_stride);
+    s_mine[threadIdx.x] =
+        reinterpret_cast<const float*>(x.gather[me] + (int64_t)parity * a.slot_stride) + (int64_t)threadIdx.x * stride;
+  }
+  __syncthreads();
+  const int64_t nv = a.n >> 2;
+  const int64_t per = (nv + gridDim.x - 1) / gridDim.x;
+  const int64_t v0 = (int64_t)blockIdx.x * per;
+  const int64_t v1 = v0 + per < nv ? v0 + per : nv;
+  const bool last = blockIdx.x == gridDim.x - 1;
+  const float scale = f.scale;
+  const bool scaled = scale != 1.0f;
+  // ---- push chunk b of my bucket into row `me` of every rank
+  if (!(a.flags & kSkipPack)) {
+    constexpr int UP = 4;
+    if (v0 < v1) {
+      int k = fused_row_covering(f, (v0 + threadIdx.x < v1 ? v0 + threadIdx.x : v0) << 2);
+      for (int64_t base = v0 + threadIdx.x; base < v1; base += (int64_t)UP * kThreads) {
+        float4 v[UP];
+        bool fast[UP];
+        int ku[UP];
+#pragma unroll
+        for (int u = 0; u < UP; ++u) {
+          const int64_t vv = base + (int64_t)u * kThreads;
+          fast[u] = false;
+          ku[u] = k;
+          if (vv < v1) {
+            const float* tp = fused_tensor(f, k, vv << 2, fast[u]);
+            ku[u] = k;
+            if (fast[u]) v[u] = *reinterpret_cast<const float4*>(tp);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < UP; ++u) {
+          const int64_t vv = base + (int64_t)u * kThreads;
+          if (vv >= v1) continue;
+          const int64_t e = vv << 2;
+          if (!fast[u]) {
+            float r[4];
+            for (int j = 0; j < 4; ++j) r[j] = *fused_tensor1(f, ku[u], e + j);
+            v[u] = make_float4(r[0], r[1], r[2], r[3]);
+          }
+          if (scaled) v[u] = fmul4(v[u], scale);
+#pragma unroll
+          for (int q = 0; q < N; ++q) *reinterpret_cast<float4*>(s_row[q] + (int64_t)me * stride + e) = v[u];
+        }
+      }
+    }
+    if (last) {
+      for (int64_t e = (nv << 2) + threadIdx.x; e < a.n; e += kThreads) {
+        float y = *fused_tensor1(f, fused_row_covering(f, e), e);
+        if (scaled) y = __fmul_rn(y, scale);
+        for (int q = 0; q < N; ++q) s_row[q][(int64_t)me * stride + e] = y;
+      }
+    }
+  }
+  int status = MGW_DEV_OK;
+  if (!(a.flags & kSkipPhase1)) {
+    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, (uint32_t)a.n, a);
+    if (status == MGW_DEV_OK) {
+      // fold chunk b from the N local rows (they play the slots of fused_reduce_range)
+      fused_reduce_range<N, U>(f, s_mine, s_end, v0, v1, nullptr);
+      if (last) fused_reduce_tail<N>(f, s_mine, s_end, nv << 2, a.n, nullptr);
+    }
+  }
+  finish_call(a);
+}
+
+template <int N>
+int launch_push1_n(const PushArgs& x, int max_ctas, cudaStream_t stream, const int64_t* per_cta) {
+  push_oneshot_kernel<N><<<collective_grid<N>(x.f.ar.n >> 2, per_cta ? per_cta[0] : 0, max_ctas), kThreads, 0,
+                           stream>>>(x);
+  MGW_CHECK_LAUNCH();
+  return MGW_OK;
+}
+
+inline int launch_push1(const PushArgs& x, int max_ctas, cudaStream_t stream, const int64_t* per_cta) {
+  max_ctas = max_ctas < kMaxBlocks ? max_ctas : kMaxBlocks;
+  switch (x.f.ar.world) {
+    case 2: return launch_push1_n<2>(x, max_ctas, stream, per_cta);
+    case 3: return launch_push1_n<3>(x, max_ctas, stream, per_cta);
+    case 4: return launch_push1_n<4>(x, max_ctas, stream, per_cta);
+    case 5: return launch_push1_n<5>(x, max_ctas, stream, per_cta);
+    case 6: return launch_push1_n<6>(x, max_ctas, stream, per_cta);
+    case 7: return launch_push1_n<7>(x, max_ctas, stream, per_cta);
+    case 8: return launch_push1_n<8>(x, max_ctas, stream, per_cta);
+    default: return set_error(MGW_EINVAL, "push one-shot needs 2..%d ranks, got %d", kMaxRanks, x.f.ar.world);
+  }
 }
 
 inline int launch_push(const PushArgs& x, int max_ctas, cudaStream_t stream, const int64_t* per_cta) {

@@ -29,13 +29,13 @@ def main():
     device = torch.device("cuda", local)
     _, session = open_session_dist(capacity_bytes=(128 << 20) + (1 << 20))
     comm = session.comm
-    sizes = [262144, 524288, 1 << 20, 2 << 20, 4 << 20, 8 << 20, 16 << 20]
+    sizes = [65536, 131072, 262144, 524288, 1 << 20, 2 << 20, 4 << 20, 8 << 20, 16 << 20]
     if os.environ.get("GRID_LARGE"):
         sizes = [8 << 20, 16 << 20, 32 << 20, 64 << 20, 128 << 20]
     out = {"world": world, "sizes": sizes, "us": {}}
     # defaults of every fused algorithm, engine mode (graph replay) and stream mode
     for name, algo in (("one", _native.ALGO_ONESHOT), ("two", _native.ALGO_TWOSHOT), ("push", _native.ALGO_PUSH),
-                       ("auto", _native.ALGO_AUTO)):
+                       ("push1", _native.ALGO_PUSH_ONESHOT), ("auto", _native.ALGO_AUTO)):
         for mode, flag in (("graph", 256), ("stream", 0)):
             t = bench._exchange_times(comm, world, device, sizes, kind=4 | flag, algo=algo, repeats=20)
             out["us"][f"{name}_default_{mode}"] = [round(x * 1e6, 2) for x in t]

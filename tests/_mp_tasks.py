@@ -76,7 +76,7 @@ def every_algorithm_task(config, session, *, arrays):
         for key, vals in arrays[config.rank].items():
             n = vals.size
             for name, algo in (("ll", _native.ALGO_LL), ("one", _native.ALGO_ONESHOT), ("two", _native.ALGO_TWOSHOT),
-                               ("push", _native.ALGO_PUSH)):
+                               ("push", _native.ALGO_PUSH), ("push1", _native.ALGO_PUSH_ONESHOT)):
                 t = torch.from_numpy(vals.copy()).to(session.device)
                 table = _native.DeviceTable([(t.data_ptr(), n, 0)])
                 _native.call("mgw_allreduce_fused", session.comm, table.ptr, 1, n, ctypes.c_float(1.0), algo, h)
