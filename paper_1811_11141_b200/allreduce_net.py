@@ -396,7 +396,7 @@ class RingSession:
             c.rounds += 1
             c.payload_bytes_received += 2 * w * n * (world - 1)
             c.payload_bytes_sent += 2 * w * n * (world - 1)
-        elif algo == _native.ALGO_ONESHOT:
+        elif algo in (_native.ALGO_ONESHOT, _native.ALGO_PUSH_ONESHOT):
             c.rounds += 1
             c.payload_bytes_received += w * n * (world - 1)
             c.payload_bytes_sent += w * n * (world - 1)
@@ -427,7 +427,9 @@ def _algo_for(session: RingSession, n: int, fused: bool = False) -> int:
         return _native.ALGO_LL
     if fused:
         if session.config.n_workers == 2:
-            return _native.ALGO_ONESHOT if 4 * n <= (16 << 20) else _native.ALGO_PUSH
+            return _native.ALGO_PUSH_ONESHOT if 4 * n <= (16 << 20) else _native.ALGO_PUSH
+        if 4 * n <= (512 << 10):
+            return _native.ALGO_PUSH_ONESHOT
         if 4 * n <= session_oneshot_max(session):
             return _native.ALGO_ONESHOT
         return _native.ALGO_PUSH if 4 * n >= (8 << 20) else _native.ALGO_TWOSHOT

@@ -228,11 +228,13 @@ int pick_fused_algo(const mgw_comm* c, int64_t n, int algo) {
   if (c->nvls_bound && c->nvls_min_bytes > 0 && n * 4 >= c->nvls_min_bytes && (size_t)n * 4 <= c->nvls_bytes)
     return MGW_ALGO_NVLS;
   if (c->world > 1 && n * 4 <= c->ll_max_bytes && n <= kLLElems) return MGW_ALGO_LL;
-  // engine-mode sweeps (profiles/grid_push_n*_r01.json, profiles/grid_large_n*_r01.json): at
-  // N = 2 the pull one-shot wins up to 16 MB; above it, and from 8 MB at N >= 3, the push
-  // two-shot beats the pull two-shot (546 vs 509 GB/s bus at N = 4, 128 MB)
+  // engine-mode sweeps (profiles/grid_{push,large,push1}_n*_r01.json): at N = 2 the push
+  // one-shot wins up to 16 MB and the push two-shot above; at N >= 3 the push one-shot up
+  // to 512 KB, the pull one-shot to 8 MB / (N - 1), the pull two-shot to 8 MB and the
+  // push two-shot above (546 vs 509 GB/s bus at N = 4, 128 MB)
   const int64_t bytes = n * 4;
-  if (c->world == 2) return bytes <= (16ll << 20) ? MGW_ALGO_ONESHOT : MGW_ALGO_PUSH;
+  if (c->world == 2) return bytes <= (16ll << 20) ? MGW_ALGO_PUSH_ONESHOT : MGW_ALGO_PUSH;
+  if (bytes <= (512ll << 10)) return MGW_ALGO_PUSH_ONESHOT;
   if (bytes <= c->oneshot_max_bytes) return MGW_ALGO_ONESHOT;
   return bytes >= (8ll << 20) ? MGW_ALGO_PUSH : MGW_ALGO_TWOSHOT;
 }
