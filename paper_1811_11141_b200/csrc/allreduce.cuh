@@ -364,11 +364,15 @@ inline int grid_for(int64_t vectors, int64_t per_cta, int max_ctas) {
 // per SM beats both fewer, fatter CTAs (load issue per SM) and two per SM (per-CTA flag
 // traffic, shared SM issue) for 0.25-8 MB; beyond 148 full batches the grid grows to the
 // CTA cap.
+#ifndef MGW_LOCAL_SPREAD
+#define MGW_LOCAL_SPREAD 1  // CTAs per SM the single-rank (HBM-bound) group kernel spreads over
+#endif
 template <int N>
 inline int collective_grid(int64_t vectors, int64_t per_cta, int max_ctas) {
   if (per_cta <= 0) {
     const int64_t full = (int64_t)kThreads * Unroll<N>::value;
-    per_cta = (vectors + kSMs - 1) / kSMs;
+    const int64_t spread = (int64_t)kSMs * (N == 1 ? MGW_LOCAL_SPREAD : 1);
+    per_cta = (vectors + spread - 1) / spread;
     per_cta = (per_cta + 127) / 128 * 128;
     per_cta = per_cta < 128 ? 128 : (per_cta > full ? full : per_cta);
   }
