@@ -41,12 +41,16 @@ def main():
             out["us"][f"{name}_default_{mode}"] = [round(x * 1e6, 2) for x in t]
     if os.environ.get("GRID_DEFAULTS_ONLY"):
         sweep = ()
+    elif os.environ.get("GRID_PUSH_ONLY"):
+        sweep = ((_native.ALGO_PUSH, 1, "push"),)
     else:
         sweep = ((_native.ALGO_ONESHOT, 0, "one"), (_native.ALGO_TWOSHOT, 1, "two"))
     for algo, key, name in sweep:
-        for cap in (148, 296, 512):
+        caps = (148, 296, 512)
+        pers = (128, 256, 512, 0) if name != "push" else (512, 1024, 2048, 4096, 0)
+        for cap in caps:
             _native.call("mgw_comm_set_max_ctas", comm, cap)
-            for per in (128, 256, 512, 0):
+            for per in pers:
                 _native.call("mgw_comm_set_tuning", comm, key, per)
                 t = bench._exchange_times(comm, world, device, sizes, kind=4 | 256, algo=algo, repeats=20)
                 out["us"][f"{name}_cap{cap}_per{per or 'dflt'}"] = [round(x * 1e6, 2) for x in t]
