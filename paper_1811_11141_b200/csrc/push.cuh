@@ -293,7 +293,16 @@ inline int launch_push1(const PushArgs& x, int max_ctas, cudaStream_t stream, co
 inline int launch_push(const PushArgs& x, int max_ctas, cudaStream_t stream, const int64_t* per_cta) {
   max_ctas = max_ctas < kMaxBlocks ? max_ctas : kMaxBlocks;
   const int64_t nv = x.f.ar.n >> 2;
-  const int64_t per = per_cta ? per_cta[1] : 0;
+  int64_t per = per_cta ? per_cta[1] : 0;
+  if (per <= 0) {
+    // large buckets stream better in long per-CTA chunks: 2048-4096 slots (32-64 KB per
+    // part) per CTA, spread over one CTA per SM (profiles/grid_pushtune_n4_r01.json:
+    // 32 MB 105 -> 98 us, 64 MB 195 -> 180 us at N = 4)
+    const int64_t part = nv / (x.f.ar.world > 0 ? x.f.ar.world : 1);
+    per = (part + kSMs - 1) / kSMs;
+    per = (per + 127) / 128 * 128;
+    per = per < 2048 ? 2048 : (per > 4096 ? 4096 : per);
+  }
   switch (x.f.ar.world) {
     case 2: push_twoshot_kernel<2><<<collective_grid<2>(nv / 2, per, max_ctas), kThreads, 0, stream>>>(x); break;
     case 3: push_twoshot_kernel<3><<<collective_grid<3>(nv / 3, per, max_ctas), kThreads, 0, stream>>>(x); break;
