@@ -442,7 +442,9 @@ def session_oneshot_max(session: RingSession) -> int:
 
 
 def set_oneshot_max(session: RingSession, nbytes: int) -> None:
-    """Crossover between the one-shot and two-shot kernels (bytes)."""
+    """Crossover between the pull one-shot and two-shot kernels (bytes) of the unfused
+    path and of the fused AUTO choice at N >= 3 (at N = 2 the fused AUTO choice is the push
+    one-shot up to 16 MB, see ``_algo_for``)."""
     _native.call("mgw_comm_set_oneshot_max", session.comm, int(nbytes))
     session.oneshot_max_bytes = int(nbytes)
 
