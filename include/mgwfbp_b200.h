@@ -146,6 +146,13 @@ int mgw_comm_calls(mgw_comm* comm, int64_t* calls);
 int mgw_time_exchange(mgw_comm* comm, const void* dev_table, int n_rows, int64_t n_elem, float* local_bucket,
                       int algo, int kind, int reps, int warmups, double* seconds_per_rep, void* stream);
 
+/* Self-timed phases of `reps` fused group exchanges (ncu cannot replay a multi-rank
+ * kernel): out[r * 8 + k], %globaltimer ns -- k = 0 first-CTA entry, 1 last-CTA exit,
+ * 2.. CTA 0's phase boundaries (entry, after pack/push, after barrier, after reduce,
+ * [after 2nd barrier, after unpack]); unused entries are 0.  Collective. */
+int mgw_probe_phases(mgw_comm* comm, const void* table, int n_rows, int64_t n_elem, int algo, int reps,
+                     uint64_t* out, void* stream);
+
 /* ---- emulated ranks on one device (test path; no barriers) ------------ */
 int mgw_allreduce_emulated(float* const* ins, float* const* outs, int world, int64_t n_elem, int algo,
                            void* stream);

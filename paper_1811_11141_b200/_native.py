@@ -82,6 +82,7 @@ _SIGNATURES = {
     "mgw_comm_set_nvls_min": ([_P, _I64], _I),
     "mgw_group_launch": ([_P, _P, _I, _I64, ctypes.c_float, _I, _P, _P, _P], _I),
     "mgw_group_launch_bf16": ([_P, _P, _I, _I64, ctypes.c_float, _I, _P, _P, _P], _I),
+    "mgw_probe_phases": ([_P, _P, _I, _I64, _I, _I, ctypes.POINTER(ctypes.c_uint64), _P], _I),
     "mgw_allreduce_fused_bf16": ([_P, _P, _I, _I64, ctypes.c_float, _I, _P], _I),
     "mgw_allreduce_fused_bf16_emulated": ([ctypes.POINTER(_P), ctypes.POINTER(_P), _I, _I64, ctypes.c_float, _I, _P],
                                           _I),

@@ -21,7 +21,7 @@
 
 namespace mgw {
 
-enum : int { kNoBarrier = 1, kSkipPhase1 = 2, kSkipPhase2 = 4, kSkipPack = 8 };
+enum : int { kNoBarrier = 1, kSkipPhase1 = 2, kSkipPhase2 = 4, kSkipPack = 8, kPhaseMarks = 16 };
 
 struct ArArgs {
   char* slot[kMaxRanks];       // slot-0 base of every rank (peer mapped; own at [rank])
@@ -39,6 +39,14 @@ struct ArArgs {
   int world;
   int flags;
 };
+
+// Phase marks (mgw_probe_phases): CTA 0 records %globaltimer at its phase boundaries into
+// stamp[2 + k] (ncu cannot replay a multi-rank kernel, so the kernels time themselves).
+__device__ __forceinline__ void phase_mark(const ArArgs& a, int k) {
+  if (!(a.flags & kPhaseMarks) || a.stamp == nullptr) return;
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.stamp[2 + k] = global_ns();
+}
 
 // Loads in flight per thread ~ 8: unroll the slot loop by 8 / N.
 template <int N>

@@ -105,6 +105,7 @@ __global__ void __launch_bounds__(kThreads, 2) ll_oneshot_kernel(const __grid_co
   const float scale = f.scale;
   const size_t my_off = ((size_t)parity * kMaxRanks + me) * kLLMaxElems;
 
+  phase_mark(a, 0);
   // 1. pack and push: my two elements of each pair to every rank's LL area
   int k = 0;
   if (p0 < p1) k = fused_row_covering(f, (p0 + threadIdx.x) * 2 < n ? (p0 + threadIdx.x) * 2 : 0);
@@ -121,6 +122,7 @@ __global__ void __launch_bounds__(kThreads, 2) ll_oneshot_kernel(const __grid_co
     for (int r = 0; r < N; ++r) st_relaxed_sys_v2(l.ll[r] + my_off + e, w0, w1);
   }
 
+  phase_mark(a, 1);
   // 2. CTA 0 checks every peer's header (length agreement)
   int status = MGW_DEV_OK;
   if (blockIdx.x == 0 && threadIdx.x < N) {
@@ -153,6 +155,7 @@ __global__ void __launch_bounds__(kThreads, 2) ll_oneshot_kernel(const __grid_co
       for (int r = 0; r < N; ++r) store_release_sys32(a.abort_flag[r], 1u);
   }
   status = s_status;
+  phase_mark(a, 2);
 
   // 3. fold every element of my pairs from the N local LL areas, write the tensors.
   //    The N sources' words of a pair are fetched as N independent 16-B loads issued
@@ -200,6 +203,7 @@ __global__ void __launch_bounds__(kThreads, 2) ll_oneshot_kernel(const __grid_co
         for (int r = 0; r < N; ++r) store_release_sys32(a.abort_flag[r], 1u);
     }
   }
+  phase_mark(a, 3);
   finish_call(a);
 }
 

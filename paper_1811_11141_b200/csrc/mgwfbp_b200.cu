@@ -270,7 +270,7 @@ int comm_pack(mgw_comm* c, const Row* host_rows, const Row* dev_rows, int n_rows
 
 // pack -> all-reduce -> unpack of one group in a single kernel (fused.cuh)
 int comm_allreduce_fused(mgw_comm* c, const Row* host_rows, const Row* dev_rows, int n_rows, int64_t n, float scale,
-                         int algo, cudaStream_t stream, uint64_t* stamp = nullptr) {
+                         int algo, cudaStream_t stream, uint64_t* stamp = nullptr, int extra_flags = 0) {
   if (n < 0 || n * 4 > c->slot_bytes)
     return set_error(MGW_EINVAL, "bucket of %lld elements exceeds slot capacity %lld B", (long long)n,
                      (long long)c->slot_bytes);
@@ -284,6 +284,7 @@ int comm_allreduce_fused(mgw_comm* c, const Row* host_rows, const Row* dev_rows,
     if (rc) return rc;
   }
   f.ar.stamp = stamp;
+  f.ar.flags |= extra_flags;
   f.use_inline = n_rows <= kInlineRows && host_rows != nullptr;
   if (f.use_inline)
     for (int k = 0; k < n_rows; ++k) f.inline_rows[k] = host_rows[k];
@@ -723,6 +724,29 @@ int mgw_allreduce_fused_bf16(mgw_comm* c, const void* table, int n_rows, int64_t
   const mgw_table_t* t = as_table(table);
   return comm_allreduce_fused_bf16(c, t->host.data(), t->dev, n_rows, n_elem, scale, algo,
                                    static_cast<cudaStream_t>(stream));
+}
+
+int mgw_probe_phases(mgw_comm* c, const void* table, int n_rows, int64_t n_elem, int algo, int reps, uint64_t* out,
+                     void* stream) {
+  if (!c || !out || reps < 1 || c->world < 2) return set_error(MGW_EINVAL, "bad phase-probe arguments");
+  int rc = check_table(table, n_rows, n_elem);
+  if (rc) return rc;
+  const mgw_table_t* t = as_table(table);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::vector<uint64_t> h((size_t)reps * 8, 0);
+  for (int r = 0; r < reps; ++r) h[(size_t)r * 8] = ~0ull;  // first-CTA entry is a min
+  uint64_t* d = nullptr;
+  MGW_CUDA(cudaMalloc(&d, h.size() * sizeof(uint64_t)));
+  cudaError_t e = cudaMemcpyAsync(d, h.data(), h.size() * sizeof(uint64_t), cudaMemcpyHostToDevice, s);
+  for (int r = 0; r < reps && rc == MGW_OK && e == cudaSuccess; ++r)
+    rc = comm_allreduce_fused(c, t->host.data(), t->dev, n_rows, n_elem, 1.f, algo, s, d + (size_t)r * 8, kPhaseMarks);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h.data(), d, h.size() * sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFree(d);
+  if (rc) return rc;
+  if (e != cudaSuccess) return set_error(MGW_ECUDA, "phase probe: %s", cudaGetErrorString(e));
+  memcpy(out, h.data(), h.size() * sizeof(uint64_t));
+  return MGW_OK;
 }
 
 int mgw_nvls_supported(int device, int* ok) {

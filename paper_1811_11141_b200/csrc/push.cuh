@@ -60,6 +60,7 @@ __global__ void __launch_bounds__(kThreads, 2) push_twoshot_kernel(const __grid_
   if (threadIdx.x <= N) s_part0[threadIdx.x] = part_begin(threadIdx.x, nv, N) << 2;
   __syncthreads();
 
+  phase_mark(a, 0);
   // ---- phase 1: push chunk b of every part p into rank p's incoming row `me`
   if (!(a.flags & kSkipPack)) {
     int cur[N];
@@ -100,11 +101,13 @@ __global__ void __launch_bounds__(kThreads, 2) push_twoshot_kernel(const __grid_
       }
     }
   }
+  phase_mark(a, 1);
   int status = MGW_DEV_OK;
   // ---- phase 2: fold my part's chunk b from the N local rows, write my tensors, push
   //      the result into every peer's gather area
   if (!(a.flags & kSkipPhase1)) {
     if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, (uint32_t)a.n, a);
+    phase_mark(a, 2);
     if (status == MGW_DEV_OK) {
       const float* in = s_in[me];
       const int64_t p0 = s_part0[me];
@@ -168,15 +171,18 @@ __global__ void __launch_bounds__(kThreads, 2) push_twoshot_kernel(const __grid_
       }
     }
   }
+  phase_mark(a, 3);
   // ---- phase 3: copy chunk b of every peer part from my gather area into my tensors
   if (status == MGW_DEV_OK && !(a.flags & kSkipPhase2)) {
     if (!(a.flags & kNoBarrier)) status = cta_barrier(a.mid, parity, epoch, (uint32_t)a.n, a);
+    phase_mark(a, 4);
     if (status == MGW_DEV_OK) {
       const float* g = s_gat[me];
       for (int p = 0; p < N; ++p)
         if (p != me) fused_scatter_range(f, g, pc.lo[p], pc.lo[p] + pc.len[p], 0, 0);
       if (last && me != N - 1) fused_scatter_range(f, g, 0, 0, tail0, a.n);
     }
+    phase_mark(a, 5);
   }
   finish_call(a);
 }
@@ -212,6 +218,7 @@ __global__ void __launch_bounds__(kThreads, 2) push_oneshot_kernel(const __grid_
   const bool last = blockIdx.x == gridDim.x - 1;
   const float scale = f.scale;
   const bool scaled = scale != 1.0f;
+  phase_mark(a, 0);
   // ---- push chunk b of my bucket into row `me` of every rank
   if (!(a.flags & kSkipPack)) {
     constexpr int UP = 4;
@@ -256,14 +263,17 @@ __global__ void __launch_bounds__(kThreads, 2) push_oneshot_kernel(const __grid_
       }
     }
   }
+  phase_mark(a, 1);
   int status = MGW_DEV_OK;
   if (!(a.flags & kSkipPhase1)) {
     if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, (uint32_t)a.n, a);
+    phase_mark(a, 2);
     if (status == MGW_DEV_OK) {
       // fold chunk b from the N local rows (they play the slots of fused_reduce_range)
       fused_reduce_range<N, U>(f, s_mine, s_end, v0, v1, nullptr);
       if (last) fused_reduce_tail<N>(f, s_mine, s_end, nv << 2, a.n, nullptr);
     }
+    phase_mark(a, 3);
   }
   finish_call(a);
 }
