@@ -70,7 +70,7 @@ __device__ __forceinline__ void scalar_op(float* t, float* b, float scale, float
 constexpr int kRowsUnroll = 4;  // 16-B slots per thread per step
 
 template <RowOp kOp, bool kScale>
-__global__ void __launch_bounds__(kThreads) rows_kernel(const __grid_constant__ RowsParam p) {
+__global__ void __launch_bounds__(kThreads, 2) rows_kernel(const __grid_constant__ RowsParam p) {
   stamp_enter(p.stamp);
   float* bucket = p.bucket;
   if (p.calls != nullptr) bucket += (int64_t)((load_volatile32(p.calls) + 1u) & 1u) * p.slot_stride_elems;
@@ -128,8 +128,9 @@ __global__ void __launch_bounds__(kThreads) rows_kernel(const __grid_constant__ 
         for (int u = 0; u < kRowsUnroll; ++u)
           if (fast[u]) *reinterpret_cast<float4*>(tp[u]) = make_float4(value[u], value[u], value[u], value[u]);
       }
-      // slow path: element by element, each finding its own row
-#pragma unroll 1
+      // slow path: element by element, each finding its own row (unrolled so the per-u
+      // arrays stay in registers)
+#pragma unroll
       for (int u = 0; u < kRowsUnroll; ++u) {
         const int64_t e = base + (int64_t)u * 4 * kThreads;
         if (fast[u] || e >= t1) continue;
@@ -148,14 +149,14 @@ __global__ void __launch_bounds__(kThreads) rows_kernel(const __grid_constant__ 
   stamp_exit(p.stamp);
 }
 
-// Tile and grid for a bucket of `total` elements.  At most one resident wave
-// (512-thread CTAs at <= 40 registers -> 3 per SM; ncu r01:
-// launch__occupancy_limit_registers = 3, a 592-CTA grid left a 1/3 tail wave).  A
-// mid-sized group (a 9.4 MB ResNet layer) is spread over the whole wave with smaller
-// tiles instead of parking on 144 CTAs of 64 KB: more SMs, more bytes in flight.
+// Tile and grid for a bucket of `total` elements.  At most one resident wave: 512-thread
+// CTAs at <= 64 registers (spill-free with the unrolled slow path) -> 2 per SM (a grid
+// beyond the resident wave leaves a tail, ncu r01).  A mid-sized group (a 9.4 MB ResNet
+// layer) is spread over the whole wave with smaller tiles instead of parking on 144
+// CTAs of 64 KB: more SMs, more bytes in flight.
 inline int rows_grid(int64_t total, int64_t* tile_out) {
   constexpr int64_t kStep = 4 * kThreads;  // one 16-B slot per thread
-  const int64_t cap = (int64_t)kSMs * 3;
+  const int64_t cap = (int64_t)kSMs * 2;
   int64_t tile = (total + cap - 1) / cap;
   tile = (tile + kStep - 1) / kStep * kStep;
   tile = tile < kStep ? kStep : (tile > kTile ? kTile : tile);
