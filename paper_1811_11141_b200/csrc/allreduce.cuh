@@ -56,6 +56,9 @@ struct Unroll {
 
 // One barrier round for this CTA.  Thread t < world signals rank t and waits for
 // rank t's matching CTA.
+#ifndef MGW_BARRIER_RELAXED_POLL
+#define MGW_BARRIER_RELAXED_POLL 0
+#endif
 __device__ __noinline__ int cta_barrier(uint64_t* const* flags, int parity, uint32_t epoch, uint32_t tag,
                                         const ArArgs& a) {
   __shared__ int s_status;
@@ -69,7 +72,11 @@ __device__ __noinline__ int cta_barrier(uint64_t* const* flags, int parity, uint
     const uint64_t start = global_ns();
     int status = MGW_DEV_OK;
     for (uint32_t spin = 0;; ++spin) {
+#if MGW_BARRIER_RELAXED_POLL
+      const uint64_t v = ld_relaxed_sys64(mine);
+#else
       const uint64_t v = load_acquire_sys(mine);
+#endif
       if ((uint32_t)(v >> 32) == epoch) {
         if ((uint32_t)v != tag) status = MGW_DEV_LENGTH_MISMATCH;
         break;
@@ -86,6 +93,9 @@ __device__ __noinline__ int cta_barrier(uint64_t* const* flags, int parity, uint
       }
     }
     if (status != MGW_DEV_OK) atomicCAS(&s_status, 0, status);
+#if MGW_BARRIER_RELAXED_POLL
+    fence_acq_rel_sys();  // one acquire fence after the relaxed polls
+#endif
   }
   __syncthreads();
   const int status = s_status;
