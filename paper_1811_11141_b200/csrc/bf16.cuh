@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(kThreads, 2) b16_twoshot_kernel(const __grid_c
 // LL push one-shot for small bf16 buckets: a word carries (epoch << 32 | two bf16), a
 // 16-B push carries four elements.  Same protocol as ll_oneshot_kernel (ll.cuh): header
 // length check by CTA 0, batched polls of the N sources, fold in the reference order in
-// fp32, one rounding.  At most 2 * kLLMaxElems elements (256 KB).
+// fp32, one rounding.  At most 2 * kLLMaxElems elements (1 MB of bf16 per parity).
 __device__ __forceinline__ uint64_t ll_b16_word(uint32_t epoch, uint16_t lo, uint16_t hi) {
   return ((uint64_t)epoch << 32) | ((uint32_t)hi << 16) | lo;
 }
@@ -483,7 +483,7 @@ inline int launch_ll_b16(const LLArgs& l, int max_ctas, cudaStream_t stream) {
   if (l.f.ar.n > 2 * kLLMaxElems)
     return set_error(MGW_EINVAL, "bf16 LL path takes at most %lld elements", (long long)(2 * kLLMaxElems));
   const int64_t quads = (l.f.ar.n + 3) >> 2;
-  const int grid = grid_for(quads, kThreads, max_ctas < 128 ? max_ctas : 128);
+  const int grid = grid_for(quads, kThreads, max_ctas < kSMs ? max_ctas : kSMs);
   switch (l.f.ar.world) {
     case 2: ll_b16_kernel<2><<<grid, kThreads, 0, stream>>>(l); break;
     case 3: ll_b16_kernel<3><<<grid, kThreads, 0, stream>>>(l); break;

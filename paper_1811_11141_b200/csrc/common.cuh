@@ -65,7 +65,7 @@ constexpr size_t kCtrlBytes = 262144;
 static_assert(kDoorOff + kMaxRanks * sizeof(uint64_t) <= kCtrlBytes, "control area overflow");
 // LL receive area u64 [2 parity][kMaxRanks src][kLLElems] follows the control area,
 // then the two bucket slots.
-constexpr int64_t kLLElems = 65536;
+constexpr int64_t kLLElems = 262144;  // 1 MB of fp32 payload per source per parity
 constexpr size_t kLLOff = kCtrlBytes;
 constexpr size_t kLLBytes = 2 * (size_t)kMaxRanks * (size_t)kLLElems * sizeof(uint64_t);
 constexpr size_t kSlotOff = kLLOff + kLLBytes;

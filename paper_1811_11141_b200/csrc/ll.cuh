@@ -19,7 +19,7 @@
 
 namespace mgw {
 
-constexpr int64_t kLLMaxElems = kLLElems;  // per rank per parity (256 KB of fp32 payload)
+constexpr int64_t kLLMaxElems = kLLElems;  // per rank per parity (1 MB of fp32 payload)
 
 struct LLArgs {
   FusedArgs f;                   // rows (layer tensors), scale, comm pointers, epochs
@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(kThreads, 2) ll_oneshot_kernel(const __grid_co
 template <int N>
 int launch_ll_n(const LLArgs& l, int max_ctas, cudaStream_t stream) {
   const int64_t pairs = (l.f.ar.n + 1) >> 1;
-  ll_oneshot_kernel<N><<<grid_for(pairs, kThreads, max_ctas < 128 ? max_ctas : 128), kThreads, 0, stream>>>(l);
+  ll_oneshot_kernel<N><<<grid_for(pairs, kThreads, max_ctas < kSMs ? max_ctas : kSMs), kThreads, 0, stream>>>(l);
   MGW_CHECK_LAUNCH();
   return MGW_OK;
 }

@@ -95,7 +95,7 @@ struct mgw_comm {
   float* result = nullptr;
   uint64_t timeout_ns = 30ull * 1000000000ull;
   int64_t oneshot_max_bytes = 1 << 20;  // set per world in mgw_comm_create
-  int64_t ll_max_bytes = kLLElems * 4;  // 256 KB: the whole LL area
+  int64_t ll_max_bytes = 256 << 10;  // AUTO's LL ceiling (the area holds kLLElems per source)
   int max_ctas = 2 * kSMs;
   int64_t vec_per_cta[2] = {0, 0};      // tuning: 16-B slots per CTA (one-shot, two-shot); 0 = default
   // NVLS (opt-in): multicast object bound to a per-rank bucket

@@ -34,11 +34,12 @@ def main():
         sizes = [8 << 20, 16 << 20, 32 << 20, 64 << 20, 128 << 20]
     out = {"world": world, "sizes": sizes, "us": {}}
     # defaults of every fused algorithm, engine mode (graph replay) and stream mode
-    for name, algo in (("one", _native.ALGO_ONESHOT), ("two", _native.ALGO_TWOSHOT), ("push", _native.ALGO_PUSH),
-                       ("push1", _native.ALGO_PUSH_ONESHOT), ("auto", _native.ALGO_AUTO)):
+    for name, algo in (("ll", _native.ALGO_LL), ("one", _native.ALGO_ONESHOT), ("two", _native.ALGO_TWOSHOT),
+                       ("push", _native.ALGO_PUSH), ("push1", _native.ALGO_PUSH_ONESHOT), ("auto", _native.ALGO_AUTO)):
+        ok = [m for m in sizes if name != "ll" or m <= (1 << 20)]
         for mode, flag in (("graph", 256), ("stream", 0)):
-            t = bench._exchange_times(comm, world, device, sizes, kind=4 | flag, algo=algo, repeats=20)
-            out["us"][f"{name}_default_{mode}"] = [round(x * 1e6, 2) for x in t]
+            t = bench._exchange_times(comm, world, device, ok, kind=4 | flag, algo=algo, repeats=20)
+            out["us"][f"{name}_default_{mode}"] = [round(x * 1e6, 2) for x in t] + [None] * (len(sizes) - len(ok))
     if os.environ.get("GRID_DEFAULTS_ONLY"):
         sweep = ()
     elif os.environ.get("GRID_PUSH_ONLY"):
