@@ -418,12 +418,17 @@ def _segments(n_elements: int, n_parts: int) -> tuple[list[int], list[int]]:
     return sizes, offsets
 
 
-LL_MAX_BYTES = 256 << 10  # push-based low-latency path (fused exchanges only)
+LL_MAX_BYTES = 256 << 10  # push-based low-latency path (fused exchanges only), N >= 5
+
+
+def ll_max_bytes(world: int) -> int:
+    """AUTO's LL ceiling (mirrors mgw_comm_create): 1 MB at N = 2, 512 KB at N <= 4."""
+    return (1 << 20) if world == 2 else ((512 << 10) if world <= 4 else LL_MAX_BYTES)
 
 
 def _algo_for(session: RingSession, n: int, fused: bool = False) -> int:
     """The algorithm the native AUTO choice takes (mirrors pick_fused_algo / pick_algo)."""
-    if fused and 4 * n <= LL_MAX_BYTES:
+    if fused and 4 * n <= ll_max_bytes(session.config.n_workers):
         return _native.ALGO_LL
     if fused:
         if session.config.n_workers == 2:
@@ -487,7 +492,7 @@ def ring_allreduce(
         algo = _algo_for(session, n, fused=True)
         handle = stream.cuda_stream
         if n and bf16:
-            if 2 * n <= LL_MAX_BYTES:
+            if 2 * n <= ll_max_bytes(config.n_workers):
                 algo = _native.ALGO_LL
             else:
                 algo = _native.ALGO_ONESHOT if 2 * n <= session_oneshot_max(session) else _native.ALGO_TWOSHOT

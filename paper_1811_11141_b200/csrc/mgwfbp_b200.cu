@@ -554,6 +554,9 @@ int mgw_comm_create(int rank, int world, int device, int64_t capacity_bytes, mgw
   // one-shot pulls (N-1) M per rank, two-shot 2 (N-1)/N M in two phases: measured
   // crossover on B200 ~ 8 MB / (N - 1) (profiles/ar_sweep_n*_r01_*.json)
   c->oneshot_max_bytes = world > 1 ? (8ll << 20) / (world - 1) : (1ll << 20);
+  // LL beats every barrier-based exchange up to 1 MB at N = 2 and 512 KB at N <= 4
+  // (engine-mode sweeps, profiles/grid_ll_n{2,4}_r01.json); its 2x wire bytes grow with N
+  c->ll_max_bytes = world == 2 ? (1ll << 20) : (world <= 4 ? (512ll << 10) : (256ll << 10));
   // [control | LL | slot 0 | slot 1 | gather 0 | gather 1] (gather: push two-shot)
   const size_t region_bytes = kSlotOff + 4 * (size_t)c->slot_bytes;
   cudaError_t e = cudaMalloc(&c->region, region_bytes);
