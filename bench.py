@@ -260,6 +260,19 @@ def _fit(sizes, times, world):
         return CommModel(a=min(times), b=0.0), False
 
 
+def _algo_mix(session, group_bytes):
+    """How many groups each AUTO algorithm serves (mirrors the native choice)."""
+    import collections
+
+    from paper_1811_11141_b200 import _native
+    from paper_1811_11141_b200.allreduce_net import _algo_for
+
+    names = {_native.ALGO_LL: "ll", _native.ALGO_ONESHOT: "oneshot", _native.ALGO_TWOSHOT: "twoshot",
+             _native.ALGO_PUSH: "push_twoshot", _native.ALGO_PUSH_ONESHOT: "push_oneshot"}
+    mix = collections.Counter(names.get(_algo_for(session, b // 4, fused=True), "other") for b in group_bytes if b)
+    return dict(sorted(mix.items()))
+
+
 class RankContext:
     """This rank's view of the run: ids, device, communicator and the L2-flush buffer."""
 
@@ -515,6 +528,7 @@ def run_ours(args) -> dict | None:
             "l2": "flushed between iterations (256 MiB write on the compute stream, outside the timed events)",
             "cuda_graph": not args.no_graph,
             "fused_group_kernel": not args.unfused,
+            "group_algorithms": _algo_mix(session, gbytes) if (session is not None and not args.unfused) else None,
         },
         "strategies": results,
         "mgwfbp_plan_equals_wfbp": same_as_wfbp,
