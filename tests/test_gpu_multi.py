@@ -108,7 +108,7 @@ def test_fused_algorithms_large_multirow_vs_oracle():
     from oracle import ring_oracle
     from paper_1811_11141_b200 import _native
 
-    sizes = (4099, 16705, 40000, 65536)
+    sizes = (4099, 16705, 40000, 65536, 131075, 262144)  # up to the LL area's 1 MB per source
     algos = (_native.ALGO_LL, _native.ALGO_ONESHOT, _native.ALGO_TWOSHOT, _native.ALGO_PUSH, _native.ALGO_PUSH_ONESHOT)
     for n in _worlds():
         res = run_workers(n, partial(_mp_tasks.sizes_task, sizes=sizes, algos=algos))
