@@ -368,7 +368,8 @@ __global__ void __launch_bounds__(kThreads, 2) ll_b16_kernel(const __grid_consta
     s_end[t] = (int64_t)(t + 1) * q + (t + 1 < r ? t + 1 : r);
   }
   if (threadIdx.x == 0) s_status = MGW_DEV_OK;
-  if (blockIdx.x == 0 && threadIdx.x < N)
+  const bool do_push = !(a.flags & kSkipPack), do_fold = !(a.flags & kSkipPhase1);  // emulation split
+  if (do_push && blockIdx.x == 0 && threadIdx.x < N)
     st_relaxed_sys_u64(l.hdr[threadIdx.x] + parity * kMaxRanks + me, ((uint64_t)epoch << 32) | b16_tag(n));
   __syncthreads();
 
@@ -382,7 +383,7 @@ __global__ void __launch_bounds__(kThreads, 2) ll_b16_kernel(const __grid_consta
   // 1. pack and push my four elements of each quad to every rank
   int k = 0;
   if (q0 < q1) k = fused_row_covering(f, (q0 + threadIdx.x) * 4 < n ? (q0 + threadIdx.x) * 4 : 0);
-  for (int64_t j = q0 + threadIdx.x; j < q1; j += kThreads) {
+  for (int64_t j = q0 + threadIdx.x; do_push && j < q1; j += kThreads) {
     const int64_t e = 4 * j;
     uint16_t x[4];
 #pragma unroll
@@ -401,7 +402,7 @@ __global__ void __launch_bounds__(kThreads, 2) ll_b16_kernel(const __grid_consta
 
   // 2. CTA 0 checks every peer's header (length and dtype agreement)
   int status = MGW_DEV_OK;
-  if (blockIdx.x == 0 && threadIdx.x < N) {
+  if (do_fold && blockIdx.x == 0 && threadIdx.x < N) {
     const uint64_t* p = l.hdr[me] + parity * kMaxRanks + threadIdx.x;
     uint64_t v = ld_relaxed_sys_u64(p);
     const uint64_t start = global_ns();
@@ -430,7 +431,7 @@ __global__ void __launch_bounds__(kThreads, 2) ll_b16_kernel(const __grid_consta
   status = s_status;
 
   // 3. fold: batched 16-B polls of the N sources, fp32 fold in the reference order
-  if (status == MGW_DEV_OK) {
+  if (do_fold && status == MGW_DEV_OK) {
     const float scale = f.scale;
     const bool scaled = scale != 1.0f;
     const uint64_t* base = l.ll[me] + (size_t)parity * kMaxRanks * kLLMaxElems;

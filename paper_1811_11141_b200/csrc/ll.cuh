@@ -92,8 +92,10 @@ __global__ void __launch_bounds__(kThreads, 2) ll_oneshot_kernel(const __grid_co
     s_end[t] = (int64_t)(t + 1) * q + (t + 1 < r ? t + 1 : r);
   }
   if (threadIdx.x == 0) s_status = MGW_DEV_OK;
-  // header: (epoch, n) to every rank (CTA 0)
-  if (blockIdx.x == 0 && threadIdx.x < N)
+  // header: (epoch, n) to every rank (CTA 0).  kSkipPack / kSkipPhase1 split the push
+  // and the fold into separate launches (emulated ranks on one device, tests only).
+  const bool do_push = !(a.flags & kSkipPack), do_fold = !(a.flags & kSkipPhase1);
+  if (do_push && blockIdx.x == 0 && threadIdx.x < N)
     st_relaxed_sys_u64(l.hdr[threadIdx.x] + parity * kMaxRanks + me, ((uint64_t)epoch << 32) | (uint32_t)n);
   __syncthreads();
 
@@ -109,7 +111,7 @@ __global__ void __launch_bounds__(kThreads, 2) ll_oneshot_kernel(const __grid_co
   // 1. pack and push: my two elements of each pair to every rank's LL area
   int k = 0;
   if (p0 < p1) k = fused_row_covering(f, (p0 + threadIdx.x) * 2 < n ? (p0 + threadIdx.x) * 2 : 0);
-  for (int64_t j = p0 + threadIdx.x; j < p1; j += kThreads) {
+  for (int64_t j = p0 + threadIdx.x; do_push && j < p1; j += kThreads) {
     const int64_t e = 2 * j;
     float x0 = *ll_tensor(f, k, e);
     float x1 = e + 1 < n ? *ll_tensor(f, k, e + 1) : 0.f;
@@ -125,7 +127,7 @@ __global__ void __launch_bounds__(kThreads, 2) ll_oneshot_kernel(const __grid_co
   phase_mark(a, 1);
   // 2. CTA 0 checks every peer's header (length agreement)
   int status = MGW_DEV_OK;
-  if (blockIdx.x == 0 && threadIdx.x < N) {
+  if (do_fold && blockIdx.x == 0 && threadIdx.x < N) {
     const uint64_t h = [&] {
       const uint64_t* p = l.hdr[me] + parity * kMaxRanks + threadIdx.x;
       uint64_t v = ld_relaxed_sys_u64(p);
@@ -161,7 +163,7 @@ __global__ void __launch_bounds__(kThreads, 2) ll_oneshot_kernel(const __grid_co
   //    The N sources' words of a pair are fetched as N independent 16-B loads issued
   //    back to back (one memory latency, not 2N serial ones); only words that do not yet
   //    carry this epoch are polled again.
-  if (status == MGW_DEV_OK) {
+  if (do_fold && status == MGW_DEV_OK) {
     const uint64_t* base = l.ll[me] + (size_t)parity * kMaxRanks * kLLMaxElems;
     int seg = 0;
     k = 0;

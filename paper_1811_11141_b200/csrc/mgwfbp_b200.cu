@@ -965,10 +965,84 @@ static int push_emulated(void* const* tables, int world, int64_t n, float scale,
   return rc;
 }
 
+// emulated LL exchange (fp32 or bf16): every rank's pushes in one pass of launches, then
+// every rank's fold in a second pass (no kernel ever waits on a later launch)
+static int ll_emulated(void* const* tables, int world, int64_t n, float scale, cudaStream_t s, bool bf16) {
+  if (world < 2) return set_error(MGW_EINVAL, "LL needs >= 2 ranks");
+  if (n > (bf16 ? 2 : 1) * kLLElems) return set_error(MGW_EINVAL, "LL path takes at most %lld elements",
+                                                      (long long)((bf16 ? 2 : 1) * kLLElems));
+  const size_t hdr_bytes = 2 * kMaxRanks * sizeof(uint64_t);
+  const size_t per_rank = kLLBytes + 256;  // LL area + headers / state / abort / error words
+  char* mem = nullptr;
+  MGW_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&mem), (size_t)world * per_rank, s));
+  LLArgs l;
+  memset(&l, 0, sizeof(l));
+  for (int r = 0; r < world; ++r) {
+    char* base = mem + (size_t)r * per_rank;
+    l.ll[r] = reinterpret_cast<uint64_t*>(base);
+    l.hdr[r] = reinterpret_cast<uint64_t*>(base + kLLBytes);
+    l.f.ar.abort_flag[r] = reinterpret_cast<uint32_t*>(base + kLLBytes + hdr_bytes);
+  }
+  l.f.ar.n = n;
+  l.f.ar.world = world;
+  l.f.ar.timeout_ns = 2000000000ull;
+  l.f.scale = scale;
+  int rc = MGW_OK;
+  for (int step = 0; step < 2 && rc == MGW_OK; ++step) {
+    for (int r = 0; r < world && rc == MGW_OK; ++r) {
+      char* ctl = mem + (size_t)r * per_rank + kLLBytes + hdr_bytes;  // [abort u32][state u32 x2][err i32]
+      if (step == 0 && r == 0) {
+        for (int q = 0; q < world; ++q) {
+          cudaError_t e = cudaMemsetAsync(mem + (size_t)q * per_rank + kLLBytes + hdr_bytes, 0, 16, s);
+          if (e != cudaSuccess) rc = set_error(MGW_ECUDA, "memset: %s", cudaGetErrorString(e));
+        }
+      }
+      // every launch of rank r sees call counter 0 -> epoch 1 (finish_call advances it)
+      cudaError_t e = cudaMemsetAsync(ctl + 4, 0, 8, s);
+      if (e != cudaSuccess) rc = set_error(MGW_ECUDA, "memset: %s", cudaGetErrorString(e));
+      const mgw_table_t* t = as_table(tables[r]);
+      const int n_rows = (int)t->host.size();
+      l.f.use_inline = n_rows <= kInlineRows;
+      if (l.f.use_inline)
+        for (int k = 0; k < n_rows; ++k) l.f.inline_rows[k] = t->host[k];
+      l.f.rows = t->dev;
+      l.f.n_rows = n_rows;
+      l.f.ar.rank = r;
+      l.f.ar.state = reinterpret_cast<uint32_t*>(ctl + 4);
+      l.f.ar.err = reinterpret_cast<int*>(ctl + 12);
+      l.f.ar.flags = step == 0 ? kSkipPhase1 : kSkipPack;
+      if (rc == MGW_OK) rc = bf16 ? launch_ll_b16(l, 2 * kSMs, s) : launch_ll(l, 2 * kSMs, s);
+    }
+  }
+  int bad = 0;
+  if (rc == MGW_OK) {  // any device error word set?
+    for (int r = 0; r < world && rc == MGW_OK; ++r) {
+      int w = 0;
+      cudaError_t e = cudaMemcpyAsync(&w, mem + (size_t)r * per_rank + kLLBytes + hdr_bytes + 12, 4,
+                                      cudaMemcpyDeviceToHost, s);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) rc = set_error(MGW_ECUDA, "LL emulation: %s", cudaGetErrorString(e));
+      bad |= w;
+    }
+  }
+  cudaError_t e = cudaFreeAsync(mem, s);
+  if (rc == MGW_OK && e != cudaSuccess) rc = set_error(MGW_ECUDA, "cudaFreeAsync: %s", cudaGetErrorString(e));
+  if (rc == MGW_OK && bad) rc = set_error(MGW_EPROTO, "emulated LL exchange raised device error %d", bad);
+  return rc;
+}
+
 int mgw_allreduce_fused_emulated(void* const* tables, float* const* slots, int world, int64_t n, float scale, int algo,
                                  void* stream) {
   if (!tables || !slots || world < 1 || world > kMaxRanks || n < 0)
     return set_error(MGW_EINVAL, "bad emulated fused arguments");
+  if (algo == MGW_ALGO_LL) {
+    for (int r = 0; r < world; ++r) {
+      const mgw_table_t* t = as_table(tables[r]);
+      int rc = check_table(tables[r], t ? (int)t->host.size() : 0, n);
+      if (rc) return rc;
+    }
+    return n == 0 ? MGW_OK : ll_emulated(tables, world, n, scale, static_cast<cudaStream_t>(stream), false);
+  }
   if (algo == MGW_ALGO_PUSH || algo == MGW_ALGO_PUSH_ONESHOT) {
     for (int r = 0; r < world; ++r) {
       const mgw_table_t* t = as_table(tables[r]);
@@ -1023,6 +1097,14 @@ int mgw_allreduce_fused_bf16_emulated(void* const* tables, void* const* slots, i
                                       int algo, void* stream) {
   if (!tables || !slots || world < 1 || world > kMaxRanks || n < 0)
     return set_error(MGW_EINVAL, "bad emulated bf16 arguments");
+  if (algo == MGW_ALGO_LL) {
+    for (int r = 0; r < world; ++r) {
+      const mgw_table_t* t = as_table(tables[r]);
+      int rc = check_table(tables[r], t ? (int)t->host.size() : 0, n);
+      if (rc) return rc;
+    }
+    return n == 0 ? MGW_OK : ll_emulated(tables, world, n, scale, static_cast<cudaStream_t>(stream), true);
+  }
   if (algo != MGW_ALGO_ONESHOT && algo != MGW_ALGO_TWOSHOT)
     return set_error(MGW_EINVAL, "emulated all-reduce needs an explicit algorithm");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
