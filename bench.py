@@ -281,7 +281,7 @@ class RankContext:
         self.comm, self.session, self.flush = comm, session, flush
 
 
-def run_strategy(ctx, profile, plan, predicted, steps, warmup, *, graph=True, fused=True, keep=False):
+def run_strategy(ctx, profile, plan, predicted, steps, warmup, *, graph=True, fused=True, keep=False, pdl=True):
     """Warm up, then time `steps` Algorithm-2 iterations of `plan` (max over ranks per
     iteration); every iteration is preceded by an L2 flush outside its events and the
     reduced gradients are verified before and after the timed region."""
@@ -291,7 +291,7 @@ def run_strategy(ctx, profile, plan, predicted, steps, warmup, *, graph=True, fu
 
     world, device = ctx.world, ctx.device
     it = OverlappedIteration(profile, plan, comm=ctx.comm, rank=ctx.rank, world=world, device=device,
-                             fill=True, graph=graph, fused=fused)
+                             fill=True, graph=graph, fused=fused, pdl=pdl)
     try:
         for _ in range(warmup):
             with torch.cuda.stream(it.compute_stream):
@@ -401,7 +401,8 @@ def run_ours(args) -> dict | None:
             sampler.__enter__()
         res, it, kern, t_iter_max, wall = run_strategy(ctx, profile, plans[name], predicted[name], args.steps,
                                                         args.warmup, graph=not args.no_graph,
-                                                        fused=not args.unfused, keep=name == "mgwfbp")
+                                                        fused=not args.unfused, keep=name == "mgwfbp",
+                                                        pdl=not args.no_pdl)
         results[name] = res
         if name == "mgwfbp":
             headline = (it, kern, it.group_bytes(), sampler, t_iter_max, wall)
@@ -528,6 +529,7 @@ def run_ours(args) -> dict | None:
             "l2": "flushed between iterations (256 MiB write on the compute stream, outside the timed events)",
             "cuda_graph": not args.no_graph,
             "fused_group_kernel": not args.unfused,
+            "programmatic_launch": not args.no_pdl,
             "group_algorithms": _algo_mix(session, gbytes) if (session is not None and not args.unfused) else None,
         },
         "strategies": results,
@@ -636,6 +638,8 @@ def main(argv=None) -> int:
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-graph", action="store_true", help="eager stream schedule instead of CUDA-graph replay")
     ap.add_argument("--unfused", action="store_true", help="separate pack / all-reduce / unpack kernels per group")
+    ap.add_argument("--no-pdl", action="store_true",
+                    help="launch each group's exchange after its gradient fill completes (no programmatic launch)")
     ap.add_argument("--nvls", action="store_true", help="also time the opt-in NVLS exchange in the sweep (N > 1)")
     ap.add_argument("--no-sweep", action="store_true", help="skip the all-reduce bus-bandwidth sweep (N > 1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -68,6 +68,7 @@ extern "C" {
 #define MGW_SCHED_GRAPH 2u /* capture the iteration once into a CUDA graph and replay it */
 #define MGW_SCHED_HOSTIO 4u /* e2e: H2D of each layer from host_src, D2H of the result to host_dst */
 #define MGW_SCHED_FUSED 8u  /* one kernel per group: pack + all-reduce + unpack (N > 1) */
+#define MGW_SCHED_PDL 16u   /* the group's exchange launches while its fill runs (programmatic event) */
 
 typedef struct mgw_comm mgw_comm;
 typedef struct mgw_sched mgw_sched;

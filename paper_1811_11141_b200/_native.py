@@ -19,7 +19,7 @@ LIB_PATH = LIB_DIR / "libmgwfbp_b200.so"
 
 MGW_OK, MGW_EINVAL, MGW_EPROTO, MGW_ECUDA = 0, 1, 2, 3
 ALGO_AUTO, ALGO_ONESHOT, ALGO_TWOSHOT, ALGO_LL, ALGO_NVLS, ALGO_PUSH, ALGO_PUSH_ONESHOT = 0, 1, 2, 3, 4, 5, 6
-SCHED_FILL, SCHED_GRAPH, SCHED_HOSTIO, SCHED_FUSED = 1, 2, 4, 8
+SCHED_FILL, SCHED_GRAPH, SCHED_HOSTIO, SCHED_FUSED, SCHED_PDL = 1, 2, 4, 8, 16
 TIME_GRAPH = 256  # mgw_time_exchange: replay the reps as one CUDA graph
 DEV_OK, DEV_LENGTH_MISMATCH, DEV_TIMEOUT, DEV_PEER_ABORT = 0, 1, 2, 3
 IPC_HANDLE_BYTES = 64

@@ -249,6 +249,7 @@ __device__ __forceinline__ void reduce_tail(const float* const* in, const int64_
 template <int N>
 __device__ __forceinline__ void kernel_prologue(const ArArgs& a, uint32_t& epoch, int& parity, const float** s_in,
                                                 int64_t* s_end) {
+  grid_dep_wait();  // inputs written by a programmatic producer (the engine's gradient fill)
   stamp_enter(a.stamp);
   epoch = a.state != nullptr ? load_volatile32(a.state) + 1u : 0u;
   parity = (int)(epoch & 1u);

@@ -355,6 +355,7 @@ template <int N>
 __global__ void __launch_bounds__(kThreads, 2) ll_b16_kernel(const __grid_constant__ LLArgs l) {
   const FusedArgs& f = l.f;
   const ArArgs& a = f.ar;
+  grid_dep_wait();
   stamp_enter(a.stamp);
   __shared__ int64_t s_end[kMaxRanks];
   __shared__ int s_status;

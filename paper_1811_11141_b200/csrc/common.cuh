@@ -117,6 +117,12 @@ __device__ __forceinline__ uint32_t load_volatile32(const uint32_t* p) {
   return *reinterpret_cast<const volatile uint32_t*>(p);
 }
 
+// Programmatic dependent launch: a kernel whose producer was launched with a
+// programmatic event may start while the producer still runs; it waits here for the
+// producer grid's completion (and memory) before touching its inputs.  A no-op for a
+// normally launched kernel.
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // Kernel span stamps: every CTA folds its entry time into stamp[0] (min) and its
 // exit time into stamp[1] (max), so [stamp[0], stamp[1]] is the kernel's execution
 // span without the ~6.5 us an event-record pair costs inside a CUDA graph.

@@ -1374,12 +1374,18 @@ static int sched_enqueue(mgw_sched* s, cudaStream_t cs, cudaStream_t ms) {
     if ((s->flags & MGW_SCHED_FILL) && gr.n_elem > 0) {
       // the layer's gradient is written at the END of its backward window (as a real
       // weight-gradient kernel would), so it does not contend with the previous group's
-      // exchange for SMs and HBM
+      // exchange for SMs and HBM.  MGW_SCHED_PDL: the ready event is the fill's
+      // programmatic event, so the group's exchange launches while the fill runs and
+      // waits for it on the device (grid_dep_wait) instead of paying a launch after it.
+      const bool pdl = (s->flags & MGW_SCHED_PDL) != 0;
       int rc = launch_rows<RowOp::kFill>(s->rows.data() + gr.desc_begin, d_rows + gr.desc_begin, gr.desc_count, nullptr,
-                                         gr.n_elem, 1.f, s->d_fill + gr.desc_begin, nullptr, 0, nullptr, cs);
+                                         gr.n_elem, 1.f, s->d_fill + gr.desc_begin, nullptr, 0, nullptr, cs, nullptr,
+                                         pdl ? s->dep_ready[g] : nullptr);
       if (rc) return rc;
+      if (!pdl) MGW_CUDA(cudaEventRecord(s->dep_ready[g], cs));
+    } else {
+      MGW_CUDA(cudaEventRecord(s->dep_ready[g], cs));
     }
-    MGW_CUDA(cudaEventRecord(s->dep_ready[g], cs));
   }
   MGW_CUDA(record_timing(s, s->t_compute, cs));
   MGW_CUDA(cudaEventRecord(s->dep_compute, cs));

@@ -52,6 +52,7 @@ template <int N>
 __global__ void __launch_bounds__(kThreads, 2) nvls_kernel(const __grid_constant__ NvlsArgs x) {
   const FusedArgs& f = x.f;
   const ArArgs& a = f.ar;
+  grid_dep_wait();
   stamp_enter(a.stamp);
   const uint32_t epoch = load_volatile32(a.state) + 1u;
   const int parity = (int)(epoch & 1u);

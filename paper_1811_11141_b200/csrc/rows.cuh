@@ -71,6 +71,7 @@ constexpr int kRowsUnroll = 4;  // 16-B slots per thread per step
 
 template <RowOp kOp, bool kScale>
 __global__ void __launch_bounds__(kThreads, 2) rows_kernel(const __grid_constant__ RowsParam p) {
+  grid_dep_wait();
   stamp_enter(p.stamp);
   float* bucket = p.bucket;
   if (p.calls != nullptr) bucket += (int64_t)((load_volatile32(p.calls) + 1u) & 1u) * p.slot_stride_elems;
@@ -170,7 +171,8 @@ inline int rows_grid(int64_t total, int64_t* tile_out) {
 template <RowOp kOp>
 int launch_rows(const Row* host_rows, const Row* dev_rows, int n_rows, float* bucket, int64_t total, float scale,
                 const float* values, const uint32_t* calls, int64_t slot_stride_elems,
-                unsigned long long* mismatches, cudaStream_t stream, uint64_t* stamp = nullptr) {
+                unsigned long long* mismatches, cudaStream_t stream, uint64_t* stamp = nullptr,
+                cudaEvent_t pdl_event = nullptr) {
   if (total <= 0 || n_rows <= 0) return MGW_OK;
   RowsParam p;
   p.use_inline = n_rows <= kInlineRows && host_rows != nullptr;
@@ -188,6 +190,25 @@ int launch_rows(const Row* host_rows, const Row* dev_rows, int n_rows, float* bu
   p.stamp = stamp;
   if (!p.use_inline && dev_rows == nullptr) return set_error(MGW_EINVAL, "row table missing");
   const int grid = rows_grid(total, &p.tile);
+  if (pdl_event != nullptr) {
+    // record `pdl_event` as a programmatic event that fires once every block has started:
+    // the consumer (the group's exchange) launches early and waits in grid_dep_wait()
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticEvent;
+    attr[0].val.programmaticEvent.event = pdl_event;
+    attr[0].val.programmaticEvent.flags = 0;
+    attr[0].val.programmaticEvent.triggerAtBlockStart = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.stream = stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = (kOp == RowOp::kPack && scale != 1.0f) ? cudaLaunchKernelEx(&cfg, rows_kernel<kOp, true>, p)
+                                                            : cudaLaunchKernelEx(&cfg, rows_kernel<kOp, false>, p);
+    if (e != cudaSuccess) return set_error(MGW_ECUDA, "programmatic launch: %s", cudaGetErrorString(e));
+    return MGW_OK;
+  }
   if (kOp == RowOp::kPack && scale != 1.0f)
     rows_kernel<kOp, true><<<grid, kThreads, 0, stream>>>(p);
   else

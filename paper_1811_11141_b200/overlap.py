@@ -95,6 +95,7 @@ class OverlappedIteration:
         algo: int = _native.ALGO_AUTO,
         tensors: dict | None = None,
         fused: bool = False,
+        pdl: bool = True,
     ) -> None:
         import torch
 
@@ -148,6 +149,8 @@ class OverlappedIteration:
         flags = (_native.SCHED_FILL if fill else 0) | (_native.SCHED_GRAPH if graph else 0)
         if fused:
             flags |= _native.SCHED_FUSED
+        if pdl and fill:
+            flags |= _native.SCHED_PDL  # the exchange launches while the fill runs
         self.fused = fused
         src_arr = dst_arr = None
         if host_io:
