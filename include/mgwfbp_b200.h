@@ -58,7 +58,7 @@ extern "C" {
 #define MGW_ALGO_AUTO 0
 #define MGW_ALGO_ONESHOT 1
 #define MGW_ALGO_TWOSHOT 2
-#define MGW_ALGO_LL 3 /* push-based low-latency one-shot (fused path only, <= 65,536 elements) */
+#define MGW_ALGO_LL 3 /* push-based low-latency one-shot (fused path only, <= 262,144 elements) */
 #define MGW_ALGO_NVLS 4 /* NVSwitch in-switch reduction (opt-in; fp32 sum, NOT the reference fold order) */
 #define MGW_ALGO_PUSH 5 /* push-based two-shot (fused path only): every NVLink byte is a store */
 #define MGW_ALGO_PUSH_ONESHOT 6 /* push-based one-shot (fused path only): stores out, local fold */
@@ -182,7 +182,7 @@ int mgw_allreduce_fused_emulated(void* const* tables, float* const* slots, int w
  * bucket and wire format.  Element e of reference segment s (allreduce_net.py:360-367)
  * becomes bf16_rn((((f32(x_s) + f32(x_s+1)) + ...) + f32(x_s+N-1)) * scale), the
  * multiply only when scale != 1: the reference ring's fold order (allreduce_net.py:401)
- * in fp32 over exactly-upcast inputs, rounded once.  Algorithms: AUTO, LL (<= 256 KB,
+ * in fp32 over exactly-upcast inputs, rounded once.  Algorithms: AUTO, LL (<= 2 MB of bf16,
  * two bf16 per pushed word), one-shot, two-shot.  Replaces ring_allreduce (allreduce_net.py:370-411) for element_bytes = 2
  * profiles (model_profile.py:24). */
 int mgw_allreduce_fused_bf16(mgw_comm* comm, const void* table, int n_rows, int64_t n_elem, float scale, int algo,
