@@ -303,3 +303,58 @@ def absent_peer_task(config, session):
         return "absent"
     ring_allreduce(GradientBuffer(1, 1, np.ones(4096, dtype="<f4")), config, session)
     return "completed"
+
+
+def stress_task(config, session, *, iterations=300, seed=2024):
+    """A seeded stream of collectives with random sizes, row splits, dtypes and algorithms
+    (the same on every rank), back to back on one communicator: integer-valued payloads
+    must come back exactly.  Exercises slot-parity / LL-area / gather-area reuse across
+    algorithm switches.  Returns the number of failures and the first few."""
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    from paper_1811_11141_b200 import _native
+
+    rng = np.random.default_rng(seed)
+    n_ranks = config.n_workers
+    algos_f32 = [_native.ALGO_AUTO, _native.ALGO_LL, _native.ALGO_ONESHOT, _native.ALGO_TWOSHOT, _native.ALGO_PUSH,
+                 _native.ALGO_PUSH_ONESHOT]
+    algos_b16 = [_native.ALGO_AUTO, _native.ALGO_LL, _native.ALGO_ONESHOT, _native.ALGO_TWOSHOT]
+    h = session.stream.cuda_stream
+    failures = []
+    with torch.cuda.device(session.device), torch.cuda.stream(session.stream):
+        for it in range(iterations):
+            bf16 = bool(rng.random() < 0.25)
+            n = int(rng.choice([1, 7, 63, 1000, 4097]) if rng.random() < 0.3 else rng.integers(1, 1 << 21))
+            if bf16:
+                algo = int(rng.choice(algos_b16))
+            else:
+                algo = int(rng.choice(algos_f32))
+            if algo == _native.ALGO_LL:
+                n = min(n, 262144 * (2 if bf16 else 1))
+            cuts = sorted(set(int(c) for c in rng.integers(0, n + 1, size=2)))
+            bounds = [0] + [c for c in cuts if 0 < c < n] + [n]
+            dtype = torch.bfloat16 if bf16 else torch.float32
+            idx = torch.arange(n, device=session.device)
+            pattern = (idx % 5).to(torch.float32)
+            x = (pattern + float(config.rank + 1)).to(dtype)
+            rows = []
+            views = []
+            for lo, hi in zip(bounds[:-1], bounds[1:]):
+                v = x[lo:hi].clone()  # separate allocations: the rows live in different tensors
+                views.append(v)
+                rows.append((v.data_ptr(), hi - lo, lo))
+            table = _native.DeviceTable(rows)
+            fn = "mgw_allreduce_fused_bf16" if bf16 else "mgw_allreduce_fused"
+            _native.call(fn, session.comm, table.ptr, len(rows), n, ctypes.c_float(1.0), algo, h)
+            got = torch.cat(views).float()
+            want = pattern * n_ranks + n_ranks * (n_ranks + 1) / 2
+            session.stream.synchronize()
+            table.close()
+            if not torch.equal(got, want):
+                bad = int((got != want).sum())
+                failures.append((it, n, algo, bf16, bad))
+    session.raise_if_failed()
+    return len(failures), failures[:5]

@@ -250,3 +250,13 @@ def test_autograd_bf16_parameters():
         for r in range(n):
             got = np.concatenate([res[r][1][layer - 1] for layer in range(high, low - 1, -1)])
             assert np.array_equal(got, want), (low, high, r, int(np.count_nonzero(got != want)))
+
+
+def test_randomized_stress_every_algorithm_and_dtype():
+    """300 back-to-back collectives per rank with random sizes (to 2 M elements), row splits,
+    dtypes and algorithms (the same sequence on every rank): exact integer results, no
+    protocol error -- buffer reuse across algorithm switches is safe."""
+    for n in _worlds():
+        res = run_workers(n, partial(_mp_tasks.stress_task, iterations=300, seed=2024 + n), timeout=600)
+        for r, (n_bad, first) in res.items():
+            assert n_bad == 0, (n, r, first)
