@@ -177,13 +177,10 @@ __global__ void __launch_bounds__(kThreads, 2) push_twoshot_kernel(const __grid_
     if (!(a.flags & kNoBarrier)) status = cta_barrier(a.mid, parity, epoch, (uint32_t)a.n, a);
     phase_mark(a, 4);
     if (status == MGW_DEV_OK) {
-      // every part sits at its bucket offset in my gather area: scatter them interleaved
-      // (N - 1 streams in flight, fused_scatter_parts) rather than one part after another
-      __shared__ const float* s_g[kMaxRanks];
-      if (threadIdx.x < N) s_g[threadIdx.x] = s_gat[me];
-      __syncthreads();
-      fused_scatter_parts<N>(f, s_g, me, pc);
-      if (last && me != N - 1) fused_scatter_range(f, s_gat[me], 0, 0, tail0, a.n);
+      const float* g = s_gat[me];
+      for (int p = 0; p < N; ++p)
+        if (p != me) fused_scatter_range(f, g, pc.lo[p], pc.lo[p] + pc.len[p], 0, 0);
+      if (last && me != N - 1) fused_scatter_range(f, g, 0, 0, tail0, a.n);
     }
     phase_mark(a, 5);
   }
