@@ -442,7 +442,9 @@ def run_ours(args) -> dict | None:
                     "achieved": round(achieved, 1),
                     "peak": NVLINK_PEAK_GBS, "unit": "GB/s", "frac": round(achieved / NVLINK_PEAK_GBS, 4),
                     "peak_source": "measured peer copy per direction, B200_PROFILING.md (900 nominal)",
-                    "algorithmic_bytes": "2(N-1)/N x group bucket bytes per launch (bus bytes)"}
+                    "algorithmic_bytes": "2(N-1)/N x group bucket bytes per launch (bus bytes)",
+                    "bound_note": "a collective is bound by the NVLink fabric, neither HBM nor tensor cores; "
+                                  "peak = the per-GPU peer-copy bandwidth of B200_PROFILING.md"}
     roofline.update({
         "bytes_per_step": per_step,
         "launches_per_step": sending,
