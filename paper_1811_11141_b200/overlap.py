@@ -76,7 +76,9 @@ class OverlappedIteration:
     the iteration packs/unpacks but exchanges nothing).  ``tensors`` maps layer
     index -> a CUDA float32 tensor of that layer's gradient; created here when
     omitted.  ``fill`` selects per-iteration gradient production with the
-    reference pattern; ``host_io`` adds the end-to-end H2D/D2H legs.
+    reference pattern; ``host_io`` adds the end-to-end H2D/D2H legs.  ``fused`` runs one
+    kernel per group (N = 1: the single-rank group kernel); ``pdl`` launches each group's
+    exchange while its gradient fill still runs (programmatic dependent launch).
     """
 
     def __init__(
