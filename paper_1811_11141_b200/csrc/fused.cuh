@@ -1,4 +1,6 @@
 // fused.cuh -- one kernel per merge group: K1 pack -> K2/K3 all-reduce -> K4 unpack.
+// Replaces, per group, the reference's per-layer pack (allreduce_net.py:544-546) and
+// ring_allreduce (allreduce_net.py:370-411) on the bucket layout of :499-509.
 //
 // The separate kernels cost three launches per group and a round trip of the whole
 // bucket through the result buffer.  Here every CTA packs exactly the bucket chunk its

@@ -1,4 +1,5 @@
-// ll.cuh -- push-based low-latency one-shot for small, startup-dominated groups.
+// ll.cuh -- push-based low-latency one-shot for small, startup-dominated groups
+// (same result as ring_allreduce, allreduce_net.py:370-411, for the group's bucket).
 //
 // The messages MG-WFBP creates by merging are small: their cost is the startup `a`
 // (paper Eq. 8), not bandwidth.  The pull one-shot pays a flag round trip (signal +

@@ -1,4 +1,6 @@
-// nvls.cuh -- opt-in NVLink-SHARP (NVSwitch multicast) exchange for large buckets.
+// nvls.cuh -- opt-in NVLink-SHARP (NVSwitch multicast) exchange for large buckets
+// (stands in for ring_allreduce, allreduce_net.py:370-411, within fp32
+// rounding only).
 //
 // Every rank's bucket is bound to one CUDA multicast object.  CTA b packs chunk b of
 // every part into its own (unicast) copy, a per-CTA barrier, then reduces chunk b of

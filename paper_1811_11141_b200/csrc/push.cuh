@@ -1,5 +1,6 @@
 // push.cuh -- push-based group exchanges: two-shot (pack -> reduce-scatter -> all-gather
-// -> unpack in one kernel) for large buckets, one-shot for mid-size ones.
+// -> unpack in one kernel) for large buckets, one-shot for mid-size ones.  Same result as
+// ring_allreduce (allreduce_net.py:370-411) on the group bucket (:499-509).
 //
 // The pull two-shot (fused.cuh) pays a remote-read round trip in each of its phases:
 // every load from a peer slot waits ~2 us for NVLink.  Here every byte crosses NVLink
