@@ -358,3 +358,26 @@ def stress_task(config, session, *, iterations=300, seed=2024):
                 failures.append((it, n, algo, bf16, bad))
     session.raise_if_failed()
     return len(failures), failures[:5]
+
+
+def empty_and_tiny_task(config, session):
+    """Zero-length buffers are still collective (the reference's ring runs its rounds on
+    empty segments); 1..N-1 elements leave some reference segments empty."""
+    import torch
+
+    out = []
+    empty = GradientBuffer(1, 1, np.zeros(0, dtype="<f4"))
+    assert ring_allreduce(empty, config, session) is empty and len(empty) == 0
+    n = config.n_workers
+    for size in range(1, n + 2):
+        buf = GradientBuffer(1, 1, np.full(size, float(config.rank + 1), dtype="<f4"))
+        ring_allreduce(buf, config, session)
+        out.append(bool((buf.values == n * (n + 1) / 2).all()))
+        t = torch.full((size,), float(config.rank + 1), dtype=torch.bfloat16, device=session.device)
+        ring_allreduce(GradientBuffer(1, 1, t), config, session)
+        out.append(bool((t.float() == n * (n + 1) / 2).all()))
+    # and the next collective after them is still in step
+    buf = GradientBuffer(1, 1, np.arange(23, dtype="<f4") + config.rank)
+    ring_allreduce(buf, config, session)
+    out.append(bool(np.array_equal(buf.values, np.arange(23, dtype="<f4") * n + n * (n - 1) / 2)))
+    return out

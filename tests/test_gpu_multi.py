@@ -47,6 +47,12 @@ def test_payload_smaller_than_group():
     assert all(run_workers(n, _mp_tasks.single_element_task).values())
 
 
+def test_empty_and_fewer_elements_than_ranks():
+    for n in _worlds():
+        for verdicts in run_workers(n, _mp_tasks.empty_and_tiny_task).values():
+            assert all(verdicts), verdicts
+
+
 def test_length_mismatch_is_a_protocol_error():
     with pytest.raises(RuntimeError) as err:
         run_workers(2, _mp_tasks.mismatched_task, timeout=60)
