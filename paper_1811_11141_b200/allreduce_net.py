@@ -505,7 +505,9 @@ def ring_allreduce(
             _native.call("mgw_allreduce_fused", session.comm, table.ptr, 1, n, ctypes.c_float(1.0),
                          _native.ALGO_AUTO, handle)
         else:
-            _native.call("mgw_allreduce", session.comm, 0, algo, handle)  # still collective
+            # nothing to reduce, but still collective: a zero-length one-shot is a barrier
+            algo = _native.ALGO_ONESHOT
+            _native.call("mgw_allreduce", session.comm, 0, algo, handle)
         stream.synchronize()
         session.raise_if_failed()
         if numpy_payload and n:
