@@ -431,13 +431,16 @@ def _algo_for(session: RingSession, n: int, fused: bool = False) -> int:
     if fused and 4 * n <= ll_max_bytes(session.config.n_workers):
         return _native.ALGO_LL
     if fused:
+        push_ok = 4 * n <= (1 << 30)
         if session.config.n_workers == 2:
-            return _native.ALGO_PUSH_ONESHOT if 4 * n <= (16 << 20) else _native.ALGO_PUSH
+            if 4 * n <= (16 << 20):
+                return _native.ALGO_PUSH_ONESHOT
+            return _native.ALGO_PUSH if push_ok else _native.ALGO_TWOSHOT
         if 4 * n <= (512 << 10):
             return _native.ALGO_PUSH_ONESHOT
         if 4 * n <= session_oneshot_max(session):
             return _native.ALGO_ONESHOT
-        return _native.ALGO_PUSH if 4 * n >= (8 << 20) else _native.ALGO_TWOSHOT
+        return _native.ALGO_PUSH if 4 * n >= (8 << 20) and push_ok else _native.ALGO_TWOSHOT
     return _native.ALGO_ONESHOT if 4 * n <= session_oneshot_max(session) else _native.ALGO_TWOSHOT
 
 

@@ -232,11 +232,16 @@ int pick_fused_algo(const mgw_comm* c, int64_t n, int algo) {
   // one-shot wins up to 16 MB and the push two-shot above; at N >= 3 the push one-shot up
   // to 512 KB, the pull one-shot to 8 MB / (N - 1), the pull two-shot to 8 MB and the
   // push two-shot above (546 vs 509 GB/s bus at N = 4, 128 MB)
+  // Beyond ~1 GB the push two-shot falls behind the pull two-shot again (synthetic
+  // 1000-layer SyncEASGD bucket, 6.75 GB: 42.4 vs 20.8 ms at N = 4; VGG-16's 553 MB still
+  // favours push, profiles/profiles_n4_r01_final.json).
   const int64_t bytes = n * 4;
-  if (c->world == 2) return bytes <= (16ll << 20) ? MGW_ALGO_PUSH_ONESHOT : MGW_ALGO_PUSH;
+  const bool push_ok = bytes <= (1ll << 30);
+  if (c->world == 2)
+    return bytes <= (16ll << 20) ? MGW_ALGO_PUSH_ONESHOT : (push_ok ? MGW_ALGO_PUSH : MGW_ALGO_TWOSHOT);
   if (bytes <= (512ll << 10)) return MGW_ALGO_PUSH_ONESHOT;
   if (bytes <= c->oneshot_max_bytes) return MGW_ALGO_ONESHOT;
-  return bytes >= (8ll << 20) ? MGW_ALGO_PUSH : MGW_ALGO_TWOSHOT;
+  return bytes >= (8ll << 20) && push_ok ? MGW_ALGO_PUSH : MGW_ALGO_TWOSHOT;
 }
 
 int comm_allreduce(mgw_comm* c, int64_t n, int algo, cudaStream_t stream, uint64_t* stamp = nullptr) {
