@@ -104,3 +104,22 @@ def test_segments_match_reference_split():
     assert _segments(10, 4) == ([3, 3, 2, 2], [0, 3, 6, 8])
     assert _segments(1, 8)[0] == [1, 0, 0, 0, 0, 0, 0, 0]
     assert _segments(0, 3) == ([0, 0, 0], [0, 0, 0])
+
+
+def test_auto_algorithm_rule_mirrors_the_native_choice():
+    """allreduce_net._algo_for (transport accounting) follows pick_fused_algo's rule."""
+    from types import SimpleNamespace
+
+    from paper_1811_11141_b200 import _native
+    from paper_1811_11141_b200.allreduce_net import _algo_for
+
+    def algo(world, nbytes):
+        return _algo_for(SimpleNamespace(config=SimpleNamespace(n_workers=world)), nbytes // 4, fused=True)
+
+    assert algo(2, 4096) == algo(2, 1 << 20) == _native.ALGO_LL
+    assert algo(2, 2 << 20) == algo(2, 16 << 20) == _native.ALGO_PUSH_ONESHOT
+    assert algo(2, 32 << 20) == _native.ALGO_PUSH and algo(2, 2 << 30) == _native.ALGO_TWOSHOT
+    assert algo(4, 512 << 10) == _native.ALGO_LL and algo(4, 1 << 20) == _native.ALGO_ONESHOT
+    assert algo(4, 4 << 20) == _native.ALGO_TWOSHOT and algo(4, 64 << 20) == _native.ALGO_PUSH
+    assert algo(8, 256 << 10) == _native.ALGO_LL and algo(8, 512 << 10) == _native.ALGO_PUSH_ONESHOT
+    assert algo(8, 1 << 20) == _native.ALGO_ONESHOT and algo(8, 2 << 30) == _native.ALGO_TWOSHOT
