@@ -96,7 +96,7 @@ struct mgw_comm {
   uint64_t timeout_ns = 30ull * 1000000000ull;
   int64_t oneshot_max_bytes = 1 << 20;  // set per world in mgw_comm_create
   int64_t ll_max_bytes = 256 << 10;  // AUTO's LL ceiling (the area holds kLLElems per source)
-  int max_ctas = kMaxBlocks;  // 512: a second wave helps >= 128 MB buckets (profiles/grid_pushtune_n4_r01.json)
+  int max_ctas = 2 * kSMs;  // one resident wave (a 512 cap helped N=4 / 128 MB but not N=2 / 102 MB)
   int64_t vec_per_cta[2] = {0, 0};      // tuning: 16-B slots per CTA (one-shot, two-shot); 0 = default
   // NVLS (opt-in): multicast object bound to a per-rank bucket
   CUmemGenericAllocationHandle nvls_mc = 0, nvls_mem = 0;
