@@ -59,7 +59,7 @@ struct Unroll {
 #ifndef MGW_BARRIER_RELAXED_POLL
 #define MGW_BARRIER_RELAXED_POLL 0
 #endif
-__device__ __noinline__ int cta_barrier(uint64_t* const* flags, int parity, uint32_t epoch, uint32_t tag,
+static __device__ __noinline__ int cta_barrier(uint64_t* const* flags, int parity, uint32_t epoch, uint32_t tag,
                                         const ArArgs& a) {
   __shared__ int s_status;
   if (threadIdx.x == 0) s_status = 0;
@@ -113,7 +113,7 @@ __device__ __noinline__ int cta_barrier(uint64_t* const* flags, int parity, uint
 // it.  Under a real backward pass ranks drift by tens of microseconds; without the
 // gate the first rank's CTAs would sit in the entry barrier holding SM slots that the
 // backward kernels need.  Door words are monotonic epochs -- no parity, no reset.
-__global__ void gate_kernel(const __grid_constant__ ArArgs a) {
+static __global__ void gate_kernel(const __grid_constant__ ArArgs a) {
   const int t = threadIdx.x;
   const uint32_t epoch = load_volatile32(a.state) + 1u;
   int status = MGW_DEV_OK;
@@ -396,34 +396,6 @@ inline int collective_grid(int64_t vectors, int64_t per_cta, int max_ctas) {
     per_cta = per_cta < 128 ? 128 : (per_cta > full ? full : per_cta);
   }
   return grid_for(vectors, per_cta, max_ctas);
-}
-
-template <int N>
-int launch_allreduce_n(const ArArgs& a, int algo, int max_ctas, cudaStream_t stream, const int64_t* per_cta) {
-  const int64_t nv = a.n >> 2;
-  if (algo == MGW_ALGO_ONESHOT) {
-    oneshot_kernel<N><<<collective_grid<N>(nv, per_cta ? per_cta[0] : 0, max_ctas), kThreads, 0, stream>>>(a);
-  } else {
-    twoshot_kernel<N><<<collective_grid<N>(nv / N, per_cta ? per_cta[1] : 0, max_ctas), kThreads, 0, stream>>>(a);
-  }
-  MGW_CHECK_LAUNCH();
-  return MGW_OK;
-}
-
-inline int launch_allreduce(const ArArgs& a, int algo, int max_ctas, cudaStream_t stream,
-                            const int64_t* per_cta = nullptr) {
-  max_ctas = max_ctas < kMaxBlocks ? max_ctas : kMaxBlocks;  // one barrier flag slot per CTA
-  switch (a.world) {
-    case 1: return launch_allreduce_n<1>(a, algo, max_ctas, stream, per_cta);
-    case 2: return launch_allreduce_n<2>(a, algo, max_ctas, stream, per_cta);
-    case 3: return launch_allreduce_n<3>(a, algo, max_ctas, stream, per_cta);
-    case 4: return launch_allreduce_n<4>(a, algo, max_ctas, stream, per_cta);
-    case 5: return launch_allreduce_n<5>(a, algo, max_ctas, stream, per_cta);
-    case 6: return launch_allreduce_n<6>(a, algo, max_ctas, stream, per_cta);
-    case 7: return launch_allreduce_n<7>(a, algo, max_ctas, stream, per_cta);
-    case 8: return launch_allreduce_n<8>(a, algo, max_ctas, stream, per_cta);
-    default: return set_error(MGW_EINVAL, "world %d outside 1..%d", a.world, kMaxRanks);
-  }
 }
 
 }  // namespace mgw

@@ -94,7 +94,7 @@ __device__ __forceinline__ int b16_first_row(const FusedArgs& f, int64_t v0, int
 
 // pack slots [v0, v1) and scalar elements [t0, t1) of the tensors into `slot` (a copy:
 // bf16 scaling happens after the fp32 fold)
-__device__ void b16_pack_range(const FusedArgs& f, uint16_t* slot, int64_t v0, int64_t v1, int64_t t0, int64_t t1) {
+static __device__ void b16_pack_range(const FusedArgs& f, uint16_t* slot, int64_t v0, int64_t v1, int64_t t0, int64_t t1) {
   if (v0 < v1) {
     int k = b16_first_row(f, v0, v1);
     for (int64_t v = v0 + threadIdx.x; v < v1; v += kThreads) {
@@ -185,7 +185,7 @@ __device__ void b16_reduce_tail(const FusedArgs& f, const uint16_t* const* in, c
 }
 
 // copy reduced slots [v0, v1) and scalars [t0, t1) of `src` into the tensors
-__device__ void b16_scatter_range(const FusedArgs& f, const uint16_t* src, int64_t v0, int64_t v1, int64_t t0,
+static __device__ void b16_scatter_range(const FusedArgs& f, const uint16_t* src, int64_t v0, int64_t v1, int64_t t0,
                                   int64_t t1) {
   constexpr int UC = 4;
   if (v0 < v1) {
@@ -479,53 +479,6 @@ __global__ void __launch_bounds__(kThreads, 2) ll_b16_kernel(const __grid_consta
     }
   }
   finish_call(a);
-}
-
-inline int launch_ll_b16(const LLArgs& l, int max_ctas, cudaStream_t stream) {
-  if (l.f.ar.n > 2 * kLLMaxElems)
-    return set_error(MGW_EINVAL, "bf16 LL path takes at most %lld elements", (long long)(2 * kLLMaxElems));
-  const int64_t quads = (l.f.ar.n + 3) >> 2;
-  const int grid = grid_for(quads, kThreads, max_ctas < kSMs ? max_ctas : kSMs);
-  switch (l.f.ar.world) {
-    case 2: ll_b16_kernel<2><<<grid, kThreads, 0, stream>>>(l); break;
-    case 3: ll_b16_kernel<3><<<grid, kThreads, 0, stream>>>(l); break;
-    case 4: ll_b16_kernel<4><<<grid, kThreads, 0, stream>>>(l); break;
-    case 5: ll_b16_kernel<5><<<grid, kThreads, 0, stream>>>(l); break;
-    case 6: ll_b16_kernel<6><<<grid, kThreads, 0, stream>>>(l); break;
-    case 7: ll_b16_kernel<7><<<grid, kThreads, 0, stream>>>(l); break;
-    case 8: ll_b16_kernel<8><<<grid, kThreads, 0, stream>>>(l); break;
-    default: return set_error(MGW_EINVAL, "LL path needs 2..%d ranks, got %d", kMaxRanks, l.f.ar.world);
-  }
-  MGW_CHECK_LAUNCH();
-  return MGW_OK;
-}
-
-template <int N>
-int launch_b16_n(const FusedArgs& f, int algo, int max_ctas, cudaStream_t stream) {
-  const int64_t nv = f.ar.n / kB16;
-  if (algo == MGW_ALGO_ONESHOT)
-    b16_oneshot_kernel<N><<<collective_grid<N>(nv, 0, max_ctas), kThreads, 0, stream>>>(f);
-  else
-    b16_twoshot_kernel<N><<<collective_grid<N>(nv / N, 0, max_ctas), kThreads, 0, stream>>>(f);
-  MGW_CHECK_LAUNCH();
-  return MGW_OK;
-}
-
-inline int launch_b16(const FusedArgs& f, int algo, int max_ctas, cudaStream_t stream) {
-  if (algo != MGW_ALGO_ONESHOT && algo != MGW_ALGO_TWOSHOT)
-    return set_error(MGW_EINVAL, "bf16 buckets support one-shot and two-shot only (algorithm %d)", algo);
-  max_ctas = max_ctas < kMaxBlocks ? max_ctas : kMaxBlocks;
-  switch (f.ar.world) {
-    case 1: return launch_b16_n<1>(f, algo, max_ctas, stream);
-    case 2: return launch_b16_n<2>(f, algo, max_ctas, stream);
-    case 3: return launch_b16_n<3>(f, algo, max_ctas, stream);
-    case 4: return launch_b16_n<4>(f, algo, max_ctas, stream);
-    case 5: return launch_b16_n<5>(f, algo, max_ctas, stream);
-    case 6: return launch_b16_n<6>(f, algo, max_ctas, stream);
-    case 7: return launch_b16_n<7>(f, algo, max_ctas, stream);
-    case 8: return launch_b16_n<8>(f, algo, max_ctas, stream);
-    default: return set_error(MGW_EINVAL, "world %d outside 1..%d", f.ar.world, kMaxRanks);
-  }
 }
 
 }  // namespace mgw

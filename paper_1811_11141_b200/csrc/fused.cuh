@@ -65,7 +65,7 @@ __device__ __forceinline__ float* fused_tensor1(const FusedArgs& f, int k, int64
 // Pack bucket vectors [v0, v1) (16-B slots) plus scalar elements [t0, t1) into `slot`.
 // UP slots per thread are loaded before any is stored (ncu r01: one outstanding 16-B load
 // per thread left the pack phase latency-bound on long-scoreboard stalls).
-__device__ void fused_pack_range(const FusedArgs& f, float* slot, int64_t v0, int64_t v1, int64_t t0, int64_t t1) {
+static __device__ void fused_pack_range(const FusedArgs& f, float* slot, int64_t v0, int64_t v1, int64_t t0, int64_t t1) {
   constexpr int UP = 4;
   const float scale = f.scale;
   const bool scaled = scale != 1.0f;
@@ -183,7 +183,7 @@ __device__ void fused_reduce_tail(const FusedArgs& f, const float* const* in, co
 }
 
 // copy reduced bucket vectors [v0, v1) (and scalars [t0, t1)) of `src` into the tensors
-__device__ void fused_scatter_range(const FusedArgs& f, const float* src, int64_t v0, int64_t v1, int64_t t0,
+static __device__ void fused_scatter_range(const FusedArgs& f, const float* src, int64_t v0, int64_t v1, int64_t t0,
                                     int64_t t1) {
   constexpr int UC = 4;
   if (v0 < v1) {
@@ -377,34 +377,6 @@ __global__ void __launch_bounds__(kThreads, 2) fused_twoshot_kernel(const __grid
     phase_mark(a, 5);
   }
   finish_call(a);
-}
-
-template <int N>
-int launch_fused_n(const FusedArgs& f, int algo, int max_ctas, cudaStream_t stream, const int64_t* per_cta) {
-  const int64_t nv = f.ar.n >> 2;
-  if (algo == MGW_ALGO_ONESHOT) {
-    fused_oneshot_kernel<N><<<collective_grid<N>(nv, per_cta ? per_cta[0] : 0, max_ctas), kThreads, 0, stream>>>(f);
-  } else {
-    fused_twoshot_kernel<N><<<collective_grid<N>(nv / N, per_cta ? per_cta[1] : 0, max_ctas), kThreads, 0, stream>>>(f);
-  }
-  MGW_CHECK_LAUNCH();
-  return MGW_OK;
-}
-
-inline int launch_fused(const FusedArgs& f, int algo, int max_ctas, cudaStream_t stream,
-                        const int64_t* per_cta = nullptr) {
-  max_ctas = max_ctas < kMaxBlocks ? max_ctas : kMaxBlocks;
-  switch (f.ar.world) {
-    case 1: return launch_fused_n<1>(f, algo, max_ctas, stream, per_cta);
-    case 2: return launch_fused_n<2>(f, algo, max_ctas, stream, per_cta);
-    case 3: return launch_fused_n<3>(f, algo, max_ctas, stream, per_cta);
-    case 4: return launch_fused_n<4>(f, algo, max_ctas, stream, per_cta);
-    case 5: return launch_fused_n<5>(f, algo, max_ctas, stream, per_cta);
-    case 6: return launch_fused_n<6>(f, algo, max_ctas, stream, per_cta);
-    case 7: return launch_fused_n<7>(f, algo, max_ctas, stream, per_cta);
-    case 8: return launch_fused_n<8>(f, algo, max_ctas, stream, per_cta);
-    default: return set_error(MGW_EINVAL, "world %d outside 1..%d", f.ar.world, kMaxRanks);
-  }
 }
 
 }  // namespace mgw

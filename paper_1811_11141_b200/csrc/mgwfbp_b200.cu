@@ -28,6 +28,7 @@
 
 #include "allreduce.cuh"
 #include "bf16.cuh"
+#include "launch.h"
 #include "common.cuh"
 #include "fused.cuh"
 #include "ll.cuh"
