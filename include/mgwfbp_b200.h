@@ -50,7 +50,9 @@ extern "C" {
 
 /* device error word values (mgw_comm_error) */
 #define MGW_DEV_OK 0
-#define MGW_DEV_LENGTH_MISMATCH 1 /* ranks disagree on the bucket length */
+#define MGW_DEV_MISMATCH 1        /* ranks disagree on the collective: bucket length, kernel,
+                                     grid, dtype, scale or group tag (allreduce_net.py:340-345) */
+#define MGW_DEV_LENGTH_MISMATCH MGW_DEV_MISMATCH /* round-1 name */
 #define MGW_DEV_TIMEOUT 2         /* a peer never arrived at the barrier */
 #define MGW_DEV_PEER_ABORT 3      /* a peer detected an error and aborted */
 
@@ -127,6 +129,23 @@ int mgw_comm_set_ll_max(mgw_comm* comm, int64_t bytes);
 int mgw_comm_set_gate(mgw_comm* comm, int enable);
 /* tuning: key 0 = one-shot 16-B slots per CTA, key 1 = two-shot slots per CTA (0 = default) */
 int mgw_comm_set_tuning(mgw_comm* comm, int key, int64_t value);
+/* group tag: folded (with length, kernel, grid, dtype and scale) into the 32-bit tag every
+ * barrier flag and LL header carries, so ranks issuing different groups, iterations or
+ * per-rank settings raise MGW_DEV_MISMATCH instead of reducing unrelated buckets
+ * (the reference's frame header check, allreduce_net.py:340-345).  Sticky until changed;
+ * the Algorithm-2 engine tags every group with its head layer. */
+int mgw_comm_set_group_tag(mgw_comm* comm, uint32_t tag);
+/* the algorithm a fused group exchange of n_elem elements of element_bytes (4: fp32, 2: bf16)
+ * runs under AUTO on this communicator, fallbacks included (TransportCounters accounting) */
+int mgw_comm_pick_algo(mgw_comm* comm, int64_t n_elem, int element_bytes, int* algo);
+/* clear the device error word and this rank's abort flag after a ProtocolError.  Collective
+ * in spirit: every rank calls it after a host-level barrier, before the next collective. */
+int mgw_comm_clear_error(mgw_comm* comm);
+/* In-process rank group on ONE device (tests and single-GPU emulation with the real barrier
+ * protocol): `world` communicators whose peer tables point at each other's regions directly
+ * (no IPC).  Launch each rank's collectives on its own stream; the CTA cap defaults to
+ * 2 * 148 / world so every rank's grid is co-resident. */
+int mgw_comm_create_local(int world, int device, int64_t capacity_bytes, mgw_comm** comms /* world */);
 int mgw_comm_input(mgw_comm* comm, float** slot); /* slot the next collective reads (syncs) */
 int mgw_comm_result(mgw_comm* comm, float** result);
 int mgw_comm_pack(mgw_comm* comm, const void* dev_table, int n, int64_t n_elem, float scale, void* stream);

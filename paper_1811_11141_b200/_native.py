@@ -21,7 +21,8 @@ MGW_OK, MGW_EINVAL, MGW_EPROTO, MGW_ECUDA = 0, 1, 2, 3
 ALGO_AUTO, ALGO_ONESHOT, ALGO_TWOSHOT, ALGO_LL, ALGO_NVLS, ALGO_PUSH, ALGO_PUSH_ONESHOT = 0, 1, 2, 3, 4, 5, 6
 SCHED_FILL, SCHED_GRAPH, SCHED_HOSTIO, SCHED_FUSED, SCHED_PDL = 1, 2, 4, 8, 16
 TIME_GRAPH = 256  # mgw_time_exchange: replay the reps as one CUDA graph
-DEV_OK, DEV_LENGTH_MISMATCH, DEV_TIMEOUT, DEV_PEER_ABORT = 0, 1, 2, 3
+DEV_OK, DEV_MISMATCH, DEV_TIMEOUT, DEV_PEER_ABORT = 0, 1, 2, 3
+DEV_LENGTH_MISMATCH = DEV_MISMATCH  # round-1 name
 IPC_HANDLE_BYTES = 64
 MAX_RANKS = 8
 
@@ -69,6 +70,10 @@ _SIGNATURES = {
     "mgw_comm_set_ll_max": ([_P, _I64], _I),
     "mgw_comm_set_gate": ([_P, _I], _I),
     "mgw_comm_set_tuning": ([_P, _I, _I64], _I),
+    "mgw_comm_set_group_tag": ([_P, ctypes.c_uint32], _I),
+    "mgw_comm_pick_algo": ([_P, _I64, _I, ctypes.POINTER(_I)], _I),
+    "mgw_comm_clear_error": ([_P], _I),
+    "mgw_comm_create_local": ([_I, _I, _I64, ctypes.POINTER(_P)], _I),
     "mgw_comm_input": ([_P, ctypes.POINTER(_P)], _I),
     "mgw_comm_result": ([_P, ctypes.POINTER(_P)], _I),
     "mgw_comm_pack": ([_P, _P, _I, _I64, ctypes.c_float, _P], _I),

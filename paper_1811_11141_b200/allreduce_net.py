@@ -59,6 +59,7 @@ __all__ = [
     "DEFAULT_CAPACITY_BYTES",
     "EmulationReport",
     "GradientBuffer",
+    "LocalGroup",
     "ProtocolError",
     "RingSession",
     "TransportCounters",
@@ -338,7 +339,18 @@ class RingSession:
         for t in self._tables.values():
             t.close()
         self._tables.clear()
+        if self._comm and getattr(self, "_local_group", False):
+            return  # an in-process group is torn down as a whole by LocalGroup.close()
         if self._comm:
+            # a peer's last pull kernel may still read this rank's slot after our last
+            # collective returned: one zero-length collective (a barrier) before the region
+            # is freed.  Best effort -- a dead or mismatched peer must not block close().
+            try:
+                _native.call("mgw_comm_set_timeout_ms", self._comm, 2000)
+                _native.call("mgw_allreduce", self._comm, 0, _native.ALGO_ONESHOT, self.stream.cuda_stream)
+                self.stream.synchronize()
+            except Exception:
+                pass
             _native.lib().mgw_comm_destroy(self._comm)
             self._comm = None
 
@@ -378,11 +390,22 @@ class RingSession:
         if code.value == _native.DEV_OK:
             return
         who = f"rank {self.config.rank}"
-        if code.value == _native.DEV_LENGTH_MISMATCH:
-            raise ProtocolError(f"{who}: peers disagree on the bucket length; buffer lengths likely disagree")
+        if code.value == _native.DEV_MISMATCH:
+            raise ProtocolError(f"{who}: peers disagree on the collective (bucket length, algorithm, grid, dtype, "
+                                "scale or group/iteration tag); buffer lengths likely disagree")
         if code.value == _native.DEV_TIMEOUT:
             raise ProtocolError(f"{who}: a peer never reached the collective within {self._timeout}s")
         raise ProtocolError(f"{who}: a peer aborted the collective")
+
+    def clear_error(self) -> None:
+        """Reset the device error word and this rank's abort flag after a ProtocolError
+        (every rank, after a host-level barrier, before the next collective)."""
+        _native.call("mgw_comm_clear_error", self.comm)
+
+    def set_group_tag(self, layer_low: int, iteration: int = 0) -> None:
+        """Tag the next collectives with (group, iteration), as the reference's frame header
+        does (allreduce_net.py:340-345): ranks that disagree raise ProtocolError."""
+        _native.call("mgw_comm_set_group_tag", self.comm, group_tag(layer_low, iteration))
 
     def account(self, n: int, algo: int, elem_bytes: int = 4) -> None:
         """NVLink payload accounting for one collective of n elements."""
@@ -426,8 +449,25 @@ def ll_max_bytes(world: int) -> int:
     return (1 << 20) if world == 2 else ((512 << 10) if world <= 4 else LL_MAX_BYTES)
 
 
-def _algo_for(session: RingSession, n: int, fused: bool = False) -> int:
-    """The algorithm the native AUTO choice takes (mirrors pick_fused_algo / pick_algo)."""
+def group_tag(layer_low: int, iteration: int = 0) -> int:
+    """32-bit group tag of (head layer, iteration) for mgw_comm_set_group_tag."""
+    return ((int(iteration) * 0x9E3779B1) ^ int(layer_low)) & 0xFFFFFFFF
+
+
+def _algo_for(session: RingSession, n: int, fused: bool = False, elem_bytes: int = 4) -> int:
+    """The algorithm a collective of n elements runs under AUTO.  Fused exchanges ask the
+    communicator itself (mgw_comm_pick_algo: thresholds set on it, NVLS, the push-row
+    fallbacks); without a native communicator the host mirror ``_auto_rule`` answers."""
+    comm = getattr(session, "_comm", None)
+    if fused and comm:
+        out = ctypes.c_int()
+        _native.call("mgw_comm_pick_algo", comm, int(n), int(elem_bytes), ctypes.byref(out))
+        return out.value
+    return _auto_rule(session, n, fused)
+
+
+def _auto_rule(session: RingSession, n: int, fused: bool = False) -> int:
+    """Host mirror of pick_fused_algo / pick_algo at the default thresholds."""
     if fused and 4 * n <= ll_max_bytes(session.config.n_workers):
         return _native.ALGO_LL
     if fused:
@@ -467,10 +507,11 @@ def ring_allreduce(
     """Element-wise sum across all ranks, in place; returns ``buffer``.
 
     Collective.  Per element the sum is folded in the reference ring's order,
-    so results are bit-identical to allreduce_net.py:370-411.  ``iteration`` is
-    accepted for signature compatibility (it only tagged TCP frames).
+    so results are bit-identical to allreduce_net.py:370-411.  ``(layer_low,
+    iteration)`` tag the collective as the reference's frame header does
+    (allreduce_net.py:340-345): a rank issuing a different group or iteration raises
+    ProtocolError on every rank instead of reducing unrelated buckets.
     """
-    del iteration
     torch = session.torch
     values = buffer.values
     n = len(buffer)
@@ -492,13 +533,10 @@ def ring_allreduce(
                 raise ValueError(f"tensor on {values.device}, session on {session.device}")
             stream.wait_stream(torch.cuda.current_stream(session.device))
             ptr = values.data_ptr()
-        algo = _algo_for(session, n, fused=True)
+        algo = _algo_for(session, n, fused=True, elem_bytes=width)
         handle = stream.cuda_stream
+        session.set_group_tag(buffer.layer_low, iteration)
         if n and bf16:
-            if 2 * n <= ll_max_bytes(config.n_workers):
-                algo = _native.ALGO_LL
-            else:
-                algo = _native.ALGO_ONESHOT if 2 * n <= session_oneshot_max(session) else _native.ALGO_TWOSHOT
             table = session.table(ptr, n)
             _native.call("mgw_allreduce_fused_bf16", session.comm, table.ptr, 1, n, ctypes.c_float(1.0),
                          _native.ALGO_AUTO, handle)
@@ -607,8 +645,9 @@ def run_emulation(
         plan = MergePlan(frozenset(), n_layers)
     if plan.num_layers != n_layers:
         raise ValueError("plan does not match the profile's layer count")
-    if profile.element_bytes != 4:
-        raise ValueError("the B200 data path reduces fp32 gradients (element_bytes == 4)")
+    # element_bytes (2, 4 or 8, model_profile.py:24) only prices messages in the cost
+    # model; the reference emulates every profile with fp32 buffers
+    # (GradientBuffer.for_group, allreduce_net.py:98-120, :495-509), and so does this path.
     from .overlap import OverlappedIteration
 
     largest = max((sum(p for _, p, _ in rows) for _, _, rows in _layout(profile, plan)), default=0)
@@ -724,6 +763,82 @@ def open_ring(
         _native.lib().mgw_comm_destroy(comm)
         raise
     return config, session
+
+
+class LocalGroup:
+    """``n_workers`` ranks inside this process on ONE device (``mgw_comm_create_local``):
+    every rank's communicator maps the others' regions directly, and every rank has its
+    own session and comm stream, so the real barrier / LL / push protocol runs between
+    concurrently executing kernels.  Drive each rank from its own thread (a collective
+    blocks until every rank has launched it), e.g. ``run(fn)`` calls ``fn(config,
+    session)`` on one thread per rank and returns the results in rank order.  Used by
+    the single-GPU parity tests; the CTA cap is 2 * 148 / N so all grids are co-resident.
+    """
+
+    def __init__(self, n_workers: int, *, device: int = 0, capacity_bytes: int = DEFAULT_CAPACITY_BYTES,
+                 timeout: float = 10.0) -> None:
+        import torch
+
+        if not isinstance(n_workers, int) or not 2 <= n_workers <= _native.MAX_RANKS:
+            raise ValueError(f"n_workers must lie in 2..{_native.MAX_RANKS}, got {n_workers!r}")
+        if not torch.cuda.is_available():
+            raise RuntimeError("no CUDA device visible: the B200 data path has no CPU fallback")
+        torch.cuda.set_device(device)
+        comms = (ctypes.c_void_p * n_workers)()
+        _native.call("mgw_comm_create_local", n_workers, device, int(capacity_bytes), comms)
+        self._comms = [comms[r] for r in range(n_workers)]
+        addresses = tuple(("local", r) for r in range(n_workers))
+        self.configs = [WorkerConfig(r, n_workers, addresses, device=device) for r in range(n_workers)]
+        self.sessions = []
+        for r in range(n_workers):
+            sess = RingSession(self.configs[r], self._comms[r], capacity_bytes=capacity_bytes, timeout=timeout)
+            sess._local_group = True
+            self.sessions.append(sess)
+
+    def run(self, fn, *args, **kwargs) -> list:
+        """``fn(config, session, *args, **kwargs)`` on one thread per rank; re-raises the
+        first rank's exception after every thread has finished."""
+        import threading
+
+        results: list = [None] * len(self.sessions)
+        errors: list = [None] * len(self.sessions)
+
+        def body(r):
+            try:
+                import torch
+
+                torch.cuda.set_device(self.sessions[r].device)
+                results[r] = fn(self.configs[r], self.sessions[r], *args, **kwargs)
+            except BaseException as exc:  # noqa: BLE001 - reported below
+                errors[r] = exc
+
+        threads = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(len(self.sessions))]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        for exc in errors:
+            if exc is not None:
+                raise exc
+        return results
+
+    def close(self) -> None:
+        for sess in self.sessions:
+            for t in sess._tables.values():
+                t.close()
+            sess._tables.clear()
+        if self._comms:
+            for c in self._comms:
+                _native.lib().mgw_comm_destroy(c)
+            for sess in self.sessions:
+                sess._comm = None
+            self._comms = []
+
+    def __enter__(self) -> "LocalGroup":
+        return self
+
+    def __exit__(self, *exc) -> None:
+        self.close()
 
 
 def exchange_handles_dist(handle: bytes, *, group=None) -> bytes:

@@ -11,11 +11,13 @@
 // N-1 of them) take a scalar path.
 //
 // Synchronisation: per-CTA flag barriers in every rank's IPC control area
-// (st.release.sys / ld.acquire.sys), flags tagged (epoch << 32 | n mod 2^32) so a
-// length disagreement between ranks is detected at the barrier; epochs come from a
-// device call counter (graph-replay safe); bounded spins set a device error word and
-// raise a sticky abort flag on every rank.
+// (st.release.sys / ld.acquire.sys), flags tagged (epoch << 32 | collective_tag) so any
+// disagreement between ranks (length, kernel, grid, dtype, scale, group) is detected at
+// the barrier; epochs come from a device call counter (graph-replay safe); bounded spins
+// set a device error word and raise a sticky abort flag on every rank.
 #pragma once
+
+#include <cstring>
 
 #include "common.cuh"
 
@@ -38,7 +40,48 @@ struct ArArgs {
   int rank;
   int world;
   int flags;
+  uint32_t tag;                // host: the caller's group tag; the launcher replaces it with
+                               // collective_tag() -- every barrier flag and LL header carries it
 };
+
+// ---- collective tag.  The reference rejects a frame whose (iteration, group_low, segment,
+// bytes) header disagrees (allreduce_net.py:340-345).  Here every barrier flag and LL
+// header carries a 32-bit digest of everything the ranks must agree on: element count,
+// dtype + kernel, grid (CTA b of every rank must handle the same chunk), scale, and the
+// caller's group tag (head layer / iteration).  A rank whose digest differs from a peer's
+// at any barrier raises MGW_DEV_MISMATCH on every rank within one flag round trip.
+enum TagKind : uint32_t {
+  kTagOneshot = 1, kTagTwoshot, kTagFusedOneshot, kTagFusedTwoshot, kTagLL, kTagNvls, kTagPush, kTagPushOneshot,
+  kTagB16Oneshot, kTagB16Twoshot, kTagB16LL
+};
+
+inline uint32_t tag_mix(uint32_t h, uint32_t k) {  // murmur3 block step
+  k *= 0xcc9e2d51u;
+  k = (k << 15) | (k >> 17);
+  k *= 0x1b873593u;
+  h ^= k;
+  h = (h << 13) | (h >> 19);
+  return h * 5u + 0xe6546b64u;
+}
+
+inline uint32_t collective_tag(uint32_t group_tag, int64_t n, uint32_t kind, int grid, float scale) {
+  uint32_t sb;
+  memcpy(&sb, &scale, sizeof(sb));
+  uint32_t h = 0x6d677766u;
+  h = tag_mix(h, group_tag);
+  h = tag_mix(h, (uint32_t)n);
+  h = tag_mix(h, (uint32_t)((uint64_t)n >> 32));
+  h = tag_mix(h, kind);
+  h = tag_mix(h, (uint32_t)grid);
+  h = tag_mix(h, sb);
+  h ^= 24u;  // murmur3 finalizer
+  h ^= h >> 16;
+  h *= 0x85ebca6bu;
+  h ^= h >> 13;
+  h *= 0xc2b2ae35u;
+  h ^= h >> 16;
+  return h;
+}
 
 // Phase marks (mgw_probe_phases): CTA 0 records %globaltimer at its phase boundaries into
 // stamp[2 + k] (ncu cannot replay a multi-rank kernel, so the kernels time themselves).
@@ -78,7 +121,7 @@ static __device__ __noinline__ int cta_barrier(uint64_t* const* flags, int parit
       const uint64_t v = load_acquire_sys(mine);
 #endif
       if ((uint32_t)(v >> 32) == epoch) {
-        if ((uint32_t)v != tag) status = MGW_DEV_LENGTH_MISMATCH;
+        if ((uint32_t)v != tag) status = MGW_DEV_MISMATCH;
         break;
       }
       if ((spin & 63) == 63) {
@@ -114,6 +157,9 @@ static __device__ __noinline__ int cta_barrier(uint64_t* const* flags, int parit
 // gate the first rank's CTAs would sit in the entry barrier holding SM slots that the
 // backward kernels need.  Door words are monotonic epochs -- no parity, no reset.
 static __global__ void gate_kernel(const __grid_constant__ ArArgs a) {
+  grid_dep_wait();  // a programmatic producer (the engine's fill) must finish before the
+                    // exchange behind this gate reads its rows (the exchange's own wait
+                    // only covers the gate)
   const int t = threadIdx.x;
   const uint32_t epoch = load_volatile32(a.state) + 1u;
   int status = MGW_DEV_OK;
@@ -272,7 +318,7 @@ __global__ void __launch_bounds__(kThreads, 2) oneshot_kernel(const __grid_const
   int parity;
   kernel_prologue<N>(a, epoch, parity, s_in, s_end);
   int status = MGW_DEV_OK;
-  if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, (uint32_t)a.n, a);
+  if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, a.tag, a);
   if (status == MGW_DEV_OK && a.n > 0) {
     float* out = a.out[a.rank];
     const int64_t nv = a.n >> 2;
@@ -311,7 +357,7 @@ __global__ void __launch_bounds__(kThreads, 2) twoshot_kernel(const __grid_const
   int status = MGW_DEV_OK;
 
   if (!(a.flags & kSkipPhase1)) {
-    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, (uint32_t)a.n, a);
+    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, a.tag, a);
     if (status == MGW_DEV_OK && a.n > 0) {
       const int64_t p0 = part_begin(me, nv, N), p1 = part_begin(me + 1, nv, N);
       const int64_t per = (p1 - p0 + G - 1) / G;
@@ -325,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, 2) twoshot_kernel(const __grid_const
   }
 
   if (status == MGW_DEV_OK && !(a.flags & kSkipPhase2)) {
-    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.mid, parity, epoch, (uint32_t)a.n, a);
+    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.mid, parity, epoch, a.tag, a);
     if (status == MGW_DEV_OK && a.n > 0) {
       // chunk b of every peer part; peers interleaved so N-1 streams are in flight.
       // Chunk bounds live in shared memory to keep the copy loop's registers for data.

@@ -31,9 +31,6 @@ __device__ __forceinline__ float b16_word_hi(uint32_t w) { return __uint_as_floa
 __device__ __forceinline__ float b16_to_f32(uint16_t h) { return __uint_as_float((uint32_t)h << 16); }
 __device__ __forceinline__ uint16_t f32_to_b16(float x) { return __bfloat16_as_ushort(__float2bfloat16_rn(x)); }
 
-// barrier tag: a rank calling the bf16 exchange while a peer calls the fp32 one (same n)
-// is reported like a length mismatch
-__device__ __forceinline__ uint32_t b16_tag(int64_t n) { return (uint32_t)n ^ 0x80000000u; }
 
 __device__ __forceinline__ uint32_t b16_word(const uint4& v, int w) {
   return w == 0 ? v.x : (w == 1 ? v.y : (w == 2 ? v.z : v.w));
@@ -293,7 +290,7 @@ __global__ void __launch_bounds__(kThreads, 2) b16_oneshot_kernel(const __grid_c
     b16_pack_range(f, const_cast<uint16_t*>(in[a.rank]), v0, v1, last ? nv * kB16 : 0, last ? a.n : 0);
   int status = MGW_DEV_OK;
   if (!(a.flags & kSkipPhase1)) {
-    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, b16_tag(a.n), a);
+    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, a.tag, a);
     if (status == MGW_DEV_OK) {
       b16_reduce_range<N, U>(f, in, s_end, v0, v1, nullptr);
       if (last) b16_reduce_tail<N>(f, in, s_end, nv * kB16, a.n, nullptr);
@@ -327,14 +324,14 @@ __global__ void __launch_bounds__(kThreads, 2) b16_twoshot_kernel(const __grid_c
   }
   int status = MGW_DEV_OK;
   if (!(a.flags & kSkipPhase1)) {
-    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, b16_tag(a.n), a);
+    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, a.tag, a);
     if (status == MGW_DEV_OK) {
       b16_reduce_range<N, U>(f, in, s_end, pc.lo[me], pc.lo[me] + pc.len[me], mine);
       if (last && me == N - 1) b16_reduce_tail<N>(f, in, s_end, tail0, a.n, mine);
     }
   }
   if (status == MGW_DEV_OK && !(a.flags & kSkipPhase2)) {
-    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.mid, parity, epoch, b16_tag(a.n), a);
+    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.mid, parity, epoch, a.tag, a);
     if (status == MGW_DEV_OK) {
       b16_scatter_parts<N>(f, in, me, pc);
       if (last && me != N - 1) b16_scatter_range(f, in[N - 1], 0, 0, tail0, a.n);
@@ -371,7 +368,7 @@ __global__ void __launch_bounds__(kThreads, 2) ll_b16_kernel(const __grid_consta
   if (threadIdx.x == 0) s_status = MGW_DEV_OK;
   const bool do_push = !(a.flags & kSkipPack), do_fold = !(a.flags & kSkipPhase1);  // emulation split
   if (do_push && blockIdx.x == 0 && threadIdx.x < N)
-    st_relaxed_sys_u64(l.hdr[threadIdx.x] + parity * kMaxRanks + me, ((uint64_t)epoch << 32) | b16_tag(n));
+    st_relaxed_sys_u64(l.hdr[threadIdx.x] + parity * kMaxRanks + me, ((uint64_t)epoch << 32) | a.tag);
   __syncthreads();
 
   // element quads of this CTA: [q0, q1) (quad j = elements 4j .. 4j+3 = words 2j, 2j+1)
@@ -420,7 +417,7 @@ __global__ void __launch_bounds__(kThreads, 2) ll_b16_kernel(const __grid_consta
       }
       v = ld_relaxed_sys_u64(p);
     }
-    if (status == MGW_DEV_OK && (uint32_t)v != b16_tag(n)) status = MGW_DEV_LENGTH_MISMATCH;
+    if (status == MGW_DEV_OK && (uint32_t)v != a.tag) status = MGW_DEV_MISMATCH;
     if (status != MGW_DEV_OK) atomicCAS(&s_status, 0, status);
   }
   __syncthreads();

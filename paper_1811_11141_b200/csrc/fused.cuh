@@ -234,9 +234,9 @@ __global__ void __launch_bounds__(kThreads, 2) fused_oneshot_kernel(const __grid
   if (!(a.flags & kSkipPack)) fused_pack_range(f, mine, v0, v1, last ? nv << 2 : 0, last ? a.n : 0);
   phase_mark(a, 1);
   int status = MGW_DEV_OK;
-  if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, (uint32_t)a.n, a);
+  if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, a.tag, a);
   phase_mark(a, 2);
-  if (status == MGW_DEV_OK) {
+  if (status == MGW_DEV_OK && !(a.flags & kSkipPhase1)) {
     fused_reduce_range<N, U>(f, s_in, s_end, v0, v1, nullptr);
     if (last) fused_reduce_tail<N>(f, s_in, s_end, nv << 2, a.n, nullptr);
   }
@@ -352,14 +352,14 @@ __global__ void __launch_bounds__(kThreads, 2) fused_twoshot_kernel(const __grid
   if (threadIdx.x == 0) part_chunks<N>(nv, b, G, pc);
   __syncthreads();
   phase_mark(a, 0);
-  if (!(a.flags & (kSkipPhase1 | kSkipPack))) {
+  if (!(a.flags & kSkipPack)) {
     fused_pack_parts<N>(f, mine, pc);
     if (last) fused_pack_range(f, mine, 0, 0, tail0, a.n);  // the n % 4 tail (part N-1)
   }
   phase_mark(a, 1);
   int status = MGW_DEV_OK;
   if (!(a.flags & kSkipPhase1)) {
-    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, (uint32_t)a.n, a);
+    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, a.tag, a);
     phase_mark(a, 2);
     if (status == MGW_DEV_OK) {
       fused_reduce_range<N, U>(f, s_in, s_end, pc.lo[me], pc.lo[me] + pc.len[me], mine);
@@ -368,7 +368,7 @@ __global__ void __launch_bounds__(kThreads, 2) fused_twoshot_kernel(const __grid
     phase_mark(a, 3);
   }
   if (status == MGW_DEV_OK && !(a.flags & kSkipPhase2)) {
-    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.mid, parity, epoch, (uint32_t)a.n, a);
+    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.mid, parity, epoch, a.tag, a);
     phase_mark(a, 4);
     if (status == MGW_DEV_OK) {
       fused_scatter_parts<N>(f, s_in, me, pc);

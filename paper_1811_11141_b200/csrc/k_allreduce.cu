@@ -6,12 +6,17 @@
 namespace mgw {
 
 template <int N>
-int launch_allreduce_n(const ArArgs& a, int algo, int max_ctas, cudaStream_t stream, const int64_t* per_cta) {
-  const int64_t nv = a.n >> 2;
+int launch_allreduce_n(const ArArgs& a0, int algo, int max_ctas, cudaStream_t stream, const int64_t* per_cta) {
+  const int64_t nv = a0.n >> 2;
+  ArArgs a = a0;
   if (algo == MGW_ALGO_ONESHOT) {
-    oneshot_kernel<N><<<collective_grid<N>(nv, per_cta ? per_cta[0] : 0, max_ctas), kThreads, 0, stream>>>(a);
+    const int grid = collective_grid<N>(nv, per_cta ? per_cta[0] : 0, max_ctas);
+    a.tag = collective_tag(a0.tag, a0.n, kTagOneshot, grid, 1.f);
+    oneshot_kernel<N><<<grid, kThreads, 0, stream>>>(a);
   } else {
-    twoshot_kernel<N><<<collective_grid<N>(nv / N, per_cta ? per_cta[1] : 0, max_ctas), kThreads, 0, stream>>>(a);
+    const int grid = collective_grid<N>(nv / N, per_cta ? per_cta[1] : 0, max_ctas);
+    a.tag = collective_tag(a0.tag, a0.n, kTagTwoshot, grid, 1.f);
+    twoshot_kernel<N><<<grid, kThreads, 0, stream>>>(a);
   }
   MGW_CHECK_LAUNCH();
   return MGW_OK;

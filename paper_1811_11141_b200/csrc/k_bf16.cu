@@ -5,11 +5,13 @@
 
 namespace mgw {
 
-int launch_ll_b16(const LLArgs& l, int max_ctas, cudaStream_t stream) {
+int launch_ll_b16(const LLArgs& l0, int max_ctas, cudaStream_t stream) {
+  LLArgs l = l0;
   if (l.f.ar.n > 2 * kLLMaxElems)
     return set_error(MGW_EINVAL, "bf16 LL path takes at most %lld elements", (long long)(2 * kLLMaxElems));
   const int64_t quads = (l.f.ar.n + 3) >> 2;
   const int grid = grid_for(quads, kThreads, max_ctas < kSMs ? max_ctas : kSMs);
+  l.f.ar.tag = collective_tag(l0.f.ar.tag, l0.f.ar.n, kTagB16LL, grid, l0.f.scale);
   switch (l.f.ar.world) {
     case 2: ll_b16_kernel<2><<<grid, kThreads, 0, stream>>>(l); break;
     case 3: ll_b16_kernel<3><<<grid, kThreads, 0, stream>>>(l); break;
@@ -25,12 +27,18 @@ int launch_ll_b16(const LLArgs& l, int max_ctas, cudaStream_t stream) {
 }
 
 template <int N>
-int launch_b16_n(const FusedArgs& f, int algo, int max_ctas, cudaStream_t stream) {
-  const int64_t nv = f.ar.n / kB16;
-  if (algo == MGW_ALGO_ONESHOT)
-    b16_oneshot_kernel<N><<<collective_grid<N>(nv, 0, max_ctas), kThreads, 0, stream>>>(f);
-  else
-    b16_twoshot_kernel<N><<<collective_grid<N>(nv / N, 0, max_ctas), kThreads, 0, stream>>>(f);
+int launch_b16_n(const FusedArgs& f0, int algo, int max_ctas, cudaStream_t stream) {
+  const int64_t nv = f0.ar.n / kB16;
+  FusedArgs f = f0;
+  if (algo == MGW_ALGO_ONESHOT) {
+    const int grid = collective_grid<N>(nv, 0, max_ctas);
+    f.ar.tag = collective_tag(f0.ar.tag, f0.ar.n, kTagB16Oneshot, grid, f0.scale);
+    b16_oneshot_kernel<N><<<grid, kThreads, 0, stream>>>(f);
+  } else {
+    const int grid = collective_grid<N>(nv / N, 0, max_ctas);
+    f.ar.tag = collective_tag(f0.ar.tag, f0.ar.n, kTagB16Twoshot, grid, f0.scale);
+    b16_twoshot_kernel<N><<<grid, kThreads, 0, stream>>>(f);
+  }
   MGW_CHECK_LAUNCH();
   return MGW_OK;
 }

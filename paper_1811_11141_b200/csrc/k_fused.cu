@@ -6,12 +6,17 @@
 namespace mgw {
 
 template <int N>
-int launch_fused_n(const FusedArgs& f, int algo, int max_ctas, cudaStream_t stream, const int64_t* per_cta) {
-  const int64_t nv = f.ar.n >> 2;
+int launch_fused_n(const FusedArgs& f0, int algo, int max_ctas, cudaStream_t stream, const int64_t* per_cta) {
+  const int64_t nv = f0.ar.n >> 2;
+  FusedArgs f = f0;
   if (algo == MGW_ALGO_ONESHOT) {
-    fused_oneshot_kernel<N><<<collective_grid<N>(nv, per_cta ? per_cta[0] : 0, max_ctas), kThreads, 0, stream>>>(f);
+    const int grid = collective_grid<N>(nv, per_cta ? per_cta[0] : 0, max_ctas);
+    f.ar.tag = collective_tag(f0.ar.tag, f0.ar.n, kTagFusedOneshot, grid, f0.scale);
+    fused_oneshot_kernel<N><<<grid, kThreads, 0, stream>>>(f);
   } else {
-    fused_twoshot_kernel<N><<<collective_grid<N>(nv / N, per_cta ? per_cta[1] : 0, max_ctas), kThreads, 0, stream>>>(f);
+    const int grid = collective_grid<N>(nv / N, per_cta ? per_cta[1] : 0, max_ctas);
+    f.ar.tag = collective_tag(f0.ar.tag, f0.ar.n, kTagFusedTwoshot, grid, f0.scale);
+    fused_twoshot_kernel<N><<<grid, kThreads, 0, stream>>>(f);
   }
   MGW_CHECK_LAUNCH();
   return MGW_OK;

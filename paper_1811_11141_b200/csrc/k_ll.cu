@@ -6,9 +6,12 @@
 namespace mgw {
 
 template <int N>
-int launch_ll_n(const LLArgs& l, int max_ctas, cudaStream_t stream) {
-  const int64_t pairs = (l.f.ar.n + 1) >> 1;
-  ll_oneshot_kernel<N><<<grid_for(pairs, kThreads, max_ctas < kSMs ? max_ctas : kSMs), kThreads, 0, stream>>>(l);
+int launch_ll_n(const LLArgs& l0, int max_ctas, cudaStream_t stream) {
+  const int64_t pairs = (l0.f.ar.n + 1) >> 1;
+  LLArgs l = l0;
+  const int grid = grid_for(pairs, kThreads, max_ctas < kSMs ? max_ctas : kSMs);
+  l.f.ar.tag = collective_tag(l0.f.ar.tag, l0.f.ar.n, kTagLL, grid, l0.f.scale);
+  ll_oneshot_kernel<N><<<grid, kThreads, 0, stream>>>(l);
   MGW_CHECK_LAUNCH();
   return MGW_OK;
 }

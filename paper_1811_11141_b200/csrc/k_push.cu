@@ -6,9 +6,11 @@
 namespace mgw {
 
 template <int N>
-int launch_push1_n(const PushArgs& x, int max_ctas, cudaStream_t stream, const int64_t* per_cta) {
-  push_oneshot_kernel<N><<<collective_grid<N>(x.f.ar.n >> 2, per_cta ? per_cta[0] : 0, max_ctas), kThreads, 0,
-                           stream>>>(x);
+int launch_push1_n(const PushArgs& x0, int max_ctas, cudaStream_t stream, const int64_t* per_cta) {
+  PushArgs x = x0;
+  const int grid = collective_grid<N>(x0.f.ar.n >> 2, per_cta ? per_cta[0] : 0, max_ctas);
+  x.f.ar.tag = collective_tag(x0.f.ar.tag, x0.f.ar.n, kTagPushOneshot, grid, x0.f.scale);
+  push_oneshot_kernel<N><<<grid, kThreads, 0, stream>>>(x);
   MGW_CHECK_LAUNCH();
   return MGW_OK;
 }
@@ -27,8 +29,9 @@ int launch_push1(const PushArgs& x, int max_ctas, cudaStream_t stream, const int
   }
 }
 
-int launch_push(const PushArgs& x, int max_ctas, cudaStream_t stream, const int64_t* per_cta) {
+int launch_push(const PushArgs& x0, int max_ctas, cudaStream_t stream, const int64_t* per_cta) {
   max_ctas = max_ctas < kMaxBlocks ? max_ctas : kMaxBlocks;
+  PushArgs x = x0;
   const int64_t nv = x.f.ar.n >> 2;
   int64_t per = per_cta ? per_cta[1] : 0;
   if (per <= 0) {
@@ -40,14 +43,16 @@ int launch_push(const PushArgs& x, int max_ctas, cudaStream_t stream, const int6
     per = (per + 127) / 128 * 128;
     per = per < 2048 ? 2048 : (per > 4096 ? 4096 : per);
   }
+  const int grid = grid_for(nv / (x0.f.ar.world > 0 ? x0.f.ar.world : 1), per, max_ctas);
+  x.f.ar.tag = collective_tag(x0.f.ar.tag, x0.f.ar.n, kTagPush, grid, x0.f.scale);
   switch (x.f.ar.world) {
-    case 2: push_twoshot_kernel<2><<<collective_grid<2>(nv / 2, per, max_ctas), kThreads, 0, stream>>>(x); break;
-    case 3: push_twoshot_kernel<3><<<collective_grid<3>(nv / 3, per, max_ctas), kThreads, 0, stream>>>(x); break;
-    case 4: push_twoshot_kernel<4><<<collective_grid<4>(nv / 4, per, max_ctas), kThreads, 0, stream>>>(x); break;
-    case 5: push_twoshot_kernel<5><<<collective_grid<5>(nv / 5, per, max_ctas), kThreads, 0, stream>>>(x); break;
-    case 6: push_twoshot_kernel<6><<<collective_grid<6>(nv / 6, per, max_ctas), kThreads, 0, stream>>>(x); break;
-    case 7: push_twoshot_kernel<7><<<collective_grid<7>(nv / 7, per, max_ctas), kThreads, 0, stream>>>(x); break;
-    case 8: push_twoshot_kernel<8><<<collective_grid<8>(nv / 8, per, max_ctas), kThreads, 0, stream>>>(x); break;
+    case 2: push_twoshot_kernel<2><<<grid, kThreads, 0, stream>>>(x); break;
+    case 3: push_twoshot_kernel<3><<<grid, kThreads, 0, stream>>>(x); break;
+    case 4: push_twoshot_kernel<4><<<grid, kThreads, 0, stream>>>(x); break;
+    case 5: push_twoshot_kernel<5><<<grid, kThreads, 0, stream>>>(x); break;
+    case 6: push_twoshot_kernel<6><<<grid, kThreads, 0, stream>>>(x); break;
+    case 7: push_twoshot_kernel<7><<<grid, kThreads, 0, stream>>>(x); break;
+    case 8: push_twoshot_kernel<8><<<grid, kThreads, 0, stream>>>(x); break;
     default: return set_error(MGW_EINVAL, "push two-shot needs 2..%d ranks, got %d", kMaxRanks, x.f.ar.world);
   }
   MGW_CHECK_LAUNCH();

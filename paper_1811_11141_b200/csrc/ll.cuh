@@ -11,8 +11,8 @@
 // on the wire, which is irrelevant at these sizes.
 //
 // Fold order is the reference's (start at the element's `_segments` segment), so the
-// result is bit-identical to K2/K3.  Length disagreement: CTA 0 of every rank also
-// pushes a header (epoch << 32 | n) and checks every peer's header before folding;
+// result is bit-identical to K2/K3.  Disagreement: CTA 0 of every rank also pushes a
+// header (epoch << 32 | collective_tag) and checks every peer's header before folding;
 // a mismatch raises the sticky abort flag that every poll loop watches.
 #pragma once
 
@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(kThreads, 2) ll_oneshot_kernel(const __grid_co
   // and the fold into separate launches (emulated ranks on one device, tests only).
   const bool do_push = !(a.flags & kSkipPack), do_fold = !(a.flags & kSkipPhase1);
   if (do_push && blockIdx.x == 0 && threadIdx.x < N)
-    st_relaxed_sys_u64(l.hdr[threadIdx.x] + parity * kMaxRanks + me, ((uint64_t)epoch << 32) | (uint32_t)n);
+    st_relaxed_sys_u64(l.hdr[threadIdx.x] + parity * kMaxRanks + me, ((uint64_t)epoch << 32) | a.tag);
   __syncthreads();
 
   // element pairs of this CTA: [p0, p1) (pair j = elements 2j, 2j+1)
@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(kThreads, 2) ll_oneshot_kernel(const __grid_co
       }
       return v;
     }();
-    if (status == MGW_DEV_OK && (uint32_t)h != (uint32_t)n) status = MGW_DEV_LENGTH_MISMATCH;
+    if (status == MGW_DEV_OK && (uint32_t)h != a.tag) status = MGW_DEV_MISMATCH;
     if (status != MGW_DEV_OK) atomicCAS(&s_status, 0, status);
   }
   __syncthreads();

@@ -106,6 +106,8 @@ struct mgw_comm {
   bool nvls_mc_valid = false, nvls_bound = false;
   int64_t nvls_min_bytes = 0;  // AUTO picks NVLS at >= this size when set (0 = never)
   bool gate = false;           // launch gate_kernel ahead of every collective (mgw_comm_set_gate)
+  uint32_t group_tag = 0;      // caller's group tag, folded into every collective's tag
+  bool local_group = false;    // in-process rank group on one device (mgw_comm_create_local)
 };
 
 struct mgw_sched {
@@ -152,7 +154,17 @@ ArArgs make_args(const mgw_comm* c, int64_t n) {
   a.timeout_ns = c->timeout_ns;
   a.rank = c->rank;
   a.world = c->world;
+  a.tag = c->group_tag;
   return a;
+}
+
+// One rank per device (IPC): wait for the device.  In-process rank group: the caller has
+// synchronised its own stream -- a device-wide sync would wait on peers' kernels that wait
+// on this rank's next collective.
+int sync_for_query(const mgw_comm* c) {
+  MGW_CUDA(cudaSetDevice(c->device));
+  if (!c->local_group) MGW_CUDA(cudaDeviceSynchronize());
+  return MGW_OK;
 }
 
 int comm_launch_allreduce(const mgw_comm* c, const ArArgs& a, int algo, cudaStream_t stream) {
@@ -245,7 +257,30 @@ int pick_fused_algo(const mgw_comm* c, int64_t n, int algo) {
   return bytes >= (8ll << 20) && push_ok ? MGW_ALGO_PUSH : MGW_ALGO_TWOSHOT;
 }
 
-int comm_allreduce(mgw_comm* c, int64_t n, int algo, cudaStream_t stream, uint64_t* stamp = nullptr) {
+// The kernel a fused fp32 group exchange of n elements actually runs: the AUTO choice,
+// then the fallbacks when the push areas cannot hold the incoming rows.
+int resolve_fused_algo(const mgw_comm* c, int64_t n, int algo) {
+  int chosen = pick_fused_algo(c, n, algo);
+  if (chosen == MGW_ALGO_PUSH_ONESHOT && c->world * round_up(n, 16) * 4 > c->slot_bytes) chosen = MGW_ALGO_ONESHOT;
+  if (chosen == MGW_ALGO_PUSH && c->world * (((n / 4 + c->world - 1) / c->world + 1) * 4) * 4 > c->slot_bytes)
+    chosen = MGW_ALGO_TWOSHOT;
+  return chosen;
+}
+
+// bf16 group exchange: LL for small buckets, else pull one-shot / two-shot
+int resolve_b16_algo(const mgw_comm* c, int64_t n, int algo) {
+  if (algo == MGW_ALGO_AUTO) {
+    if (c->world > 1 && n * 2 <= c->ll_max_bytes && n <= 2 * kLLElems)
+      algo = MGW_ALGO_LL;
+    else
+      algo = n * 2 <= c->oneshot_max_bytes ? MGW_ALGO_ONESHOT : MGW_ALGO_TWOSHOT;
+  }
+  if (algo == MGW_ALGO_LL && c->world == 1) algo = MGW_ALGO_ONESHOT;
+  return algo;
+}
+
+int comm_allreduce(mgw_comm* c, int64_t n, int algo, cudaStream_t stream, uint64_t* stamp = nullptr,
+                   int64_t group_tag = -1) {
   if (n < 0 || n * 4 > c->slot_bytes)
     return set_error(MGW_EINVAL, "bucket of %lld elements exceeds slot capacity %lld B", (long long)n,
                      (long long)c->slot_bytes);
@@ -255,6 +290,7 @@ int comm_allreduce(mgw_comm* c, int64_t n, int algo, cudaStream_t stream, uint64
   }
   if (!c->peers_open) return set_error(MGW_EINVAL, "peers not opened (call mgw_comm_open_peers)");
   ArArgs a = make_args(c, n);
+  if (group_tag >= 0) a.tag = (uint32_t)group_tag;
   if (c->gate) {
     int rc = launch_gate(a, stream);
     if (rc) return rc;
@@ -276,7 +312,8 @@ int comm_pack(mgw_comm* c, const Row* host_rows, const Row* dev_rows, int n_rows
 
 // pack -> all-reduce -> unpack of one group in a single kernel (fused.cuh)
 int comm_allreduce_fused(mgw_comm* c, const Row* host_rows, const Row* dev_rows, int n_rows, int64_t n, float scale,
-                         int algo, cudaStream_t stream, uint64_t* stamp = nullptr, int extra_flags = 0) {
+                         int algo, cudaStream_t stream, uint64_t* stamp = nullptr, int extra_flags = 0,
+                         int64_t group_tag = -1) {
   if (n < 0 || n * 4 > c->slot_bytes)
     return set_error(MGW_EINVAL, "bucket of %lld elements exceeds slot capacity %lld B", (long long)n,
                      (long long)c->slot_bytes);
@@ -285,6 +322,7 @@ int comm_allreduce_fused(mgw_comm* c, const Row* host_rows, const Row* dev_rows,
   FusedArgs f;
   memset(&f, 0, sizeof(f));
   f.ar = make_args(c, n);
+  if (group_tag >= 0) f.ar.tag = (uint32_t)group_tag;
   if (c->world > 1 && c->gate) {
     int rc = launch_gate(f.ar, stream);
     if (rc) return rc;
@@ -297,7 +335,7 @@ int comm_allreduce_fused(mgw_comm* c, const Row* host_rows, const Row* dev_rows,
   f.rows = dev_rows;
   f.n_rows = n_rows;
   f.scale = scale;
-  int chosen = pick_fused_algo(c, n, algo);
+  const int chosen = resolve_fused_algo(c, n, algo);
   if (chosen == MGW_ALGO_NVLS) {
     if (!c->nvls_bound) return set_error(MGW_EINVAL, "NVLS not set up on this communicator");
     if ((size_t)n * 4 > c->nvls_bytes)
@@ -319,29 +357,16 @@ int comm_allreduce_fused(mgw_comm* c, const Row* host_rows, const Row* dev_rows,
     }
     return launch_ll(l, c->max_ctas, stream);
   }
-  if (chosen == MGW_ALGO_PUSH_ONESHOT) {
-    const int64_t stride = round_up(n, 16);  // one 64-B aligned row per source
-    if (c->world * stride * 4 <= c->slot_bytes) {
-      PushArgs x;
-      memset(&x, 0, sizeof(x));
-      x.f = f;
-      x.stride = stride;
-      for (int s = 0; s < c->world; ++s) x.gather[s] = c->peer[s] + kSlotOff + 2 * c->slot_bytes;
-      return launch_push1(x, c->max_ctas, stream, c->vec_per_cta);
-    }
-    chosen = MGW_ALGO_ONESHOT;  // the rows do not fit: pull one-shot
-  }
-  if (chosen == MGW_ALGO_PUSH) {
-    const int64_t stride = ((n / 4 + c->world - 1) / c->world + 1) * 4;  // push_stride()
-    if (c->world * stride * 4 <= c->slot_bytes) {
-      PushArgs x;
-      memset(&x, 0, sizeof(x));
-      x.f = f;
-      x.stride = stride;
-      for (int s = 0; s < c->world; ++s) x.gather[s] = c->peer[s] + kSlotOff + 2 * c->slot_bytes;
-      return launch_push(x, c->max_ctas, stream, c->vec_per_cta);
-    }
-    chosen = MGW_ALGO_TWOSHOT;  // the incoming rows do not fit the slot: pull two-shot
+  if (chosen == MGW_ALGO_PUSH_ONESHOT || chosen == MGW_ALGO_PUSH) {
+    // incoming rows: one 64-B aligned row per source (one-shot), or one part + tail per
+    // source (two-shot, push_stride()); resolve_fused_algo checked that they fit the slot
+    const bool one = chosen == MGW_ALGO_PUSH_ONESHOT;
+    PushArgs x;
+    memset(&x, 0, sizeof(x));
+    x.f = f;
+    x.stride = one ? round_up(n, 16) : ((n / 4 + c->world - 1) / c->world + 1) * 4;
+    for (int s = 0; s < c->world; ++s) x.gather[s] = c->peer[s] + kSlotOff + 2 * c->slot_bytes;
+    return one ? launch_push1(x, c->max_ctas, stream, c->vec_per_cta) : launch_push(x, c->max_ctas, stream, c->vec_per_cta);
   }
   return launch_fused(f, chosen, c->max_ctas, stream, c->vec_per_cta);
 }
@@ -377,13 +402,7 @@ int comm_allreduce_fused_bf16(mgw_comm* c, const Row* host_rows, const Row* dev_
   if (c->world > 1 && !c->peers_open) return set_error(MGW_EINVAL, "peers not opened (call mgw_comm_open_peers)");
   if (n == 0 || n_rows == 0) return MGW_OK;
   if (c->world == 1 && scale == 1.0f) return MGW_OK;  // nothing to exchange or scale
-  if (algo == MGW_ALGO_AUTO) {
-    if (c->world > 1 && n * 2 <= c->ll_max_bytes && n <= 2 * kLLElems)
-      algo = MGW_ALGO_LL;
-    else
-      algo = n * 2 <= c->oneshot_max_bytes ? MGW_ALGO_ONESHOT : MGW_ALGO_TWOSHOT;
-  }
-  if (algo == MGW_ALGO_LL && c->world == 1) algo = MGW_ALGO_ONESHOT;
+  algo = resolve_b16_algo(c, n, algo);
   FusedArgs f;
   memset(&f, 0, sizeof(f));
   f.ar = make_args(c, n);
@@ -524,11 +543,13 @@ int mgw_check_const(const void* table, int n, const float* values_dev, int64_t* 
   if (rc) return rc;
   const mgw_table_t* t = as_table(table);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // stream-ordered scratch: no cudaFree (an implicit device-wide sync would stall an
+  // in-process rank group whose peers are mid-collective)
   unsigned long long* d_bad = nullptr;
-  MGW_CUDA(cudaMalloc(&d_bad, sizeof(unsigned long long)));
+  MGW_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_bad), sizeof(unsigned long long), s));
   cudaError_t e = cudaMemsetAsync(d_bad, 0, sizeof(unsigned long long), s);
   if (e != cudaSuccess) {
-    cudaFree(d_bad);
+    cudaFreeAsync(d_bad, s);
     return set_error(MGW_ECUDA, "check: %s", cudaGetErrorString(e));
   }
   rc = launch_rows<RowOp::kCheck>(t->host.data(), t->dev, n, nullptr, t->extent, 1.f, values_dev, nullptr, 0, d_bad, s);
@@ -538,7 +559,7 @@ int mgw_check_const(const void* table, int n, const float* values_dev, int64_t* 
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) rc = set_error(MGW_ECUDA, "check: %s", cudaGetErrorString(e));
   }
-  cudaFree(d_bad);
+  cudaFreeAsync(d_bad, s);
   *mismatches = (int64_t)bad;
   return rc;
 }
@@ -625,8 +646,9 @@ int mgw_comm_destroy(mgw_comm* c) {
     if (c->nvls_mem) d.mem_release(c->nvls_mem);
     if (c->nvls_mc_valid) d.mem_release(c->nvls_mc);
   }
-  for (int s = 0; s < kMaxRanks; ++s)
-    if (s != c->rank && c->peer[s]) cudaIpcCloseMemHandle(c->peer[s]);
+  if (!c->local_group)
+    for (int s = 0; s < kMaxRanks; ++s)
+      if (s != c->rank && c->peer[s]) cudaIpcCloseMemHandle(c->peer[s]);
   if (c->region) cudaFree(c->region);
   if (c->state) cudaFree(c->state);
   if (c->err) cudaFree(c->err);
@@ -668,6 +690,50 @@ int mgw_comm_set_max_ctas(mgw_comm* c, int ctas) {
 int mgw_comm_set_gate(mgw_comm* c, int enable) {
   if (!c) return set_error(MGW_EINVAL, "communicator is null");
   c->gate = enable != 0;
+  return MGW_OK;
+}
+
+int mgw_comm_set_group_tag(mgw_comm* c, uint32_t tag) {
+  if (!c) return set_error(MGW_EINVAL, "communicator is null");
+  c->group_tag = tag;
+  return MGW_OK;
+}
+
+int mgw_comm_pick_algo(mgw_comm* c, int64_t n_elem, int element_bytes, int* algo) {
+  if (!c || !algo || n_elem < 0 || (element_bytes != 2 && element_bytes != 4))
+    return set_error(MGW_EINVAL, "bad algorithm query");
+  *algo = element_bytes == 2 ? resolve_b16_algo(c, n_elem, MGW_ALGO_AUTO) : resolve_fused_algo(c, n_elem, MGW_ALGO_AUTO);
+  return MGW_OK;
+}
+
+int mgw_comm_clear_error(mgw_comm* c) {
+  if (!c) return set_error(MGW_EINVAL, "communicator is null");
+  if (int rc = sync_for_query(c)) return rc;
+  const uint32_t zero = 0;
+  MGW_CUDA(cudaMemcpy(c->err, &zero, sizeof(zero), cudaMemcpyHostToDevice));
+  MGW_CUDA(cudaMemcpy(c->region + kAbortOff, &zero, sizeof(zero), cudaMemcpyHostToDevice));
+  return MGW_OK;
+}
+
+int mgw_comm_create_local(int world, int device, int64_t capacity_bytes, mgw_comm** comms) {
+  if (!comms || world < 1 || world > kMaxRanks) return set_error(MGW_EINVAL, "bad local group arguments");
+  for (int r = 0; r < world; ++r) comms[r] = nullptr;
+  for (int r = 0; r < world; ++r) {
+    int rc = mgw_comm_create(r, world, device, capacity_bytes, &comms[r], nullptr);
+    if (rc) {
+      for (int q = 0; q < r; ++q) mgw_comm_destroy(comms[q]);
+      for (int q = 0; q < world; ++q) comms[q] = nullptr;
+      return rc;
+    }
+  }
+  for (int r = 0; r < world; ++r) {
+    mgw_comm* c = comms[r];
+    for (int s = 0; s < world; ++s) c->peer[s] = comms[s]->region;
+    c->peers_open = true;
+    c->local_group = true;
+    // every rank's grid must be co-resident on the one device: 2 CTAs of 512 threads per SM
+    c->max_ctas = std::max(1, 2 * kSMs / world);
+  }
   return MGW_OK;
 }
 
@@ -876,8 +942,7 @@ int mgw_group_launch_bf16(mgw_comm* c, const void* table, int n_rows, int64_t n_
 
 int mgw_comm_error(mgw_comm* c, int* code) {
   if (!c || !code) return set_error(MGW_EINVAL, "bad arguments");
-  MGW_CUDA(cudaSetDevice(c->device));
-  MGW_CUDA(cudaDeviceSynchronize());
+  if (int rc = sync_for_query(c)) return rc;
   MGW_CUDA(cudaMemcpy(code, c->err, sizeof(int), cudaMemcpyDeviceToHost));
   return MGW_OK;
 }
@@ -885,8 +950,7 @@ int mgw_comm_error(mgw_comm* c, int* code) {
 int mgw_comm_calls(mgw_comm* c, int64_t* calls) {
   if (!c || !calls) return set_error(MGW_EINVAL, "bad arguments");
   uint32_t v = 0;
-  MGW_CUDA(cudaSetDevice(c->device));
-  MGW_CUDA(cudaDeviceSynchronize());
+  if (int rc = sync_for_query(c)) return rc;
   MGW_CUDA(cudaMemcpy(&v, c->state, sizeof(v), cudaMemcpyDeviceToHost));
   *calls = v;
   return MGW_OK;
@@ -1068,19 +1132,28 @@ int mgw_allreduce_fused_emulated(void* const* tables, float* const* slots, int w
     if (rc) return rc;
   }
   if (n == 0) return MGW_OK;
-  for (int r = 0; r < world; ++r) {
-    const mgw_table_t* t = as_table(tables[r]);
-    int rc = launch_rows<RowOp::kPack>(t->host.data(), t->dev, (int)t->host.size(), slots[r], n, scale, nullptr, nullptr,
-                                       0, nullptr, s);
-    if (rc) return rc;
-  }
   FusedArgs f;
   memset(&f, 0, sizeof(f));
   for (int r = 0; r < world; ++r) f.ar.slot[r] = reinterpret_cast<char*>(slots[r]);
   f.ar.n = n;
   f.ar.world = world;
   f.scale = scale;
+  // step 0: every rank packs with the kernel's own pack (one-shot: its chunk of the bucket,
+  // two-shot: chunk b of every part); then the one-shot fold, or the two-shot's two phases
   const int phases = algo == MGW_ALGO_ONESHOT ? 1 : 2;
+  for (int r = 0; r < world; ++r) {
+    const mgw_table_t* t = as_table(tables[r]);
+    const int n_rows = (int)t->host.size();
+    f.use_inline = n_rows <= kInlineRows;
+    if (f.use_inline)
+      for (int k = 0; k < n_rows; ++k) f.inline_rows[k] = t->host[k];
+    f.rows = t->dev;
+    f.n_rows = n_rows;
+    f.ar.rank = r;
+    f.ar.flags = kNoBarrier | kSkipPhase1 | kSkipPhase2;
+    int rc = launch_fused(f, algo, 2 * kSMs, s);
+    if (rc) return rc;
+  }
   for (int phase = 0; phase < phases; ++phase) {
     for (int r = 0; r < world; ++r) {
       const mgw_table_t* t = as_table(tables[r]);
@@ -1416,12 +1489,13 @@ static int sched_enqueue(mgw_sched* s, cudaStream_t cs, cudaStream_t ms) {
                                        nullptr, ms, st + 4);
       if (rc) return rc;
     } else if (s->flags & MGW_SCHED_FUSED) {
-      rc = comm_allreduce_fused(s->comm, hrows, grows, gr.desc_count, gr.n_elem, s->scale, gr.algo, ms, st + 2);
+      rc = comm_allreduce_fused(s->comm, hrows, grows, gr.desc_count, gr.n_elem, s->scale, gr.algo, ms, st + 2, 0,
+                                (uint32_t)gr.head_layer);
       if (rc) return rc;
     } else {
       rc = comm_pack(s->comm, hrows, grows, gr.desc_count, gr.n_elem, s->scale, ms, st);
       if (rc) return rc;
-      rc = comm_allreduce(s->comm, gr.n_elem, gr.algo, ms, st + 2);
+      rc = comm_allreduce(s->comm, gr.n_elem, gr.algo, ms, st + 2, (uint32_t)gr.head_layer);
       if (rc) return rc;
       rc = launch_rows<RowOp::kUnpack>(hrows, grows, gr.desc_count, s->comm->result, gr.n_elem, 1.f, nullptr, nullptr, 0,
                                        nullptr, ms, st + 4);

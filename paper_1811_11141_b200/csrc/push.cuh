@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(kThreads, 2) push_twoshot_kernel(const __grid_
   // ---- phase 2: fold my part's chunk b from the N local rows, write my tensors, push
   //      the result into every peer's gather area
   if (!(a.flags & kSkipPhase1)) {
-    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, (uint32_t)a.n, a);
+    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, a.tag, a);
     phase_mark(a, 2);
     if (status == MGW_DEV_OK) {
       const float* in = s_in[me];
@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(kThreads, 2) push_twoshot_kernel(const __grid_
   phase_mark(a, 3);
   // ---- phase 3: copy chunk b of every peer part from my gather area into my tensors
   if (status == MGW_DEV_OK && !(a.flags & kSkipPhase2)) {
-    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.mid, parity, epoch, (uint32_t)a.n, a);
+    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.mid, parity, epoch, a.tag, a);
     phase_mark(a, 4);
     if (status == MGW_DEV_OK) {
       const float* g = s_gat[me];
@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(kThreads, 2) push_oneshot_kernel(const __grid_
   phase_mark(a, 1);
   int status = MGW_DEV_OK;
   if (!(a.flags & kSkipPhase1)) {
-    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, (uint32_t)a.n, a);
+    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, a.tag, a);
     phase_mark(a, 2);
     if (status == MGW_DEV_OK) {
       // fold chunk b from the N local rows (they play the slots of fused_reduce_range)

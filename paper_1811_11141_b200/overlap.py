@@ -101,8 +101,8 @@ class OverlappedIteration:
     ) -> None:
         import torch
 
-        if profile.element_bytes != 4:
-            raise ValueError("the B200 data path reduces fp32 gradients (element_bytes == 4)")
+        # element_bytes (2, 4, 8) only prices messages in the cost model: the emulation
+        # moves fp32 buffers for every profile, as the reference does (allreduce_net.py:495-509)
         if plan is None:
             plan = MergePlan(frozenset(), profile.num_layers)
         if plan.num_layers != profile.num_layers:
