@@ -141,11 +141,23 @@ int mgw_comm_pick_algo(mgw_comm* comm, int64_t n_elem, int element_bytes, int* a
 /* clear the device error word and this rank's abort flag after a ProtocolError.  Collective
  * in spirit: every rank calls it after a host-level barrier, before the next collective. */
 int mgw_comm_clear_error(mgw_comm* comm);
-/* In-process rank group on ONE device (tests and single-GPU emulation with the real barrier
+/* In-process rank group on ONE device (tests and single-GPU emulation of the real barrier
  * protocol): `world` communicators whose peer tables point at each other's regions directly
- * (no IPC).  Launch each rank's collectives on its own stream; the CTA cap defaults to
- * 2 * 148 / world so every rank's grid is co-resident. */
+ * (no IPC).  Their collectives run through mgw_group_allreduce_fused; the CTA cap defaults
+ * to 2 * 148 / world so all ranks' grids fit one co-resident cooperative launch. */
 int mgw_comm_create_local(int world, int device, int64_t capacity_bytes, mgw_comm** comms /* world */);
+/* Every rank of such a group runs its fused group exchange (rows in tables[r], n_elem[r]
+ * elements, scale[r]; element_bytes 4 = fp32, 2 = bf16) in ONE cooperative launch on
+ * `stream`: arguments, algorithm, grid and tag come from each rank's own communicator as
+ * in mgw_allreduce_fused[_bf16], so the real barrier / LL / push protocol -- and any
+ * disagreement between the ranks -- runs between co-resident CTAs (kernels that wait on
+ * one another are never separate launches on one device).  n_elem[r] < 0: rank r is
+ * absent.  Afterwards read each rank's outcome with mgw_comm_error. */
+int mgw_group_allreduce_fused(mgw_comm* const* comms, void* const* tables, const int64_t* n_elem, const float* scale,
+                              int world, int algo, int element_bytes, void* stream);
+/* the 32-bit collective tag the launchers stamp into barrier flags / LL headers
+ * (kind: 1..11, see TagKind in csrc/allreduce.cuh) -- exposed for host-side tests */
+int mgw_debug_collective_tag(uint32_t group_tag, int64_t n_elem, int kind, int grid, float scale, uint32_t* out);
 int mgw_comm_input(mgw_comm* comm, float** slot); /* slot the next collective reads (syncs) */
 int mgw_comm_result(mgw_comm* comm, float** result);
 int mgw_comm_pack(mgw_comm* comm, const void* dev_table, int n, int64_t n_elem, float scale, void* stream);

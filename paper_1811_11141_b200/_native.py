@@ -74,6 +74,9 @@ _SIGNATURES = {
     "mgw_comm_pick_algo": ([_P, _I64, _I, ctypes.POINTER(_I)], _I),
     "mgw_comm_clear_error": ([_P], _I),
     "mgw_comm_create_local": ([_I, _I, _I64, ctypes.POINTER(_P)], _I),
+    "mgw_group_allreduce_fused": ([ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.POINTER(_I64),
+                                   ctypes.POINTER(ctypes.c_float), _I, _I, _I, _P], _I),
+    "mgw_debug_collective_tag": ([ctypes.c_uint32, _I64, _I, _I, ctypes.c_float, ctypes.POINTER(ctypes.c_uint32)], _I),
     "mgw_comm_input": ([_P, ctypes.POINTER(_P)], _I),
     "mgw_comm_result": ([_P, ctypes.POINTER(_P)], _I),
     "mgw_comm_pack": ([_P, _P, _I, _I64, ctypes.c_float, _P], _I),

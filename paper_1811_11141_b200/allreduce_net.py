@@ -767,12 +767,13 @@ def open_ring(
 
 class LocalGroup:
     """``n_workers`` ranks inside this process on ONE device (``mgw_comm_create_local``):
-    every rank's communicator maps the others' regions directly, and every rank has its
-    own session and comm stream, so the real barrier / LL / push protocol runs between
-    concurrently executing kernels.  Drive each rank from its own thread (a collective
-    blocks until every rank has launched it), e.g. ``run(fn)`` calls ``fn(config,
-    session)`` on one thread per rank and returns the results in rank order.  Used by
-    the single-GPU parity tests; the CTA cap is 2 * 148 / N so all grids are co-resident.
+    every rank's communicator maps the others' regions directly and has its own session
+    (settings, tags, error word).  ``allreduce_fused`` runs every rank's fused group
+    exchange in ONE cooperative launch (``mgw_group_allreduce_fused``), so the real
+    barrier / LL / push protocol -- and any disagreement between the ranks' settings --
+    plays out between co-resident CTAs; kernels that wait on one another are never
+    separate launches on one GPU.  Used by the single-GPU parity and protocol tests; the
+    CTA cap is 2 * 148 / N so all ranks fit one launch.
     """
 
     def __init__(self, n_workers: int, *, device: int = 0, capacity_bytes: int = DEFAULT_CAPACITY_BYTES,
@@ -784,6 +785,7 @@ class LocalGroup:
         if not torch.cuda.is_available():
             raise RuntimeError("no CUDA device visible: the B200 data path has no CPU fallback")
         torch.cuda.set_device(device)
+        self.torch = torch
         comms = (ctypes.c_void_p * n_workers)()
         _native.call("mgw_comm_create_local", n_workers, device, int(capacity_bytes), comms)
         self._comms = [comms[r] for r in range(n_workers)]
@@ -794,33 +796,53 @@ class LocalGroup:
             sess = RingSession(self.configs[r], self._comms[r], capacity_bytes=capacity_bytes, timeout=timeout)
             sess._local_group = True
             self.sessions.append(sess)
+        self.stream = torch.cuda.Stream(device=device)
 
-    def run(self, fn, *args, **kwargs) -> list:
-        """``fn(config, session, *args, **kwargs)`` on one thread per rank; re-raises the
-        first rank's exception after every thread has finished."""
-        import threading
+    @property
+    def n_workers(self) -> int:
+        return len(self.sessions)
 
-        results: list = [None] * len(self.sessions)
-        errors: list = [None] * len(self.sessions)
-
-        def body(r):
+    def allreduce_fused(self, rank_tensors, algo: int = _native.ALGO_AUTO, *, scales=None, absent=()) -> list:
+        """In-place fused exchange of ``rank_tensors[r]`` (rank r's layer tensors in bucket
+        order, all fp32 or all bf16) on every rank; returns each rank's ProtocolError or
+        None.  Ranks listed in ``absent`` launch nothing (their peers time out)."""
+        torch = self.torch
+        world = self.n_workers
+        bf16 = rank_tensors[0][0].dtype == torch.bfloat16
+        tables, ns = [], []
+        for r in range(world):
+            rows, off = [], 0
+            for t in rank_tensors[r]:
+                rows.append((t.data_ptr(), t.numel(), off))
+                off += t.numel()
+            tables.append(_native.DeviceTable(rows))
+            ns.append(-1 if r in absent else off)
+        scales = [1.0] * world if scales is None else list(scales)
+        try:
+            self.stream.wait_stream(torch.cuda.current_stream())
+            _native.call("mgw_group_allreduce_fused", (ctypes.c_void_p * world)(*self._comms),
+                         (ctypes.c_void_p * world)(*[t.ptr for t in tables]), (ctypes.c_int64 * world)(*ns),
+                         (ctypes.c_float * world)(*scales), world, int(algo), 2 if bf16 else 4,
+                         self.stream.cuda_stream)
+            self.stream.synchronize()
+        finally:
+            for t in tables:
+                t.close()
+        errors = []
+        for r, sess in enumerate(self.sessions):
+            if r in absent:
+                errors.append(None)
+                continue
             try:
-                import torch
+                sess.raise_if_failed()
+                errors.append(None)
+            except ProtocolError as exc:
+                errors.append(exc)
+        return errors
 
-                torch.cuda.set_device(self.sessions[r].device)
-                results[r] = fn(self.configs[r], self.sessions[r], *args, **kwargs)
-            except BaseException as exc:  # noqa: BLE001 - reported below
-                errors[r] = exc
-
-        threads = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(len(self.sessions))]
-        for t in threads:
-            t.start()
-        for t in threads:
-            t.join()
-        for exc in errors:
-            if exc is not None:
-                raise exc
-        return results
+    def clear_errors(self) -> None:
+        for sess in self.sessions:
+            sess.clear_error()
 
     def close(self) -> None:
         for sess in self.sessions:
@@ -828,6 +850,7 @@ class LocalGroup:
                 t.close()
             sess._tables.clear()
         if self._comms:
+            self.stream.synchronize()
             for c in self._comms:
                 _native.lib().mgw_comm_destroy(c)
             for sess in self.sessions:

@@ -85,11 +85,37 @@ inline uint32_t collective_tag(uint32_t group_tag, int64_t n, uint32_t kind, int
 
 // Phase marks (mgw_probe_phases): CTA 0 records %globaltimer at its phase boundaries into
 // stamp[2 + k] (ncu cannot replay a multi-rank kernel, so the kernels time themselves).
-__device__ __forceinline__ void phase_mark(const ArArgs& a, int k) {
+__device__ __forceinline__ void phase_mark(const ArArgs& a, int k, int cta) {
   if (!(a.flags & kPhaseMarks) || a.stamp == nullptr) return;
   __syncthreads();
-  if (blockIdx.x == 0 && threadIdx.x == 0) a.stamp[2 + k] = global_ns();
+  if (cta == 0 && threadIdx.x == 0) a.stamp[2 + k] = global_ns();
 }
+
+// Kernel bodies take their CTA index `cta` and grid size `ctas` as arguments: the plain
+// kernel passes (blockIdx.x, gridDim.x); the rank-group kernel (one cooperative launch
+// holding every rank's CTAs on one device, tests and single-GPU emulation of the real
+// barrier protocol) passes each rank's own index and count.
+template <class Args>
+struct RankGroup {
+  Args args[kMaxRanks];
+  int first[kMaxRanks + 1];  // CTA range of rank r: [first[r], first[r + 1])
+  __device__ __forceinline__ int rank_of(int block) const {
+    int r = 0;
+    while (block >= first[r + 1]) ++r;
+    return r;
+  }
+};
+
+#define MGW_DEFINE_KERNELS(name, Args)                                                              \
+  template <int N>                                                                                 \
+  __global__ void __launch_bounds__(kThreads, 2) name##_kernel(const __grid_constant__ Args x) {   \
+    name##_body<N>(x, blockIdx.x, gridDim.x);                                                      \
+  }                                                                                                \
+  template <int N>                                                                                 \
+  __global__ void __launch_bounds__(kThreads, 2) name##_group(const __grid_constant__ RankGroup<Args> g) { \
+    const int r = g.rank_of(blockIdx.x);                                                           \
+    name##_body<N>(g.args[r], blockIdx.x - g.first[r], g.first[r + 1] - g.first[r]);               \
+  }
 
 // Loads in flight per thread ~ 8: unroll the slot loop by 8 / N.
 template <int N>
@@ -103,13 +129,13 @@ struct Unroll {
 #define MGW_BARRIER_RELAXED_POLL 0
 #endif
 static __device__ __noinline__ int cta_barrier(uint64_t* const* flags, int parity, uint32_t epoch, uint32_t tag,
-                                        const ArArgs& a) {
+                                               const ArArgs& a, int cta) {
   __shared__ int s_status;
   if (threadIdx.x == 0) s_status = 0;
   __syncthreads();  // also orders this CTA's earlier stores before the release below
   const int t = threadIdx.x;
   if (t < a.world) {
-    const size_t base = ((size_t)parity * kMaxBlocks + blockIdx.x) * kMaxRanks;
+    const size_t base = ((size_t)parity * kMaxBlocks + cta) * kMaxRanks;
     store_release_sys(flags[t] + base + a.rank, ((uint64_t)epoch << 32) | tag);
     const uint64_t* mine = flags[a.rank] + base + t;
     const uint64_t start = global_ns();
@@ -198,13 +224,13 @@ inline int launch_gate(const ArArgs& a, cudaStream_t stream) {
 
 // Last CTA out advances the call counter (epochs and slot parity come from it).
 // Kernel completion publishes the counter to the next kernel on the stream.
-__device__ __forceinline__ void finish_call(const ArArgs& a) {
+__device__ __forceinline__ void finish_call(const ArArgs& a, int ctas) {
   stamp_exit(a.stamp);
   if (a.state == nullptr) return;
   __syncthreads();
   if (threadIdx.x == 0) {
     const uint32_t ticket = atomicAdd(&a.state[1], 1u);
-    if (ticket == gridDim.x - 1) {
+    if (ticket == (uint32_t)ctas - 1) {
       a.state[1] = 0u;
       atomicAdd(&a.state[0], 1u);
     }
@@ -318,7 +344,7 @@ __global__ void __launch_bounds__(kThreads, 2) oneshot_kernel(const __grid_const
   int parity;
   kernel_prologue<N>(a, epoch, parity, s_in, s_end);
   int status = MGW_DEV_OK;
-  if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, a.tag, a);
+  if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, a.tag, a, blockIdx.x);
   if (status == MGW_DEV_OK && a.n > 0) {
     float* out = a.out[a.rank];
     const int64_t nv = a.n >> 2;
@@ -330,7 +356,7 @@ __global__ void __launch_bounds__(kThreads, 2) oneshot_kernel(const __grid_const
       reduce_slots<N, U>(s_in, s_end, seg, v, v1, kThreads, out, nullptr);
     if (blockIdx.x == gridDim.x - 1) reduce_tail<N>(s_in, s_end, nv << 2, a.n, out, nullptr);
   }
-  finish_call(a);
+  finish_call(a, gridDim.x);
 }
 
 // 16-B aligned work parts of the two-shot: rank p owns vectors [part(p), part(p+1));
@@ -357,7 +383,7 @@ __global__ void __launch_bounds__(kThreads, 2) twoshot_kernel(const __grid_const
   int status = MGW_DEV_OK;
 
   if (!(a.flags & kSkipPhase1)) {
-    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, a.tag, a);
+    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, a.tag, a, blockIdx.x);
     if (status == MGW_DEV_OK && a.n > 0) {
       const int64_t p0 = part_begin(me, nv, N), p1 = part_begin(me + 1, nv, N);
       const int64_t per = (p1 - p0 + G - 1) / G;
@@ -371,7 +397,7 @@ __global__ void __launch_bounds__(kThreads, 2) twoshot_kernel(const __grid_const
   }
 
   if (status == MGW_DEV_OK && !(a.flags & kSkipPhase2)) {
-    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.mid, parity, epoch, a.tag, a);
+    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.mid, parity, epoch, a.tag, a, blockIdx.x);
     if (status == MGW_DEV_OK && a.n > 0) {
       // chunk b of every peer part; peers interleaved so N-1 streams are in flight.
       // Chunk bounds live in shared memory to keep the copy loop's registers for data.
@@ -412,7 +438,7 @@ __global__ void __launch_bounds__(kThreads, 2) twoshot_kernel(const __grid_const
         for (int64_t e = (nv << 2) + threadIdx.x; e < a.n; e += blockDim.x) out[e] = __ldcg(s_in[N - 1] + e);
     }
   }
-  finish_call(a);
+  finish_call(a, gridDim.x);
 }
 
 inline int grid_for(int64_t vectors, int64_t per_cta, int max_ctas) {
@@ -432,8 +458,22 @@ inline int grid_for(int64_t vectors, int64_t per_cta, int max_ctas) {
 #ifndef MGW_LOCAL_SPREAD
 #define MGW_LOCAL_SPREAD 1  // CTAs per SM the single-rank (HBM-bound) group kernel spreads over
 #endif
+inline int unroll_of(int world) { return world <= 2 ? 4 : (world <= 4 ? 2 : 1); }  // == Unroll<N>::value
+
+inline int collective_grid_rt(int world, int64_t vectors, int64_t per_cta, int max_ctas) {
+  if (per_cta <= 0) {
+    const int64_t full = (int64_t)kThreads * unroll_of(world);
+    const int64_t spread = (int64_t)kSMs * (world == 1 ? MGW_LOCAL_SPREAD : 1);
+    per_cta = (vectors + spread - 1) / spread;
+    per_cta = (per_cta + 127) / 128 * 128;
+    per_cta = per_cta < 128 ? 128 : (per_cta > full ? full : per_cta);
+  }
+  return grid_for(vectors, per_cta, max_ctas);
+}
+
 template <int N>
 inline int collective_grid(int64_t vectors, int64_t per_cta, int max_ctas) {
+  static_assert(Unroll<N>::value == (N <= 2 ? 4 : (N <= 4 ? 2 : 1)), "unroll_of mirrors Unroll<N>");
   if (per_cta <= 0) {
     const int64_t full = (int64_t)kThreads * Unroll<N>::value;
     const int64_t spread = (int64_t)kSMs * (N == 1 ? MGW_LOCAL_SPREAD : 1);

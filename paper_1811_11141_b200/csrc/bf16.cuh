@@ -272,7 +272,7 @@ __device__ void b16_scatter_parts(const FusedArgs& f, const uint16_t* const* in,
 }
 
 template <int N>
-__global__ void __launch_bounds__(kThreads, 2) b16_oneshot_kernel(const __grid_constant__ FusedArgs f) {
+__device__ __forceinline__ void b16_oneshot_body(const FusedArgs& f, const int cta, const int ctas) {
   constexpr int U = Unroll<N>::value;
   const ArArgs& a = f.ar;
   __shared__ const float* s_in[kMaxRanks];
@@ -282,25 +282,27 @@ __global__ void __launch_bounds__(kThreads, 2) b16_oneshot_kernel(const __grid_c
   kernel_prologue<N>(a, epoch, parity, s_in, s_end);
   const uint16_t* const* in = reinterpret_cast<const uint16_t* const*>(s_in);
   const int64_t nv = a.n / kB16;
-  const int64_t per = (nv + gridDim.x - 1) / gridDim.x;
-  const int64_t v0 = (int64_t)blockIdx.x * per;
+  const int64_t per = (nv + ctas - 1) / ctas;
+  const int64_t v0 = (int64_t)cta * per;
   const int64_t v1 = v0 + per < nv ? v0 + per : nv;
-  const bool last = blockIdx.x == gridDim.x - 1;
+  const bool last = cta == ctas - 1;
   if (!(a.flags & kSkipPack))
     b16_pack_range(f, const_cast<uint16_t*>(in[a.rank]), v0, v1, last ? nv * kB16 : 0, last ? a.n : 0);
   int status = MGW_DEV_OK;
   if (!(a.flags & kSkipPhase1)) {
-    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, a.tag, a);
+    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, a.tag, a, cta);
     if (status == MGW_DEV_OK) {
       b16_reduce_range<N, U>(f, in, s_end, v0, v1, nullptr);
       if (last) b16_reduce_tail<N>(f, in, s_end, nv * kB16, a.n, nullptr);
     }
   }
-  finish_call(a);
+  finish_call(a, ctas);
 }
 
+MGW_DEFINE_KERNELS(b16_oneshot, FusedArgs)
+
 template <int N>
-__global__ void __launch_bounds__(kThreads, 2) b16_twoshot_kernel(const __grid_constant__ FusedArgs f) {
+__device__ __forceinline__ void b16_twoshot_body(const FusedArgs& f, const int cta, const int ctas) {
   constexpr int U = Unroll<N>::value;
   const ArArgs& a = f.ar;
   __shared__ const float* s_in[kMaxRanks];
@@ -310,7 +312,7 @@ __global__ void __launch_bounds__(kThreads, 2) b16_twoshot_kernel(const __grid_c
   kernel_prologue<N>(a, epoch, parity, s_in, s_end);
   const uint16_t* const* in = reinterpret_cast<const uint16_t* const*>(s_in);
   const int me = a.rank;
-  const int b = blockIdx.x, G = gridDim.x;
+  const int b = cta, G = ctas;
   const int64_t nv = a.n / kB16;
   const bool last = b == G - 1;
   const int64_t tail0 = nv * kB16;
@@ -324,21 +326,23 @@ __global__ void __launch_bounds__(kThreads, 2) b16_twoshot_kernel(const __grid_c
   }
   int status = MGW_DEV_OK;
   if (!(a.flags & kSkipPhase1)) {
-    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, a.tag, a);
+    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, a.tag, a, cta);
     if (status == MGW_DEV_OK) {
       b16_reduce_range<N, U>(f, in, s_end, pc.lo[me], pc.lo[me] + pc.len[me], mine);
       if (last && me == N - 1) b16_reduce_tail<N>(f, in, s_end, tail0, a.n, mine);
     }
   }
   if (status == MGW_DEV_OK && !(a.flags & kSkipPhase2)) {
-    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.mid, parity, epoch, a.tag, a);
+    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.mid, parity, epoch, a.tag, a, cta);
     if (status == MGW_DEV_OK) {
       b16_scatter_parts<N>(f, in, me, pc);
       if (last && me != N - 1) b16_scatter_range(f, in[N - 1], 0, 0, tail0, a.n);
     }
   }
-  finish_call(a);
+  finish_call(a, ctas);
 }
+
+MGW_DEFINE_KERNELS(b16_twoshot, FusedArgs)
 
 // LL push one-shot for small bf16 buckets: a word carries (epoch << 32 | two bf16), a
 // 16-B push carries four elements.  Same protocol as ll_oneshot_kernel (ll.cuh): header
@@ -349,7 +353,7 @@ __device__ __forceinline__ uint64_t ll_b16_word(uint32_t epoch, uint16_t lo, uin
 }
 
 template <int N>
-__global__ void __launch_bounds__(kThreads, 2) ll_b16_kernel(const __grid_constant__ LLArgs l) {
+__device__ __forceinline__ void ll_b16_body(const LLArgs& l, const int cta, const int ctas) {
   const FusedArgs& f = l.f;
   const ArArgs& a = f.ar;
   grid_dep_wait();
@@ -367,14 +371,14 @@ __global__ void __launch_bounds__(kThreads, 2) ll_b16_kernel(const __grid_consta
   }
   if (threadIdx.x == 0) s_status = MGW_DEV_OK;
   const bool do_push = !(a.flags & kSkipPack), do_fold = !(a.flags & kSkipPhase1);  // emulation split
-  if (do_push && blockIdx.x == 0 && threadIdx.x < N)
+  if (do_push && cta == 0 && threadIdx.x < N)
     st_relaxed_sys_u64(l.hdr[threadIdx.x] + parity * kMaxRanks + me, ((uint64_t)epoch << 32) | a.tag);
   __syncthreads();
 
   // element quads of this CTA: [q0, q1) (quad j = elements 4j .. 4j+3 = words 2j, 2j+1)
   const int64_t quads = (n + 3) >> 2;
-  const int64_t per = (quads + gridDim.x - 1) / gridDim.x;
-  const int64_t q0 = (int64_t)blockIdx.x * per;
+  const int64_t per = (quads + ctas - 1) / ctas;
+  const int64_t q0 = (int64_t)cta * per;
   const int64_t q1 = q0 + per < quads ? q0 + per : quads;
   const size_t my_off = ((size_t)parity * kMaxRanks + me) * kLLMaxElems;
 
@@ -400,7 +404,7 @@ __global__ void __launch_bounds__(kThreads, 2) ll_b16_kernel(const __grid_consta
 
   // 2. CTA 0 checks every peer's header (length and dtype agreement)
   int status = MGW_DEV_OK;
-  if (do_fold && blockIdx.x == 0 && threadIdx.x < N) {
+  if (do_fold && cta == 0 && threadIdx.x < N) {
     const uint64_t* p = l.hdr[me] + parity * kMaxRanks + threadIdx.x;
     uint64_t v = ld_relaxed_sys_u64(p);
     const uint64_t start = global_ns();
@@ -475,7 +479,9 @@ __global__ void __launch_bounds__(kThreads, 2) ll_b16_kernel(const __grid_consta
         for (int r = 0; r < N; ++r) store_release_sys32(a.abort_flag[r], 1u);
     }
   }
-  finish_call(a);
+  finish_call(a, ctas);
 }
+
+MGW_DEFINE_KERNELS(ll_b16, LLArgs)
 
 }  // namespace mgw

@@ -216,7 +216,7 @@ static __device__ void fused_scatter_range(const FusedArgs& f, const float* src,
 }
 
 template <int N>
-__global__ void __launch_bounds__(kThreads, 2) fused_oneshot_kernel(const __grid_constant__ FusedArgs f) {
+__device__ __forceinline__ void fused_oneshot_body(const FusedArgs& f, const int cta, const int ctas) {
   constexpr int U = Unroll<N>::value;
   const ArArgs& a = f.ar;
   __shared__ const float* s_in[kMaxRanks];
@@ -225,24 +225,26 @@ __global__ void __launch_bounds__(kThreads, 2) fused_oneshot_kernel(const __grid
   int parity;
   kernel_prologue<N>(a, epoch, parity, s_in, s_end);
   const int64_t nv = a.n >> 2;
-  const int64_t per = (nv + gridDim.x - 1) / gridDim.x;
-  const int64_t v0 = (int64_t)blockIdx.x * per;
+  const int64_t per = (nv + ctas - 1) / ctas;
+  const int64_t v0 = (int64_t)cta * per;
   const int64_t v1 = v0 + per < nv ? v0 + per : nv;
-  const bool last = blockIdx.x == gridDim.x - 1;
+  const bool last = cta == ctas - 1;
   float* mine = const_cast<float*>(s_in[a.rank]);
-  phase_mark(a, 0);
+  phase_mark(a, 0, cta);
   if (!(a.flags & kSkipPack)) fused_pack_range(f, mine, v0, v1, last ? nv << 2 : 0, last ? a.n : 0);
-  phase_mark(a, 1);
+  phase_mark(a, 1, cta);
   int status = MGW_DEV_OK;
-  if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, a.tag, a);
-  phase_mark(a, 2);
+  if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, a.tag, a, cta);
+  phase_mark(a, 2, cta);
   if (status == MGW_DEV_OK && !(a.flags & kSkipPhase1)) {
     fused_reduce_range<N, U>(f, s_in, s_end, v0, v1, nullptr);
     if (last) fused_reduce_tail<N>(f, s_in, s_end, nv << 2, a.n, nullptr);
   }
-  phase_mark(a, 3);
-  finish_call(a);
+  phase_mark(a, 3, cta);
+  finish_call(a, ctas);
 }
+
+MGW_DEFINE_KERNELS(fused_oneshot, FusedArgs)
 
 // Interleaved walk over chunk b of several parts: slot i of every part is handled in the
 // same loop trip, so the parts' memory streams are in flight together (one round trip
@@ -334,7 +336,7 @@ __device__ void fused_scatter_parts(const FusedArgs& f, const float* const* in, 
 }
 
 template <int N>
-__global__ void __launch_bounds__(kThreads, 2) fused_twoshot_kernel(const __grid_constant__ FusedArgs f) {
+__device__ __forceinline__ void fused_twoshot_body(const FusedArgs& f, const int cta, const int ctas) {
   constexpr int U = Unroll<N>::value;
   const ArArgs& a = f.ar;
   __shared__ const float* s_in[kMaxRanks];
@@ -343,7 +345,7 @@ __global__ void __launch_bounds__(kThreads, 2) fused_twoshot_kernel(const __grid
   int parity;
   kernel_prologue<N>(a, epoch, parity, s_in, s_end);
   const int me = a.rank;
-  const int b = blockIdx.x, G = gridDim.x;
+  const int b = cta, G = ctas;
   const int64_t nv = a.n >> 2;
   const bool last = b == G - 1;
   const int64_t tail0 = nv << 2;
@@ -351,32 +353,34 @@ __global__ void __launch_bounds__(kThreads, 2) fused_twoshot_kernel(const __grid
   __shared__ PartChunks<N> pc;  // CTA-uniform: keep it out of the registers
   if (threadIdx.x == 0) part_chunks<N>(nv, b, G, pc);
   __syncthreads();
-  phase_mark(a, 0);
+  phase_mark(a, 0, cta);
   if (!(a.flags & kSkipPack)) {
     fused_pack_parts<N>(f, mine, pc);
     if (last) fused_pack_range(f, mine, 0, 0, tail0, a.n);  // the n % 4 tail (part N-1)
   }
-  phase_mark(a, 1);
+  phase_mark(a, 1, cta);
   int status = MGW_DEV_OK;
   if (!(a.flags & kSkipPhase1)) {
-    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, a.tag, a);
-    phase_mark(a, 2);
+    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, a.tag, a, cta);
+    phase_mark(a, 2, cta);
     if (status == MGW_DEV_OK) {
       fused_reduce_range<N, U>(f, s_in, s_end, pc.lo[me], pc.lo[me] + pc.len[me], mine);
       if (last && me == N - 1) fused_reduce_tail<N>(f, s_in, s_end, tail0, a.n, mine);
     }
-    phase_mark(a, 3);
+    phase_mark(a, 3, cta);
   }
   if (status == MGW_DEV_OK && !(a.flags & kSkipPhase2)) {
-    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.mid, parity, epoch, a.tag, a);
-    phase_mark(a, 4);
+    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.mid, parity, epoch, a.tag, a, cta);
+    phase_mark(a, 4, cta);
     if (status == MGW_DEV_OK) {
       fused_scatter_parts<N>(f, s_in, me, pc);
       if (last && me != N - 1) fused_scatter_range(f, s_in[N - 1], 0, 0, tail0, a.n);
     }
-    phase_mark(a, 5);
+    phase_mark(a, 5, cta);
   }
-  finish_call(a);
+  finish_call(a, ctas);
 }
+
+MGW_DEFINE_KERNELS(fused_twoshot, FusedArgs)
 
 }  // namespace mgw

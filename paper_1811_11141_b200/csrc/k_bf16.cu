@@ -5,13 +5,18 @@
 
 namespace mgw {
 
-int launch_ll_b16(const LLArgs& l0, int max_ctas, cudaStream_t stream) {
-  LLArgs l = l0;
-  if (l.f.ar.n > 2 * kLLMaxElems)
-    return set_error(MGW_EINVAL, "bf16 LL path takes at most %lld elements", (long long)(2 * kLLMaxElems));
+int plan_ll_b16(LLArgs& l, int max_ctas) {
   const int64_t quads = (l.f.ar.n + 3) >> 2;
   const int grid = grid_for(quads, kThreads, max_ctas < kSMs ? max_ctas : kSMs);
-  l.f.ar.tag = collective_tag(l0.f.ar.tag, l0.f.ar.n, kTagB16LL, grid, l0.f.scale);
+  l.f.ar.tag = collective_tag(l.f.ar.tag, l.f.ar.n, kTagB16LL, grid, l.f.scale);
+  return grid;
+}
+
+int launch_ll_b16(const LLArgs& l0, int max_ctas, cudaStream_t stream) {
+  if (l0.f.ar.n > 2 * kLLMaxElems)
+    return set_error(MGW_EINVAL, "bf16 LL path takes at most %lld elements", (long long)(2 * kLLMaxElems));
+  LLArgs l = l0;
+  const int grid = plan_ll_b16(l, max_ctas);
   switch (l.f.ar.world) {
     case 2: ll_b16_kernel<2><<<grid, kThreads, 0, stream>>>(l); break;
     case 3: ll_b16_kernel<3><<<grid, kThreads, 0, stream>>>(l); break;
@@ -26,37 +31,73 @@ int launch_ll_b16(const LLArgs& l0, int max_ctas, cudaStream_t stream) {
   return MGW_OK;
 }
 
+int plan_b16(FusedArgs& f, int algo, int max_ctas) {
+  max_ctas = max_ctas < kMaxBlocks ? max_ctas : kMaxBlocks;
+  const int w = f.ar.world > 0 ? f.ar.world : 1;
+  const int64_t nv = f.ar.n / kB16;
+  const bool one = algo == MGW_ALGO_ONESHOT;
+  const int grid = one ? collective_grid_rt(w, nv, 0, max_ctas) : collective_grid_rt(w, nv / w, 0, max_ctas);
+  f.ar.tag = collective_tag(f.ar.tag, f.ar.n, one ? kTagB16Oneshot : kTagB16Twoshot, grid, f.scale);
+  return grid;
+}
+
 template <int N>
-int launch_b16_n(const FusedArgs& f0, int algo, int max_ctas, cudaStream_t stream) {
-  const int64_t nv = f0.ar.n / kB16;
-  FusedArgs f = f0;
-  if (algo == MGW_ALGO_ONESHOT) {
-    const int grid = collective_grid<N>(nv, 0, max_ctas);
-    f.ar.tag = collective_tag(f0.ar.tag, f0.ar.n, kTagB16Oneshot, grid, f0.scale);
+static int launch_b16_n(const FusedArgs& f, int algo, int grid, cudaStream_t stream) {
+  if (algo == MGW_ALGO_ONESHOT)
     b16_oneshot_kernel<N><<<grid, kThreads, 0, stream>>>(f);
-  } else {
-    const int grid = collective_grid<N>(nv / N, 0, max_ctas);
-    f.ar.tag = collective_tag(f0.ar.tag, f0.ar.n, kTagB16Twoshot, grid, f0.scale);
+  else
     b16_twoshot_kernel<N><<<grid, kThreads, 0, stream>>>(f);
-  }
   MGW_CHECK_LAUNCH();
   return MGW_OK;
 }
 
-int launch_b16(const FusedArgs& f, int algo, int max_ctas, cudaStream_t stream) {
+int launch_b16(const FusedArgs& f0, int algo, int max_ctas, cudaStream_t stream) {
   if (algo != MGW_ALGO_ONESHOT && algo != MGW_ALGO_TWOSHOT)
     return set_error(MGW_EINVAL, "bf16 buckets support one-shot and two-shot only (algorithm %d)", algo);
-  max_ctas = max_ctas < kMaxBlocks ? max_ctas : kMaxBlocks;
+  FusedArgs f = f0;
+  const int grid = plan_b16(f, algo, max_ctas);
   switch (f.ar.world) {
-    case 1: return launch_b16_n<1>(f, algo, max_ctas, stream);
-    case 2: return launch_b16_n<2>(f, algo, max_ctas, stream);
-    case 3: return launch_b16_n<3>(f, algo, max_ctas, stream);
-    case 4: return launch_b16_n<4>(f, algo, max_ctas, stream);
-    case 5: return launch_b16_n<5>(f, algo, max_ctas, stream);
-    case 6: return launch_b16_n<6>(f, algo, max_ctas, stream);
-    case 7: return launch_b16_n<7>(f, algo, max_ctas, stream);
-    case 8: return launch_b16_n<8>(f, algo, max_ctas, stream);
+    case 1: return launch_b16_n<1>(f, algo, grid, stream);
+    case 2: return launch_b16_n<2>(f, algo, grid, stream);
+    case 3: return launch_b16_n<3>(f, algo, grid, stream);
+    case 4: return launch_b16_n<4>(f, algo, grid, stream);
+    case 5: return launch_b16_n<5>(f, algo, grid, stream);
+    case 6: return launch_b16_n<6>(f, algo, grid, stream);
+    case 7: return launch_b16_n<7>(f, algo, grid, stream);
+    case 8: return launch_b16_n<8>(f, algo, grid, stream);
     default: return set_error(MGW_EINVAL, "world %d outside 1..%d", f.ar.world, kMaxRanks);
+  }
+}
+
+template <int N>
+static int group_b16_n(const RankGroup<FusedArgs>& g, int algo, cudaStream_t stream) {
+  return algo == MGW_ALGO_ONESHOT ? launch_cooperative(b16_oneshot_group<N>, g, stream)
+                                  : launch_cooperative(b16_twoshot_group<N>, g, stream);
+}
+
+int launch_b16_group(const RankGroup<FusedArgs>& g, int world, int algo, cudaStream_t stream) {
+  switch (world) {
+    case 2: return group_b16_n<2>(g, algo, stream);
+    case 3: return group_b16_n<3>(g, algo, stream);
+    case 4: return group_b16_n<4>(g, algo, stream);
+    case 5: return group_b16_n<5>(g, algo, stream);
+    case 6: return group_b16_n<6>(g, algo, stream);
+    case 7: return group_b16_n<7>(g, algo, stream);
+    case 8: return group_b16_n<8>(g, algo, stream);
+    default: return set_error(MGW_EINVAL, "rank group of %d outside 2..%d", world, kMaxRanks);
+  }
+}
+
+int launch_ll_b16_group(const RankGroup<LLArgs>& g, int world, cudaStream_t stream) {
+  switch (world) {
+    case 2: return launch_cooperative(ll_b16_group<2>, g, stream);
+    case 3: return launch_cooperative(ll_b16_group<3>, g, stream);
+    case 4: return launch_cooperative(ll_b16_group<4>, g, stream);
+    case 5: return launch_cooperative(ll_b16_group<5>, g, stream);
+    case 6: return launch_cooperative(ll_b16_group<6>, g, stream);
+    case 7: return launch_cooperative(ll_b16_group<7>, g, stream);
+    case 8: return launch_cooperative(ll_b16_group<8>, g, stream);
+    default: return set_error(MGW_EINVAL, "rank group of %d outside 2..%d", world, kMaxRanks);
   }
 }
 

@@ -5,58 +5,82 @@
 
 namespace mgw {
 
-template <int N>
-int launch_push1_n(const PushArgs& x0, int max_ctas, cudaStream_t stream, const int64_t* per_cta) {
-  PushArgs x = x0;
-  const int grid = collective_grid<N>(x0.f.ar.n >> 2, per_cta ? per_cta[0] : 0, max_ctas);
-  x.f.ar.tag = collective_tag(x0.f.ar.tag, x0.f.ar.n, kTagPushOneshot, grid, x0.f.scale);
-  push_oneshot_kernel<N><<<grid, kThreads, 0, stream>>>(x);
-  MGW_CHECK_LAUNCH();
-  return MGW_OK;
+int plan_push1(PushArgs& x, int max_ctas, const int64_t* per_cta) {
+  max_ctas = max_ctas < kMaxBlocks ? max_ctas : kMaxBlocks;
+  const int grid = collective_grid_rt(x.f.ar.world, x.f.ar.n >> 2, per_cta ? per_cta[0] : 0, max_ctas);
+  x.f.ar.tag = collective_tag(x.f.ar.tag, x.f.ar.n, kTagPushOneshot, grid, x.f.scale);
+  return grid;
 }
 
-int launch_push1(const PushArgs& x, int max_ctas, cudaStream_t stream, const int64_t* per_cta) {
+int plan_push(PushArgs& x, int max_ctas, const int64_t* per_cta) {
   max_ctas = max_ctas < kMaxBlocks ? max_ctas : kMaxBlocks;
-  switch (x.f.ar.world) {
-    case 2: return launch_push1_n<2>(x, max_ctas, stream, per_cta);
-    case 3: return launch_push1_n<3>(x, max_ctas, stream, per_cta);
-    case 4: return launch_push1_n<4>(x, max_ctas, stream, per_cta);
-    case 5: return launch_push1_n<5>(x, max_ctas, stream, per_cta);
-    case 6: return launch_push1_n<6>(x, max_ctas, stream, per_cta);
-    case 7: return launch_push1_n<7>(x, max_ctas, stream, per_cta);
-    case 8: return launch_push1_n<8>(x, max_ctas, stream, per_cta);
-    default: return set_error(MGW_EINVAL, "push one-shot needs 2..%d ranks, got %d", kMaxRanks, x.f.ar.world);
-  }
-}
-
-int launch_push(const PushArgs& x0, int max_ctas, cudaStream_t stream, const int64_t* per_cta) {
-  max_ctas = max_ctas < kMaxBlocks ? max_ctas : kMaxBlocks;
-  PushArgs x = x0;
+  const int w = x.f.ar.world > 0 ? x.f.ar.world : 1;
   const int64_t nv = x.f.ar.n >> 2;
   int64_t per = per_cta ? per_cta[1] : 0;
   if (per <= 0) {
     // large buckets stream better in long per-CTA chunks: 2048-4096 slots (32-64 KB per
     // part) per CTA, spread over one CTA per SM (profiles/grid_pushtune_n4_r01.json:
     // 32 MB 105 -> 98 us, 64 MB 195 -> 180 us at N = 4)
-    const int64_t part = nv / (x.f.ar.world > 0 ? x.f.ar.world : 1);
-    per = (part + kSMs - 1) / kSMs;
+    per = (nv / w + kSMs - 1) / kSMs;
     per = (per + 127) / 128 * 128;
     per = per < 2048 ? 2048 : (per > 4096 ? 4096 : per);
   }
-  const int grid = grid_for(nv / (x0.f.ar.world > 0 ? x0.f.ar.world : 1), per, max_ctas);
-  x.f.ar.tag = collective_tag(x0.f.ar.tag, x0.f.ar.n, kTagPush, grid, x0.f.scale);
-  switch (x.f.ar.world) {
-    case 2: push_twoshot_kernel<2><<<grid, kThreads, 0, stream>>>(x); break;
-    case 3: push_twoshot_kernel<3><<<grid, kThreads, 0, stream>>>(x); break;
-    case 4: push_twoshot_kernel<4><<<grid, kThreads, 0, stream>>>(x); break;
-    case 5: push_twoshot_kernel<5><<<grid, kThreads, 0, stream>>>(x); break;
-    case 6: push_twoshot_kernel<6><<<grid, kThreads, 0, stream>>>(x); break;
-    case 7: push_twoshot_kernel<7><<<grid, kThreads, 0, stream>>>(x); break;
-    case 8: push_twoshot_kernel<8><<<grid, kThreads, 0, stream>>>(x); break;
-    default: return set_error(MGW_EINVAL, "push two-shot needs 2..%d ranks, got %d", kMaxRanks, x.f.ar.world);
-  }
+  const int grid = grid_for(nv / w, per, max_ctas);
+  x.f.ar.tag = collective_tag(x.f.ar.tag, x.f.ar.n, kTagPush, grid, x.f.scale);
+  return grid;
+}
+
+template <int N>
+static int launch_push_n(const PushArgs& x, bool one, int grid, cudaStream_t stream) {
+  if (one)
+    push_oneshot_kernel<N><<<grid, kThreads, 0, stream>>>(x);
+  else
+    push_twoshot_kernel<N><<<grid, kThreads, 0, stream>>>(x);
   MGW_CHECK_LAUNCH();
   return MGW_OK;
+}
+
+static int launch_push_any(const PushArgs& x0, bool one, int max_ctas, cudaStream_t stream, const int64_t* per_cta) {
+  PushArgs x = x0;
+  const int grid = one ? plan_push1(x, max_ctas, per_cta) : plan_push(x, max_ctas, per_cta);
+  switch (x.f.ar.world) {
+    case 2: return launch_push_n<2>(x, one, grid, stream);
+    case 3: return launch_push_n<3>(x, one, grid, stream);
+    case 4: return launch_push_n<4>(x, one, grid, stream);
+    case 5: return launch_push_n<5>(x, one, grid, stream);
+    case 6: return launch_push_n<6>(x, one, grid, stream);
+    case 7: return launch_push_n<7>(x, one, grid, stream);
+    case 8: return launch_push_n<8>(x, one, grid, stream);
+    default:
+      return set_error(MGW_EINVAL, "push %s needs 2..%d ranks, got %d", one ? "one-shot" : "two-shot", kMaxRanks,
+                       x.f.ar.world);
+  }
+}
+
+int launch_push1(const PushArgs& x, int max_ctas, cudaStream_t stream, const int64_t* per_cta) {
+  return launch_push_any(x, true, max_ctas, stream, per_cta);
+}
+
+int launch_push(const PushArgs& x, int max_ctas, cudaStream_t stream, const int64_t* per_cta) {
+  return launch_push_any(x, false, max_ctas, stream, per_cta);
+}
+
+template <int N>
+static int group_push_n(const RankGroup<PushArgs>& g, bool one, cudaStream_t stream) {
+  return one ? launch_cooperative(push_oneshot_group<N>, g, stream) : launch_cooperative(push_twoshot_group<N>, g, stream);
+}
+
+int launch_push_group(const RankGroup<PushArgs>& g, int world, bool one, cudaStream_t stream) {
+  switch (world) {
+    case 2: return group_push_n<2>(g, one, stream);
+    case 3: return group_push_n<3>(g, one, stream);
+    case 4: return group_push_n<4>(g, one, stream);
+    case 5: return group_push_n<5>(g, one, stream);
+    case 6: return group_push_n<6>(g, one, stream);
+    case 7: return group_push_n<7>(g, one, stream);
+    case 8: return group_push_n<8>(g, one, stream);
+    default: return set_error(MGW_EINVAL, "rank group of %d outside 2..%d", world, kMaxRanks);
+  }
 }
 
 }  // namespace mgw

@@ -21,6 +21,42 @@ int launch_ll_b16(const LLArgs& l, int max_ctas, cudaStream_t stream);
 int launch_b16(const FusedArgs& f, int algo, int max_ctas, cudaStream_t stream);
 int launch_nvls(const NvlsArgs& x, int max_ctas, cudaStream_t stream, const int64_t* per_cta);
 
+// plan_*: the grid a launch uses for these arguments and settings; stamps the collective
+// tag into the arguments (the plain launchers above plan, then launch).
+int plan_fused(FusedArgs& f, int algo, int max_ctas, const int64_t* per_cta);
+int plan_push(PushArgs& x, int max_ctas, const int64_t* per_cta);
+int plan_push1(PushArgs& x, int max_ctas, const int64_t* per_cta);
+int plan_ll(LLArgs& l, int max_ctas);
+int plan_ll_b16(LLArgs& l, int max_ctas);
+int plan_b16(FusedArgs& f, int algo, int max_ctas);
+
+// Rank-group launches: every rank's planned CTAs in ONE cooperative launch on one device
+// (co-residency guaranteed, so ranks that wait on one another always run together).
+int launch_fused_group(const RankGroup<FusedArgs>& g, int world, int algo, cudaStream_t stream);
+int launch_push_group(const RankGroup<PushArgs>& g, int world, bool one, cudaStream_t stream);
+int launch_ll_group(const RankGroup<LLArgs>& g, int world, cudaStream_t stream);
+int launch_b16_group(const RankGroup<FusedArgs>& g, int world, int algo, cudaStream_t stream);
+int launch_ll_b16_group(const RankGroup<LLArgs>& g, int world, cudaStream_t stream);
+
+template <class Args>
+inline int launch_cooperative(void (*kernel)(const RankGroup<Args>), const RankGroup<Args>& g, cudaStream_t stream) {
+  const int blocks = g.first[kMaxRanks];
+  if (blocks <= 0) return MGW_OK;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(kThreads);
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, g);
+  if (e != cudaSuccess)
+    return set_error(MGW_ECUDA, "cooperative rank-group launch of %d CTAs: %s", blocks, cudaGetErrorString(e));
+  return MGW_OK;
+}
+
 template <RowOp kOp>
 int launch_rows(const Row* host_rows, const Row* dev_rows, int n_rows, float* bucket, int64_t total, float scale,
                 const float* values, const uint32_t* calls, int64_t slot_stride_elems,

@@ -77,7 +77,7 @@ __device__ __forceinline__ float* ll_tensor(const FusedArgs& f, int& k, int64_t 
 }
 
 template <int N>
-__global__ void __launch_bounds__(kThreads, 2) ll_oneshot_kernel(const __grid_constant__ LLArgs l) {
+__device__ __forceinline__ void ll_oneshot_body(const LLArgs& l, const int cta, const int ctas) {
   const FusedArgs& f = l.f;
   const ArArgs& a = f.ar;
   grid_dep_wait();
@@ -97,19 +97,19 @@ __global__ void __launch_bounds__(kThreads, 2) ll_oneshot_kernel(const __grid_co
   // header: (epoch, n) to every rank (CTA 0).  kSkipPack / kSkipPhase1 split the push
   // and the fold into separate launches (emulated ranks on one device, tests only).
   const bool do_push = !(a.flags & kSkipPack), do_fold = !(a.flags & kSkipPhase1);
-  if (do_push && blockIdx.x == 0 && threadIdx.x < N)
+  if (do_push && cta == 0 && threadIdx.x < N)
     st_relaxed_sys_u64(l.hdr[threadIdx.x] + parity * kMaxRanks + me, ((uint64_t)epoch << 32) | a.tag);
   __syncthreads();
 
   // element pairs of this CTA: [p0, p1) (pair j = elements 2j, 2j+1)
   const int64_t pairs = (n + 1) >> 1;
-  const int64_t per = (pairs + gridDim.x - 1) / gridDim.x;
-  const int64_t p0 = (int64_t)blockIdx.x * per;
+  const int64_t per = (pairs + ctas - 1) / ctas;
+  const int64_t p0 = (int64_t)cta * per;
   const int64_t p1 = p0 + per < pairs ? p0 + per : pairs;
   const float scale = f.scale;
   const size_t my_off = ((size_t)parity * kMaxRanks + me) * kLLMaxElems;
 
-  phase_mark(a, 0);
+  phase_mark(a, 0, cta);
   // 1. pack and push: my two elements of each pair to every rank's LL area
   int k = 0;
   if (p0 < p1) k = fused_row_covering(f, (p0 + threadIdx.x) * 2 < n ? (p0 + threadIdx.x) * 2 : 0);
@@ -126,10 +126,10 @@ __global__ void __launch_bounds__(kThreads, 2) ll_oneshot_kernel(const __grid_co
     for (int r = 0; r < N; ++r) st_relaxed_sys_v2(l.ll[r] + my_off + e, w0, w1);
   }
 
-  phase_mark(a, 1);
+  phase_mark(a, 1, cta);
   // 2. CTA 0 checks every peer's header (length agreement)
   int status = MGW_DEV_OK;
-  if (do_fold && blockIdx.x == 0 && threadIdx.x < N) {
+  if (do_fold && cta == 0 && threadIdx.x < N) {
     const uint64_t h = [&] {
       const uint64_t* p = l.hdr[me] + parity * kMaxRanks + threadIdx.x;
       uint64_t v = ld_relaxed_sys_u64(p);
@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(kThreads, 2) ll_oneshot_kernel(const __grid_co
       for (int r = 0; r < N; ++r) store_release_sys32(a.abort_flag[r], 1u);
   }
   status = s_status;
-  phase_mark(a, 2);
+  phase_mark(a, 2, cta);
 
   // 3. fold every element of my pairs from the N local LL areas, write the tensors.
   //    The N sources' words of a pair are fetched as N independent 16-B loads issued
@@ -207,8 +207,10 @@ __global__ void __launch_bounds__(kThreads, 2) ll_oneshot_kernel(const __grid_co
         for (int r = 0; r < N; ++r) store_release_sys32(a.abort_flag[r], 1u);
     }
   }
-  phase_mark(a, 3);
-  finish_call(a);
+  phase_mark(a, 3, cta);
+  finish_call(a, ctas);
 }
+
+MGW_DEFINE_KERNELS(ll_oneshot, LLArgs)
 
 }  // namespace mgw

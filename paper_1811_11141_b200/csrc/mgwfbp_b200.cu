@@ -22,6 +22,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -712,6 +713,97 @@ int mgw_comm_clear_error(mgw_comm* c) {
   const uint32_t zero = 0;
   MGW_CUDA(cudaMemcpy(c->err, &zero, sizeof(zero), cudaMemcpyHostToDevice));
   MGW_CUDA(cudaMemcpy(c->region + kAbortOff, &zero, sizeof(zero), cudaMemcpyHostToDevice));
+  return MGW_OK;
+}
+
+// Every rank of an in-process group (mgw_comm_create_local) runs its fused group exchange
+// in ONE cooperative launch: each rank's arguments, algorithm, grid and tag come from its
+// own communicator exactly as mgw_allreduce_fused[_bf16] would build them, so the real
+// barrier / LL / push protocol (and any disagreement between the ranks) plays out between
+// co-resident CTAs.  n_elem[r] < 0: rank r is absent (launches no CTAs).
+int mgw_group_allreduce_fused(mgw_comm* const* comms, void* const* tables, const int64_t* n_elem, const float* scale,
+                              int world, int algo, int element_bytes, void* stream) {
+  if (!comms || !tables || !n_elem || !scale || world < 2 || world > kMaxRanks)
+    return set_error(MGW_EINVAL, "bad rank-group arguments");
+  if (element_bytes != 4 && element_bytes != 2) return set_error(MGW_EINVAL, "element_bytes must be 4 or 2");
+  const bool b16 = element_bytes == 2;
+  int chosen = -1;
+  for (int r = 0; r < world; ++r) {
+    const mgw_comm* c = comms[r];
+    if (!c || !c->local_group || c->rank != r || c->world != world)
+      return set_error(MGW_EINVAL, "rank %d: not rank %d of an in-process group of %d", r, r, world);
+    if (n_elem[r] < 0) continue;
+    if (n_elem[r] == 0 || (int64_t)n_elem[r] * element_bytes > c->slot_bytes)
+      return set_error(MGW_EINVAL, "rank %d: bucket of %lld elements outside (0, slot]", r, (long long)n_elem[r]);
+    const mgw_table_t* t = as_table(tables[r]);
+    if (int rc = check_table(tables[r], t ? (int)t->host.size() : 0, n_elem[r])) return rc;
+    const int a = b16 ? resolve_b16_algo(c, n_elem[r], algo) : resolve_fused_algo(c, n_elem[r], algo);
+    if (chosen >= 0 && a != chosen)
+      return set_error(MGW_EINVAL, "a rank-group launch runs one kernel: ranks resolved algorithms %d and %d", chosen, a);
+    chosen = a;
+  }
+  if (chosen < 0) return MGW_OK;
+  if (chosen == MGW_ALGO_NVLS) return set_error(MGW_EINVAL, "NVLS has no rank-group launch");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const bool ll = chosen == MGW_ALGO_LL, push = chosen == MGW_ALGO_PUSH || chosen == MGW_ALGO_PUSH_ONESHOT;
+  // the argument blocks are large (8 ranks x ~1.5 KB): build them on the heap
+  std::unique_ptr<RankGroup<FusedArgs>> gf(new RankGroup<FusedArgs>());
+  std::unique_ptr<RankGroup<PushArgs>> gp(new RankGroup<PushArgs>());
+  std::unique_ptr<RankGroup<LLArgs>> gl(new RankGroup<LLArgs>());
+  memset(gf.get(), 0, sizeof(*gf));
+  memset(gp.get(), 0, sizeof(*gp));
+  memset(gl.get(), 0, sizeof(*gl));
+  int first = 0;
+  for (int r = 0; r < world; ++r) {
+    gf->first[r] = gp->first[r] = gl->first[r] = first;
+    if (n_elem[r] < 0) continue;
+    const mgw_comm* c = comms[r];
+    const mgw_table_t* t = as_table(tables[r]);
+    const int64_t n = n_elem[r];
+    FusedArgs f;
+    memset(&f, 0, sizeof(f));
+    f.ar = make_args(c, n);
+    const int n_rows = (int)t->host.size();
+    f.use_inline = n_rows <= kInlineRows;
+    if (f.use_inline)
+      for (int k = 0; k < n_rows; ++k) f.inline_rows[k] = t->host[k];
+    f.rows = t->dev;
+    f.n_rows = n_rows;
+    f.scale = scale[r];
+    int grid = 0;
+    if (ll) {
+      LLArgs& l = gl->args[r];
+      l.f = f;
+      for (int q = 0; q < world; ++q) {
+        l.ll[q] = reinterpret_cast<uint64_t*>(c->peer[q] + kLLOff);
+        l.hdr[q] = reinterpret_cast<uint64_t*>(c->peer[q] + kHdrOff);
+      }
+      if (n > (b16 ? 2 : 1) * kLLElems) return set_error(MGW_EINVAL, "LL bucket of %lld elements too large", (long long)n);
+      grid = b16 ? plan_ll_b16(l, c->max_ctas) : plan_ll(l, c->max_ctas);
+    } else if (push) {
+      const bool one = chosen == MGW_ALGO_PUSH_ONESHOT;
+      PushArgs& x = gp->args[r];
+      x.f = f;
+      x.stride = one ? round_up(n, 16) : ((n / 4 + world - 1) / world + 1) * 4;
+      for (int q = 0; q < world; ++q) x.gather[q] = c->peer[q] + kSlotOff + 2 * c->slot_bytes;
+      grid = one ? plan_push1(x, c->max_ctas, c->vec_per_cta) : plan_push(x, c->max_ctas, c->vec_per_cta);
+    } else {
+      gf->args[r] = f;
+      grid = b16 ? plan_b16(gf->args[r], chosen, c->max_ctas) : plan_fused(gf->args[r], chosen, c->max_ctas, c->vec_per_cta);
+    }
+    first += grid;
+  }
+  for (int r = world; r <= kMaxRanks; ++r) gf->first[r] = gp->first[r] = gl->first[r] = first;
+  if (first > 2 * kSMs)
+    return set_error(MGW_EINVAL, "rank group needs %d co-resident CTAs (> %d): lower the CTA caps", first, 2 * kSMs);
+  if (ll) return b16 ? launch_ll_b16_group(*gl, world, s) : launch_ll_group(*gl, world, s);
+  if (push) return launch_push_group(*gp, world, chosen == MGW_ALGO_PUSH_ONESHOT, s);
+  return b16 ? launch_b16_group(*gf, world, chosen, s) : launch_fused_group(*gf, world, chosen, s);
+}
+
+int mgw_debug_collective_tag(uint32_t group_tag, int64_t n_elem, int kind, int grid, float scale, uint32_t* out) {
+  if (!out) return set_error(MGW_EINVAL, "out is null");
+  *out = collective_tag(group_tag, n_elem, (uint32_t)kind, grid, scale);
   return MGW_OK;
 }
 

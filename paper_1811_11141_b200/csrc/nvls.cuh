@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(kThreads, 2) nvls_kernel(const __grid_constant
   // 1. pack chunk b of every part into my unicast copy
   fused_pack_parts<N>(f, x.uc, pc);
   if (last) fused_pack_range(f, x.uc, 0, 0, tail0, a.n);
-  int status = cta_barrier(a.arrive, parity, epoch, a.tag, a);
+  int status = cta_barrier(a.arrive, parity, epoch, a.tag, a, blockIdx.x);
   if (status == MGW_DEV_OK) {
     // 2. reduce my part's chunk b in the switch and broadcast it to every copy
     constexpr int U = 4;
@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(kThreads, 2) nvls_kernel(const __grid_constant
     if (last && me == N - 1)
       for (int64_t e = tail0 + threadIdx.x; e < a.n; e += kThreads) multimem_st1(x.mc + e, multimem_ld_reduce_add1(x.mc + e));
     __threadfence_system();
-    status = cta_barrier(a.mid, parity, epoch, a.tag, a);
+    status = cta_barrier(a.mid, parity, epoch, a.tag, a, blockIdx.x);
   }
   if (status == MGW_DEV_OK) {
     // 3. unpack chunk b of every part (now reduced in my copy) into the tensors
@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(kThreads, 2) nvls_kernel(const __grid_constant
     for (int p = 0; p < N; ++p) fused_scatter_range(f, uc, pc.lo[p], pc.lo[p] + pc.len[p], 0, 0);
     if (last) fused_scatter_range(f, uc, 0, 0, tail0, a.n);
   }
-  finish_call(a);
+  finish_call(a, gridDim.x);
 }
 
 }  // namespace mgw

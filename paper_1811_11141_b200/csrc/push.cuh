@@ -37,7 +37,7 @@ __device__ __forceinline__ int64_t push_stride(int64_t nv, int world) {
 }
 
 template <int N>
-__global__ void __launch_bounds__(kThreads, 2) push_twoshot_kernel(const __grid_constant__ PushArgs x) {
+__device__ __forceinline__ void push_twoshot_body(const PushArgs& x, const int cta, const int ctas) {
   const FusedArgs& f = x.f;
   const ArArgs& a = f.ar;
   __shared__ const float* s_in[kMaxRanks];  // incoming area of every rank (this parity)
@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(kThreads, 2) push_twoshot_kernel(const __grid_
   kernel_prologue<N>(a, epoch, parity, s_in, s_end);
   if (threadIdx.x < N) s_gat[threadIdx.x] = reinterpret_cast<float*>(x.gather[threadIdx.x] + (int64_t)parity * a.slot_stride);
   const int me = a.rank;
-  const int b = blockIdx.x, G = gridDim.x;
+  const int b = cta, G = ctas;
   const int64_t nv = a.n >> 2;
   const bool last = b == G - 1;
   const int64_t tail0 = nv << 2;
@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(kThreads, 2) push_twoshot_kernel(const __grid_
   if (threadIdx.x <= N) s_part0[threadIdx.x] = part_begin(threadIdx.x, nv, N) << 2;
   __syncthreads();
 
-  phase_mark(a, 0);
+  phase_mark(a, 0, cta);
   // ---- phase 1: push chunk b of every part p into rank p's incoming row `me`
   if (!(a.flags & kSkipPack)) {
     int cur[N];
@@ -102,13 +102,13 @@ __global__ void __launch_bounds__(kThreads, 2) push_twoshot_kernel(const __grid_
       }
     }
   }
-  phase_mark(a, 1);
+  phase_mark(a, 1, cta);
   int status = MGW_DEV_OK;
   // ---- phase 2: fold my part's chunk b from the N local rows, write my tensors, push
   //      the result into every peer's gather area
   if (!(a.flags & kSkipPhase1)) {
-    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, a.tag, a);
-    phase_mark(a, 2);
+    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, a.tag, a, cta);
+    phase_mark(a, 2, cta);
     if (status == MGW_DEV_OK) {
       const float* in = s_in[me];
       const int64_t p0 = s_part0[me];
@@ -172,28 +172,30 @@ __global__ void __launch_bounds__(kThreads, 2) push_twoshot_kernel(const __grid_
       }
     }
   }
-  phase_mark(a, 3);
+  phase_mark(a, 3, cta);
   // ---- phase 3: copy chunk b of every peer part from my gather area into my tensors
   if (status == MGW_DEV_OK && !(a.flags & kSkipPhase2)) {
-    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.mid, parity, epoch, a.tag, a);
-    phase_mark(a, 4);
+    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.mid, parity, epoch, a.tag, a, cta);
+    phase_mark(a, 4, cta);
     if (status == MGW_DEV_OK) {
       const float* g = s_gat[me];
       for (int p = 0; p < N; ++p)
         if (p != me) fused_scatter_range(f, g, pc.lo[p], pc.lo[p] + pc.len[p], 0, 0);
       if (last && me != N - 1) fused_scatter_range(f, g, 0, 0, tail0, a.n);
     }
-    phase_mark(a, 5);
+    phase_mark(a, 5, cta);
   }
-  finish_call(a);
+  finish_call(a, ctas);
 }
+
+MGW_DEFINE_KERNELS(push_twoshot, PushArgs)
 
 // Push one-shot: CTA b stores chunk b of its (scaled) bucket into row `me` of every
 // rank's incoming area (x.gather[r], rows of `stride` = n rounded to 16 B), one barrier,
 // then folds chunk b from the N local rows in the reference order into its tensors.
 // (N-1)·M NVLink bytes out per rank, all as stores; no remote loads.
 template <int N>
-__global__ void __launch_bounds__(kThreads, 2) push_oneshot_kernel(const __grid_constant__ PushArgs x) {
+__device__ __forceinline__ void push_oneshot_body(const PushArgs& x, const int cta, const int ctas) {
   constexpr int U = Unroll<N>::value;
   const FusedArgs& f = x.f;
   const ArArgs& a = f.ar;
@@ -213,13 +215,13 @@ __global__ void __launch_bounds__(kThreads, 2) push_oneshot_kernel(const __grid_
   }
   __syncthreads();
   const int64_t nv = a.n >> 2;
-  const int64_t per = (nv + gridDim.x - 1) / gridDim.x;
-  const int64_t v0 = (int64_t)blockIdx.x * per;
+  const int64_t per = (nv + ctas - 1) / ctas;
+  const int64_t v0 = (int64_t)cta * per;
   const int64_t v1 = v0 + per < nv ? v0 + per : nv;
-  const bool last = blockIdx.x == gridDim.x - 1;
+  const bool last = cta == ctas - 1;
   const float scale = f.scale;
   const bool scaled = scale != 1.0f;
-  phase_mark(a, 0);
+  phase_mark(a, 0, cta);
   // ---- push chunk b of my bucket into row `me` of every rank
   if (!(a.flags & kSkipPack)) {
     constexpr int UP = 4;
@@ -264,19 +266,21 @@ __global__ void __launch_bounds__(kThreads, 2) push_oneshot_kernel(const __grid_
       }
     }
   }
-  phase_mark(a, 1);
+  phase_mark(a, 1, cta);
   int status = MGW_DEV_OK;
   if (!(a.flags & kSkipPhase1)) {
-    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, a.tag, a);
-    phase_mark(a, 2);
+    if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, a.tag, a, cta);
+    phase_mark(a, 2, cta);
     if (status == MGW_DEV_OK) {
       // fold chunk b from the N local rows (they play the slots of fused_reduce_range)
       fused_reduce_range<N, U>(f, s_mine, s_end, v0, v1, nullptr);
       if (last) fused_reduce_tail<N>(f, s_mine, s_end, nv << 2, a.n, nullptr);
     }
-    phase_mark(a, 3);
+    phase_mark(a, 3, cta);
   }
-  finish_call(a);
+  finish_call(a, ctas);
 }
+
+MGW_DEFINE_KERNELS(push_oneshot, PushArgs)
 
 }  // namespace mgw

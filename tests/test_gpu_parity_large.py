@@ -223,29 +223,14 @@ def test_r50_wfbp_layer_buckets_auto(torch_cuda, n_ranks):
 
 @pytest.mark.parametrize("n_ranks", [2, 4, 8])
 def test_r50_bucket_real_barriers_auto(torch_cuda, n_ranks):
-    """The 102 MB SyncEASGD bucket through ``mgw_allreduce_fused`` (AUTO: push two-shot) with
-    the real flag barriers between concurrently running ranks (in-process rank group)."""
+    """The 102 MB SyncEASGD bucket (54 rows) under AUTO (push two-shot) with the real flag
+    barriers: every rank's CTAs in one cooperative launch (in-process rank group)."""
     from paper_1811_11141_b200.allreduce_net import LocalGroup
 
     torch = torch_cuda
     c = get_case(torch, "r50_bucket", n_ranks)
     c.reset()
     torch.cuda.synchronize()
-    grp = LocalGroup(n_ranks, device=0, capacity_bytes=4 * c.total, timeout=20.0)
-    try:
-        def body(cfg, sess):
-            rows, off = [], 0
-            for t, p in zip(c.tensors[cfg.rank], c.counts):
-                rows.append((t.data_ptr(), p, off))
-                off += p
-            table = _native.DeviceTable(rows)
-            _native.call("mgw_allreduce_fused", sess.comm, table.ptr, table.n, c.total, ctypes.c_float(1.0),
-                         _native.ALGO_AUTO, sess.stream.cuda_stream)
-            sess.stream.synchronize()
-            sess.raise_if_failed()
-            table.close()
-
-        grp.run(body)
-    finally:
-        grp.close()
+    with LocalGroup(n_ranks, device=0, capacity_bytes=4 * c.total, timeout=20.0) as grp:
+        assert grp.allreduce_fused(c.tensors) == [None] * n_ranks
     assert c.mismatches() == []

@@ -58,3 +58,38 @@ def test_missing_library_fails_loudly(monkeypatch, tmp_path):
     monkeypatch.setenv("MGWFBP_B200_LIB", str(tmp_path / "absent.so"))
     with pytest.raises(RuntimeError, match="native data path missing"):
         _native.lib()
+
+
+def _tag(group, n, kind, grid, scale=1.0):
+    out = ctypes.c_uint32()
+    _native.call("mgw_debug_collective_tag", group, n, kind, grid, ctypes.c_float(scale), ctypes.byref(out))
+    return out.value
+
+
+def test_collective_tag_separates_every_field():
+    """The 32-bit tag in every barrier flag / LL header (the reference's frame header check,
+    allreduce_net.py:340-345) changes with each thing ranks must agree on: length (also
+    beyond 2^32), kernel family incl. dtype (kinds 1..11), grid, scale and group tag."""
+    base = _tag(7, 100_000, 3, 98)
+    variants = {
+        "length": _tag(7, 100_001, 3, 98),
+        "length_2^32": _tag(7, 100_000 + (1 << 32), 3, 98),
+        "grid": _tag(7, 100_000, 3, 97),
+        "scale": _tag(7, 100_000, 3, 98, 0.5),
+        "group": _tag(8, 100_000, 3, 98),
+    }
+    for kind in range(1, 12):
+        if kind != 3:
+            variants[f"kind{kind}"] = _tag(7, 100_000, kind, 98)
+    assert base == _tag(7, 100_000, 3, 98)  # deterministic: every rank computes the same
+    for name, t in variants.items():
+        assert t != base, name
+    assert len(set(variants.values())) == len(variants)
+
+
+def test_group_tag_mixes_layer_and_iteration():
+    from paper_1811_11141_b200.allreduce_net import group_tag
+
+    tags = {group_tag(low, it) for low in range(1, 60) for it in range(0, 50)}
+    assert len(tags) == 59 * 50
+    assert all(0 <= t < 1 << 32 for t in tags)
