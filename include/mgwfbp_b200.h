@@ -155,6 +155,11 @@ int mgw_comm_create_local(int world, int device, int64_t capacity_bytes, mgw_com
  * absent.  Afterwards read each rank's outcome with mgw_comm_error. */
 int mgw_group_allreduce_fused(mgw_comm* const* comms, void* const* tables, const int64_t* n_elem, const float* scale,
                               int world, int algo, int element_bytes, void* stream);
+/* process-wide options (A/B runs): MGW_OPT_ROWS_PATH 0 = auto (TMA bulk copies for
+ * pack / unpack of large buckets with 16-B aligned rows), 1 = LDG kernel only, 2 = bulk
+ * wherever the alignment allows */
+#define MGW_OPT_ROWS_PATH 1
+int mgw_set_option(int key, int64_t value);
 /* the 32-bit collective tag the launchers stamp into barrier flags / LL headers
  * (kind: 1..11, see TagKind in csrc/allreduce.cuh) -- exposed for host-side tests */
 int mgw_debug_collective_tag(uint32_t group_tag, int64_t n_elem, int kind, int grid, float scale, uint32_t* out);

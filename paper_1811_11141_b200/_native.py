@@ -20,6 +20,7 @@ LIB_PATH = LIB_DIR / "libmgwfbp_b200.so"
 MGW_OK, MGW_EINVAL, MGW_EPROTO, MGW_ECUDA = 0, 1, 2, 3
 ALGO_AUTO, ALGO_ONESHOT, ALGO_TWOSHOT, ALGO_LL, ALGO_NVLS, ALGO_PUSH, ALGO_PUSH_ONESHOT = 0, 1, 2, 3, 4, 5, 6
 SCHED_FILL, SCHED_GRAPH, SCHED_HOSTIO, SCHED_FUSED, SCHED_PDL = 1, 2, 4, 8, 16
+OPT_ROWS_PATH = 1  # mgw_set_option key: 0 auto, 1 LDG only, 2 TMA bulk wherever allowed
 TIME_GRAPH = 256  # mgw_time_exchange: replay the reps as one CUDA graph
 DEV_OK, DEV_MISMATCH, DEV_TIMEOUT, DEV_PEER_ABORT = 0, 1, 2, 3
 DEV_LENGTH_MISMATCH = DEV_MISMATCH  # round-1 name
@@ -76,6 +77,7 @@ _SIGNATURES = {
     "mgw_comm_create_local": ([_I, _I, _I64, ctypes.POINTER(_P)], _I),
     "mgw_group_allreduce_fused": ([ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.POINTER(_I64),
                                    ctypes.POINTER(ctypes.c_float), _I, _I, _I, _P], _I),
+    "mgw_set_option": ([_I, _I64], _I),
     "mgw_debug_collective_tag": ([ctypes.c_uint32, _I64, _I, _I, ctypes.c_float, ctypes.POINTER(ctypes.c_uint32)], _I),
     "mgw_comm_input": ([_P, ctypes.POINTER(_P)], _I),
     "mgw_comm_result": ([_P, ctypes.POINTER(_P)], _I),

@@ -57,6 +57,8 @@ inline int launch_cooperative(void (*kernel)(const RankGroup<Args>), const RankG
   return MGW_OK;
 }
 
+int set_rows_path(int v);  // 0 auto, 1 LDG rows_kernel only, 2 TMA bulk wherever allowed
+
 template <RowOp kOp>
 int launch_rows(const Row* host_rows, const Row* dev_rows, int n_rows, float* bucket, int64_t total, float scale,
                 const float* values, const uint32_t* calls, int64_t slot_stride_elems,

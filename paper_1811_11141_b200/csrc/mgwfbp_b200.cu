@@ -801,6 +801,13 @@ int mgw_group_allreduce_fused(mgw_comm* const* comms, void* const* tables, const
   return b16 ? launch_b16_group(*gf, world, chosen, s) : launch_fused_group(*gf, world, chosen, s);
 }
 
+int mgw_set_option(int key, int64_t value) {
+  switch (key) {
+    case MGW_OPT_ROWS_PATH: return set_rows_path((int)value);
+    default: return set_error(MGW_EINVAL, "unknown option %d", key);
+  }
+}
+
 int mgw_debug_collective_tag(uint32_t group_tag, int64_t n_elem, int kind, int grid, float scale, uint32_t* out) {
   if (!out) return set_error(MGW_EINVAL, "out is null");
   *out = collective_tag(group_tag, n_elem, (uint32_t)kind, grid, scale);

@@ -292,3 +292,41 @@ def test_bf16_rejects_unsupported_algorithms(torch_cuda):
         _native.call("mgw_allreduce_fused_bf16_emulated", tp, sp, 2, 64, ctypes.c_float(1.0), _native.ALGO_NVLS,
                      torch.cuda.current_stream().cuda_stream)
     table.close()
+
+
+@pytest.mark.parametrize("path", [1, 2])
+@pytest.mark.parametrize("misaligned_every", [0, 7])
+def test_pack_unpack_paths_r50_bucket(torch_cuda, path, misaligned_every):
+    """K1/K4 on the 102 MB ResNet-50 whole-model bucket through the LDG kernel (path 1) and
+    the TMA bulk kernel (path 2): bitwise equal to the oracle layout (allreduce_net.py:
+    499-509), with every 7th row at a misaligned tensor address (scalar fallback rows)."""
+    from paper_1811_11141_b200 import resnet50_like
+
+    torch = torch_cuda
+    counts = list(reversed(resnet50_like().param_counts()))
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    tensors = []
+    for k, p in enumerate(counts):
+        shift = 1 if misaligned_every and k % misaligned_every == 3 else 0
+        tensors.append(torch.randn(p + shift, generator=gen, device="cuda")[shift:])
+    rows, total = _rows_for(tensors, counts)
+    table = _native.DeviceTable(rows)
+    bucket = torch.full((total,), float("nan"), device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+    try:
+        _native.call("mgw_set_option", _native.OPT_ROWS_PATH, path)
+        _native.call("mgw_pack", table.ptr, table.n, bucket.data_ptr(), total, ctypes.c_float(1.0), stream)
+        want = torch.cat(tensors)
+        assert torch.equal(bucket.view(torch.int32), want.view(torch.int32))
+        outs = [torch.zeros(t.numel() + 1, device="cuda")[1 if k % 5 == 0 else 0:][:t.numel()]
+                for k, t in enumerate(tensors)]
+        out_rows, _ = _rows_for(outs, counts)
+        out_table = _native.DeviceTable(out_rows)
+        _native.call("mgw_unpack", out_table.ptr, out_table.n, bucket.data_ptr(), total, stream)
+        torch.cuda.synchronize()
+        for a, b in zip(outs, tensors):
+            assert torch.equal(a.view(torch.int32), b.view(torch.int32))
+        out_table.close()
+    finally:
+        _native.call("mgw_set_option", _native.OPT_ROWS_PATH, 0)
+        table.close()
