@@ -58,6 +58,42 @@ def peaks():
 
 
 NVLINK_PEAK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md); 900 nominal
+L2_POLICY = ("GPU arm: a 256 MiB buffer (> 126 MB L2) is written and then read back between iterations, outside "
+             "the timed events (the read-back evicts the dirty lines, so no write-back lands in the next iteration)")
+
+
+def workload_config(bwd, fwd, world):
+    """The workload keys both arms report identically (the driver compares them)."""
+    return {
+        "workload": "resnet50_like (54 layers, 25,503,912 fp32 params = 102,015,648 B), MG-WFBP iteration",
+        "backward_s": bwd,
+        "forward_s": fwd,
+        "timings": "B200-class: torchvision ResNet-50 bs32 fwd/bwd measured on one B200, split by the "
+                   "reference FLOPs proxy",
+        "strategy": "mgwfbp",
+        "parallelism": f"dp{world}",
+        "l2": L2_POLICY,
+    }
+
+
+def l2_flush(buf):
+    """Write then read a buffer larger than L2 on the current stream."""
+    buf.zero_()
+    buf.sum()
+
+
+def host_cpu():
+    """(cores this process may run on, CPU model) of the host."""
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    model = "unknown"
+    try:
+        for line in pathlib.Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return cores, model
 
 
 # --------------------------------------------------------------------- clocks
@@ -295,7 +331,7 @@ def run_strategy(ctx, profile, plan, predicted, steps, warmup, *, graph=True, fu
     try:
         for _ in range(warmup):
             with torch.cuda.stream(it.compute_stream):
-                ctx.flush.zero_()
+                l2_flush(ctx.flush)
             it.run()
         if not it.verify():
             raise RuntimeError(f"{profile.name}: reduced gradients differ from the expected sums")
@@ -305,7 +341,7 @@ def run_strategy(ctx, profile, plan, predicted, steps, warmup, *, graph=True, fu
         t_iter, compute, exposed, kern = [], [], [], []
         for _ in range(steps):
             with torch.cuda.stream(it.compute_stream):
-                ctx.flush.zero_()  # L2 flush between iterations, outside the iteration's events
+                l2_flush(ctx.flush)  # L2 flush between iterations, outside the iteration's events
             times = it.run()
             t_iter.append(times.t_iter)
             compute.append(times.compute_time)
@@ -341,6 +377,58 @@ def run_strategy(ctx, profile, plan, predicted, steps, warmup, *, graph=True, fu
         it.close()
         it = None
     return res, it, kern, t_iter_max, wall
+
+
+def pack_unpack_bench(profile, device, flush, hbm_peak, reps=10, warmup=3):
+    """Median event-timed K1 pack and K4 unpack of the whole-model bucket (54 rows of one
+    contiguous gradient buffer, layer `high` first), each after an L2 flush; algorithmic
+    bytes 2 x bucket (read + write).  The kernels AUTO picks here: the TMA bulk path."""
+    import ctypes
+
+    import torch
+
+    from paper_1811_11141_b200 import _native
+
+    counts = list(reversed(profile.param_counts()))
+    total = sum(counts)
+    flat = torch.ones(total, device=device)
+    bucket = torch.empty(total, device=device)
+    rows, off = [], 0
+    for c in counts:
+        rows.append((flat[off:off + c].data_ptr(), c, off))
+        off += c
+    table = _native.DeviceTable(rows)
+    stream = torch.cuda.current_stream(device)
+    out = {"bytes": 4 * total, "rows": len(rows), "kernel": "bulk_rows_kernel (TMA cp.async.bulk, 4-stage smem ring)",
+           "algorithmic_bytes": "2 x bucket bytes per launch", "timing": "one CUDA event pair per launch, "
+           "L2 written and read back before each"}
+    try:
+        for op in ("pack", "unpack"):
+            times = []
+            for i in range(warmup + reps):
+                l2_flush(flush)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                if op == "pack":
+                    _native.call("mgw_pack", table.ptr, table.n, bucket.data_ptr(), total, ctypes.c_float(1.0),
+                                 stream.cuda_stream)
+                else:
+                    _native.call("mgw_unpack", table.ptr, table.n, bucket.data_ptr(), total, stream.cuda_stream)
+                b.record(stream)
+                b.synchronize()
+                if i >= warmup:
+                    times.append(a.elapsed_time(b) * 1e-3)
+            t = statistics.median(times)
+            gbs = 2 * 4 * total / t / 1e9
+            out[op] = {"us": round(t * 1e6, 2), "achieved": round(gbs, 1), "frac": round(gbs / hbm_peak, 4)}
+        out["round_trip_exact"] = bool(torch.equal(flat, torch.ones_like(flat)))
+    finally:
+        table.close()
+    traffic_file = ROOT / "profiles" / "roofline_traffic.json"
+    if traffic_file.exists():
+        doc = json.loads(traffic_file.read_text())
+        out["traffic"] = {op: doc.get(f"K1 pack@102MB" if op == "pack" else "K4 unpack@102MB") for op in ("pack", "unpack")}
+    return out
 
 
 def run_ours(args) -> dict | None:
@@ -425,6 +513,9 @@ def run_ours(args) -> dict | None:
     hbm_peak, hbm_src = peaks()
     names = {"pack": "K1 pack", "unpack": "K4 unpack", "allreduce": "K2/K3 all-reduce",
              "fused": "fused K1+K4 (N=1)" if world == 1 else "fused K1+K2/K3+K4"}
+    n1_note = ("N=1 has nothing to exchange: the group kernel runs as the stand-in of the N>1 exchange "
+               "(pack -> one-input fold -> write-back per group, the exchange's local HBM legs) so every N "
+               "runs the same per-group launch schedule; its small groups are launch/latency-bound")
     if world == 1 or dominant in ("pack", "unpack"):
         # HBM: pack / unpack read + write every bucket byte once; the N=1 fused kernel does both
         per_unit = 4 if dominant == "fused" else 2
@@ -434,6 +525,8 @@ def run_ours(args) -> dict | None:
                     "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                     "frac": round(achieved / hbm_peak, 4), "peak_source": hbm_src,
                     "algorithmic_bytes": f"{per_unit} x group bucket bytes per launch"}
+        if world == 1 and dominant == "fused":
+            roofline["note"] = n1_note
     else:
         per_unit = 2 * (world - 1) / world
         per_step = int(per_unit * total_bytes)  # nccl-tests bus bytes
@@ -465,6 +558,10 @@ def run_ours(args) -> dict | None:
                                       "achieved": round(big_bw, 1),
                                       "frac": round(big_bw / (hbm_peak if roofline["bound"] == "hbm" else NVLINK_PEAK_GBS), 4),
                                       "timing": "one CUDA event pair around 20 back-to-back launches"}
+    # K1 pack / K4 unpack alone on the whole-model bucket (the SyncEASGD group), each launch
+    # timed by its own event pair after an L2 flush: the HBM-bound kernels at full size
+    if world == 1:
+        roofline["pack_unpack_whole_model"] = pack_unpack_bench(profile, device, flush, hbm_peak)
 
     # e2e: the same MG-WFBP iteration with host buffers (H2D of every layer's gradient,
     # D2H of every reduced gradient) inside the timed region
@@ -479,7 +576,7 @@ def run_ours(args) -> dict | None:
         e2e_times = []
         for _ in range(args.steps):
             with torch.cuda.stream(e2e_it.compute_stream):
-                flush.zero_()
+                l2_flush(flush)
             e2e_times.append(e2e_it.run().t_iter)
         e2e_ok = e2e_it.verify()
         h2d, d2h = e2e_it.io_bytes()
@@ -513,13 +610,8 @@ def run_ours(args) -> dict | None:
         "vs_baseline": None,
         "dtype": "fp32",
         "data": "synthetic (reference gradient pattern rank+1+layer%5, rewritten every iteration)",
-        "config": {
-            "workload": "resnet50_like (54 layers, 25,503,912 fp32 params = 102,015,648 B), MG-WFBP iteration",
-            "backward_s": bwd,
-            "forward_s": fwd,
-            "timings": "B200-class: torchvision ResNet-50 bs32 fwd/bwd measured on one B200, split by the "
-                       "reference FLOPs proxy",
-            "strategy": "mgwfbp",
+        "config": workload_config(bwd, fwd, world),
+        "run": {
             "plan_groups": len(plans["mgwfbp"].groups()),
             "merged_layers": sorted(plans["mgwfbp"].merged_layers),
             "fitted_a_us": round(model.a * 1e6, 3),
@@ -527,8 +619,6 @@ def run_ours(args) -> dict | None:
             "fit_ok": fit_ok,
             "fitted_a_graph_us": round(model_graph.a * 1e6, 3),
             "fitted_b_graph_ns_per_byte": model_graph.b * 1e9,
-            "parallelism": f"dp{world}",
-            "l2": "flushed between iterations (256 MiB write on the compute stream, outside the timed events)",
             "cuda_graph": not args.no_graph,
             "fused_group_kernel": not args.unfused,
             "programmatic_launch": not args.no_pdl,
@@ -573,10 +663,13 @@ def cpu_baseline(profile, plan, n_ranks, seconds):
     from oracle import emulation
 
     walls, ok = emulation.emulate(profile, plan, n_ranks, 10_000, warmup=1, time_budget_s=seconds)
+    host_cores, cpu_model = host_cpu()
     return {
         "value": round(statistics.fmean(walls) * 1e3, 3),
         "unit": "ms",
         "cores": max(1, n_ranks),
+        "host_cores": host_cores,
+        "cpu_model": cpu_model,
         "kind": "port",
         "sample": f"{len(walls)} Algorithm-2 iterations of the same resnet50_like profile/plan with {n_ranks} "
                   f"simulated rank(s) (oracle/emulation.py: reference _delay + C ring, one thread per rank), "
@@ -600,6 +693,7 @@ def run_reference(args) -> dict | None:
     wall = time.perf_counter() - t0
     value = round(statistics.fmean(walls) * 1e3, 3)
     cores = max(1, n_ranks)
+    host_cores, cpu_model = host_cpu()
     return {
         "impl": "reference",
         "metric": METRIC,
@@ -614,17 +708,15 @@ def run_reference(args) -> dict | None:
         "vs_baseline": None,
         "dtype": "fp32",
         "data": "synthetic (reference gradient pattern rank+1+layer%5)",
-        "config": {
-            "workload": "resnet50_like (54 layers, 25,503,912 fp32 params = 102,015,648 B), MG-WFBP iteration",
-            "backward_s": bwd,
-            "forward_s": fwd,
-            "strategy": "mgwfbp",
+        "config": workload_config(bwd, fwd, n_ranks),
+        "run": {
             "plan_groups": len(plan.groups()),
             "fitted_a_us": None if model is None else round(model.a * 1e6, 3),
             "fitted_b_ns_per_byte": None if model is None else model.b * 1e9,
-            "parallelism": f"{n_ranks} simulated ranks on host cores",
+            "ranks": f"{n_ranks} simulated ranks on host cores (one thread each)",
         },
-        "cpu_baseline": {"value": value, "unit": "ms", "cores": cores, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": "ms", "cores": cores, "host_cores": host_cores,
+                         "cpu_model": cpu_model, "kind": "port",
                          "sample": f"{len(walls)} iterations, {n_ranks} simulated rank(s), oracle/emulation.py "
                                    f"(reference Algorithm 2: _delay agent thread + C ring one thread per rank), "
                                    f"verified={ok}, wall {wall:.1f} s"},
