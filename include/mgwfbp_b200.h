@@ -160,6 +160,10 @@ int mgw_group_allreduce_fused(mgw_comm* const* comms, void* const* tables, const
  * wherever the alignment allows */
 #define MGW_OPT_ROWS_PATH 1
 int mgw_set_option(int key, int64_t value);
+/* bounds-checked build (-DMGW_CHECKED, libmgwfbp_b200_checked.so): index violations the
+ * kernels counted since the last reset (every row walk, bucket / slot / LL / push index and
+ * flag slot is validated); *checked = 0 in the production build (total always 0) */
+int mgw_checked_violations(int reset, uint64_t* total, int* checked);
 /* the 32-bit collective tag the launchers stamp into barrier flags / LL headers
  * (kind: 1..11, see TagKind in csrc/allreduce.cuh) -- exposed for host-side tests */
 int mgw_debug_collective_tag(uint32_t group_tag, int64_t n_elem, int kind, int grid, float scale, uint32_t* out);

@@ -78,6 +78,7 @@ _SIGNATURES = {
     "mgw_group_allreduce_fused": ([ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.POINTER(_I64),
                                    ctypes.POINTER(ctypes.c_float), _I, _I, _I, _P], _I),
     "mgw_set_option": ([_I, _I64], _I),
+    "mgw_checked_violations": ([_I, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(_I)], _I),
     "mgw_debug_collective_tag": ([ctypes.c_uint32, _I64, _I, _I, ctypes.c_float, ctypes.POINTER(ctypes.c_uint32)], _I),
     "mgw_comm_input": ([_P, ctypes.POINTER(_P)], _I),
     "mgw_comm_result": ([_P, ctypes.POINTER(_P)], _I),

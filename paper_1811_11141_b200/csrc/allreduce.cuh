@@ -134,6 +134,7 @@ static __device__ __noinline__ int cta_barrier(uint64_t* const* flags, int parit
   if (threadIdx.x == 0) s_status = 0;
   __syncthreads();  // also orders this CTA's earlier stores before the release below
   const int t = threadIdx.x;
+  MGW_EXPECT(cta >= 0 && cta < kMaxBlocks && a.world <= kMaxRanks && a.rank < a.world);
   if (t < a.world) {
     const size_t base = ((size_t)parity * kMaxBlocks + cta) * kMaxRanks;
     store_release_sys(flags[t] + base + a.rank, ((uint64_t)epoch << 32) | tag);
@@ -325,6 +326,7 @@ __device__ __forceinline__ void kernel_prologue(const ArArgs& a, uint32_t& epoch
   stamp_enter(a.stamp);
   epoch = a.state != nullptr ? load_volatile32(a.state) + 1u : 0u;
   parity = (int)(epoch & 1u);
+  MGW_EXPECT(a.slot_stride == 0 || a.n * 2 <= a.slot_stride);  // the bucket fits its slot (bf16 bound)
   if (threadIdx.x < N) {
     const int t = threadIdx.x;
     s_in[t] = reinterpret_cast<const float*>(a.slot[t] + (int64_t)parity * a.slot_stride);

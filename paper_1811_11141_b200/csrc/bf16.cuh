@@ -71,16 +71,14 @@ __device__ __forceinline__ uint16_t b16_fold1(const uint16_t* const* in, int s, 
 // tensor address of bucket element e (row cursor k monotone per thread);
 // fast: the 16-B slot at e lies inside one row at a 16-B aligned tensor address
 __device__ __forceinline__ uint16_t* b16_tensor(const FusedArgs& f, int& k, int64_t e, bool& fast) {
-  Row r = fused_row(f, k);
-  while (e >= r.offset + r.count) r = fused_row(f, ++k);
+  const Row r = walk_row(f, k, e);
   uint16_t* p = reinterpret_cast<uint16_t*>(r.ptr) + (e - r.offset);
   fast = e + kB16 <= r.offset + r.count && (reinterpret_cast<uintptr_t>(p) & 15) == 0;
   return p;
 }
 
 __device__ __forceinline__ uint16_t* b16_tensor1(const FusedArgs& f, int k, int64_t e) {
-  Row r = fused_row(f, k);
-  while (e >= r.offset + r.count) r = fused_row(f, ++k);
+  const Row r = walk_row(f, k, e);
   return reinterpret_cast<uint16_t*>(r.ptr) + (e - r.offset);
 }
 

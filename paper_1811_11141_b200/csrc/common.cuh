@@ -77,6 +77,46 @@ struct Row {  // identical layout to mgw_tensor_desc
 };
 static_assert(sizeof(Row) == sizeof(mgw_tensor_desc), "Row must mirror mgw_tensor_desc");
 
+// ------------------------------------------------------------ checked build
+// -DMGW_CHECKED (__graft_entry__.build(checked=True) -> _lib/libmgwfbp_b200_checked.so):
+// every tensor row walk, bucket / slot index, barrier flag slot, LL area index and push
+// row offset the kernels compute is validated against its extent, and violations are
+// counted in a per-translation-unit device word (mgw_checked_violations) instead of
+// trapping.  compute-sanitizer is closed on this pool; this also catches overruns that
+// stay inside one allocation (a slot overrunning into the next), which memcheck cannot.
+#ifdef MGW_CHECKED
+static __device__ unsigned long long g_violations;
+#define MGW_EXPECT(cond)                                  \
+  do {                                                    \
+    if (!(cond)) atomicAdd(&::mgw::g_violations, 1ull);  \
+  } while (0)
+#define MGW_CHECKED_ONLY(x) x
+#else
+#define MGW_EXPECT(cond) \
+  do {                   \
+  } while (0)
+#define MGW_CHECKED_ONLY(x)
+#endif
+
+// host side: read (and optionally reset) this translation unit's violation count
+#ifdef MGW_CHECKED
+#define MGW_DEFINE_VIOLATIONS(tu)                                                               \
+  int violations_##tu(unsigned long long* out, bool reset) {                                   \
+    if (cudaMemcpyFromSymbol(out, g_violations, sizeof(*out)) != cudaSuccess) return MGW_ECUDA; \
+    if (reset) {                                                                                \
+      const unsigned long long zero = 0;                                                        \
+      if (cudaMemcpyToSymbol(g_violations, &zero, sizeof(zero)) != cudaSuccess) return MGW_ECUDA; \
+    }                                                                                           \
+    return MGW_OK;                                                                              \
+  }
+#else
+#define MGW_DEFINE_VIOLATIONS(tu)                               \
+  int violations_##tu(unsigned long long* out, bool) {         \
+    *out = 0;                                                  \
+    return MGW_OK;                                             \
+  }
+#endif
+
 // ------------------------------------------------------------ device utils
 
 __device__ __forceinline__ uint64_t global_ns() {

@@ -48,17 +48,30 @@ __device__ __forceinline__ int fused_row_covering(const FusedArgs& f, int64_t e)
 
 // Tensor address of bucket element e; `k` is a monotone per-thread row cursor.
 // fast4: the 16-B slot at e is inside one row at a 16-B aligned tensor address.
-__device__ __forceinline__ float* fused_tensor(const FusedArgs& f, int& k, int64_t e, bool& fast4) {
+// Row of bucket element e, advancing the monotone cursor k (checked build: the walk never
+// leaves the table and e lies inside the row and the bucket).
+__device__ __forceinline__ Row walk_row(const FusedArgs& f, int& k, int64_t e) {
   Row r = fused_row(f, k);
-  while (e >= r.offset + r.count) r = fused_row(f, ++k);
+  while (e >= r.offset + r.count) {
+    MGW_CHECKED_ONLY(if (k + 1 >= f.n_rows) {
+      MGW_EXPECT(false);
+      break;
+    })
+    r = fused_row(f, ++k);
+  }
+  MGW_EXPECT(k < f.n_rows && e >= r.offset && e < r.offset + r.count && e < f.ar.n);
+  return r;
+}
+
+__device__ __forceinline__ float* fused_tensor(const FusedArgs& f, int& k, int64_t e, bool& fast4) {
+  const Row r = walk_row(f, k, e);
   float* p = r.ptr + (e - r.offset);
   fast4 = e + 4 <= r.offset + r.count && (reinterpret_cast<uintptr_t>(p) & 15) == 0;
   return p;
 }
 
 __device__ __forceinline__ float* fused_tensor1(const FusedArgs& f, int k, int64_t e) {
-  Row r = fused_row(f, k);
-  while (e >= r.offset + r.count) r = fused_row(f, ++k);
+  const Row r = walk_row(f, k, e);
   return r.ptr + (e - r.offset);
 }
 
@@ -224,6 +237,7 @@ __device__ __forceinline__ void fused_oneshot_body(const FusedArgs& f, const int
   uint32_t epoch;
   int parity;
   kernel_prologue<N>(a, epoch, parity, s_in, s_end);
+  MGW_EXPECT(a.slot_stride == 0 || a.n * 4 <= a.slot_stride);  // fp32 bucket fits its slot
   const int64_t nv = a.n >> 2;
   const int64_t per = (nv + ctas - 1) / ctas;
   const int64_t v0 = (int64_t)cta * per;
@@ -344,6 +358,7 @@ __device__ __forceinline__ void fused_twoshot_body(const FusedArgs& f, const int
   uint32_t epoch;
   int parity;
   kernel_prologue<N>(a, epoch, parity, s_in, s_end);
+  MGW_EXPECT(a.slot_stride == 0 || a.n * 4 <= a.slot_stride);  // fp32 bucket fits its slot
   const int me = a.rank;
   const int b = cta, G = ctas;
   const int64_t nv = a.n >> 2;

@@ -38,4 +38,6 @@ int launch_allreduce(const ArArgs& a, int algo, int max_ctas, cudaStream_t strea
   }
 }
 
+MGW_DEFINE_VIOLATIONS(allreduce)
+
 }  // namespace mgw

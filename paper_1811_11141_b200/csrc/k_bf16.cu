@@ -101,4 +101,6 @@ int launch_ll_b16_group(const RankGroup<LLArgs>& g, int world, cudaStream_t stre
   }
 }
 
+MGW_DEFINE_VIOLATIONS(bf16)
+
 }  // namespace mgw

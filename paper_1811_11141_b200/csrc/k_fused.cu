@@ -61,4 +61,6 @@ int launch_fused_group(const RankGroup<FusedArgs>& g, int world, int algo, cudaS
   }
 }
 
+MGW_DEFINE_VIOLATIONS(fused)
+
 }  // namespace mgw

@@ -48,4 +48,6 @@ int launch_ll_group(const RankGroup<LLArgs>& g, int world, cudaStream_t stream) 
   }
 }
 
+MGW_DEFINE_VIOLATIONS(ll)
+
 }  // namespace mgw

@@ -26,4 +26,6 @@ int launch_nvls(const NvlsArgs& x0, int max_ctas, cudaStream_t stream, const int
   return MGW_OK;
 }
 
+MGW_DEFINE_VIOLATIONS(nvls)
+
 }  // namespace mgw

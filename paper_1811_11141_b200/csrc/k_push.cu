@@ -83,4 +83,6 @@ int launch_push_group(const RankGroup<PushArgs>& g, int world, bool one, cudaStr
   }
 }
 
+MGW_DEFINE_VIOLATIONS(push)
+
 }  // namespace mgw

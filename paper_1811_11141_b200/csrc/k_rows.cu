@@ -112,4 +112,6 @@ template int launch_rows<RowOp::kFill>(const Row*, const Row*, int, float*, int6
 template int launch_rows<RowOp::kCheck>(const Row*, const Row*, int, float*, int64_t, float, const float*,
                                         const uint32_t*, int64_t, unsigned long long*, cudaStream_t, uint64_t*,
                                         cudaEvent_t);
+MGW_DEFINE_VIOLATIONS(rows)
+
 }  // namespace mgw

@@ -57,7 +57,16 @@ inline int launch_cooperative(void (*kernel)(const RankGroup<Args>), const RankG
   return MGW_OK;
 }
 
-int set_rows_path(int v);  // 0 auto, 1 LDG rows_kernel only, 2 TMA bulk wherever allowed
+int set_rows_path(int v);
+
+// checked build: per translation unit violation counters (MGW_EXPECT in common.cuh)
+int violations_allreduce(unsigned long long* out, bool reset);
+int violations_bf16(unsigned long long* out, bool reset);
+int violations_fused(unsigned long long* out, bool reset);
+int violations_ll(unsigned long long* out, bool reset);
+int violations_nvls(unsigned long long* out, bool reset);
+int violations_push(unsigned long long* out, bool reset);
+int violations_rows(unsigned long long* out, bool reset);  // 0 auto, 1 LDG rows_kernel only, 2 TMA bulk wherever allowed
 
 template <RowOp kOp>
 int launch_rows(const Row* host_rows, const Row* dev_rows, int n_rows, float* bucket, int64_t total, float scale,

@@ -71,8 +71,7 @@ __device__ __forceinline__ uint64_t ll_word(uint32_t epoch, float x) {
 }
 
 __device__ __forceinline__ float* ll_tensor(const FusedArgs& f, int& k, int64_t e) {
-  Row r = fused_row(f, k);
-  while (e >= r.offset + r.count) r = fused_row(f, ++k);
+  const Row r = walk_row(f, k, e);
   return r.ptr + (e - r.offset);
 }
 

@@ -808,6 +808,25 @@ int mgw_set_option(int key, int64_t value) {
   }
 }
 
+int mgw_checked_violations(int reset, uint64_t* total, int* checked) {
+  if (!total || !checked) return set_error(MGW_EINVAL, "bad arguments");
+#ifdef MGW_CHECKED
+  *checked = 1;
+#else
+  *checked = 0;
+#endif
+  unsigned long long sum = 0;
+  int (*getters[])(unsigned long long*, bool) = {violations_allreduce, violations_bf16, violations_fused, violations_ll,
+                                                 violations_nvls,      violations_push, violations_rows};
+  for (auto get : getters) {
+    unsigned long long v = 0;
+    if (get(&v, reset != 0) != MGW_OK) return set_error(MGW_ECUDA, "reading the checked-build violation counters");
+    sum += v;
+  }
+  *total = sum;
+  return MGW_OK;
+}
+
 int mgw_debug_collective_tag(uint32_t group_tag, int64_t n_elem, int kind, int grid, float scale, uint32_t* out) {
   if (!out) return set_error(MGW_EINVAL, "out is null");
   *out = collective_tag(group_tag, n_elem, (uint32_t)kind, grid, scale);

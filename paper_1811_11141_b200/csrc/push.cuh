@@ -84,6 +84,8 @@ __device__ __forceinline__ void push_twoshot_body(const PushArgs& x, const int c
         if (i >= pc.len[p]) continue;
         const int64_t e = (pc.lo[p] + i) << 2;
         float* dst = const_cast<float*>(s_in[p]) + (int64_t)me * stride + (e - s_part0[p]);
+        MGW_EXPECT(e >= s_part0[p] && e + 4 <= s_part0[p] + stride &&
+                   (a.slot_stride == 0 || (int64_t)N * stride * 4 <= a.slot_stride));
         if (fast[p]) {
           *reinterpret_cast<float4*>(dst) = scaled ? fmul4(v[p], scale) : v[p];
         } else {
@@ -253,6 +255,7 @@ __device__ __forceinline__ void push_oneshot_body(const PushArgs& x, const int c
             v[u] = make_float4(r[0], r[1], r[2], r[3]);
           }
           if (scaled) v[u] = fmul4(v[u], scale);
+          MGW_EXPECT(e + 4 <= stride && (a.slot_stride == 0 || (int64_t)N * stride * 4 <= a.slot_stride));
 #pragma unroll
           for (int q = 0; q < N; ++q) *reinterpret_cast<float4*>(s_row[q] + (int64_t)me * stride + e) = v[u];
         }

@@ -20,6 +20,7 @@ import bench  # noqa: E402
 def main() -> int:
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--no-pdl", action="store_true")
     args = ap.parse_args()
     import torch
 
@@ -31,7 +32,8 @@ def main() -> int:
     profile, _, _ = bench.b200_profile()
     plan = MergePlan(frozenset(), profile.num_layers)
     flush = torch.empty(bench.L2_FLUSH_BYTES // 4, device=device)
-    it = OverlappedIteration(profile, plan, comm=None, rank=0, world=1, device=device, graph=True, fused=True)
+    it = OverlappedIteration(profile, plan, comm=None, rank=0, world=1, device=device, graph=True, fused=True,
+                            pdl=not args.no_pdl)
     spans = []
     try:
         for i in range(3 + args.iters):

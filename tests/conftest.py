@@ -122,3 +122,23 @@ def need_gpu():
 def need_two_gpus():
     if cuda_devices() < 2:
         pytest.skip("needs >= 2 CUDA devices (one process per GPU)")
+
+
+@pytest.fixture(scope="session", autouse=True)
+def _checked_build_violations():
+    """With the bounds-checked library (MGWFBP_B200_LIB=..._checked.so), every index the
+    kernels computed during the session must have been inside its extent."""
+    yield
+    import ctypes
+    import os
+
+    if "checked" not in os.environ.get("MGWFBP_B200_LIB", ""):
+        return
+    from paper_1811_11141_b200 import _native
+
+    if _native._lib is None:
+        return
+    total, checked = ctypes.c_uint64(), ctypes.c_int()
+    _native.call("mgw_checked_violations", 0, ctypes.byref(total), ctypes.byref(checked))
+    print(f"\nchecked build: {total.value} index violations (checked={checked.value})")
+    assert checked.value == 1 and total.value == 0, f"{total.value} index violations in the checked build"
