@@ -75,6 +75,36 @@ __device__ __forceinline__ float* fused_tensor1(const FusedArgs& f, int k, int64
   return r.ptr + (e - r.offset);
 }
 
+// Out-of-line slow paths (a 16-B slot straddling two rows or two reference segments, or
+// sitting at a misaligned tensor address).  Inlined into every unrolled hot loop they made
+// the N = 1 group kernel 82 KB of SASS; a small group's launch runs ~2 us, so fetching a
+// large kernel body from L2 on cold SMs is a visible share of it.
+static __device__ __noinline__ void pack4_slow(const FusedArgs& f, float* slot, int k, int64_t e, float scale) {
+  for (int j = 0; j < 4; ++j) {
+    const float y = *fused_tensor1(f, k, e + j);
+    slot[e + j] = scale != 1.0f ? __fmul_rn(y, scale) : y;
+  }
+}
+
+static __device__ __noinline__ void store4_slow(const FusedArgs& f, int k, int64_t e, float4 v) {
+  *fused_tensor1(f, k, e) = v.x;
+  *fused_tensor1(f, k, e + 1) = v.y;
+  *fused_tensor1(f, k, e + 2) = v.z;
+  *fused_tensor1(f, k, e + 3) = v.w;
+}
+
+// four elements whose fold starts differ (the slot straddles a reference segment boundary)
+template <int N>
+__device__ __noinline__ void fold4_slow(const FusedArgs& f, const float* const* in, const int64_t* seg_end, int s, int k,
+                                        int64_t e, float* own) {
+  for (int j = 0; j < 4; ++j) {
+    s = advance_segment(s, e + j, seg_end);
+    const float y = fold1<N>(in, s, e + j);
+    if (own) own[e + j] = y;
+    *fused_tensor1(f, k, e + j) = y;
+  }
+}
+
 // Pack bucket vectors [v0, v1) (16-B slots) plus scalar elements [t0, t1) into `slot`.
 // UP slots per thread are loaded before any is stored (ncu r01: one outstanding 16-B load
 // per thread left the pack phase latency-bound on long-scoreboard stalls).
@@ -105,14 +135,10 @@ static __device__ void fused_pack_range(const FusedArgs& f, float* slot, int64_t
         const int64_t vv = base + (int64_t)u * kThreads;
         if (vv >= v1) continue;
         const int64_t e = vv << 2;
-        if (fast[u]) {
+        if (fast[u])
           *reinterpret_cast<float4*>(slot + e) = scaled ? fmul4(x[u], scale) : x[u];
-        } else {
-          for (int j = 0; j < 4; ++j) {
-            const float y = *fused_tensor1(f, ku[u], e + j);
-            slot[e + j] = scaled ? __fmul_rn(y, scale) : y;
-          }
-        }
+        else
+          pack4_slow(f, slot, ku[u], e, scale);
       }
     }
   }
@@ -165,20 +191,12 @@ __device__ void fused_reduce_range(const FusedArgs& f, const float* const* in, c
 #pragma unroll
         for (int kk = 1; kk < N; ++kk) acc = fadd4(acc, x[u][kk]);
         if (own) *reinterpret_cast<float4*>(own + e) = acc;
-        if (fast) {
+        if (fast)
           *reinterpret_cast<float4*>(tp) = acc;
-        } else {
-          const float y[4] = {acc.x, acc.y, acc.z, acc.w};
-          for (int j = 0; j < 4; ++j) *fused_tensor1(f, k, e + j) = y[j];
-        }
+        else
+          store4_slow(f, k, e, acc);
       } else {
-        int s = su[u];
-        for (int j = 0; j < 4; ++j) {
-          s = advance_segment(s, e + j, seg_end);
-          const float y = fold1<N>(in, s, e + j);
-          if (own) own[e + j] = y;
-          *fused_tensor1(f, k, e + j) = y;
-        }
+        fold4_slow<N>(f, in, seg_end, su[u], k, e, own);
       }
     }
   }
@@ -215,12 +233,10 @@ static __device__ void fused_scatter_range(const FusedArgs& f, const float* src,
         const int64_t e = vv << 2;
         bool fast;
         float* tp = fused_tensor(f, k, e, fast);
-        if (fast) {
+        if (fast)
           *reinterpret_cast<float4*>(tp) = x[u];
-        } else {
-          const float y[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
-          for (int j = 0; j < 4; ++j) *fused_tensor1(f, k, e + j) = y[j];
-        }
+        else
+          store4_slow(f, k, e, x[u]);
       }
     }
   }
@@ -310,14 +326,10 @@ __device__ void fused_pack_parts(const FusedArgs& f, float* slot, const PartChun
     for (int p = 0; p < N; ++p) {
       if (i >= pc.len[p]) continue;
       const int64_t e = (pc.lo[p] + i) << 2;
-      if (fast[p]) {
+      if (fast[p])
         *reinterpret_cast<float4*>(slot + e) = scaled ? fmul4(x[p], scale) : x[p];
-      } else {
-        for (int j = 0; j < 4; ++j) {
-          const float y = *fused_tensor1(f, cur[p], e + j);
-          slot[e + j] = scaled ? __fmul_rn(y, scale) : y;
-        }
-      }
+      else
+        pack4_slow(f, slot, cur[p], e, scale);
     }
   }
 }
@@ -339,12 +351,10 @@ __device__ void fused_scatter_parts(const FusedArgs& f, const float* const* in, 
       const int64_t e = (pc.lo[p] + i) << 2;
       bool fast;
       float* tp = fused_tensor(f, cur[p], e, fast);
-      if (fast) {
+      if (fast)
         *reinterpret_cast<float4*>(tp) = x[p];
-      } else {
-        const float y[4] = {x[p].x, x[p].y, x[p].z, x[p].w};
-        for (int j = 0; j < 4; ++j) *fused_tensor1(f, cur[p], e + j) = y[j];
-      }
+      else
+        store4_slow(f, cur[p], e, x[p]);
     }
   }
 }

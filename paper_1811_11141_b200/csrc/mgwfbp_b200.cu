@@ -376,14 +376,14 @@ int comm_allreduce_fused(mgw_comm* c, const Row* host_rows, const Row* dev_rows,
 // one-input fold, write back -- one launch per group like the multi-rank path.  Every
 // thread re-reads only the bucket slots it packed itself, so no barrier is needed.
 int local_fused(float* bucket, const Row* host_rows, const Row* dev_rows, int n_rows, int64_t n, float scale,
-                cudaStream_t stream, uint64_t* stamp = nullptr) {
+                cudaStream_t stream, uint64_t* stamp = nullptr, int extra_flags = 0) {
   if (n == 0 || n_rows == 0) return MGW_OK;
   FusedArgs f;
   memset(&f, 0, sizeof(f));
   f.ar.slot[0] = reinterpret_cast<char*>(bucket);
   f.ar.n = n;
   f.ar.world = 1;
-  f.ar.flags = kNoBarrier;
+  f.ar.flags = kNoBarrier | extra_flags;
   f.ar.stamp = stamp;
   f.use_inline = n_rows <= kInlineRows && host_rows != nullptr;
   if (f.use_inline)
@@ -921,7 +921,7 @@ int mgw_allreduce_fused_bf16(mgw_comm* c, const void* table, int n_rows, int64_t
 
 int mgw_probe_phases(mgw_comm* c, const void* table, int n_rows, int64_t n_elem, int algo, int reps, uint64_t* out,
                      void* stream) {
-  if (!c || !out || reps < 1 || c->world < 2) return set_error(MGW_EINVAL, "bad phase-probe arguments");
+  if (!c || !out || reps < 1) return set_error(MGW_EINVAL, "bad phase-probe arguments");
   int rc = check_table(table, n_rows, n_elem);
   if (rc) return rc;
   const mgw_table_t* t = as_table(table);
@@ -932,7 +932,11 @@ int mgw_probe_phases(mgw_comm* c, const void* table, int n_rows, int64_t n_elem,
   MGW_CUDA(cudaMalloc(&d, h.size() * sizeof(uint64_t)));
   cudaError_t e = cudaMemcpyAsync(d, h.data(), h.size() * sizeof(uint64_t), cudaMemcpyHostToDevice, s);
   for (int r = 0; r < reps && rc == MGW_OK && e == cudaSuccess; ++r)
-    rc = comm_allreduce_fused(c, t->host.data(), t->dev, n_rows, n_elem, 1.f, algo, s, d + (size_t)r * 8, kPhaseMarks);
+    rc = c->world == 1  // the single-rank group kernel (pack -> one-input fold -> write-back)
+             ? local_fused(reinterpret_cast<float*>(c->region + kSlotOff), t->host.data(), t->dev, n_rows, n_elem, 1.f,
+                           s, d + (size_t)r * 8, kPhaseMarks)
+             : comm_allreduce_fused(c, t->host.data(), t->dev, n_rows, n_elem, 1.f, algo, s, d + (size_t)r * 8,
+                                    kPhaseMarks);
   if (e == cudaSuccess) e = cudaMemcpyAsync(h.data(), d, h.size() * sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   cudaFree(d);

@@ -381,3 +381,58 @@ def empty_and_tiny_task(config, session):
     ring_allreduce(buf, config, session)
     out.append(bool(np.array_equal(buf.values, np.arange(23, dtype="<f4") * n + n * (n - 1) / 2)))
     return out
+
+
+def _timed_collective(config, session, buf_values, layer_low=1, iteration=0):
+    """One ring_allreduce; returns (seconds, error text or None)."""
+    import time
+
+    from paper_1811_11141_b200 import ProtocolError
+
+    t0 = time.perf_counter()
+    try:
+        ring_allreduce(GradientBuffer(layer_low, layer_low, buf_values), config, session, iteration=iteration)
+        return time.perf_counter() - t0, None
+    except ProtocolError as exc:
+        return time.perf_counter() - t0, str(exc)
+
+
+def cta_cap_mismatch_task(config, session):
+    """Rank 0 caps its collectives at 8 CTAs, the others keep the default: the grids differ,
+    so the collective tags differ at the first barrier (allreduce_net.py:340-345)."""
+    from paper_1811_11141_b200 import _native
+
+    _native.call("mgw_comm_set_timeout_ms", session.comm, 20000)
+    if config.rank == 0:
+        _native.call("mgw_comm_set_max_ctas", session.comm, 8)
+    return _timed_collective(config, session, np.ones(3_000_000, dtype="<f4"))
+
+
+def threshold_mismatch_task(config, session):
+    """Rank 0 disables LL (ll_max 0) and the one-shot (oneshot_max 0): its AUTO choice for a
+    64 KiB and a 2 MiB bucket differs from its peers' -> ProtocolError, not crossed data."""
+    from paper_1811_11141_b200 import _native
+
+    _native.call("mgw_comm_set_timeout_ms", session.comm, 20000)
+    if config.rank == 0:
+        _native.call("mgw_comm_set_ll_max", session.comm, 0)
+        _native.call("mgw_comm_set_oneshot_max", session.comm, 0)
+    return [_timed_collective(config, session, np.ones(16384, dtype="<f4"))]
+
+
+def swapped_groups_task(config, session):
+    """Two equal-size merge groups issued in opposite orders on rank 0 and the others: the
+    group tag (head layer) differs at the barrier -> ProtocolError on every rank."""
+    from paper_1811_11141_b200 import _native
+
+    _native.call("mgw_comm_set_timeout_ms", session.comm, 20000)
+    order = (3, 5) if config.rank == 0 else (5, 3)
+    return _timed_collective(config, session, np.ones(100_000, dtype="<f4"), layer_low=order[0])
+
+
+def iteration_mismatch_task(config, session):
+    """Same group, different iteration numbers (the reference header's iteration field)."""
+    from paper_1811_11141_b200 import _native
+
+    _native.call("mgw_comm_set_timeout_ms", session.comm, 20000)
+    return _timed_collective(config, session, np.ones(5000, dtype="<f4"), layer_low=2, iteration=config.rank)

@@ -266,3 +266,23 @@ def test_randomized_stress_every_algorithm_and_dtype():
         res = run_workers(n, partial(_mp_tasks.stress_task, iterations=300, seed=2024 + n), timeout=600)
         for r, (n_bad, first) in res.items():
             assert n_bad == 0, (n, r, first)
+
+
+@pytest.mark.parametrize("task", ["cta_cap_mismatch_task", "swapped_groups_task", "iteration_mismatch_task"])
+def test_settings_disagreement_raises_fast(task):
+    """Per-rank CTA caps, swapped group order, different iterations: every rank raises
+    ProtocolError within a second (the collective tag in every barrier flag / LL header,
+    the reference's frame header check allreduce_net.py:340-345) -- no 20 s timeout, no
+    silently crossed sums."""
+    results = run_workers(2, getattr(_mp_tasks, task), timeout=120)
+    for rank, (seconds, err) in results.items():
+        assert err is not None and ("disagree" in err or "aborted" in err), (rank, err)
+        assert seconds < 1.0, (rank, seconds)
+
+
+def test_threshold_disagreement_raises_fast():
+    results = run_workers(2, _mp_tasks.threshold_mismatch_task, timeout=120)
+    for rank, outcomes in results.items():
+        for seconds, err in outcomes:
+            assert err is not None and ("disagree" in err or "aborted" in err), (rank, err)
+            assert seconds < 1.0, (rank, seconds)
