@@ -370,7 +370,7 @@ __device__ __forceinline__ void ll_b16_body(const LLArgs& l, const int cta, cons
   if (threadIdx.x == 0) s_status = MGW_DEV_OK;
   const bool do_push = !(a.flags & kSkipPack), do_fold = !(a.flags & kSkipPhase1);  // emulation split
   if (do_push && cta == 0 && threadIdx.x < N)
-    st_relaxed_sys_u64(l.hdr[threadIdx.x] + parity * kMaxRanks + me, ((uint64_t)epoch << 32) | a.tag);
+    st_relaxed_sys_u64(l.hdr[threadIdx.x] + parity * l.hdr_stride + me, ((uint64_t)epoch << 32) | a.tag);
   __syncthreads();
 
   // element quads of this CTA: [q0, q1) (quad j = elements 4j .. 4j+3 = words 2j, 2j+1)
@@ -403,7 +403,7 @@ __device__ __forceinline__ void ll_b16_body(const LLArgs& l, const int cta, cons
   // 2. CTA 0 checks every peer's header (length and dtype agreement)
   int status = MGW_DEV_OK;
   if (do_fold && cta == 0 && threadIdx.x < N) {
-    const uint64_t* p = l.hdr[me] + parity * kMaxRanks + threadIdx.x;
+    const uint64_t* p = l.hdr[me] + parity * l.hdr_stride + threadIdx.x;
     uint64_t v = ld_relaxed_sys_u64(p);
     const uint64_t start = global_ns();
     for (uint32_t spin = 0; (uint32_t)(v >> 32) != epoch; ++spin) {

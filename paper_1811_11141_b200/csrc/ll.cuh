@@ -25,7 +25,11 @@ constexpr int64_t kLLMaxElems = kLLElems;  // per rank per parity (1 MB of fp32 
 struct LLArgs {
   FusedArgs f;                   // rows (layer tensors), scale, comm pointers, epochs
   uint64_t* ll[kMaxRanks];       // per-rank LL receive area base: [2 parity][kMaxRanks src][kLLMaxElems]
-  uint64_t* hdr[kMaxRanks];      // per-rank header words: [2 parity][kMaxRanks src]
+  uint64_t* hdr[kMaxRanks];      // per-rank header words: [2 parity][... src]; a communicator
+                                 // points them at its arrive barrier flags of CTA 0, so an LL
+                                 // header and a barrier flag of a rank running another kernel
+                                 // meet in the same word and the tag check sees the mismatch
+  int64_t hdr_stride;            // words from parity 0 to parity 1 of hdr
 };
 
 __device__ __forceinline__ void st_relaxed_sys_v2(uint64_t* p, uint64_t a, uint64_t b) {
@@ -97,7 +101,7 @@ __device__ __forceinline__ void ll_oneshot_body(const LLArgs& l, const int cta, 
   // and the fold into separate launches (emulated ranks on one device, tests only).
   const bool do_push = !(a.flags & kSkipPack), do_fold = !(a.flags & kSkipPhase1);
   if (do_push && cta == 0 && threadIdx.x < N)
-    st_relaxed_sys_u64(l.hdr[threadIdx.x] + parity * kMaxRanks + me, ((uint64_t)epoch << 32) | a.tag);
+    st_relaxed_sys_u64(l.hdr[threadIdx.x] + parity * l.hdr_stride + me, ((uint64_t)epoch << 32) | a.tag);
   __syncthreads();
 
   // element pairs of this CTA: [p0, p1) (pair j = elements 2j, 2j+1)
@@ -130,7 +134,7 @@ __device__ __forceinline__ void ll_oneshot_body(const LLArgs& l, const int cta, 
   int status = MGW_DEV_OK;
   if (do_fold && cta == 0 && threadIdx.x < N) {
     const uint64_t h = [&] {
-      const uint64_t* p = l.hdr[me] + parity * kMaxRanks + threadIdx.x;
+      const uint64_t* p = l.hdr[me] + parity * l.hdr_stride + threadIdx.x;
       uint64_t v = ld_relaxed_sys_u64(p);
       const uint64_t start = global_ns();
       for (uint32_t spin = 0; (uint32_t)(v >> 32) != epoch; ++spin) {

@@ -354,8 +354,9 @@ int comm_allreduce_fused(mgw_comm* c, const Row* host_rows, const Row* dev_rows,
     l.f = f;
     for (int s = 0; s < c->world; ++s) {
       l.ll[s] = reinterpret_cast<uint64_t*>(c->peer[s] + kLLOff);
-      l.hdr[s] = reinterpret_cast<uint64_t*>(c->peer[s] + kHdrOff);
+      l.hdr[s] = reinterpret_cast<uint64_t*>(c->peer[s] + kArriveOff);  // CTA 0's arrive flags
     }
+    l.hdr_stride = (int64_t)kMaxBlocks * kMaxRanks;
     return launch_ll(l, c->max_ctas, stream);
   }
   if (chosen == MGW_ALGO_PUSH_ONESHOT || chosen == MGW_ALGO_PUSH) {
@@ -425,8 +426,9 @@ int comm_allreduce_fused_bf16(mgw_comm* c, const Row* host_rows, const Row* dev_
     l.f = f;
     for (int s = 0; s < c->world; ++s) {
       l.ll[s] = reinterpret_cast<uint64_t*>(c->peer[s] + kLLOff);
-      l.hdr[s] = reinterpret_cast<uint64_t*>(c->peer[s] + kHdrOff);
+      l.hdr[s] = reinterpret_cast<uint64_t*>(c->peer[s] + kArriveOff);  // CTA 0's arrive flags
     }
+    l.hdr_stride = (int64_t)kMaxBlocks * kMaxRanks;
     return launch_ll_b16(l, c->max_ctas, stream);
   }
   return launch_b16(f, algo, c->max_ctas, stream);
@@ -776,8 +778,9 @@ int mgw_group_allreduce_fused(mgw_comm* const* comms, void* const* tables, const
       l.f = f;
       for (int q = 0; q < world; ++q) {
         l.ll[q] = reinterpret_cast<uint64_t*>(c->peer[q] + kLLOff);
-        l.hdr[q] = reinterpret_cast<uint64_t*>(c->peer[q] + kHdrOff);
+        l.hdr[q] = reinterpret_cast<uint64_t*>(c->peer[q] + kArriveOff);
       }
+      l.hdr_stride = (int64_t)kMaxBlocks * kMaxRanks;
       if (n > (b16 ? 2 : 1) * kLLElems) return set_error(MGW_EINVAL, "LL bucket of %lld elements too large", (long long)n);
       grid = b16 ? plan_ll_b16(l, c->max_ctas) : plan_ll(l, c->max_ctas);
     } else if (push) {
@@ -1173,6 +1176,7 @@ static int ll_emulated(void* const* tables, int world, int64_t n, float scale, c
     char* base = mem + (size_t)r * per_rank;
     l.ll[r] = reinterpret_cast<uint64_t*>(base);
     l.hdr[r] = reinterpret_cast<uint64_t*>(base + kLLBytes);
+    l.hdr_stride = kMaxRanks;
     l.f.ar.abort_flag[r] = reinterpret_cast<uint32_t*>(base + kLLBytes + hdr_bytes);
   }
   l.f.ar.n = n;

@@ -28,20 +28,30 @@ sys.path.insert(0, str(pathlib.Path(__file__).resolve().parents[1]))
 import bench  # noqa: E402
 
 
-def nvlink_kib(handle, pynvml):
-    """(data TX, data RX, raw TX, raw RX) KiB summed over this GPU's NVLinks."""
-    ids = (pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX,
-           pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_RAW_TX, pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_RAW_RX)
-    tot = [0, 0, 0, 0]
-    for link in range(18):
-        try:
-            res = pynvml.nvmlDeviceGetFieldValues(handle, [(fid, link) for fid in ids])
-        except Exception:
-            continue
-        for i, r in enumerate(res):
-            if r.nvmlReturn == 0:
-                tot[i] += int(r.value.ullVal)
-    return tot
+COUNTERS = {
+    # name: (TX field, RX field, unit bytes)
+    "count_bytes": (202, 204, 1),  # NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES / RCV_BYTES (Blackwell)
+    "throughput_data_kib": (138, 139, 1024),  # NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX / RX
+    "throughput_raw_kib": (140, 141, 1024),  # NVML_FI_DEV_NVLINK_THROUGHPUT_RAW_TX / RX
+}
+
+
+def nvlink_counters(handle, pynvml):
+    """{counter: (TX bytes, RX bytes, links answering)} summed over this GPU's NVLinks."""
+    out = {}
+    for name, (ftx, frx, unit) in COUNTERS.items():
+        tx = rx = links = 0
+        for link in range(18):
+            try:
+                res = pynvml.nvmlDeviceGetFieldValues(handle, [(ftx, link), (frx, link)])
+            except Exception:
+                continue
+            if res[0].nvmlReturn == 0 and res[1].nvmlReturn == 0:
+                links += 1
+                tx += int(res[0].value.ullVal) * unit
+                rx += int(res[1].value.ullVal) * unit
+        out[name] = (tx, rx, links)
+    return out
 
 
 def main() -> int:
@@ -91,22 +101,24 @@ def main() -> int:
         torch.cuda.synchronize()
         bench._barrier(world)
         time.sleep(0.2)
-        before = nvlink_kib(handle, pynvml)
+        before = nvlink_counters(handle, pynvml)
         _native.call("mgw_time_exchange", comm, table.ptr, 1, n, None, algo, 4, args.reps, 0, ctypes.byref(sec),
                      stream.cuda_stream)
         torch.cuda.synchronize()
         time.sleep(0.2)
-        after = nvlink_kib(handle, pynvml)
+        after = nvlink_counters(handle, pynvml)
         table.close()
         bench._barrier(world)
-        d = [(a - b) * 1024 / args.reps for a, b in zip(after, before)]
         direction, formula = expected[name]
         want = formula(nbytes)
-        got = d[0] if direction == "tx" else d[1]
-        out["algos"][name] = {"bytes": nbytes, "data_tx_per_exchange": round(d[0]), "data_rx_per_exchange": round(d[1]),
-                              "raw_tx_per_exchange": round(d[2]), "raw_rx_per_exchange": round(d[3]),
-                              "expected_" + direction: round(want), "ratio": round(got / want, 4) if want else None,
-                              "exchange_us": round(sec.value * 1e6, 2)}
+        rec = {"bytes": nbytes, "expected_" + direction: round(want), "exchange_us": round(sec.value * 1e6, 2)}
+        for cname in COUNTERS:
+            tx = (after[cname][0] - before[cname][0]) / args.reps
+            rx = (after[cname][1] - before[cname][1]) / args.reps
+            got = tx if direction == "tx" else rx
+            rec[cname] = {"tx_per_exchange": round(tx), "rx_per_exchange": round(rx), "links": after[cname][2],
+                          "ratio": round(got / want, 4) if want else None}
+        out["algos"][name] = rec
     session.raise_if_failed()
     session.close()
     gathered = [None] * world
