@@ -7,7 +7,7 @@
 #include "fused.cuh"
 #include "ll.cuh"
 #include "nvls.cuh"
-#include "push.cuh"
+#include "pipe.cuh"
 #include "rows.cuh"
 
 namespace mgw {
@@ -16,6 +16,7 @@ int launch_allreduce(const ArArgs& a, int algo, int max_ctas, cudaStream_t strea
 int launch_fused(const FusedArgs& f, int algo, int max_ctas, cudaStream_t stream, const int64_t* per_cta = nullptr);
 int launch_push(const PushArgs& x, int max_ctas, cudaStream_t stream, const int64_t* per_cta);
 int launch_push1(const PushArgs& x, int max_ctas, cudaStream_t stream, const int64_t* per_cta);
+int launch_push_pipe(const PushArgs& x, int max_ctas, cudaStream_t stream, const int64_t* per_cta);
 int launch_ll(const LLArgs& l, int max_ctas, cudaStream_t stream);
 int launch_ll_b16(const LLArgs& l, int max_ctas, cudaStream_t stream);
 int launch_b16(const FusedArgs& f, int algo, int max_ctas, cudaStream_t stream);
@@ -26,6 +27,7 @@ int launch_nvls(const NvlsArgs& x, int max_ctas, cudaStream_t stream, const int6
 int plan_fused(FusedArgs& f, int algo, int max_ctas, const int64_t* per_cta);
 int plan_push(PushArgs& x, int max_ctas, const int64_t* per_cta);
 int plan_push1(PushArgs& x, int max_ctas, const int64_t* per_cta);
+int plan_push_pipe(PushArgs& x, int max_ctas, const int64_t* per_cta);
 int plan_ll(LLArgs& l, int max_ctas);
 int plan_ll_b16(LLArgs& l, int max_ctas);
 int plan_b16(FusedArgs& f, int algo, int max_ctas);
@@ -33,7 +35,8 @@ int plan_b16(FusedArgs& f, int algo, int max_ctas);
 // Rank-group launches: every rank's planned CTAs in ONE cooperative launch on one device
 // (co-residency guaranteed, so ranks that wait on one another always run together).
 int launch_fused_group(const RankGroup<FusedArgs>& g, int world, int algo, cudaStream_t stream);
-int launch_push_group(const RankGroup<PushArgs>& g, int world, bool one, cudaStream_t stream);
+int launch_push_group(const RankGroup<PushArgs>& g, int world, int kind /* 0 two-shot, 1 one-shot, 2 pipe */,
+                      cudaStream_t stream);
 int launch_ll_group(const RankGroup<LLArgs>& g, int world, cudaStream_t stream);
 int launch_b16_group(const RankGroup<FusedArgs>& g, int world, int algo, cudaStream_t stream);
 int launch_ll_b16_group(const RankGroup<LLArgs>& g, int world, cudaStream_t stream);

@@ -263,7 +263,8 @@ int pick_fused_algo(const mgw_comm* c, int64_t n, int algo) {
 int resolve_fused_algo(const mgw_comm* c, int64_t n, int algo) {
   int chosen = pick_fused_algo(c, n, algo);
   if (chosen == MGW_ALGO_PUSH_ONESHOT && c->world * round_up(n, 16) * 4 > c->slot_bytes) chosen = MGW_ALGO_ONESHOT;
-  if (chosen == MGW_ALGO_PUSH && c->world * (((n / 4 + c->world - 1) / c->world + 1) * 4) * 4 > c->slot_bytes)
+  if ((chosen == MGW_ALGO_PUSH || chosen == MGW_ALGO_PUSH_PIPE) &&
+      c->world * (((n / 4 + c->world - 1) / c->world + 1) * 4) * 4 > c->slot_bytes)
     chosen = MGW_ALGO_TWOSHOT;
   return chosen;
 }
@@ -359,7 +360,7 @@ int comm_allreduce_fused(mgw_comm* c, const Row* host_rows, const Row* dev_rows,
     l.hdr_stride = (int64_t)kMaxBlocks * kMaxRanks;
     return launch_ll(l, c->max_ctas, stream);
   }
-  if (chosen == MGW_ALGO_PUSH_ONESHOT || chosen == MGW_ALGO_PUSH) {
+  if (chosen == MGW_ALGO_PUSH_ONESHOT || chosen == MGW_ALGO_PUSH || chosen == MGW_ALGO_PUSH_PIPE) {
     // incoming rows: one 64-B aligned row per source (one-shot), or one part + tail per
     // source (two-shot, push_stride()); resolve_fused_algo checked that they fit the slot
     const bool one = chosen == MGW_ALGO_PUSH_ONESHOT;
@@ -367,7 +368,11 @@ int comm_allreduce_fused(mgw_comm* c, const Row* host_rows, const Row* dev_rows,
     memset(&x, 0, sizeof(x));
     x.f = f;
     x.stride = one ? round_up(n, 16) : ((n / 4 + c->world - 1) / c->world + 1) * 4;
-    for (int s = 0; s < c->world; ++s) x.gather[s] = c->peer[s] + kSlotOff + 2 * c->slot_bytes;
+    for (int s = 0; s < c->world; ++s) {
+      x.gather[s] = c->peer[s] + kSlotOff + 2 * c->slot_bytes;
+      x.pipe[s] = reinterpret_cast<uint64_t*>(c->peer[s] + kPipeOff);
+    }
+    if (chosen == MGW_ALGO_PUSH_PIPE) return launch_push_pipe(x, c->max_ctas, stream, c->vec_per_cta);
     return one ? launch_push1(x, c->max_ctas, stream, c->vec_per_cta) : launch_push(x, c->max_ctas, stream, c->vec_per_cta);
   }
   return launch_fused(f, chosen, c->max_ctas, stream, c->vec_per_cta);
@@ -747,7 +752,8 @@ int mgw_group_allreduce_fused(mgw_comm* const* comms, void* const* tables, const
   if (chosen < 0) return MGW_OK;
   if (chosen == MGW_ALGO_NVLS) return set_error(MGW_EINVAL, "NVLS has no rank-group launch");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const bool ll = chosen == MGW_ALGO_LL, push = chosen == MGW_ALGO_PUSH || chosen == MGW_ALGO_PUSH_ONESHOT;
+  const bool ll = chosen == MGW_ALGO_LL,
+             push = chosen == MGW_ALGO_PUSH || chosen == MGW_ALGO_PUSH_ONESHOT || chosen == MGW_ALGO_PUSH_PIPE;
   // the argument blocks are large (8 ranks x ~1.5 KB): build them on the heap
   std::unique_ptr<RankGroup<FusedArgs>> gf(new RankGroup<FusedArgs>());
   std::unique_ptr<RankGroup<PushArgs>> gp(new RankGroup<PushArgs>());
@@ -788,8 +794,13 @@ int mgw_group_allreduce_fused(mgw_comm* const* comms, void* const* tables, const
       PushArgs& x = gp->args[r];
       x.f = f;
       x.stride = one ? round_up(n, 16) : ((n / 4 + world - 1) / world + 1) * 4;
-      for (int q = 0; q < world; ++q) x.gather[q] = c->peer[q] + kSlotOff + 2 * c->slot_bytes;
-      grid = one ? plan_push1(x, c->max_ctas, c->vec_per_cta) : plan_push(x, c->max_ctas, c->vec_per_cta);
+      for (int q = 0; q < world; ++q) {
+        x.gather[q] = c->peer[q] + kSlotOff + 2 * c->slot_bytes;
+        x.pipe[q] = reinterpret_cast<uint64_t*>(c->peer[q] + kPipeOff);
+      }
+      grid = one ? plan_push1(x, c->max_ctas, c->vec_per_cta)
+                 : (chosen == MGW_ALGO_PUSH_PIPE ? plan_push_pipe(x, c->max_ctas, c->vec_per_cta)
+                                                 : plan_push(x, c->max_ctas, c->vec_per_cta));
     } else {
       gf->args[r] = f;
       grid = b16 ? plan_b16(gf->args[r], chosen, c->max_ctas) : plan_fused(gf->args[r], chosen, c->max_ctas, c->vec_per_cta);
@@ -800,7 +811,8 @@ int mgw_group_allreduce_fused(mgw_comm* const* comms, void* const* tables, const
   if (first > 2 * kSMs)
     return set_error(MGW_EINVAL, "rank group needs %d co-resident CTAs (> %d): lower the CTA caps", first, 2 * kSMs);
   if (ll) return b16 ? launch_ll_b16_group(*gl, world, s) : launch_ll_group(*gl, world, s);
-  if (push) return launch_push_group(*gp, world, chosen == MGW_ALGO_PUSH_ONESHOT, s);
+  if (push)
+    return launch_push_group(*gp, world, chosen == MGW_ALGO_PUSH_ONESHOT ? 1 : (chosen == MGW_ALGO_PUSH_PIPE ? 2 : 0), s);
   return b16 ? launch_b16_group(*gf, world, chosen, s) : launch_fused_group(*gf, world, chosen, s);
 }
 
@@ -894,7 +906,7 @@ int mgw_allreduce(mgw_comm* c, int64_t n_elem, int algo, void* stream) {
 int mgw_allreduce_fused(mgw_comm* c, const void* table, int n_rows, int64_t n_elem, float scale, int algo,
                         void* stream) {
   if (!c) return set_error(MGW_EINVAL, "comm is null");
-  if (algo < MGW_ALGO_AUTO || algo > MGW_ALGO_PUSH_ONESHOT) return set_error(MGW_EINVAL, "unknown algorithm %d", algo);
+  if (algo < MGW_ALGO_AUTO || algo > MGW_ALGO_PUSH_PIPE) return set_error(MGW_EINVAL, "unknown algorithm %d", algo);
   int rc = check_table(table, n_rows, n_elem);
   if (rc) return rc;
   const mgw_table_t* t = as_table(table);
@@ -1122,7 +1134,8 @@ int mgw_allreduce_emulated(float* const* ins, float* const* outs, int world, int
 // Emulated ranks on one device: every rank packs its own layer tensors into its
 // slot, then the fused kernel (no barriers) folds and writes back, phase by phase.
 // emulated push exchanges: incoming rows and gather areas allocated here (test path)
-static int push_emulated(void* const* tables, int world, int64_t n, float scale, cudaStream_t s, bool oneshot) {
+static int push_emulated(void* const* tables, int world, int64_t n, float scale, cudaStream_t s, bool oneshot,
+                         bool pipe = false) {
   if (world < 2) return set_error(MGW_EINVAL, "push exchanges need >= 2 ranks");
   const int64_t stride = oneshot ? round_up(n, 16) : ((n / 4 + world - 1) / world + 1) * 4;
   char* mem = nullptr;
@@ -1152,7 +1165,8 @@ static int push_emulated(void* const* tables, int world, int64_t n, float scale,
       x.f.ar.rank = r;
       x.f.ar.flags = kNoBarrier | (step == 0 ? kSkipPhase1 | kSkipPhase2
                                              : kSkipPack | (step == 1 ? kSkipPhase2 : kSkipPhase1));
-      rc = oneshot ? launch_push1(x, 2 * kSMs, s, nullptr) : launch_push(x, 2 * kSMs, s, nullptr);
+      rc = oneshot ? launch_push1(x, 2 * kSMs, s, nullptr)
+                   : (pipe ? launch_push_pipe(x, 2 * kSMs, s, nullptr) : launch_push(x, 2 * kSMs, s, nullptr));
     }
   }
   cudaError_t e = cudaFreeAsync(mem, s);
@@ -1239,7 +1253,7 @@ int mgw_allreduce_fused_emulated(void* const* tables, float* const* slots, int w
     }
     return n == 0 ? MGW_OK : ll_emulated(tables, world, n, scale, static_cast<cudaStream_t>(stream), false);
   }
-  if (algo == MGW_ALGO_PUSH || algo == MGW_ALGO_PUSH_ONESHOT) {
+  if (algo == MGW_ALGO_PUSH || algo == MGW_ALGO_PUSH_ONESHOT || algo == MGW_ALGO_PUSH_PIPE) {
     for (int r = 0; r < world; ++r) {
       const mgw_table_t* t = as_table(tables[r]);
       int rc = check_table(tables[r], t ? (int)t->host.size() : 0, n);
@@ -1247,7 +1261,7 @@ int mgw_allreduce_fused_emulated(void* const* tables, float* const* slots, int w
     }
     return n == 0 ? MGW_OK
                   : push_emulated(tables, world, n, scale, static_cast<cudaStream_t>(stream),
-                                  algo == MGW_ALGO_PUSH_ONESHOT);
+                                  algo == MGW_ALGO_PUSH_ONESHOT, algo == MGW_ALGO_PUSH_PIPE);
   }
   if (algo != MGW_ALGO_ONESHOT && algo != MGW_ALGO_TWOSHOT)
     return set_error(MGW_EINVAL, "emulated all-reduce needs an explicit algorithm");

@@ -30,6 +30,8 @@ struct PushArgs {
   FusedArgs f;                 // f.ar.slot[r] = rank r's slot 0 (incoming area for parity 0)
   char* gather[kMaxRanks];     // rank r's gather area 0 (parity 1 follows at f.ar.slot_stride)
   int64_t stride;              // incoming row stride in elements (multiple of 4)
+  uint64_t* pipe[kMaxRanks];   // pipelined two-shot (pipe.cuh): rank r's sub-chunk flags
+  int subs;                    // pipelined two-shot: sub-chunks per CTA chunk
 };
 
 __device__ __forceinline__ int64_t push_stride(int64_t nv, int world) {

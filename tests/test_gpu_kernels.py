@@ -191,7 +191,7 @@ def _fused_emulated(torch, per_rank_tensors, counts, algo, scale=1.0):
 
 
 @pytest.mark.parametrize("algo", [_native.ALGO_ONESHOT, _native.ALGO_TWOSHOT, _native.ALGO_PUSH,
-                                  _native.ALGO_PUSH_ONESHOT, _native.ALGO_LL])
+                                  _native.ALGO_PUSH_ONESHOT, _native.ALGO_LL, _native.ALGO_PUSH_PIPE])
 @pytest.mark.parametrize("n_ranks", [2, 3, 4, 8])
 @pytest.mark.parametrize("shift", [0, 1])
 def test_fused_exchange_bit_exact(torch_cuda, algo, n_ranks, shift):
@@ -330,3 +330,25 @@ def test_pack_unpack_paths_r50_bucket(torch_cuda, path, misaligned_every):
     finally:
         _native.call("mgw_set_option", _native.OPT_ROWS_PATH, 0)
         table.close()
+
+
+@pytest.mark.parametrize("n_ranks", [2, 3, 4, 8])
+@pytest.mark.parametrize("n", [2_000_003, 4_194_304 + 1, 12_582_917])
+def test_push_pipe_sub_chunks_bit_exact(torch_cuda, n_ranks, n):
+    """Pipelined push two-shot with several sub-chunks per CTA chunk (sizes where S > 1),
+    segment-straddling slots and an n % 4 tail: bit-exact with the reference ring."""
+    torch = torch_cuda
+    gen = torch.Generator(device="cuda").manual_seed(n_ranks * 31 + n)
+    ins = [torch.randn(n, generator=gen, device="cuda") for _ in range(n_ranks)]
+    want = ring_oracle.ring_allreduce([x.cpu().numpy() for x in ins])[0]
+    tables = [_native.DeviceTable([(x.data_ptr(), n, 0)]) for x in ins]
+    slots = [torch.empty(n, device="cuda") for _ in range(n_ranks)]
+    tp = (ctypes.c_void_p * n_ranks)(*[t.ptr for t in tables])
+    sp = (ctypes.c_void_p * n_ranks)(*[x.data_ptr() for x in slots])
+    _native.call("mgw_allreduce_fused_emulated", tp, sp, n_ranks, n, ctypes.c_float(1.0), _native.ALGO_PUSH_PIPE,
+                 torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    for t in tables:
+        t.close()
+    for x in ins:
+        assert np.array_equal(x.cpu().numpy().view("<u4"), want.view("<u4"))
