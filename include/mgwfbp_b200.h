@@ -72,6 +72,8 @@ extern "C" {
 #define MGW_SCHED_HOSTIO 4u /* e2e: H2D of each layer from host_src, D2H of the result to host_dst */
 #define MGW_SCHED_FUSED 8u  /* one kernel per group: pack + all-reduce + unpack (N > 1) */
 #define MGW_SCHED_PDL 16u   /* the group's exchange launches while its fill runs (programmatic event) */
+#define MGW_SCHED_BF16 32u  /* rows are bf16 tensors (counts in bf16 elements): bf16 fill, bf16 group
+                               exchange with fp32 accumulation (mgw_allreduce_fused_bf16), always fused */
 
 typedef struct mgw_comm mgw_comm;
 typedef struct mgw_sched mgw_sched;

@@ -626,6 +626,7 @@ def run_emulation(
     warmup: int = 2,
     graph: bool = False,
     fused: bool = True,
+    dtype=None,
 ) -> EmulationReport:
     """Measure the overlapped iteration (Algorithm 2) on the GPUs.
 
@@ -650,10 +651,13 @@ def run_emulation(
     # (GradientBuffer.for_group, allreduce_net.py:98-120, :495-509), and so does this path.
     from .overlap import OverlappedIteration
 
-    largest = max((sum(p for _, p, _ in rows) for _, _, rows in _layout(profile, plan)), default=0)
-    if 4 * largest > session.capacity_bytes:
-        raise ValueError(f"largest group needs {4 * largest} B, session capacity is {session.capacity_bytes} B")
     torch = session.torch
+    # dtype=torch.bfloat16: the same Algorithm 2 on bf16 gradients (bf16 wire, fp32
+    # accumulation); default fp32 as the reference
+    width = 2 if dtype == torch.bfloat16 else 4
+    largest = max((sum(p for _, p, _ in rows) for _, _, rows in _layout(profile, plan)), default=0)
+    if width * largest > session.capacity_bytes:
+        raise ValueError(f"largest group needs {width * largest} B, session capacity is {session.capacity_bytes} B")
     with torch.cuda.device(session.device):
         it = OverlappedIteration(
             profile,
@@ -665,6 +669,7 @@ def run_emulation(
             fill=True,
             graph=graph,
             fused=fused,
+            dtype=dtype,
         )
         try:
             walls, computes, exposed = [], [], []
@@ -679,7 +684,7 @@ def run_emulation(
                 for (low, _, rows), t in zip(it.layout, times.group_comm):
                     if rows:
                         size = sum(p for _, p, _ in rows)
-                        session.account(size, _algo_for(session, size, fused=fused))
+                        session.account(size, _algo_for(session, size, fused=fused, elem_bytes=width), width)
                         if k >= warmup:
                             per_group[low].append(t)
                 if k >= warmup:

@@ -27,6 +27,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda_bf16.h>
+
 #include "allreduce.cuh"
 #include "bf16.cuh"
 #include "launch.h"
@@ -63,6 +65,17 @@ __global__ void clock_mark_kernel(uint64_t* clock) {
 // advances the device call counter by one (timing of the gate alone, kind 6)
 __global__ void finish_kernel(uint32_t* state) {
   if (threadIdx.x == 0) state[0] += 1u;
+}
+
+// bf16 gradient "production" of the engine (MGW_SCHED_BF16): row k of the group gets
+// values[k] (the reference pattern rank + 1 + layer % 5, exact in bf16)
+__global__ void fill_b16_kernel(const Row* rows, int n_rows, const float* values) {
+  for (int k = 0; k < n_rows; ++k) {
+    uint16_t* p = reinterpret_cast<uint16_t*>(rows[k].ptr);
+    const uint16_t v = __bfloat16_as_ushort(__float2bfloat16_rn(values[k]));
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows[k].count; e += (int64_t)gridDim.x * blockDim.x)
+      p[e] = v;
+  }
 }
 
 __global__ void spin_until_kernel(const uint64_t* clock, int64_t deadline_ns) {
@@ -400,9 +413,31 @@ int local_fused(float* bucket, const Row* host_rows, const Row* dev_rows, int n_
   return launch_fused(f, MGW_ALGO_ONESHOT, 2 * kSMs, stream);
 }
 
+// Single rank, bf16 gradients: the bf16 group kernel with N = 1 (pack -> one-input fold
+// in fp32 -> bf16 write-back), the engine's stand-in like local_fused.
+int local_fused_b16(uint16_t* bucket, const Row* host_rows, const Row* dev_rows, int n_rows, int64_t n, float scale,
+                    cudaStream_t stream, uint64_t* stamp = nullptr) {
+  if (n == 0 || n_rows == 0) return MGW_OK;
+  FusedArgs f;
+  memset(&f, 0, sizeof(f));
+  f.ar.slot[0] = reinterpret_cast<char*>(bucket);
+  f.ar.n = n;
+  f.ar.world = 1;
+  f.ar.flags = kNoBarrier;
+  f.ar.stamp = stamp;
+  f.use_inline = n_rows <= kInlineRows && host_rows != nullptr;
+  if (f.use_inline)
+    for (int k = 0; k < n_rows; ++k) f.inline_rows[k] = host_rows[k];
+  f.rows = dev_rows;
+  f.n_rows = n_rows;
+  f.scale = scale;
+  return launch_b16(f, MGW_ALGO_ONESHOT, 2 * kSMs, stream);
+}
+
 // bf16 group exchange with fp32 accumulation (bf16.cuh): one-shot / two-shot only
 int comm_allreduce_fused_bf16(mgw_comm* c, const Row* host_rows, const Row* dev_rows, int n_rows, int64_t n,
-                              float scale, int algo, cudaStream_t stream, uint64_t* stamp = nullptr) {
+                              float scale, int algo, cudaStream_t stream, uint64_t* stamp = nullptr,
+                              int64_t group_tag = -1) {
   if (n < 0 || n * 2 > c->slot_bytes)
     return set_error(MGW_EINVAL, "bf16 bucket of %lld elements exceeds slot capacity %lld B", (long long)n,
                      (long long)c->slot_bytes);
@@ -413,6 +448,7 @@ int comm_allreduce_fused_bf16(mgw_comm* c, const Row* host_rows, const Row* dev_
   FusedArgs f;
   memset(&f, 0, sizeof(f));
   f.ar = make_args(c, n);
+  if (group_tag >= 0) f.ar.tag = (uint32_t)group_tag;
   if (c->world > 1 && c->gate) {
     int rc = launch_gate(f.ar, stream);
     if (rc) return rc;
@@ -1487,6 +1523,8 @@ int mgw_sched_create(mgw_comm* comm, const mgw_tensor_desc* rows, int n_rows, co
   if ((flags & MGW_SCHED_FILL) && !fill_values) return set_error(MGW_EINVAL, "MGW_SCHED_FILL needs fill_values");
   if ((flags & MGW_SCHED_HOSTIO) && (!host_src || !host_dst))
     return set_error(MGW_EINVAL, "MGW_SCHED_HOSTIO needs host_src and host_dst");
+  if ((flags & MGW_SCHED_BF16) && (flags & MGW_SCHED_HOSTIO))
+    return set_error(MGW_EINVAL, "MGW_SCHED_HOSTIO moves fp32 host buffers; it does not combine with MGW_SCHED_BF16");
   int64_t max_elems = 0;
   for (int g = 0; g < n_groups; ++g) {
     const mgw_group& gr = groups[g];
@@ -1504,7 +1542,7 @@ int mgw_sched_create(mgw_comm* comm, const mgw_tensor_desc* rows, int n_rows, co
     max_elems = std::max(max_elems, gr.n_elem);
   }
   const int world = comm ? comm->world : 1;
-  if (comm && max_elems * 4 > comm->slot_bytes)
+  if (comm && max_elems * ((flags & MGW_SCHED_BF16) ? 2 : 4) > comm->slot_bytes)
     return set_error(MGW_EINVAL, "largest group (%lld B) exceeds the communicator slot (%lld B)",
                      (long long)(max_elems * 4), (long long)comm->slot_bytes);
   mgw_sched* s = new mgw_sched();
@@ -1551,7 +1589,7 @@ int mgw_sched_create(mgw_comm* comm, const mgw_tensor_desc* rows, int n_rows, co
     launches += 1;  // spin
     if (groups[g].n_elem == 0) continue;
     launches += (flags & MGW_SCHED_FILL) ? 1 : 0;  // gradient production
-    if (flags & MGW_SCHED_FUSED)
+    if (flags & (MGW_SCHED_FUSED | MGW_SCHED_BF16))
       launches += 1 + (world > 1 && comm->gate ? 1 : 0);  // (gate +) fused pack + all-reduce + unpack
     else
       launches += world > 1 ? 3 : 2;               // pack (+ all-reduce) + unpack
@@ -1596,7 +1634,13 @@ static int sched_enqueue(mgw_sched* s, cudaStream_t cs, cudaStream_t ms) {
       // exchange for SMs and HBM.  MGW_SCHED_PDL: the ready event is the fill's
       // programmatic event, so the group's exchange launches while the fill runs and
       // waits for it on the device (grid_dep_wait) instead of paying a launch after it.
-      const bool pdl = (s->flags & MGW_SCHED_PDL) != 0;
+      const bool pdl = (s->flags & MGW_SCHED_PDL) != 0 && !(s->flags & MGW_SCHED_BF16);
+      if (s->flags & MGW_SCHED_BF16) {
+        fill_b16_kernel<<<2 * kSMs, kThreads, 0, cs>>>(d_rows + gr.desc_begin, gr.desc_count, s->d_fill + gr.desc_begin);
+        MGW_CHECK_LAUNCH();
+        MGW_CUDA(cudaEventRecord(s->dep_ready[g], cs));
+        continue;
+      }
       int rc = launch_rows<RowOp::kFill>(s->rows.data() + gr.desc_begin, d_rows + gr.desc_begin, gr.desc_count, nullptr,
                                          gr.n_elem, 1.f, s->d_fill + gr.desc_begin, nullptr, 0, nullptr, cs, nullptr,
                                          pdl ? s->dep_ready[g] : nullptr);
@@ -1618,7 +1662,13 @@ static int sched_enqueue(mgw_sched* s, cudaStream_t cs, cudaStream_t ms) {
     MGW_CUDA(cudaStreamWaitEvent(ms, s->dep_ready[g], 0));
     if (gr.n_elem == 0) continue;  // silent group: nothing to send (allreduce_net.py:549)
     int rc;
-    if (s->world == 1 && (s->flags & MGW_SCHED_FUSED)) {
+    if (s->flags & MGW_SCHED_BF16) {  // bf16 gradients, fp32 accumulation (bf16.cuh), always fused
+      rc = s->world == 1 ? local_fused_b16(reinterpret_cast<uint16_t*>(s->local_bucket), hrows, grows, gr.desc_count,
+                                           gr.n_elem, s->scale, ms, st + 2)
+                         : comm_allreduce_fused_bf16(s->comm, hrows, grows, gr.desc_count, gr.n_elem, s->scale, gr.algo,
+                                                     ms, st + 2, (uint32_t)gr.head_layer);
+      if (rc) return rc;
+    } else if (s->world == 1 && (s->flags & MGW_SCHED_FUSED)) {
       rc = local_fused(s->local_bucket, hrows, grows, gr.desc_count, gr.n_elem, s->scale, ms, st + 2);
       if (rc) return rc;
     } else if (s->world == 1) {

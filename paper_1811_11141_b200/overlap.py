@@ -98,6 +98,7 @@ class OverlappedIteration:
         tensors: dict | None = None,
         fused: bool = False,
         pdl: bool = True,
+        dtype=None,
     ) -> None:
         import torch
 
@@ -114,10 +115,16 @@ class OverlappedIteration:
             fill = False  # gradients arrive from the host instead
         self.fill, self.host_io, self.scale = fill, host_io, float(scale)
         self.torch = torch
+        self.dtype = torch.float32 if dtype is None else dtype
+        if self.dtype not in (torch.float32, torch.bfloat16):
+            raise ValueError(f"gradients are fp32 or bf16, got {self.dtype}")
+        self.bf16 = self.dtype == torch.bfloat16
+        if self.bf16 and host_io:
+            raise ValueError("the end-to-end host legs move fp32 buffers")
         counts = profile.param_counts()
         if tensors is None:
             tensors = {
-                layer: torch.zeros(p, dtype=torch.float32, device=self.device)
+                layer: torch.zeros(p, dtype=self.dtype, device=self.device)
                 for layer, p in enumerate(counts, start=1)
                 if p
             }
@@ -133,8 +140,8 @@ class OverlappedIteration:
             n_elem = 0
             for layer, p, off in grows:
                 t = tensors[layer]
-                if t.numel() != p or t.dtype != torch.float32 or not t.is_contiguous():
-                    raise ValueError(f"layer {layer}: need a contiguous float32 tensor of {p} elements")
+                if t.numel() != p or t.dtype != self.dtype or not t.is_contiguous():
+                    raise ValueError(f"layer {layer}: need a contiguous {self.dtype} tensor of {p} elements")
                 rows.append((t.data_ptr(), p, off))
                 fills.append(float(rank + 1 + layer % 5))
                 n_elem += p
@@ -151,6 +158,8 @@ class OverlappedIteration:
         flags = (_native.SCHED_FILL if fill else 0) | (_native.SCHED_GRAPH if graph else 0)
         if fused:
             flags |= _native.SCHED_FUSED
+        if self.bf16:
+            flags |= _native.SCHED_BF16  # bf16 wire and bucket, fp32 accumulation (always fused)
         if pdl and fill:
             flags |= _native.SCHED_PDL  # the exchange launches while the fill runs
         self.fused = fused
@@ -231,7 +240,8 @@ class OverlappedIteration:
 
     def group_bytes(self) -> tuple[int, ...]:
         """Bucket bytes of each group, send order."""
-        return tuple(4 * sum(p for _, p, _ in rows) for _, _, rows in self.layout)
+        width = 2 if self.bf16 else 4
+        return tuple(width * sum(p for _, p, _ in rows) for _, _, rows in self.layout)
 
     def verify(self) -> bool:
         """Every layer equals the reference's expected reduced constant
@@ -239,6 +249,11 @@ class OverlappedIteration:
         torch = self.torch
         if not self._check_rows:
             return True
+        if self.bf16:  # the expected sums are small integers, exact in bf16
+            self.compute_stream.synchronize()
+            self.comm_stream.synchronize()
+            return all(bool((self.tensors[layer] == self._expected(layer)).all())
+                       for _, _, grows in self.layout for layer, _, _ in grows)
         if self._check_table is None:
             self._check_table = _native.DeviceTable(self._check_rows)
             self._expect_dev = torch.tensor(self._expect, dtype=torch.float32, device=self.device)

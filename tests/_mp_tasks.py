@@ -436,3 +436,14 @@ def iteration_mismatch_task(config, session):
 
     _native.call("mgw_comm_set_timeout_ms", session.comm, 20000)
     return _timed_collective(config, session, np.ones(5000, dtype="<f4"), layer_low=2, iteration=config.rank)
+
+
+def emulate_bf16_task(config, session, *, profile, plan):
+    """run_emulation on bf16 gradients (bf16 wire, fp32 accumulation) with the reference's
+    exact-sum verification."""
+    import torch
+
+    from paper_1811_11141_b200 import run_emulation
+
+    rep = run_emulation(profile, plan, config, session, 3, warmup=1, graph=True, dtype=torch.bfloat16)
+    return rep.verified, rep.allreduce_count

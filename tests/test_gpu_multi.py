@@ -10,12 +10,14 @@ import pytest
 import _mp_tasks
 from conftest import ROOT, cuda_devices, golden_ring, make_profile
 from paper_1811_11141_b200 import (
+    CommModel,
     EmulationReport,
     MergePlan,
     bench_local,
     emulate_local,
     find_merge_plan,
     fit_ab,
+    resnet50_like,
     run_workers,
     simulate_mgwfbp,
     synth_profile,
@@ -286,3 +288,15 @@ def test_threshold_disagreement_raises_fast():
         for seconds, err in outcomes:
             assert err is not None and ("disagree" in err or "aborted" in err), (rank, err)
             assert seconds < 1.0, (rank, seconds)
+
+
+def test_emulate_bf16_engine_verified():
+    from functools import partial
+
+    profile = resnet50_like(backward_seconds=4e-3, forward_seconds=2e-3)
+    plan = find_merge_plan(profile, CommModel(a=2e-5, b=1.5e-12))
+    for n in _worlds():
+        res = run_workers(n, partial(_mp_tasks.emulate_bf16_task, profile=profile, plan=plan))
+        for verified, count in res.values():
+            assert verified
+            assert count == 4 * len(plan.groups())

@@ -115,3 +115,26 @@ def test_autograd_sync_single_gpu(torch_cuda):
             assert torch.equal(p.grad, w)
     finally:
         sync.close()
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_bf16_engine_single_gpu(torch_cuda, graph):
+    """Algorithm 2 on bf16 gradients (MGW_SCHED_BF16: bf16 fill, the bf16 group kernel with
+    fp32 accumulation): every plan verifies the reference's exact sums, timeline as fp32."""
+    torch = torch_cuda
+    profile = resnet50_like(backward_seconds=4e-3, forward_seconds=2e-3)
+    compute = profile.forward_time + profile.total_backward_time
+    for name, plan in _plans(profile).items():
+        it = OverlappedIteration(profile, plan, comm=None, rank=0, world=1, device="cuda:0", graph=graph, fused=True,
+                                 dtype=torch.bfloat16)
+        try:
+            for _ in range(3):
+                t = it.run()
+            assert it.verify(), name
+            assert abs(t.compute_time - compute) / compute < 0.02, (name, t)
+            assert it.group_bytes()[0] == 2 * sum(p for _, p, _ in it.layout[0][2])
+        finally:
+            it.close()
+    with pytest.raises(ValueError):
+        OverlappedIteration(profile, None, comm=None, rank=0, world=1, device="cuda:0", host_io=True,
+                            dtype=torch.bfloat16)
