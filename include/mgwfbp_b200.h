@@ -245,6 +245,11 @@ int mgw_sched_times(mgw_sched* sched, double* t_iter_s, double* compute_s, doubl
 /* per-group kernel execution spans of the last iteration, from %globaltimer stamps the
  * kernels write themselves (first CTA entry .. last CTA exit) */
 int mgw_sched_kernel_times(mgw_sched* sched, double* pack_s, double* allreduce_s, double* unpack_s);
+/* measured schedule of the last iteration, seconds from its clock mark (the simulated
+ * backward's time origin, schedule_sim.py:103-127): per group, when its gradients were
+ * produced (end of its fill kernel; -1 without MGW_SCHED_FILL) and its exchange window
+ * (first kernel entry .. last kernel exit) -- the rows of a measured Timeline (Timeline.events) */
+int mgw_sched_events(mgw_sched* sched, double* ready_s, double* comm_start_s, double* comm_end_s);
 int mgw_sched_launches(mgw_sched* sched, int* kernels_per_iteration);
 int mgw_sched_destroy(mgw_sched* sched);
 

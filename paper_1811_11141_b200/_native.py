@@ -112,6 +112,8 @@ _SIGNATURES = {
     "mgw_sched_run": ([_P, _P, _P], _I),
     "mgw_sched_times": ([_P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)], _I),
     "mgw_sched_kernel_times": ([_P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)], _I),
+    "mgw_sched_events": ([_P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                          ctypes.POINTER(ctypes.c_double)], _I),
     "mgw_sched_launches": ([_P, ctypes.POINTER(_I)], _I),
     "mgw_sched_destroy": ([_P], _I),
 }

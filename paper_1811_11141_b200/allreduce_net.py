@@ -197,6 +197,9 @@ class EmulationReport:
     allreduce_count: int
     compute_seconds: tuple[float, ...] = ()
     t_c_no_seconds: tuple[float, ...] = ()
+    # Gantt rows (layer, kind, start_s, end_s) of the last iteration, measured by the
+    # kernels' own stamps (Timeline.events, schedule_sim.py:88-100)
+    events: tuple[tuple[int, str, float, float], ...] = ()
 
 
 # ----------------------------------------------------------------- bootstrap
@@ -691,6 +694,7 @@ def run_emulation(
                     walls.append(times.t_iter)
                     computes.append(times.compute_time)
                     exposed.append(times.t_c_no)
+            events = tuple(it.measured_timeline().events(profile))
         finally:
             it.close()
     return EmulationReport(
@@ -704,6 +708,7 @@ def run_emulation(
         allreduce_count=count,
         compute_seconds=tuple(computes),
         t_c_no_seconds=tuple(exposed),
+        events=events,
     )
 
 

@@ -69,13 +69,15 @@ __global__ void finish_kernel(uint32_t* state) {
 
 // bf16 gradient "production" of the engine (MGW_SCHED_BF16): row k of the group gets
 // values[k] (the reference pattern rank + 1 + layer % 5, exact in bf16)
-__global__ void fill_b16_kernel(const Row* rows, int n_rows, const float* values) {
+__global__ void fill_b16_kernel(const Row* rows, int n_rows, const float* values, uint64_t* stamp) {
+  stamp_enter(stamp);
   for (int k = 0; k < n_rows; ++k) {
     uint16_t* p = reinterpret_cast<uint16_t*>(rows[k].ptr);
     const uint16_t v = __bfloat16_as_ushort(__float2bfloat16_rn(values[k]));
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows[k].count; e += (int64_t)gridDim.x * blockDim.x)
       p[e] = v;
   }
+  stamp_exit(stamp);
 }
 
 __global__ void spin_until_kernel(const uint64_t* clock, int64_t deadline_ns) {
@@ -124,6 +126,8 @@ struct mgw_comm {
   bool local_group = false;    // in-process rank group on one device (mgw_comm_create_local)
 };
 
+constexpr int kSchedStamps = 8;  // per group: [pack][all-reduce / fused][unpack][fill] x [start, end]
+
 struct mgw_sched {
   mgw_comm* comm = nullptr;
   int world = 1;
@@ -133,7 +137,7 @@ struct mgw_sched {
   float* d_fill = nullptr;
   float* local_bucket = nullptr;  // single-rank bucket
   uint64_t* d_clock = nullptr;
-  uint64_t* d_stamps = nullptr;   // per group: pack, all-reduce, unpack spans (3 x [start, end])
+  uint64_t* d_stamps = nullptr;   // per group: pack, all-reduce / fused, unpack, fill spans (4 x [start, end])
   std::vector<uint64_t> h_stamps;
   float scale = 1.f;
   uint32_t flags = 0;
@@ -1556,7 +1560,7 @@ int mgw_sched_create(mgw_comm* comm, const mgw_tensor_desc* rows, int n_rows, co
     s->host_src.assign(host_src, host_src + n_rows);
     s->host_dst.assign(host_dst, host_dst + n_rows);
   }
-  s->h_stamps.assign((size_t)n_groups * 6, 0);
+  s->h_stamps.assign((size_t)n_groups * kSchedStamps + 1, 0);  // + the iteration's clock mark
   cudaError_t e = cudaMalloc(&s->d_rows, sizeof(Row) * (size_t)std::max(1, n_rows));
   if (e == cudaSuccess && n_rows > 0) e = cudaMemcpy(s->d_rows, rows, sizeof(Row) * (size_t)n_rows, cudaMemcpyHostToDevice);
   if (e == cudaSuccess && (flags & MGW_SCHED_FILL)) {
@@ -1567,8 +1571,8 @@ int mgw_sched_create(mgw_comm* comm, const mgw_tensor_desc* rows, int n_rows, co
   if (e == cudaSuccess && world == 1) e = cudaMalloc(&s->local_bucket, std::max<size_t>(256, (size_t)max_elems * 4));
   if (e == cudaSuccess) e = cudaMalloc(&s->d_clock, sizeof(uint64_t));
   if (e == cudaSuccess) e = cudaMemset(s->d_clock, 0, sizeof(uint64_t));
-  if (e == cudaSuccess) e = cudaMalloc(&s->d_stamps, sizeof(uint64_t) * (size_t)n_groups * 6);
-  if (e == cudaSuccess) e = cudaMemset(s->d_stamps, 0, sizeof(uint64_t) * (size_t)n_groups * 6);
+  if (e == cudaSuccess) e = cudaMalloc(&s->d_stamps, sizeof(uint64_t) * (size_t)n_groups * kSchedStamps);
+  if (e == cudaSuccess) e = cudaMemset(s->d_stamps, 0, sizeof(uint64_t) * (size_t)n_groups * kSchedStamps);
   auto mk = [&](cudaEvent_t* ev, bool timing) {
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, timing ? cudaEventDefault : cudaEventDisableTiming);
   };
@@ -1613,7 +1617,7 @@ static int sched_enqueue(mgw_sched* s, cudaStream_t cs, cudaStream_t ms) {
     int rc = comm_allreduce(s->comm, 0, MGW_ALGO_ONESHOT, cs);
     if (rc) return rc;
   }
-  stamps_reset_kernel<<<1, 256, 0, cs>>>(s->d_stamps, n_groups * 3);
+  stamps_reset_kernel<<<1, 256, 0, cs>>>(s->d_stamps, n_groups * kSchedStamps / 2);
   MGW_CHECK_LAUNCH();
   MGW_CUDA(record_timing(s, s->t_start, cs));
   MGW_CUDA(cudaEventRecord(s->dep_fork, cs));
@@ -1636,14 +1640,15 @@ static int sched_enqueue(mgw_sched* s, cudaStream_t cs, cudaStream_t ms) {
       // waits for it on the device (grid_dep_wait) instead of paying a launch after it.
       const bool pdl = (s->flags & MGW_SCHED_PDL) != 0 && !(s->flags & MGW_SCHED_BF16);
       if (s->flags & MGW_SCHED_BF16) {
-        fill_b16_kernel<<<2 * kSMs, kThreads, 0, cs>>>(d_rows + gr.desc_begin, gr.desc_count, s->d_fill + gr.desc_begin);
+        fill_b16_kernel<<<2 * kSMs, kThreads, 0, cs>>>(d_rows + gr.desc_begin, gr.desc_count, s->d_fill + gr.desc_begin,
+                                                     s->d_stamps + kSchedStamps * (size_t)g + 6);
         MGW_CHECK_LAUNCH();
         MGW_CUDA(cudaEventRecord(s->dep_ready[g], cs));
         continue;
       }
       int rc = launch_rows<RowOp::kFill>(s->rows.data() + gr.desc_begin, d_rows + gr.desc_begin, gr.desc_count, nullptr,
-                                         gr.n_elem, 1.f, s->d_fill + gr.desc_begin, nullptr, 0, nullptr, cs, nullptr,
-                                         pdl ? s->dep_ready[g] : nullptr);
+                                         gr.n_elem, 1.f, s->d_fill + gr.desc_begin, nullptr, 0, nullptr, cs,
+                                         s->d_stamps + kSchedStamps * (size_t)g + 6, pdl ? s->dep_ready[g] : nullptr);
       if (rc) return rc;
       if (!pdl) MGW_CUDA(cudaEventRecord(s->dep_ready[g], cs));
     } else {
@@ -1658,7 +1663,7 @@ static int sched_enqueue(mgw_sched* s, cudaStream_t cs, cudaStream_t ms) {
     const mgw_group& gr = s->groups[g];
     const Row* grows = d_rows + gr.desc_begin;
     const Row* hrows = s->rows.data() + gr.desc_begin;
-    uint64_t* st = s->d_stamps + 6 * (size_t)g;
+    uint64_t* st = s->d_stamps + kSchedStamps * (size_t)g;
     MGW_CUDA(cudaStreamWaitEvent(ms, s->dep_ready[g], 0));
     if (gr.n_elem == 0) continue;  // silent group: nothing to send (allreduce_net.py:549)
     int rc;
@@ -1731,8 +1736,23 @@ int mgw_sched_run(mgw_sched* s, void* compute_stream, void* comm_stream) {
 
 static int sched_fetch_stamps(mgw_sched* s) {
   MGW_CUDA(cudaEventSynchronize(s->t_end));
-  MGW_CUDA(cudaMemcpy(s->h_stamps.data(), s->d_stamps, sizeof(uint64_t) * s->h_stamps.size(), cudaMemcpyDeviceToHost));
+  const size_t n = s->groups.size() * kSchedStamps;
+  MGW_CUDA(cudaMemcpy(s->h_stamps.data(), s->d_stamps, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
+  MGW_CUDA(cudaMemcpy(s->h_stamps.data() + n, s->d_clock, sizeof(uint64_t), cudaMemcpyDeviceToHost));
   return MGW_OK;
+}
+
+// the group's exchange window from its kernel stamps [pack, all-reduce / fused, unpack]
+static bool exchange_window(const uint64_t* st, uint64_t* t0, uint64_t* t1) {
+  uint64_t lo = ~0ull, hi = 0;
+  for (int k = 0; k < 3; ++k) {
+    if (st[2 * k] == ~0ull || st[2 * k + 1] < st[2 * k]) continue;  // kernel not launched
+    lo = st[2 * k] < lo ? st[2 * k] : lo;
+    hi = st[2 * k + 1] > hi ? st[2 * k + 1] : hi;
+  }
+  *t0 = lo;
+  *t1 = hi;
+  return lo != ~0ull;
 }
 
 static double span_s(const uint64_t* st) {
@@ -1754,9 +1774,10 @@ int mgw_sched_times(mgw_sched* s, double* t_iter_s, double* compute_s, double* g
   }
   if (group_comm_s) {
     for (size_t g = 0; g < s->groups.size(); ++g) {
-      const uint64_t* st = &s->h_stamps[6 * g];
-      // pack entry .. unpack exit: the group's whole exchange on the comm stream
-      group_comm_s[g] = (st[0] == ~0ull || st[5] < st[0]) ? 0.0 : (double)(st[5] - st[0]) * 1e-9;
+      // first kernel entry .. last kernel exit of the group's exchange on the comm stream
+      // (unfused: pack .. unpack; fused: the one kernel)
+      uint64_t t0, t1;
+      group_comm_s[g] = exchange_window(&s->h_stamps[kSchedStamps * g], &t0, &t1) ? (double)(t1 - t0) * 1e-9 : 0.0;
     }
   }
   return MGW_OK;
@@ -1767,10 +1788,30 @@ int mgw_sched_kernel_times(mgw_sched* s, double* pack_s, double* allreduce_s, do
   int rc = sched_fetch_stamps(s);
   if (rc) return rc;
   for (size_t g = 0; g < s->groups.size(); ++g) {
-    const uint64_t* st = &s->h_stamps[6 * g];
+    const uint64_t* st = &s->h_stamps[kSchedStamps * g];
     pack_s[g] = span_s(st);
     allreduce_s[g] = span_s(st + 2);
     unpack_s[g] = span_s(st + 4);
+  }
+  return MGW_OK;
+}
+
+int mgw_sched_events(mgw_sched* s, double* ready_s, double* comm_start_s, double* comm_end_s) {
+  if (!s || !ready_s || !comm_start_s || !comm_end_s) return set_error(MGW_EINVAL, "bad arguments");
+  int rc = sched_fetch_stamps(s);
+  if (rc) return rc;
+  const uint64_t origin = s->h_stamps[s->groups.size() * kSchedStamps];  // the iteration's clock mark
+  for (size_t g = 0; g < s->groups.size(); ++g) {
+    const uint64_t* st = &s->h_stamps[kSchedStamps * g];
+    const bool filled = st[6] != ~0ull && st[7] >= st[6];
+    ready_s[g] = filled ? ((double)st[7] - (double)origin) * 1e-9 : -1.0;
+    uint64_t t0, t1;
+    if (exchange_window(st, &t0, &t1)) {
+      comm_start_s[g] = ((double)t0 - (double)origin) * 1e-9;
+      comm_end_s[g] = ((double)t1 - (double)origin) * 1e-9;
+    } else {
+      comm_start_s[g] = comm_end_s[g] = -1.0;
+    }
   }
   return MGW_OK;
 }

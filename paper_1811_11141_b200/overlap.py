@@ -238,6 +238,39 @@ class OverlappedIteration:
         g = self.n_groups
         return tuple(pack[:g]), tuple(ar[:g]), tuple(unpack[:g])
 
+    def measured_timeline(self, strategy=None):
+        """The last iteration as a ``Timeline`` (schedule_sim.py:65-100), from the kernels'
+        own %globaltimer stamps relative to the iteration's clock mark (the simulated
+        backward's origin): a group's backward is shifted by how late its gradient fill
+        ended against the schedule, its head layer's comm row is the measured exchange
+        window (first kernel entry .. last exit), merged layers carry zero-length rows as
+        in the simulator, and t_iter = the later of the last exchange and the backward.
+        ``Timeline.events(profile)`` then gives the measured Gantt rows."""
+        from .schedule_sim import OverlapCase, Strategy, Timeline
+
+        k = max(1, self.n_groups)
+        ready, c0, c1 = (ctypes.c_double * k)(), (ctypes.c_double * k)(), (ctypes.c_double * k)()
+        _native.call("mgw_sched_events", self._sched, ready, c0, c1)
+        prof = self.profile
+        n = prof.num_layers
+        t_b = prof.backward_times()
+        tau_sim = backward_start_times(prof)
+        tau_b, tau_c, t_c, comm_end = list(tau_sim), [0.0] * n, [0.0] * n, [0.0] * n
+        for g, (low, high, grows) in enumerate(self.layout):
+            due = tau_sim[low - 1] + t_b[low - 1]
+            late = ready[g] - due if ready[g] >= 0.0 else 0.0
+            for layer in range(low, high + 1):
+                tau_b[layer - 1] = tau_sim[layer - 1] + late
+            start, end = (c0[g], c1[g]) if (grows and c0[g] >= 0.0) else (due + late, due + late)
+            for layer in range(low, high + 1):
+                tau_c[layer - 1] = comm_end[layer - 1] = start
+            tau_c[low - 1], comm_end[low - 1], t_c[low - 1] = start, end, end - start
+        compute = tau_b[0] + t_b[0]
+        t_iter = max([compute] + comm_end)
+        return Timeline(strategy=strategy or Strategy.MGWFBP, tau_b=tuple(tau_b), tau_c=tuple(tau_c),
+                        t_c=tuple(t_c), comm_end=tuple(comm_end), t_iter=t_iter, compute_time=compute,
+                        t_c_no=t_iter - compute, case=OverlapCase.NOT_APPLICABLE)
+
     def group_bytes(self) -> tuple[int, ...]:
         """Bucket bytes of each group, send order."""
         width = 2 if self.bf16 else 4

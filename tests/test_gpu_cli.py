@@ -46,12 +46,17 @@ def test_emulate_verb_verified(tmp_path, two_gpus):
     plan = tmp_path / "plan.json"
     plan.write_text("[2, 3, 4]\n")
     report = tmp_path / "report.json"
+    events = tmp_path / "events.csv"
     proc = _run(["emulate", "--profile", str(ppath), "--nodes", "2", "--plan", str(plan), "--iterations", "3",
-                 "--warmup", "1", "--out", str(report)])
+                 "--warmup", "1", "--out", str(report), "--events-csv", str(events)])
     assert proc.returncode == 0, proc.stderr
     assert "verified=True" in proc.stdout
     doc = json.loads(report.read_text())
-    assert doc
+    assert set(doc) == {"0", "1"} and all(d["verified"] for d in doc.values())
+    rows = events.read_text().splitlines()
+    assert rows[0] == "layer,kind,start_s,end_s"
+    kinds = [r.split(",")[1] for r in rows[1:]]
+    assert kinds.count("backward") == 54 and kinds.count("comm") == 51  # groups {2,3,4} -> 51 messages
 
 
 def test_worker_subcommand_pair(tmp_path, two_gpus):

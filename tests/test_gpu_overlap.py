@@ -138,3 +138,34 @@ def test_bf16_engine_single_gpu(torch_cuda, graph):
     with pytest.raises(ValueError):
         OverlappedIteration(profile, None, comm=None, rank=0, world=1, device="cuda:0", host_io=True,
                             dtype=torch.bfloat16)
+
+
+@pytest.mark.parametrize("plan_name", ["wfbp", "mgwfbp", "synceasgd"])
+def test_measured_timeline_events(torch_cuda, plan_name):
+    """The engine's own stamps give a measured Timeline (schedule_sim.py:65-100): one
+    backward row per layer, one comm row per sending group (at its head layer), every
+    exchange starting after its gradients were produced, t_iter >= compute, and the
+    measured compute / exposed time close to the event-timed IterationTimes."""
+    from paper_1811_11141_b200.schedule_sim import Timeline
+
+    profile = resnet50_like(backward_seconds=4e-3, forward_seconds=2e-3)
+    plan = _plans(profile)[plan_name]
+    it = OverlappedIteration(profile, plan, comm=None, rank=0, world=1, device="cuda:0", graph=True, fused=True)
+    try:
+        for _ in range(3):
+            times = it.run()
+        tl = it.measured_timeline()
+    finally:
+        it.close()
+    assert isinstance(tl, Timeline)
+    rows = tl.events(profile)
+    back = [r for r in rows if r[1] == "backward"]
+    comm = [r for r in rows if r[1] == "comm"]
+    assert len(back) == profile.num_layers
+    assert {r[0] for r in comm} == {low for low, _ in plan.groups()}
+    for layer, _, t0, t1 in comm:
+        ready = tl.tau_b[layer - 1] + profile.backward_times()[layer - 1]
+        assert t0 >= ready - 1e-6 and t1 >= t0, (layer, t0, ready)
+    assert tl.t_iter >= tl.compute_time
+    assert abs(tl.compute_time - times.compute_time) < 5e-5
+    assert abs(tl.t_c_no - times.t_c_no) < 2e-5
