@@ -75,18 +75,20 @@ __device__ __forceinline__ float* fused_tensor1(const FusedArgs& f, int k, int64
   return r.ptr + (e - r.offset);
 }
 
-// Out-of-line slow paths (a 16-B slot straddling two rows or two reference segments, or
-// sitting at a misaligned tensor address).  Inlined into every unrolled hot loop they made
-// the N = 1 group kernel 82 KB of SASS; a small group's launch runs ~2 us, so fetching a
-// large kernel body from L2 on cold SMs is a visible share of it.
-static __device__ __noinline__ void pack4_slow(const FusedArgs& f, float* slot, int k, int64_t e, float scale) {
+// Slow paths (a 16-B slot straddling two rows or two reference segments, or sitting at a
+// misaligned tensor address).  kOol = out of line: the N = 1 group kernel calls them as
+// functions -- inlined into every unrolled hot loop they made it 82 KB of SASS, and a small
+// group's launch runs ~2 us, so fetching a large body from L2 on cold SMs is a visible share
+// of it (in-step spans -5 %, profiles/n1_group_spans_r02.json).  The N >= 2 kernels inline
+// them: a call there makes the caller spill around it.
+__device__ __forceinline__ void pack4_body(const FusedArgs& f, float* slot, int k, int64_t e, float scale) {
   for (int j = 0; j < 4; ++j) {
     const float y = *fused_tensor1(f, k, e + j);
     slot[e + j] = scale != 1.0f ? __fmul_rn(y, scale) : y;
   }
 }
 
-static __device__ __noinline__ void store4_slow(const FusedArgs& f, int k, int64_t e, float4 v) {
+__device__ __forceinline__ void store4_body(const FusedArgs& f, int k, int64_t e, float4 v) {
   *fused_tensor1(f, k, e) = v.x;
   *fused_tensor1(f, k, e + 1) = v.y;
   *fused_tensor1(f, k, e + 2) = v.z;
@@ -95,8 +97,8 @@ static __device__ __noinline__ void store4_slow(const FusedArgs& f, int k, int64
 
 // four elements whose fold starts differ (the slot straddles a reference segment boundary)
 template <int N>
-__device__ __noinline__ void fold4_slow(const FusedArgs& f, const float* const* in, const int64_t* seg_end, int s, int k,
-                                        int64_t e, float* own) {
+__device__ __forceinline__ void fold4_body(const FusedArgs& f, const float* const* in, const int64_t* seg_end, int s,
+                                           int k, int64_t e, float* own) {
   for (int j = 0; j < 4; ++j) {
     s = advance_segment(s, e + j, seg_end);
     const float y = fold1<N>(in, s, e + j);
@@ -105,10 +107,37 @@ __device__ __noinline__ void fold4_slow(const FusedArgs& f, const float* const* 
   }
 }
 
+static __device__ __noinline__ void pack4_ool(const FusedArgs& f, float* slot, int k, int64_t e, float scale) {
+  pack4_body(f, slot, k, e, scale);
+}
+static __device__ __noinline__ void store4_ool(const FusedArgs& f, int k, int64_t e, float4 v) {
+  store4_body(f, k, e, v);
+}
+template <int N>
+__device__ __noinline__ void fold4_ool(const FusedArgs& f, const float* const* in, const int64_t* seg_end, int s, int k,
+                                       int64_t e, float* own) {
+  fold4_body<N>(f, in, seg_end, s, k, e, own);
+}
+
+template <bool kOol>
+__device__ __forceinline__ void pack4_slow(const FusedArgs& f, float* slot, int k, int64_t e, float scale) {
+  if constexpr (kOol) pack4_ool(f, slot, k, e, scale); else pack4_body(f, slot, k, e, scale);
+}
+template <bool kOol>
+__device__ __forceinline__ void store4_slow(const FusedArgs& f, int k, int64_t e, float4 v) {
+  if constexpr (kOol) store4_ool(f, k, e, v); else store4_body(f, k, e, v);
+}
+template <int N, bool kOol>
+__device__ __forceinline__ void fold4_slow(const FusedArgs& f, const float* const* in, const int64_t* seg_end, int s,
+                                           int k, int64_t e, float* own) {
+  if constexpr (kOol) fold4_ool<N>(f, in, seg_end, s, k, e, own); else fold4_body<N>(f, in, seg_end, s, k, e, own);
+}
+
 // Pack bucket vectors [v0, v1) (16-B slots) plus scalar elements [t0, t1) into `slot`.
 // UP slots per thread are loaded before any is stored (ncu r01: one outstanding 16-B load
 // per thread left the pack phase latency-bound on long-scoreboard stalls).
-static __device__ void fused_pack_range(const FusedArgs& f, float* slot, int64_t v0, int64_t v1, int64_t t0, int64_t t1) {
+template <bool kOol = false>
+__device__ void fused_pack_range(const FusedArgs& f, float* slot, int64_t v0, int64_t v1, int64_t t0, int64_t t1) {
   constexpr int UP = 4;
   const float scale = f.scale;
   const bool scaled = scale != 1.0f;
@@ -138,7 +167,7 @@ static __device__ void fused_pack_range(const FusedArgs& f, float* slot, int64_t
         if (fast[u])
           *reinterpret_cast<float4*>(slot + e) = scaled ? fmul4(x[u], scale) : x[u];
         else
-          pack4_slow(f, slot, ku[u], e, scale);
+          pack4_slow<kOol>(f, slot, ku[u], e, scale);
       }
     }
   }
@@ -194,9 +223,9 @@ __device__ void fused_reduce_range(const FusedArgs& f, const float* const* in, c
         if (fast)
           *reinterpret_cast<float4*>(tp) = acc;
         else
-          store4_slow(f, k, e, acc);
+          store4_slow<N == 1>(f, k, e, acc);
       } else {
-        fold4_slow<N>(f, in, seg_end, su[u], k, e, own);
+        fold4_slow<N, N == 1>(f, in, seg_end, su[u], k, e, own);
       }
     }
   }
@@ -236,7 +265,7 @@ static __device__ void fused_scatter_range(const FusedArgs& f, const float* src,
         if (fast)
           *reinterpret_cast<float4*>(tp) = x[u];
         else
-          store4_slow(f, k, e, x[u]);
+          store4_slow<false>(f, k, e, x[u]);
       }
     }
   }
@@ -261,7 +290,7 @@ __device__ __forceinline__ void fused_oneshot_body(const FusedArgs& f, const int
   const bool last = cta == ctas - 1;
   float* mine = const_cast<float*>(s_in[a.rank]);
   phase_mark(a, 0, cta);
-  if (!(a.flags & kSkipPack)) fused_pack_range(f, mine, v0, v1, last ? nv << 2 : 0, last ? a.n : 0);
+  if (!(a.flags & kSkipPack)) fused_pack_range<N == 1>(f, mine, v0, v1, last ? nv << 2 : 0, last ? a.n : 0);
   phase_mark(a, 1, cta);
   int status = MGW_DEV_OK;
   if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, a.tag, a, cta);
@@ -309,27 +338,31 @@ __device__ void fused_pack_parts(const FusedArgs& f, float* slot, const PartChun
   int cur[N];
 #pragma unroll
   for (int p = 0; p < N; ++p) cur[p] = fused_row_covering(f, (pc.lo[p] + (threadIdx.x < pc.len[p] ? threadIdx.x : 0)) << 2);
+  constexpr int PB = N <= 4 ? N : 4;  // parts per batch of loads in flight (N = 7, 8 spilled)
   for (int64_t i = threadIdx.x; i < pc.longest; i += kThreads) {
-    float4 x[N];
-    float* tp[N];
-    bool fast[N];
 #pragma unroll
-    for (int p = 0; p < N; ++p) {
-      fast[p] = false;
-      if (i < pc.len[p]) {
-        const int64_t e = (pc.lo[p] + i) << 2;
-        tp[p] = fused_tensor(f, cur[p], e, fast[p]);
-        if (fast[p]) x[p] = *reinterpret_cast<const float4*>(tp[p]);
+    for (int pb = 0; pb < N; pb += PB) {
+      float4 x[PB];
+      bool fast[PB];
+#pragma unroll
+      for (int q = 0; q < PB; ++q) {
+        const int p = pb + q;
+        fast[q] = false;
+        if (p < N && i < pc.len[p]) {
+          const float* tp = fused_tensor(f, cur[p], (pc.lo[p] + i) << 2, fast[q]);
+          if (fast[q]) x[q] = *reinterpret_cast<const float4*>(tp);
+        }
       }
-    }
 #pragma unroll
-    for (int p = 0; p < N; ++p) {
-      if (i >= pc.len[p]) continue;
-      const int64_t e = (pc.lo[p] + i) << 2;
-      if (fast[p])
-        *reinterpret_cast<float4*>(slot + e) = scaled ? fmul4(x[p], scale) : x[p];
-      else
-        pack4_slow(f, slot, cur[p], e, scale);
+      for (int q = 0; q < PB; ++q) {
+        const int p = pb + q;
+        if (p >= N || i >= pc.len[p]) continue;
+        const int64_t e = (pc.lo[p] + i) << 2;
+        if (fast[q])
+          *reinterpret_cast<float4*>(slot + e) = scaled ? fmul4(x[q], scale) : x[q];
+        else
+          pack4_slow<false>(f, slot, cur[p], e, scale);
+      }
     }
   }
 }
@@ -354,7 +387,7 @@ __device__ void fused_scatter_parts(const FusedArgs& f, const float* const* in, 
       if (fast)
         *reinterpret_cast<float4*>(tp) = x[p];
       else
-        store4_slow(f, cur[p], e, x[p]);
+        store4_slow<false>(f, cur[p], e, x[p]);
     }
   }
 }

@@ -18,10 +18,16 @@ int plan_fused(FusedArgs& f, int algo, int max_ctas, const int64_t* per_cta) {
 
 template <int N>
 static int launch_fused_n(const FusedArgs& f, int algo, int grid, cudaStream_t stream) {
-  if (algo == MGW_ALGO_ONESHOT)
+  if (N == 1 && algo != MGW_ALGO_ONESHOT)  // one rank: the one-input fold is the one-shot
+    return set_error(MGW_EINVAL, "a single rank runs the one-shot group kernel only");
+  if constexpr (N == 1) {
     fused_oneshot_kernel<N><<<grid, kThreads, 0, stream>>>(f);
-  else
-    fused_twoshot_kernel<N><<<grid, kThreads, 0, stream>>>(f);
+  } else {
+    if (algo == MGW_ALGO_ONESHOT)
+      fused_oneshot_kernel<N><<<grid, kThreads, 0, stream>>>(f);
+    else
+      fused_twoshot_kernel<N><<<grid, kThreads, 0, stream>>>(f);
+  }
   MGW_CHECK_LAUNCH();
   return MGW_OK;
 }

@@ -151,7 +151,7 @@ __device__ __forceinline__ void push_pipe_body(const PushArgs& x, const int cta,
           if (fast[p])
             *reinterpret_cast<float4*>(dst) = scaled ? fmul4(v[p], scale) : v[p];
           else
-            pack4_slow(f, dst - e, cur[p], e, scale);  // dst - e: the row base, indexed by e
+            pack4_slow<false>(f, dst - e, cur[p], e, scale);  // dst - e: the row base, indexed by e
         }
       }
       if (last && it == S - 1) {  // the n % 4 tail belongs to part N-1
@@ -210,7 +210,7 @@ __device__ __forceinline__ void push_pipe_body(const PushArgs& x, const int cta,
         if (fast)
           *reinterpret_cast<float4*>(tp) = y;
         else
-          store4_slow(f, k, e, y);
+          store4_slow<false>(f, k, e, y);
       }
       if (last && me == N - 1 && jb == S - 1) {
         for (int64_t e = tail0 + threadIdx.x; e < a.n; e += kThreads) {

@@ -70,31 +70,35 @@ __device__ __forceinline__ void push_twoshot_body(const PushArgs& x, const int c
 #pragma unroll
     for (int p = 0; p < N; ++p)
       cur[p] = fused_row_covering(f, (pc.lo[p] + (threadIdx.x < pc.len[p] ? threadIdx.x : 0)) << 2);
+    // parts in batches of at most PB loads in flight: N = 8 with all parts at once
+    // overflowed the 64 registers of the (512, 2) launch bounds and spilled
+    constexpr int PB = N <= 4 ? N : 4;
     for (int64_t i = threadIdx.x; i < pc.longest; i += kThreads) {
-      float4 v[N];
-      bool fast[N];
 #pragma unroll
-      for (int p = 0; p < N; ++p) {
-        fast[p] = false;
-        if (i < pc.len[p]) {
-          const float* tp = fused_tensor(f, cur[p], (pc.lo[p] + i) << 2, fast[p]);
-          if (fast[p]) v[p] = *reinterpret_cast<const float4*>(tp);
-        }
-      }
+      for (int pb = 0; pb < N; pb += PB) {
+        float4 v[PB];
+        bool fast[PB];
 #pragma unroll
-      for (int p = 0; p < N; ++p) {
-        if (i >= pc.len[p]) continue;
-        const int64_t e = (pc.lo[p] + i) << 2;
-        float* dst = const_cast<float*>(s_in[p]) + (int64_t)me * stride + (e - s_part0[p]);
-        MGW_EXPECT(e >= s_part0[p] && e + 4 <= s_part0[p] + stride &&
-                   (a.slot_stride == 0 || (int64_t)N * stride * 4 <= a.slot_stride));
-        if (fast[p]) {
-          *reinterpret_cast<float4*>(dst) = scaled ? fmul4(v[p], scale) : v[p];
-        } else {
-          for (int j = 0; j < 4; ++j) {
-            const float y = *fused_tensor1(f, cur[p], e + j);
-            dst[j] = scaled ? __fmul_rn(y, scale) : y;
+        for (int q = 0; q < PB; ++q) {
+          const int p = pb + q;
+          fast[q] = false;
+          if (p < N && i < pc.len[p]) {
+            const float* tp = fused_tensor(f, cur[p], (pc.lo[p] + i) << 2, fast[q]);
+            if (fast[q]) v[q] = *reinterpret_cast<const float4*>(tp);
           }
+        }
+#pragma unroll
+        for (int q = 0; q < PB; ++q) {
+          const int p = pb + q;
+          if (p >= N || i >= pc.len[p]) continue;
+          const int64_t e = (pc.lo[p] + i) << 2;
+          float* dst = const_cast<float*>(s_in[p]) + (int64_t)me * stride + (e - s_part0[p]);
+          MGW_EXPECT(e >= s_part0[p] && e + 4 <= s_part0[p] + stride &&
+                     (a.slot_stride == 0 || (int64_t)N * stride * 4 <= a.slot_stride));
+          if (fast[q])
+            *reinterpret_cast<float4*>(dst) = scaled ? fmul4(v[q], scale) : v[q];
+          else
+            pack4_slow<false>(f, dst - e, cur[p], e, scale);  // dst - e: the row base, indexed by e
         }
       }
     }
