@@ -68,10 +68,10 @@ static_assert(kDoorOff + kMaxRanks * sizeof(uint64_t) <= kCtrlBytes, "control ar
 constexpr int64_t kLLElems = 262144;  // 1 MB of fp32 payload per source per parity
 constexpr size_t kLLOff = kCtrlBytes;
 constexpr size_t kLLBytes = 2 * (size_t)kMaxRanks * (size_t)kLLElems * sizeof(uint64_t);
-// pipelined two-shot flags u64 [2 kind][2 parity][kMaxBlocks][kPipeSub][kMaxRanks src]
+// pipelined two-shot flags u64 [2 kind][2 parity][kMaxBlocks][16 warp][kPipeSub][kMaxRanks src]
 constexpr int kPipeSub = 8;
 constexpr size_t kPipeOff = kLLOff + kLLBytes;
-constexpr size_t kPipeBytes = 2 * 2 * (size_t)kMaxBlocks * kPipeSub * kMaxRanks * sizeof(uint64_t);
+constexpr size_t kPipeBytes = 2 * 2 * (size_t)kMaxBlocks * (kThreads / 32) * kPipeSub * kMaxRanks * sizeof(uint64_t);
 constexpr size_t kSlotOff = kPipeOff + kPipeBytes;
 
 struct Row {  // identical layout to mgw_tensor_desc

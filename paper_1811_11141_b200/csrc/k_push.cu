@@ -32,12 +32,20 @@ int plan_push(PushArgs& x, int max_ctas, const int64_t* per_cta) {
 
 // the pipelined two-shot: the push two-shot's grid, S sub-chunks of >= one slot per thread
 // per part (at most kPipeSub) -- S follows from n and the grid, so every rank agrees
+static int64_t g_pipe_sub_slots = kThreads;  // slots per sub-chunk per part (mgw_set_option)
+
+int set_pipe_sub_slots(int64_t v) {
+  if (v < 32 || v > (1 << 20)) return set_error(MGW_EINVAL, "pipe sub-chunk slots must lie in 32..2^20");
+  g_pipe_sub_slots = v;
+  return MGW_OK;
+}
+
 int plan_push_pipe(PushArgs& x, int max_ctas, const int64_t* per_cta) {
   const uint32_t user_tag = x.f.ar.tag;
   const int grid = plan_push(x, max_ctas, per_cta);
   const int w = x.f.ar.world > 0 ? x.f.ar.world : 1;
   const int64_t chunk = ((x.f.ar.n >> 2) / w + grid - 1) / grid;  // slots per CTA per part
-  int64_t subs = chunk / kThreads;
+  int64_t subs = chunk / g_pipe_sub_slots;
   x.subs = (int)(subs < 1 ? 1 : (subs > kPipeSub ? kPipeSub : subs));
   x.f.ar.tag = collective_tag(user_tag, x.f.ar.n, kTagPushPipe, grid * 16 + x.subs, x.f.scale);
   return grid;

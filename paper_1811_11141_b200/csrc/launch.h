@@ -61,6 +61,7 @@ inline int launch_cooperative(void (*kernel)(const RankGroup<Args>), const RankG
 }
 
 int set_rows_path(int v);
+int set_pipe_sub_slots(int64_t v);  // pipelined two-shot: slots per sub-chunk per part
 
 // checked build: per translation unit violation counters (MGW_EXPECT in common.cuh)
 int violations_allreduce(unsigned long long* out, bool reset);

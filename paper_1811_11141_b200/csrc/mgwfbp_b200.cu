@@ -859,6 +859,7 @@ int mgw_group_allreduce_fused(mgw_comm* const* comms, void* const* tables, const
 int mgw_set_option(int key, int64_t value) {
   switch (key) {
     case MGW_OPT_ROWS_PATH: return set_rows_path((int)value);
+    case MGW_OPT_PIPE_SUB_SLOTS: return set_pipe_sub_slots(value);
     default: return set_error(MGW_EINVAL, "unknown option %d", key);
   }
 }

@@ -20,36 +20,41 @@
 // so the NVLink stores of stage A (sub-chunk i) and B (sub-chunk i-1) are in flight
 // together and a late peer delays one sub-chunk, not the whole chunk.  Deadlock-free:
 // within an iteration every signal precedes every wait, and the waits of iteration i need
-// only signals of iterations <= i-1.  Flags: (epoch << 32 | collective tag) at
-// pipe[r][kind][parity][b][sub][src], reuse distance 2 by parity as for the barrier flags.
+// only signals of iterations <= i-1.  Thread t handles the same slots (t, t + 512, ...) of a
+// sub-chunk in all three stages on every rank, so warp w only ever waits for warp w of its
+// peers: flags are per warp, the pipeline has no CTA-wide barrier, and while one warp's
+// release fence waits for its NVLink stores to land the other 15 keep issuing (a CTA-wide
+// flag stalled the whole CTA for a round trip per sub-chunk stage -- 2x slower, measured).
+// Flags: (epoch << 32 | collective tag) at pipe[r][kind][parity][b][warp][sub][src], reuse
+// distance 2 by parity as for the barrier flags.
 #pragma once
 
 #include "push.cuh"
 
 namespace mgw {
 
-__device__ __forceinline__ size_t pipe_index(int kind, int parity, int cta, int sub, int src) {
-  return ((((size_t)kind * 2 + parity) * kMaxBlocks + cta) * kPipeSub + sub) * kMaxRanks + src;
+constexpr int kWarps = kThreads / 32;
+
+__device__ __forceinline__ size_t pipe_index(int kind, int parity, int cta, int warp, int sub, int src) {
+  return (((((size_t)kind * 2 + parity) * kMaxBlocks + cta) * kWarps + warp) * kPipeSub + sub) * kMaxRanks + src;
 }
 
-// every peer learns that this CTA finished stage `kind` of sub-chunk `sub`
+// this warp's stage `kind` of sub-chunk `sub` is done: tell every peer (its stores first)
 __device__ __forceinline__ void pipe_signal(const PushArgs& x, int kind, int parity, int cta, int sub, uint64_t word) {
-  __syncthreads();  // orders the CTA's data stores before the release below
-  const int t = threadIdx.x;
-  if (t < x.f.ar.world && t != x.f.ar.rank) store_release_sys(x.pipe[t] + pipe_index(kind, parity, cta, sub, x.f.ar.rank), word);
+  __syncwarp();  // orders the warp's data stores before the release below
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane < x.f.ar.world && lane != x.f.ar.rank)
+    store_release_sys(x.pipe[lane] + pipe_index(kind, parity, cta, warp, sub, x.f.ar.rank), word);
 }
 
-// wait until every peer signalled stage `kind` of sub-chunk `sub` for this CTA index
+// wait until the same warp of every peer's CTA `cta` signalled stage `kind` of `sub`
 static __device__ __noinline__ int pipe_wait(const PushArgs& x, int kind, int parity, int cta, int sub, uint32_t epoch) {
   const ArArgs& a = x.f.ar;
-  __shared__ int s_status;
-  if (threadIdx.x == 0) s_status = MGW_DEV_OK;
-  __syncthreads();
-  const int t = threadIdx.x;
-  if (t < a.world && t != a.rank) {
-    const uint64_t* mine = x.pipe[a.rank] + pipe_index(kind, parity, cta, sub, t);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int status = MGW_DEV_OK;
+  if (lane < a.world && lane != a.rank) {
+    const uint64_t* mine = x.pipe[a.rank] + pipe_index(kind, parity, cta, warp, sub, lane);
     const uint64_t start = global_ns();
-    int status = MGW_DEV_OK;
     for (uint32_t spin = 0;; ++spin) {
       const uint64_t v = load_acquire_sys(mine);
       if ((uint32_t)(v >> 32) == epoch) {
@@ -67,11 +72,11 @@ static __device__ __noinline__ int pipe_wait(const PushArgs& x, int kind, int pa
         }
       }
     }
-    if (status != MGW_DEV_OK) atomicCAS(&s_status, 0, status);
   }
-  __syncthreads();
-  const int status = s_status;
-  if (status != MGW_DEV_OK && threadIdx.x == 0) {
+  // the warp agrees on the worst status (max: MISMATCH 1 < TIMEOUT 2 < PEER_ABORT 3 -- any
+  // non-zero stops the warp) and orders its later reads after the acquiring lanes' loads
+  status = __reduce_max_sync(0xffffffffu, status);
+  if (status != MGW_DEV_OK && lane == 0) {
     atomicCAS(a.err, 0, status);
     if (status != MGW_DEV_PEER_ABORT)
       for (int r = 0; r < a.world; ++r) store_release_sys32(a.abort_flag[r], 1u);
@@ -107,54 +112,61 @@ __device__ __forceinline__ void push_pipe_body(const PushArgs& x, const int cta,
   if (threadIdx.x <= N) s_part0[threadIdx.x] = part_begin(threadIdx.x, nv, N) << 2;
   __syncthreads();
   MGW_EXPECT(S >= 1 && S <= kPipeSub && (a.slot_stride == 0 || (int64_t)N * stride * 4 <= a.slot_stride));
-  // sub-chunk j of part p: slots [sub_lo(p, j), sub_lo(p, j + 1))
-  auto sub_lo = [&](int p, int j) { return pc.lo[p] + pc.len[p] * j / S; };
+  // sub-chunk j of part p: slots [s_sub[p][j], s_sub[p][j + 1]) (shared: the bounds stay out of
+  // the registers); thread t always handles the slots t, t + 512, ... of a sub-chunk in every
+  // stage, so warp w depends only on warp w of every peer (per-warp flags: no CTA-wide
+  // barrier inside the pipeline)
+  __shared__ int64_t s_sub[kMaxRanks][kPipeSub + 1];
+  if (threadIdx.x < N * (S + 1)) {
+    const int p = threadIdx.x / (S + 1), j = threadIdx.x % (S + 1);
+    s_sub[p][j] = pc.lo[p] + pc.len[p] * j / S;
+  }
+  __syncthreads();
+  auto sub_lo = [&](int p, int j) { return s_sub[p][j]; };
+  constexpr int PB = N <= 4 ? N : 4;  // parts per batch of loads in flight
 
   int status = MGW_DEV_OK;
   for (int it = 0; it < S + 2 && status == MGW_DEV_OK; ++it) {
     // ---- A: push sub-chunk `it` of every part p into rank p's incoming row `me`
     if (do_push && it < S) {
-      // this sub-chunk's bounds per part live in shared memory (registers go to the data)
-      __shared__ int64_t lo[kMaxRanks], len[kMaxRanks], s_longest;
-      __syncthreads();  // the previous iteration's readers are done with lo / len
-      if (threadIdx.x == 0) {
+#pragma unroll
+      for (int pb = 0; pb < N; pb += PB) {
         int64_t longest = 0;
-        for (int p = 0; p < N; ++p) {
-          lo[p] = sub_lo(p, it);
-          len[p] = sub_lo(p, it + 1) - lo[p];
-          longest = len[p] > longest ? len[p] : longest;
+        int cur[PB];
+#pragma unroll
+        for (int q = 0; q < PB; ++q) {
+          const int p = pb + q < N ? pb + q : N - 1;
+          const int64_t len = pb + q < N ? sub_lo(p, it + 1) - sub_lo(p, it) : 0;
+          longest = len > longest ? len : longest;
+          cur[q] = fused_row_covering(f, (sub_lo(p, it) + (threadIdx.x < len ? threadIdx.x : 0)) << 2);
         }
-        s_longest = longest;
-      }
-      __syncthreads();
-      const int64_t longest = s_longest;
-      int cur[N];
+        for (int64_t i = threadIdx.x; i < longest; i += kThreads) {
+          float4 v[PB];
+          bool fast[PB];
 #pragma unroll
-      for (int p = 0; p < N; ++p) cur[p] = fused_row_covering(f, (lo[p] + (threadIdx.x < len[p] ? threadIdx.x : 0)) << 2);
-      for (int64_t i = threadIdx.x; i < longest; i += kThreads) {
-        float4 v[N];
-        bool fast[N];
+          for (int q = 0; q < PB; ++q) {
+            fast[q] = false;
+            const int p = pb + q < N ? pb + q : N - 1;
+            if (pb + q < N && i < sub_lo(p, it + 1) - sub_lo(p, it)) {
+              const float* tp = fused_tensor(f, cur[q], (sub_lo(p, it) + i) << 2, fast[q]);
+              if (fast[q]) v[q] = *reinterpret_cast<const float4*>(tp);
+            }
+          }
 #pragma unroll
-        for (int p = 0; p < N; ++p) {
-          fast[p] = false;
-          if (i < len[p]) {
-            const float* tp = fused_tensor(f, cur[p], (lo[p] + i) << 2, fast[p]);
-            if (fast[p]) v[p] = *reinterpret_cast<const float4*>(tp);
+          for (int q = 0; q < PB; ++q) {
+            const int p = pb + q;
+            if (p >= N || i >= sub_lo(p, it + 1) - sub_lo(p, it)) continue;
+            const int64_t e = (sub_lo(p, it) + i) << 2;
+            float* dst = const_cast<float*>(s_in[p]) + (int64_t)me * stride + (e - s_part0[p]);
+            MGW_EXPECT(e >= s_part0[p] && e + 4 <= s_part0[p] + stride);
+            if (fast[q])
+              *reinterpret_cast<float4*>(dst) = scaled ? fmul4(v[q], scale) : v[q];
+            else
+              pack4_slow<false>(f, dst - e, cur[q], e, scale);  // dst - e: the row base, indexed by e
           }
         }
-#pragma unroll
-        for (int p = 0; p < N; ++p) {
-          if (i >= len[p]) continue;
-          const int64_t e = (lo[p] + i) << 2;
-          float* dst = const_cast<float*>(s_in[p]) + (int64_t)me * stride + (e - s_part0[p]);
-          MGW_EXPECT(e >= s_part0[p] && e + 4 <= s_part0[p] + stride);
-          if (fast[p])
-            *reinterpret_cast<float4*>(dst) = scaled ? fmul4(v[p], scale) : v[p];
-          else
-            pack4_slow<false>(f, dst - e, cur[p], e, scale);  // dst - e: the row base, indexed by e
-        }
       }
-      if (last && it == S - 1) {  // the n % 4 tail belongs to part N-1
+      if (last && it == S - 1) {  // the n % 4 tail belongs to part N-1 (threads 0..2: warp 0)
         float* dst = const_cast<float*>(s_in[N - 1]) + (int64_t)me * stride - s_part0[N - 1];
         for (int64_t e = tail0 + threadIdx.x; e < a.n; e += kThreads) {
           const float y = *fused_tensor1(f, fused_row_covering(f, e), e);

@@ -24,6 +24,7 @@ def main() -> int:
     ap.add_argument("--mib", default="1,4,8,16,32,64,128")
     ap.add_argument("--algos", default="twoshot,push,push_pipe,auto")
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--pipe-subs", default="", help="comma list of pipelined sub-chunk slots to sweep")
     args = ap.parse_args()
     import torch
 
@@ -48,6 +49,14 @@ def main() -> int:
             key = name + ("@graph" if graph else "@stream")
             out["us"][key] = [round(x * 1e6, 2) for x in t]
             out["bus_gbs"][key] = [round(2 * (world - 1) / world * s / x / 1e9, 1) for s, x in zip(sizes, t)]
+    for slots in [int(v) for v in args.pipe_subs.split(",") if v]:
+        _native.call("mgw_set_option", _native.OPT_PIPE_SUB_SLOTS, slots)
+        t = bench._exchange_times(comm, world, device, sizes, kind=4 | 256, algo=_native.ALGO_PUSH_PIPE,
+                                  repeats=args.reps)
+        key = f"push_pipe_sub{slots}@graph"
+        out["us"][key] = [round(x * 1e6, 2) for x in t]
+        out["bus_gbs"][key] = [round(2 * (world - 1) / world * s / x / 1e9, 1) for s, x in zip(sizes, t)]
+    _native.call("mgw_set_option", _native.OPT_PIPE_SUB_SLOTS, 512)
     nccl = bench._nccl_times(world, device, sizes, repeats=args.reps)
     out["us"]["nccl@stream"] = [round(x * 1e6, 2) for x in nccl]
     out["bus_gbs"]["nccl@stream"] = [round(2 * (world - 1) / world * s / x / 1e9, 1) for s, x in zip(sizes, nccl)]
