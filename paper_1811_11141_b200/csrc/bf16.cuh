@@ -400,38 +400,11 @@ __device__ __forceinline__ void ll_b16_body(const LLArgs& l, const int cta, cons
     for (int r = 0; r < N; ++r) st_relaxed_sys_v2(l.ll[r] + my_off + 2 * j, w0, w1);
   }
 
-  // 2. CTA 0 checks every peer's header (length and dtype agreement)
   int status = MGW_DEV_OK;
-  if (do_fold && cta == 0 && threadIdx.x < N) {
-    const uint64_t* p = l.hdr[me] + parity * l.hdr_stride + threadIdx.x;
-    uint64_t v = ld_relaxed_sys_u64(p);
-    const uint64_t start = global_ns();
-    for (uint32_t spin = 0; (uint32_t)(v >> 32) != epoch; ++spin) {
-      if ((spin & 31) == 31) {
-        if (load_relaxed_sys32(a.abort_flag[me]) != 0u) {
-          status = MGW_DEV_PEER_ABORT;
-          break;
-        }
-        if (global_ns() - start > a.timeout_ns) {
-          status = MGW_DEV_TIMEOUT;
-          break;
-        }
-      }
-      v = ld_relaxed_sys_u64(p);
-    }
-    if (status == MGW_DEV_OK && (uint32_t)v != a.tag) status = MGW_DEV_MISMATCH;
-    if (status != MGW_DEV_OK) atomicCAS(&s_status, 0, status);
-  }
-  __syncthreads();
-  if (s_status != MGW_DEV_OK && threadIdx.x == 0) {
-    atomicCAS(a.err, 0, s_status);
-    if (s_status != MGW_DEV_PEER_ABORT)
-      for (int r = 0; r < N; ++r) store_release_sys32(a.abort_flag[r], 1u);
-  }
-  status = s_status;
+  const uint64_t* hdr_mine = l.hdr[me] + parity * l.hdr_stride;
 
-  // 3. fold: batched 16-B polls of the N sources, fp32 fold in the reference order
-  if (do_fold && status == MGW_DEV_OK) {
+  // 2. fold: batched 16-B polls of the N sources, fp32 fold in the reference order
+  if (do_fold) {
     const float scale = f.scale;
     const bool scaled = scale != 1.0f;
     const uint64_t* base = l.ll[me] + (size_t)parity * kMaxRanks * kLLMaxElems;
@@ -446,7 +419,7 @@ __device__ __forceinline__ void ll_b16_body(const LLArgs& l, const int cta, cons
 #pragma unroll
       for (int src = 0; src < N; ++src) {
         if ((uint32_t)(w0[src] >> 32) != epoch || (uint32_t)(w1[src] >> 32) != epoch)
-          ll_wait2(base + (size_t)src * kLLMaxElems + 2 * j, epoch, a, status, w0[src], w1[src]);
+          ll_wait2(base + (size_t)src * kLLMaxElems + 2 * j, hdr_mine + src, epoch, a, status, w0[src], w1[src]);
       }
       if (status != MGW_DEV_OK) break;
 #pragma unroll
@@ -471,12 +444,9 @@ __device__ __forceinline__ void ll_b16_body(const LLArgs& l, const int cta, cons
         reinterpret_cast<uint16_t*>(r.ptr)[eh - r.offset] = y;
       }
     }
-    if (status != MGW_DEV_OK) {
-      atomicCAS(a.err, 0, status);
-      if (status != MGW_DEV_PEER_ABORT)
-        for (int r = 0; r < N; ++r) store_release_sys32(a.abort_flag[r], 1u);
-    }
   }
+  // 3. the length / dtype / collective agreement check (CTA 0), error reporting
+  if (do_fold) ll_header_check(l, epoch, parity, cta == 0, status, &s_status);
   finish_call(a, ctas);
 }
 

@@ -50,14 +50,21 @@ __device__ __forceinline__ void ld_relaxed_sys_v2(const uint64_t* p, uint64_t& a
   asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
 }
 
-// Re-poll a pair of words until both carry `epoch`.  Bounded; watches the abort flag.
-__device__ __forceinline__ void ll_wait2(const uint64_t* p, uint32_t epoch, const ArArgs& a, int& status, uint64_t& w0,
-                                      uint64_t& w1) {
+// Re-poll a pair of words until both carry `epoch`.  Bounded; watches the abort flag and
+// the source's header word `hdr`: a peer running a different collective (length, kernel,
+// group ...) never sends these words, and its header tells us so without the timeout.
+__device__ __forceinline__ void ll_wait2(const uint64_t* p, const uint64_t* hdr, uint32_t epoch, const ArArgs& a,
+                                         int& status, uint64_t& w0, uint64_t& w1) {
   const uint64_t start = global_ns();
   for (uint32_t spin = 0;; ++spin) {
     ld_relaxed_sys_v2(p, w0, w1);
     if ((uint32_t)(w0 >> 32) == epoch && (uint32_t)(w1 >> 32) == epoch) return;
     if ((spin & 31) == 31) {
+      const uint64_t h = ld_relaxed_sys_u64(hdr);
+      if ((uint32_t)(h >> 32) == epoch && (uint32_t)h != a.tag) {
+        status = MGW_DEV_MISMATCH;
+        return;
+      }
       if (load_relaxed_sys32(a.abort_flag[a.rank]) != 0u) {
         status = MGW_DEV_PEER_ABORT;
         return;
@@ -68,6 +75,48 @@ __device__ __forceinline__ void ll_wait2(const uint64_t* p, uint32_t epoch, cons
       }
     }
   }
+}
+
+// After the fold: CTA 0's threads < N wait (briefly -- the headers were pushed before the
+// data they have just folded) for every peer's header of this epoch and compare its tag.
+// The header check used to come before the fold and cost a full poll round trip on the
+// critical path of every small exchange.  Returns the CTA-uniform status; reports errors.
+__device__ __forceinline__ int ll_header_check(const LLArgs& l, uint32_t epoch, int parity, bool active, int status,
+                                               int* s_status) {
+  const ArArgs& a = l.f.ar;
+  const int me = a.rank;
+  if (threadIdx.x == 0) *s_status = MGW_DEV_OK;
+  __syncthreads();
+  if (status != MGW_DEV_OK) atomicCAS(s_status, 0, status);  // a fold thread's error
+  if (active && status == MGW_DEV_OK && threadIdx.x < a.world) {
+    const uint64_t* p = l.hdr[me] + parity * l.hdr_stride + threadIdx.x;
+    uint64_t v = ld_relaxed_sys_u64(p);
+    const uint64_t start = global_ns();
+    int st = MGW_DEV_OK;
+    for (uint32_t spin = 0; (uint32_t)(v >> 32) != epoch; ++spin) {
+      if ((spin & 31) == 31) {
+        if (load_relaxed_sys32(a.abort_flag[me]) != 0u) {
+          st = MGW_DEV_PEER_ABORT;
+          break;
+        }
+        if (global_ns() - start > a.timeout_ns) {
+          st = MGW_DEV_TIMEOUT;
+          break;
+        }
+      }
+      v = ld_relaxed_sys_u64(p);
+    }
+    if (st == MGW_DEV_OK && (uint32_t)v != a.tag) st = MGW_DEV_MISMATCH;
+    if (st != MGW_DEV_OK) atomicCAS(s_status, 0, st);
+  }
+  __syncthreads();
+  const int out = *s_status;
+  if (out != MGW_DEV_OK && threadIdx.x == 0) {
+    atomicCAS(a.err, 0, out);
+    if (out != MGW_DEV_PEER_ABORT)
+      for (int r = 0; r < a.world; ++r) store_release_sys32(a.abort_flag[r], 1u);
+  }
+  return out;
 }
 
 __device__ __forceinline__ uint64_t ll_word(uint32_t epoch, float x) {
@@ -130,45 +179,15 @@ __device__ __forceinline__ void ll_oneshot_body(const LLArgs& l, const int cta, 
   }
 
   phase_mark(a, 1, cta);
-  // 2. CTA 0 checks every peer's header (length agreement)
   int status = MGW_DEV_OK;
-  if (do_fold && cta == 0 && threadIdx.x < N) {
-    const uint64_t h = [&] {
-      const uint64_t* p = l.hdr[me] + parity * l.hdr_stride + threadIdx.x;
-      uint64_t v = ld_relaxed_sys_u64(p);
-      const uint64_t start = global_ns();
-      for (uint32_t spin = 0; (uint32_t)(v >> 32) != epoch; ++spin) {
-        if ((spin & 31) == 31) {
-          if (load_relaxed_sys32(a.abort_flag[me]) != 0u) {
-            status = MGW_DEV_PEER_ABORT;
-            break;
-          }
-          if (global_ns() - start > a.timeout_ns) {
-            status = MGW_DEV_TIMEOUT;
-            break;
-          }
-        }
-        v = ld_relaxed_sys_u64(p);
-      }
-      return v;
-    }();
-    if (status == MGW_DEV_OK && (uint32_t)h != a.tag) status = MGW_DEV_MISMATCH;
-    if (status != MGW_DEV_OK) atomicCAS(&s_status, 0, status);
-  }
-  __syncthreads();
-  if (s_status != MGW_DEV_OK && threadIdx.x == 0) {
-    atomicCAS(a.err, 0, s_status);
-    if (s_status != MGW_DEV_PEER_ABORT)
-      for (int r = 0; r < N; ++r) store_release_sys32(a.abort_flag[r], 1u);
-  }
-  status = s_status;
   phase_mark(a, 2, cta);
 
-  // 3. fold every element of my pairs from the N local LL areas, write the tensors.
+  // 2. fold every element of my pairs from the N local LL areas, write the tensors.
   //    The N sources' words of a pair are fetched as N independent 16-B loads issued
   //    back to back (one memory latency, not 2N serial ones); only words that do not yet
   //    carry this epoch are polled again.
-  if (do_fold && status == MGW_DEV_OK) {
+  const uint64_t* hdr_mine = l.hdr[me] + parity * l.hdr_stride;
+  if (do_fold) {
     const uint64_t* base = l.ll[me] + (size_t)parity * kMaxRanks * kLLMaxElems;
     int seg = 0;
     k = 0;
@@ -181,7 +200,7 @@ __device__ __forceinline__ void ll_oneshot_body(const LLArgs& l, const int cta, 
 #pragma unroll
       for (int src = 0; src < N; ++src) {
         if ((uint32_t)(w0[src] >> 32) != epoch || (uint32_t)(w1[src] >> 32) != epoch)
-          ll_wait2(base + (size_t)src * kLLMaxElems + e, epoch, a, status, w0[src], w1[src]);
+          ll_wait2(base + (size_t)src * kLLMaxElems + e, hdr_mine + src, epoch, a, status, w0[src], w1[src]);
       }
       if (status != MGW_DEV_OK) break;
 #pragma unroll
@@ -204,12 +223,9 @@ __device__ __forceinline__ void ll_oneshot_body(const LLArgs& l, const int cta, 
         *ll_tensor(f, k, eh) = acc;
       }
     }
-    if (status != MGW_DEV_OK) {
-      atomicCAS(a.err, 0, status);
-      if (status != MGW_DEV_PEER_ABORT)
-        for (int r = 0; r < N; ++r) store_release_sys32(a.abort_flag[r], 1u);
-    }
   }
+  // 3. the length / collective agreement check (CTA 0), error reporting
+  if (do_fold) ll_header_check(l, epoch, parity, cta == 0, status, &s_status);
   phase_mark(a, 3, cta);
   finish_call(a, ctas);
 }
