@@ -400,11 +400,12 @@ __device__ __forceinline__ void ll_b16_body(const LLArgs& l, const int cta, cons
     for (int r = 0; r < N; ++r) st_relaxed_sys_v2(l.ll[r] + my_off + 2 * j, w0, w1);
   }
 
-  int status = MGW_DEV_OK;
+  // 2. CTA 0 checks every peer's header (length and dtype agreement)
+  int status = do_fold ? ll_header_check(l, epoch, parity, cta == 0, MGW_DEV_OK, &s_status) : MGW_DEV_OK;
   const uint64_t* hdr_mine = l.hdr[me] + parity * l.hdr_stride;
 
-  // 2. fold: batched 16-B polls of the N sources, fp32 fold in the reference order
-  if (do_fold) {
+  // 3. fold: batched 16-B polls of the N sources, fp32 fold in the reference order
+  if (do_fold && status == MGW_DEV_OK) {
     const float scale = f.scale;
     const bool scaled = scale != 1.0f;
     const uint64_t* base = l.ll[me] + (size_t)parity * kMaxRanks * kLLMaxElems;
@@ -445,8 +446,7 @@ __device__ __forceinline__ void ll_b16_body(const LLArgs& l, const int cta, cons
       }
     }
   }
-  // 3. the length / dtype / collective agreement check (CTA 0), error reporting
-  if (do_fold) ll_header_check(l, epoch, parity, cta == 0, status, &s_status);
+  if (status != MGW_DEV_OK && status != s_status) ll_report(a, status);  // a fold thread's own error
   finish_call(a, ctas);
 }
 

@@ -77,10 +77,16 @@ __device__ __forceinline__ void ll_wait2(const uint64_t* p, const uint64_t* hdr,
   }
 }
 
-// After the fold: CTA 0's threads < N wait (briefly -- the headers were pushed before the
-// data they have just folded) for every peer's header of this epoch and compare its tag.
-// The header check used to come before the fold and cost a full poll round trip on the
-// critical path of every small exchange.  Returns the CTA-uniform status; reports errors.
+// error word + abort flags (a peer abort is only recorded)
+__device__ __forceinline__ void ll_report(const ArArgs& a, int status) {
+  atomicCAS(a.err, 0, status);
+  if (status != MGW_DEV_PEER_ABORT)
+    for (int r = 0; r < a.world; ++r) store_release_sys32(a.abort_flag[r], 1u);
+}
+
+// CTA 0's threads < N wait for every peer's header of this epoch and compare its tag (the
+// peer's length / kernel / dtype / group); the other CTAs pass straight through.  Returns
+// the CTA-uniform status; reports errors.
 __device__ __forceinline__ int ll_header_check(const LLArgs& l, uint32_t epoch, int parity, bool active, int status,
                                                int* s_status) {
   const ArArgs& a = l.f.ar;
@@ -111,11 +117,7 @@ __device__ __forceinline__ int ll_header_check(const LLArgs& l, uint32_t epoch, 
   }
   __syncthreads();
   const int out = *s_status;
-  if (out != MGW_DEV_OK && threadIdx.x == 0) {
-    atomicCAS(a.err, 0, out);
-    if (out != MGW_DEV_PEER_ABORT)
-      for (int r = 0; r < a.world; ++r) store_release_sys32(a.abort_flag[r], 1u);
-  }
+  if (out != MGW_DEV_OK && threadIdx.x == 0) ll_report(a, out);
   return out;
 }
 
@@ -179,15 +181,18 @@ __device__ __forceinline__ void ll_oneshot_body(const LLArgs& l, const int cta, 
   }
 
   phase_mark(a, 1, cta);
-  int status = MGW_DEV_OK;
+  // 2. CTA 0 checks every peer's header first (length / collective agreement); measured:
+  //    checking after the fold was slower (512 threads polling data words that are still in
+  //    flight instead of N threads polling headers)
+  int status = do_fold ? ll_header_check(l, epoch, parity, cta == 0, MGW_DEV_OK, &s_status) : MGW_DEV_OK;
   phase_mark(a, 2, cta);
 
-  // 2. fold every element of my pairs from the N local LL areas, write the tensors.
+  // 3. fold every element of my pairs from the N local LL areas, write the tensors.
   //    The N sources' words of a pair are fetched as N independent 16-B loads issued
   //    back to back (one memory latency, not 2N serial ones); only words that do not yet
   //    carry this epoch are polled again.
   const uint64_t* hdr_mine = l.hdr[me] + parity * l.hdr_stride;
-  if (do_fold) {
+  if (do_fold && status == MGW_DEV_OK) {
     const uint64_t* base = l.ll[me] + (size_t)parity * kMaxRanks * kLLMaxElems;
     int seg = 0;
     k = 0;
@@ -224,8 +229,7 @@ __device__ __forceinline__ void ll_oneshot_body(const LLArgs& l, const int cta, 
       }
     }
   }
-  // 3. the length / collective agreement check (CTA 0), error reporting
-  if (do_fold) ll_header_check(l, epoch, parity, cta == 0, status, &s_status);
+  if (status != MGW_DEV_OK && status != s_status) ll_report(a, status);  // a fold thread's own error
   phase_mark(a, 3, cta);
   finish_call(a, ctas);
 }
