@@ -398,6 +398,8 @@ int comm_allreduce_fused(mgw_comm* c, const Row* host_rows, const Row* dev_rows,
 // Single rank: the group's fused kernel with N = 1 -- pack into the local bucket, the
 // one-input fold, write back -- one launch per group like the multi-rank path.  Every
 // thread re-reads only the bucket slots it packed itself, so no barrier is needed.
+int64_t g_local_min_slots = 128;  // mgw_set_option(MGW_OPT_LOCAL_MIN_SLOTS)
+
 int local_fused(float* bucket, const Row* host_rows, const Row* dev_rows, int n_rows, int64_t n, float scale,
                 cudaStream_t stream, uint64_t* stamp = nullptr, int extra_flags = 0) {
   if (n == 0 || n_rows == 0) return MGW_OK;
@@ -414,7 +416,15 @@ int local_fused(float* bucket, const Row* host_rows, const Row* dev_rows, int n_
   f.rows = dev_rows;
   f.n_rows = n_rows;
   f.scale = scale;
-  return launch_fused(f, MGW_ALGO_ONESHOT, 2 * kSMs, stream);
+  // slots per CTA: the group spread over one CTA per SM, but at least g_local_min_slots per
+  // CTA (fewer, fuller CTAs for small groups: less CTA start skew in a ~2 us kernel)
+  const int64_t nv = n >> 2;
+  int64_t per = (nv + kSMs - 1) / kSMs;
+  per = (per + 127) / 128 * 128;
+  const int64_t full = (int64_t)kThreads * 4;
+  per = per < g_local_min_slots ? g_local_min_slots : (per > full ? full : per);
+  const int64_t per_cta[2] = {per, 0};
+  return launch_fused(f, MGW_ALGO_ONESHOT, 2 * kSMs, stream, per_cta);
 }
 
 // Single rank, bf16 gradients: the bf16 group kernel with N = 1 (pack -> one-input fold
@@ -860,6 +870,10 @@ int mgw_set_option(int key, int64_t value) {
   switch (key) {
     case MGW_OPT_ROWS_PATH: return set_rows_path((int)value);
     case MGW_OPT_PIPE_SUB_SLOTS: return set_pipe_sub_slots(value);
+    case MGW_OPT_LOCAL_MIN_SLOTS:
+      if (value < 128 || value > kThreads * 4 || value % 128) return set_error(MGW_EINVAL, "local min slots: 128..2048, x128");
+      g_local_min_slots = value;
+      return MGW_OK;
     default: return set_error(MGW_EINVAL, "unknown option %d", key);
   }
 }

@@ -21,14 +21,17 @@ def main() -> int:
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--no-pdl", action="store_true")
+    ap.add_argument("--local-min-slots", type=int, default=0)
     args = ap.parse_args()
     import torch
 
-    from paper_1811_11141_b200 import MergePlan
+    from paper_1811_11141_b200 import MergePlan, _native
     from paper_1811_11141_b200.overlap import OverlappedIteration
 
     torch.cuda.set_device(0)
     device = torch.device("cuda", 0)
+    if args.local_min_slots:
+        _native.call("mgw_set_option", _native.OPT_LOCAL_MIN_SLOTS, args.local_min_slots)
     profile, _, _ = bench.b200_profile()
     plan = MergePlan(frozenset(), profile.num_layers)
     flush = torch.empty(bench.L2_FLUSH_BYTES // 4, device=device)
