@@ -1,7 +1,7 @@
 // k_bf16.cu -- host launchers of the bf16.cuh kernels (own translation unit: the kernel
 // families compile in parallel, see __graft_entry__.build).
 #include "launch.h"
-#include "bf16.cuh"
+#include "b16push.cuh"
 
 namespace mgw {
 
@@ -84,6 +84,49 @@ int launch_b16_group(const RankGroup<FusedArgs>& g, int world, int algo, cudaStr
     case 6: return group_b16_n<6>(g, algo, stream);
     case 7: return group_b16_n<7>(g, algo, stream);
     case 8: return group_b16_n<8>(g, algo, stream);
+    default: return set_error(MGW_EINVAL, "rank group of %d outside 2..%d", world, kMaxRanks);
+  }
+}
+
+// bf16 push two-shot: the push two-shot's grid rule in bf16 16-B slots
+int plan_b16_push(PushArgs& x, int max_ctas) {
+  max_ctas = max_ctas < kMaxBlocks ? max_ctas : kMaxBlocks;
+  const int w = x.f.ar.world > 0 ? x.f.ar.world : 1;
+  const int64_t nv = x.f.ar.n / kB16;
+  int64_t per = (nv / w + kSMs - 1) / kSMs;
+  per = (per + 127) / 128 * 128;
+  per = per < 2048 ? 2048 : (per > 4096 ? 4096 : per);
+  const int grid = grid_for(nv / w, per, max_ctas);
+  x.f.ar.tag = collective_tag(x.f.ar.tag, x.f.ar.n, kTagB16Push, grid, x.f.scale);
+  return grid;
+}
+
+int launch_b16_push(const PushArgs& x0, int max_ctas, cudaStream_t stream) {
+  PushArgs x = x0;
+  const int grid = plan_b16_push(x, max_ctas);
+  switch (x.f.ar.world) {
+    case 2: b16_push_kernel<2><<<grid, kThreads, 0, stream>>>(x); break;
+    case 3: b16_push_kernel<3><<<grid, kThreads, 0, stream>>>(x); break;
+    case 4: b16_push_kernel<4><<<grid, kThreads, 0, stream>>>(x); break;
+    case 5: b16_push_kernel<5><<<grid, kThreads, 0, stream>>>(x); break;
+    case 6: b16_push_kernel<6><<<grid, kThreads, 0, stream>>>(x); break;
+    case 7: b16_push_kernel<7><<<grid, kThreads, 0, stream>>>(x); break;
+    case 8: b16_push_kernel<8><<<grid, kThreads, 0, stream>>>(x); break;
+    default: return set_error(MGW_EINVAL, "bf16 push two-shot needs 2..%d ranks, got %d", kMaxRanks, x.f.ar.world);
+  }
+  MGW_CHECK_LAUNCH();
+  return MGW_OK;
+}
+
+int launch_b16_push_group(const RankGroup<PushArgs>& g, int world, cudaStream_t stream) {
+  switch (world) {
+    case 2: return launch_cooperative(b16_push_group<2>, g, stream);
+    case 3: return launch_cooperative(b16_push_group<3>, g, stream);
+    case 4: return launch_cooperative(b16_push_group<4>, g, stream);
+    case 5: return launch_cooperative(b16_push_group<5>, g, stream);
+    case 6: return launch_cooperative(b16_push_group<6>, g, stream);
+    case 7: return launch_cooperative(b16_push_group<7>, g, stream);
+    case 8: return launch_cooperative(b16_push_group<8>, g, stream);
     default: return set_error(MGW_EINVAL, "rank group of %d outside 2..%d", world, kMaxRanks);
   }
 }

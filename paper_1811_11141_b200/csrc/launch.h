@@ -8,6 +8,7 @@
 #include "ll.cuh"
 #include "nvls.cuh"
 #include "pipe.cuh"
+#include "b16push.cuh"
 #include "rows.cuh"
 
 namespace mgw {
@@ -20,6 +21,7 @@ int launch_push_pipe(const PushArgs& x, int max_ctas, cudaStream_t stream, const
 int launch_ll(const LLArgs& l, int max_ctas, cudaStream_t stream);
 int launch_ll_b16(const LLArgs& l, int max_ctas, cudaStream_t stream);
 int launch_b16(const FusedArgs& f, int algo, int max_ctas, cudaStream_t stream);
+int launch_b16_push(const PushArgs& x, int max_ctas, cudaStream_t stream);
 int launch_nvls(const NvlsArgs& x, int max_ctas, cudaStream_t stream, const int64_t* per_cta);
 
 // plan_*: the grid a launch uses for these arguments and settings; stamps the collective
@@ -31,6 +33,7 @@ int plan_push_pipe(PushArgs& x, int max_ctas, const int64_t* per_cta);
 int plan_ll(LLArgs& l, int max_ctas);
 int plan_ll_b16(LLArgs& l, int max_ctas);
 int plan_b16(FusedArgs& f, int algo, int max_ctas);
+int plan_b16_push(PushArgs& x, int max_ctas);
 
 // Rank-group launches: every rank's planned CTAs in ONE cooperative launch on one device
 // (co-residency guaranteed, so ranks that wait on one another always run together).
@@ -40,6 +43,7 @@ int launch_push_group(const RankGroup<PushArgs>& g, int world, int kind /* 0 two
 int launch_ll_group(const RankGroup<LLArgs>& g, int world, cudaStream_t stream);
 int launch_b16_group(const RankGroup<FusedArgs>& g, int world, int algo, cudaStream_t stream);
 int launch_ll_b16_group(const RankGroup<LLArgs>& g, int world, cudaStream_t stream);
+int launch_b16_push_group(const RankGroup<PushArgs>& g, int world, cudaStream_t stream);
 
 template <class Args>
 inline int launch_cooperative(void (*kernel)(const RankGroup<Args>), const RankGroup<Args>& g, cudaStream_t stream) {

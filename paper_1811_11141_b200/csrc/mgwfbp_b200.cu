@@ -277,6 +277,8 @@ int pick_fused_algo(const mgw_comm* c, int64_t n, int algo) {
 
 // The kernel a fused fp32 group exchange of n elements actually runs: the AUTO choice,
 // then the fallbacks when the push areas cannot hold the incoming rows.
+constexpr int64_t kB16PushMinBytes = 8ll << 20;  // bf16 AUTO: push two-shot at >= 8 MB (as fp32 at N >= 3)
+
 int resolve_fused_algo(const mgw_comm* c, int64_t n, int algo) {
   int chosen = pick_fused_algo(c, n, algo);
   if (chosen == MGW_ALGO_PUSH_ONESHOT && c->world * round_up(n, 16) * 4 > c->slot_bytes) chosen = MGW_ALGO_ONESHOT;
@@ -291,10 +293,14 @@ int resolve_b16_algo(const mgw_comm* c, int64_t n, int algo) {
   if (algo == MGW_ALGO_AUTO) {
     if (c->world > 1 && n * 2 <= c->ll_max_bytes && n <= 2 * kLLElems)
       algo = MGW_ALGO_LL;
-    else
-      algo = n * 2 <= c->oneshot_max_bytes ? MGW_ALGO_ONESHOT : MGW_ALGO_TWOSHOT;
+    else if (n * 2 <= c->oneshot_max_bytes)
+      algo = MGW_ALGO_ONESHOT;
+    else  // large bf16 buckets: the store-only push two-shot (b16push.cuh), as for fp32
+      algo = c->world > 1 && n * 2 >= kB16PushMinBytes ? MGW_ALGO_PUSH : MGW_ALGO_TWOSHOT;
   }
   if (algo == MGW_ALGO_LL && c->world == 1) algo = MGW_ALGO_ONESHOT;
+  if (algo == MGW_ALGO_PUSH && (c->world == 1 || c->world * b16_push_stride(n, c->world) * 2 > c->slot_bytes))
+    algo = MGW_ALGO_TWOSHOT;  // one rank, or the incoming rows do not fit the slot
   return algo;
 }
 
@@ -485,6 +491,14 @@ int comm_allreduce_fused_bf16(mgw_comm* c, const Row* host_rows, const Row* dev_
     }
     l.hdr_stride = (int64_t)kMaxBlocks * kMaxRanks;
     return launch_ll_b16(l, c->max_ctas, stream);
+  }
+  if (algo == MGW_ALGO_PUSH) {
+    PushArgs x;
+    memset(&x, 0, sizeof(x));
+    x.f = f;
+    x.stride = b16_push_stride(n, c->world);
+    for (int s = 0; s < c->world; ++s) x.gather[s] = c->peer[s] + kSlotOff + 2 * c->slot_bytes;
+    return launch_b16_push(x, c->max_ctas, stream);
   }
   return launch_b16(f, algo, c->max_ctas, stream);
 }
@@ -839,6 +853,12 @@ int mgw_group_allreduce_fused(mgw_comm* const* comms, void* const* tables, const
       l.hdr_stride = (int64_t)kMaxBlocks * kMaxRanks;
       if (n > (b16 ? 2 : 1) * kLLElems) return set_error(MGW_EINVAL, "LL bucket of %lld elements too large", (long long)n);
       grid = b16 ? plan_ll_b16(l, c->max_ctas) : plan_ll(l, c->max_ctas);
+    } else if (push && b16) {
+      PushArgs& x = gp->args[r];
+      x.f = f;
+      x.stride = b16_push_stride(n, world);
+      for (int q = 0; q < world; ++q) x.gather[q] = c->peer[q] + kSlotOff + 2 * c->slot_bytes;
+      grid = plan_b16_push(x, c->max_ctas);
     } else if (push) {
       const bool one = chosen == MGW_ALGO_PUSH_ONESHOT;
       PushArgs& x = gp->args[r];
@@ -861,6 +881,7 @@ int mgw_group_allreduce_fused(mgw_comm* const* comms, void* const* tables, const
   if (first > 2 * kSMs)
     return set_error(MGW_EINVAL, "rank group needs %d co-resident CTAs (> %d): lower the CTA caps", first, 2 * kSMs);
   if (ll) return b16 ? launch_ll_b16_group(*gl, world, s) : launch_ll_group(*gl, world, s);
+  if (push && b16) return launch_b16_push_group(*gp, world, s);
   if (push)
     return launch_push_group(*gp, world, chosen == MGW_ALGO_PUSH_ONESHOT ? 1 : (chosen == MGW_ALGO_PUSH_PIPE ? 2 : 0), s);
   return b16 ? launch_b16_group(*gf, world, chosen, s) : launch_fused_group(*gf, world, chosen, s);
@@ -980,8 +1001,9 @@ int mgw_allreduce_fused(mgw_comm* c, const void* table, int n_rows, int64_t n_el
 int mgw_allreduce_fused_bf16(mgw_comm* c, const void* table, int n_rows, int64_t n_elem, float scale, int algo,
                              void* stream) {
   if (!c) return set_error(MGW_EINVAL, "comm is null");
-  if (algo != MGW_ALGO_AUTO && algo != MGW_ALGO_ONESHOT && algo != MGW_ALGO_TWOSHOT && algo != MGW_ALGO_LL)
-    return set_error(MGW_EINVAL, "bf16 buckets support AUTO, LL, one-shot and two-shot (got %d)", algo);
+  if (algo != MGW_ALGO_AUTO && algo != MGW_ALGO_ONESHOT && algo != MGW_ALGO_TWOSHOT && algo != MGW_ALGO_LL &&
+      algo != MGW_ALGO_PUSH)
+    return set_error(MGW_EINVAL, "bf16 buckets support AUTO, LL, one-shot, two-shot and push two-shot (got %d)", algo);
   int rc = check_table(table, n_rows, n_elem);
   if (rc) return rc;
   const mgw_table_t* t = as_table(table);
@@ -1229,6 +1251,45 @@ static int push_emulated(void* const* tables, int world, int64_t n, float scale,
   return rc;
 }
 
+// emulated bf16 push two-shot: incoming rows and gather areas allocated here (test path)
+static int b16_push_emulated(void* const* tables, int world, int64_t n, float scale, cudaStream_t s) {
+  if (world < 2) return set_error(MGW_EINVAL, "push exchanges need >= 2 ranks");
+  const int64_t stride = b16_push_stride(n, world);
+  char* mem = nullptr;
+  const size_t in_bytes = (size_t)round_up((int64_t)world * stride * 2, 256);
+  const size_t g_bytes = (size_t)round_up(n * 2, 256);
+  MGW_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&mem), (size_t)world * (in_bytes + g_bytes), s));
+  PushArgs x;
+  memset(&x, 0, sizeof(x));
+  for (int r = 0; r < world; ++r) {
+    x.f.ar.slot[r] = mem + (size_t)r * in_bytes;
+    x.gather[r] = mem + (size_t)world * in_bytes + (size_t)r * g_bytes;
+  }
+  x.f.ar.n = n;
+  x.f.ar.world = world;
+  x.f.scale = scale;
+  x.stride = stride;
+  int rc = MGW_OK;
+  for (int step = 0; step < 3 && rc == MGW_OK; ++step) {
+    for (int r = 0; r < world && rc == MGW_OK; ++r) {
+      const mgw_table_t* t = as_table(tables[r]);
+      const int n_rows = (int)t->host.size();
+      x.f.use_inline = n_rows <= kInlineRows;
+      if (x.f.use_inline)
+        for (int k = 0; k < n_rows; ++k) x.f.inline_rows[k] = t->host[k];
+      x.f.rows = t->dev;
+      x.f.n_rows = n_rows;
+      x.f.ar.rank = r;
+      x.f.ar.flags = kNoBarrier | (step == 0 ? kSkipPhase1 | kSkipPhase2
+                                             : kSkipPack | (step == 1 ? kSkipPhase2 : kSkipPhase1));
+      rc = launch_b16_push(x, 2 * kSMs, s);
+    }
+  }
+  cudaError_t e = cudaFreeAsync(mem, s);
+  if (rc == MGW_OK && e != cudaSuccess) rc = set_error(MGW_ECUDA, "cudaFreeAsync: %s", cudaGetErrorString(e));
+  return rc;
+}
+
 // emulated LL exchange (fp32 or bf16): every rank's pushes in one pass of launches, then
 // every rank's fold in a second pass (no kernel ever waits on a later launch)
 static int ll_emulated(void* const* tables, int world, int64_t n, float scale, cudaStream_t s, bool bf16) {
@@ -1378,6 +1439,14 @@ int mgw_allreduce_fused_bf16_emulated(void* const* tables, void* const* slots, i
       if (rc) return rc;
     }
     return n == 0 ? MGW_OK : ll_emulated(tables, world, n, scale, static_cast<cudaStream_t>(stream), true);
+  }
+  if (algo == MGW_ALGO_PUSH) {
+    for (int r = 0; r < world; ++r) {
+      const mgw_table_t* t = as_table(tables[r]);
+      int rc = check_table(tables[r], t ? (int)t->host.size() : 0, n);
+      if (rc) return rc;
+    }
+    return n == 0 ? MGW_OK : b16_push_emulated(tables, world, n, scale, static_cast<cudaStream_t>(stream));
   }
   if (algo != MGW_ALGO_ONESHOT && algo != MGW_ALGO_TWOSHOT)
     return set_error(MGW_EINVAL, "emulated all-reduce needs an explicit algorithm");

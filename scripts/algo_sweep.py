@@ -25,6 +25,7 @@ def main() -> int:
     ap.add_argument("--algos", default="twoshot,push,push_pipe,auto")
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--pipe-subs", default="", help="comma list of pipelined sub-chunk slots to sweep")
+    ap.add_argument("--bf16", action="store_true", help="bf16 gradients (fp32 accumulation) vs NCCL bf16")
     args = ap.parse_args()
     import torch
 
@@ -44,7 +45,7 @@ def main() -> int:
     out = {"world": world, "sizes": sizes, "bus_gbs": {}, "us": {}}
     for name in args.algos.split(","):
         for graph in (False, True):
-            kind = 4 | (256 if graph else 0)
+            kind = (5 if args.bf16 else 4) | (256 if graph else 0)
             t = bench._exchange_times(comm, world, device, sizes, kind=kind, algo=ids[name], repeats=args.reps)
             key = name + ("@graph" if graph else "@stream")
             out["us"][key] = [round(x * 1e6, 2) for x in t]
@@ -57,7 +58,7 @@ def main() -> int:
         out["us"][key] = [round(x * 1e6, 2) for x in t]
         out["bus_gbs"][key] = [round(2 * (world - 1) / world * s / x / 1e9, 1) for s, x in zip(sizes, t)]
     _native.call("mgw_set_option", _native.OPT_PIPE_SUB_SLOTS, 512)
-    nccl = bench._nccl_times(world, device, sizes, repeats=args.reps)
+    nccl = bench._nccl_times(world, device, sizes, repeats=args.reps, bf16=args.bf16)
     out["us"]["nccl@stream"] = [round(x * 1e6, 2) for x in nccl]
     out["bus_gbs"]["nccl@stream"] = [round(2 * (world - 1) / world * s / x / 1e9, 1) for s, x in zip(sizes, nccl)]
     session.raise_if_failed()
