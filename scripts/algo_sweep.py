@@ -26,6 +26,7 @@ def main() -> int:
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--pipe-subs", default="", help="comma list of pipelined sub-chunk slots to sweep")
     ap.add_argument("--bf16", action="store_true", help="bf16 gradients (fp32 accumulation) vs NCCL bf16")
+    ap.add_argument("--max-ctas", default="", help="comma list of CTA caps to sweep for the listed algorithms")
     args = ap.parse_args()
     import torch
 
@@ -50,6 +51,15 @@ def main() -> int:
             key = name + ("@graph" if graph else "@stream")
             out["us"][key] = [round(x * 1e6, 2) for x in t]
             out["bus_gbs"][key] = [round(2 * (world - 1) / world * s / x / 1e9, 1) for s, x in zip(sizes, t)]
+    for cap in [int(v) for v in args.max_ctas.split(",") if v]:
+        _native.call("mgw_comm_set_max_ctas", comm, cap)
+        for name in args.algos.split(","):
+            t = bench._exchange_times(comm, world, device, sizes, kind=(5 if args.bf16 else 4) | 256, algo=ids[name],
+                                      repeats=args.reps)
+            key = f"{name}_cap{cap}@graph"
+            out["us"][key] = [round(x * 1e6, 2) for x in t]
+            out["bus_gbs"][key] = [round(2 * (world - 1) / world * s / x / 1e9, 1) for s, x in zip(sizes, t)]
+    _native.call("mgw_comm_set_max_ctas", comm, 296)
     for slots in [int(v) for v in args.pipe_subs.split(",") if v]:
         _native.call("mgw_set_option", _native.OPT_PIPE_SUB_SLOTS, slots)
         t = bench._exchange_times(comm, world, device, sizes, kind=4 | 256, algo=_native.ALGO_PUSH_PIPE,
