@@ -164,6 +164,8 @@ int mgw_group_allreduce_fused(mgw_comm* const* comms, void* const* tables, const
 #define MGW_OPT_ROWS_PATH 1
 #define MGW_OPT_PIPE_SUB_SLOTS 2 /* pipelined two-shot: 16-B slots per sub-chunk per part (default 512) */
 #define MGW_OPT_LOCAL_MIN_SLOTS 3 /* single-rank group kernel: minimum 16-B slots per CTA (128..2048) */
+#define MGW_OPT_WIDE_MIN_BYTES 4  /* push two-shot over IPC: buckets >= this many bytes launch 512 CTAs
+                                     (default 112 MiB, 0 = always the comm's CTA cap) */
 int mgw_set_option(int key, int64_t value);
 /* bounds-checked build (-DMGW_CHECKED, libmgwfbp_b200_checked.so): index violations the
  * kernels counted since the last reset (every row walk, bucket / slot / LL / push index and

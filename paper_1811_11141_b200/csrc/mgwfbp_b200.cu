@@ -335,6 +335,20 @@ int comm_pack(mgw_comm* c, const Row* host_rows, const Row* dev_rows, int n_rows
                                    nullptr, stream, stamp);
 }
 
+// CTA cap of the push two-shot over IPC: buckets >= g_wide_min_bytes take kMaxBlocks CTAs
+// (a second, partial wave) -- the 4096-slot chunks keep streaming while the first wave's
+// CTAs sit in their barriers (profiles/cta_cap_n{2,4}_r02.json: 128 MiB at N = 4 546 -> 592
+// bus GB/s, 256 MiB 559 -> 609; neutral at <= 64 MiB).  Forward progress: CTAs dispatch in
+// index order, so the lowest unfinished CTA index is resident on every rank.  Not for the
+// cooperative single-device groups (every CTA must be co-resident there).
+int64_t g_wide_min_bytes = 112ll << 20;  // mgw_set_option(MGW_OPT_WIDE_MIN_BYTES); 0 = off
+
+static int push_cap(const mgw_comm* c, int64_t bytes) {
+  if (g_wide_min_bytes > 0 && bytes >= g_wide_min_bytes && !c->local_group)
+    return c->max_ctas > kMaxBlocks ? c->max_ctas : kMaxBlocks;
+  return c->max_ctas;
+}
+
 // pack -> all-reduce -> unpack of one group in a single kernel (fused.cuh)
 int comm_allreduce_fused(mgw_comm* c, const Row* host_rows, const Row* dev_rows, int n_rows, int64_t n, float scale,
                          int algo, cudaStream_t stream, uint64_t* stamp = nullptr, int extra_flags = 0,
@@ -396,7 +410,8 @@ int comm_allreduce_fused(mgw_comm* c, const Row* host_rows, const Row* dev_rows,
       x.pipe[s] = reinterpret_cast<uint64_t*>(c->peer[s] + kPipeOff);
     }
     if (chosen == MGW_ALGO_PUSH_PIPE) return launch_push_pipe(x, c->max_ctas, stream, c->vec_per_cta);
-    return one ? launch_push1(x, c->max_ctas, stream, c->vec_per_cta) : launch_push(x, c->max_ctas, stream, c->vec_per_cta);
+    return one ? launch_push1(x, c->max_ctas, stream, c->vec_per_cta)
+               : launch_push(x, push_cap(c, n * 4), stream, c->vec_per_cta);
   }
   return launch_fused(f, chosen, c->max_ctas, stream, c->vec_per_cta);
 }
@@ -498,7 +513,7 @@ int comm_allreduce_fused_bf16(mgw_comm* c, const Row* host_rows, const Row* dev_
     x.f = f;
     x.stride = b16_push_stride(n, c->world);
     for (int s = 0; s < c->world; ++s) x.gather[s] = c->peer[s] + kSlotOff + 2 * c->slot_bytes;
-    return launch_b16_push(x, c->max_ctas, stream);
+    return launch_b16_push(x, push_cap(c, n * 2), stream);
   }
   return launch_b16(f, algo, c->max_ctas, stream);
 }
@@ -894,6 +909,10 @@ int mgw_set_option(int key, int64_t value) {
     case MGW_OPT_LOCAL_MIN_SLOTS:
       if (value < 128 || value > kThreads * 4 || value % 128) return set_error(MGW_EINVAL, "local min slots: 128..2048, x128");
       g_local_min_slots = value;
+      return MGW_OK;
+    case MGW_OPT_WIDE_MIN_BYTES:
+      if (value < 0) return set_error(MGW_EINVAL, "wide min bytes must be >= 0");
+      g_wide_min_bytes = value;
       return MGW_OK;
     default: return set_error(MGW_EINVAL, "unknown option %d", key);
   }

@@ -51,6 +51,8 @@ def main() -> int:
             key = name + ("@graph" if graph else "@stream")
             out["us"][key] = [round(x * 1e6, 2) for x in t]
             out["bus_gbs"][key] = [round(2 * (world - 1) / world * s / x / 1e9, 1) for s, x in zip(sizes, t)]
+    if args.max_ctas:
+        _native.call("mgw_set_option", _native.OPT_WIDE_MIN_BYTES, 0)  # the cap as given
     for cap in [int(v) for v in args.max_ctas.split(",") if v]:
         _native.call("mgw_comm_set_max_ctas", comm, cap)
         for name in args.algos.split(","):
@@ -60,6 +62,7 @@ def main() -> int:
             out["us"][key] = [round(x * 1e6, 2) for x in t]
             out["bus_gbs"][key] = [round(2 * (world - 1) / world * s / x / 1e9, 1) for s, x in zip(sizes, t)]
     _native.call("mgw_comm_set_max_ctas", comm, 296)
+    _native.call("mgw_set_option", _native.OPT_WIDE_MIN_BYTES, 112 << 20)
     for slots in [int(v) for v in args.pipe_subs.split(",") if v]:
         _native.call("mgw_set_option", _native.OPT_PIPE_SUB_SLOTS, slots)
         t = bench._exchange_times(comm, world, device, sizes, kind=4 | 256, algo=_native.ALGO_PUSH_PIPE,

@@ -447,3 +447,50 @@ def emulate_bf16_task(config, session, *, profile, plan):
 
     rep = run_emulation(profile, plan, config, session, 3, warmup=1, graph=True, dtype=torch.bfloat16)
     return rep.verified, rep.allreduce_count
+
+
+def wide_push_task(config, session, *, n32, n16):
+    """Buckets above the wide-grid threshold (push two-shot at 512 CTAs, a second partial
+    wave): fp32 in three ragged rows and bf16 through AUTO (= the bf16 push), each rank
+    regenerating every rank's seeded input to check its result against the oracle in place
+    (the arrays are too large to ship back).  Returns mismatch counts."""
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    from oracle import ring_oracle
+    from paper_1811_11141_b200 import _native
+
+    h = session.stream.cuda_stream
+    n = config.n_workers
+    out = {}
+    ins = [np.random.default_rng(1000 + r).standard_normal(n32).astype("<f4") for r in range(n)]
+    want = ring_oracle.ring_allreduce(ins)[0]
+    cuts = [0, 257, 257 + n32 // 3 + 1, n32]
+    with torch.cuda.device(session.device), torch.cuda.stream(session.stream):
+        t = torch.from_numpy(ins[config.rank]).to(session.device)
+        parts = [t[cuts[i]:cuts[i + 1]] for i in range(3)]
+        table = _native.DeviceTable([(p.data_ptr(), p.numel(), cuts[i]) for i, p in enumerate(parts)])
+        _native.call("mgw_allreduce_fused", session.comm, table.ptr, 3, n32, ctypes.c_float(1.0), _native.ALGO_PUSH, h)
+        session.stream.synchronize()
+        session.raise_if_failed()
+        out["f32_bad"] = int(np.count_nonzero(t.cpu().numpy().view("<u4") != want.view("<u4")))
+        table.close()
+    del ins, want
+    ins16 = []
+    for r in range(n):
+        g = torch.Generator().manual_seed(77 + r)
+        ins16.append((torch.randn(n16, generator=g) * 4).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16))
+    want16 = ring_oracle.ring_allreduce_bf16(ins16, scale=0.5)
+    with torch.cuda.device(session.device), torch.cuda.stream(session.stream):
+        t = torch.from_numpy(ins16[config.rank].view(np.int16).copy()).view(torch.bfloat16).to(session.device)
+        table = _native.DeviceTable([(t.data_ptr(), n16, 0)])
+        _native.call("mgw_allreduce_fused_bf16", session.comm, table.ptr, 1, n16, ctypes.c_float(0.5),
+                     _native.ALGO_AUTO, h)
+        session.stream.synchronize()
+        session.raise_if_failed()
+        got = t.view(torch.int16).cpu().numpy().view(np.uint16)
+        out["b16_bad"] = int(np.count_nonzero(got != want16))
+        table.close()
+    return out

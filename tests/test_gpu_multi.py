@@ -300,3 +300,15 @@ def test_emulate_bf16_engine_verified():
         for verified, count in res.values():
             assert verified
             assert count == 4 * len(plan.groups())
+
+
+def test_wide_push_grid_above_threshold_vs_oracle():
+    """Buckets >= 112 MiB launch the push two-shot with 512 CTAs (two waves over the 296
+    resident): still bit-exact vs the oracle, fp32 (ragged rows) and bf16 (AUTO -> push)."""
+    n32 = (112 << 20) // 4 + 12_347
+    n16 = (112 << 20) // 2 + 9_001
+    n = min(_worlds())
+    res = run_workers(n, partial(_mp_tasks.wide_push_task, n32=n32, n16=n16), capacity_bytes=(120 << 20),
+                      timeout=300.0)
+    for r in range(n):
+        assert res[r] == {"f32_bad": 0, "b16_bad": 0}, (r, res[r])
