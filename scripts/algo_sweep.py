@@ -27,6 +27,7 @@ def main() -> int:
     ap.add_argument("--pipe-subs", default="", help="comma list of pipelined sub-chunk slots to sweep")
     ap.add_argument("--bf16", action="store_true", help="bf16 gradients (fp32 accumulation) vs NCCL bf16")
     ap.add_argument("--max-ctas", default="", help="comma list of CTA caps to sweep for the listed algorithms")
+    ap.add_argument("--per-cta", default="", help="comma list of two-shot / push slots per CTA to sweep")
     args = ap.parse_args()
     import torch
 
@@ -63,6 +64,15 @@ def main() -> int:
             out["bus_gbs"][key] = [round(2 * (world - 1) / world * s / x / 1e9, 1) for s, x in zip(sizes, t)]
     _native.call("mgw_comm_set_max_ctas", comm, 296)
     _native.call("mgw_set_option", _native.OPT_WIDE_MIN_BYTES, 112 << 20)
+    for per in [int(v) for v in args.per_cta.split(",") if v]:
+        _native.call("mgw_comm_set_tuning", comm, 1, per)
+        for name in args.algos.split(","):
+            t = bench._exchange_times(comm, world, device, sizes, kind=(5 if args.bf16 else 4) | 256, algo=ids[name],
+                                      repeats=args.reps)
+            key = f"{name}_per{per}@graph"
+            out["us"][key] = [round(x * 1e6, 2) for x in t]
+            out["bus_gbs"][key] = [round(2 * (world - 1) / world * s / x / 1e9, 1) for s, x in zip(sizes, t)]
+    _native.call("mgw_comm_set_tuning", comm, 1, 0)
     for slots in [int(v) for v in args.pipe_subs.split(",") if v]:
         _native.call("mgw_set_option", _native.OPT_PIPE_SUB_SLOTS, slots)
         t = bench._exchange_times(comm, world, device, sizes, kind=4 | 256, algo=_native.ALGO_PUSH_PIPE,
