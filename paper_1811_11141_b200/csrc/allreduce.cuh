@@ -361,9 +361,27 @@ __global__ void __launch_bounds__(kThreads, 2) oneshot_kernel(const __grid_const
   finish_call(a, gridDim.x);
 }
 
-// 16-B aligned work parts of the two-shot: rank p owns vectors [part(p), part(p+1));
-// the n % 4 tail elements belong to rank N-1.
-__device__ __forceinline__ int64_t part_begin(int p, int64_t nv, int world) { return (int64_t)p * nv / world; }
+// Work parts of the two-shot: rank p owns 16-B slots [part(p), part(p+1)); the n % 4 tail
+// elements belong to rank N-1.  Part and per-CTA chunk boundaries fall on kPartAlign slots
+// (512 B: one warp's 16-B accesses), so no warp store straddles a chunk edge -- unaligned
+// chunks cost the push two-shot 7 % at 32 MiB (profiles/per_cta_n4_r02.json).  Parts only
+// partition the work: the fold order follows the reference's segments (s_end), not parts.
+constexpr int64_t kPartAlign = 32;
+__host__ __device__ __forceinline__ int64_t part_begin(int p, int64_t nv, int world) {
+  return p >= world ? nv : ((int64_t)p * nv / world) & ~(kPartAlign - 1);
+}
+// slots per CTA when `len` slots are split over `ctas` CTAs (a multiple of kPartAlign)
+__host__ __device__ __forceinline__ int64_t chunk_per(int64_t len, int ctas) {
+  const int64_t per = (len + ctas - 1) / ctas;
+  return (per + kPartAlign - 1) / kPartAlign * kPartAlign;
+}
+// CTA b's chunk [lo, hi) of [q0, q1)
+__host__ __device__ __forceinline__ void cta_chunk(int64_t q0, int64_t q1, int b, int ctas, int64_t& lo, int64_t& hi) {
+  const int64_t per = chunk_per(q1 - q0, ctas);
+  lo = q0 + (int64_t)b * per;
+  if (lo > q1) lo = q1;
+  hi = lo + per < q1 ? lo + per : q1;
+}
 
 // K3: phase 1 reduces this rank's part (fold order per slot) into its own slot (in
 // place) and into out; phase 2 copies every peer's reduced part into out.
@@ -387,10 +405,8 @@ __global__ void __launch_bounds__(kThreads, 2) twoshot_kernel(const __grid_const
   if (!(a.flags & kSkipPhase1)) {
     if (!(a.flags & kNoBarrier)) status = cta_barrier(a.arrive, parity, epoch, a.tag, a, blockIdx.x);
     if (status == MGW_DEV_OK && a.n > 0) {
-      const int64_t p0 = part_begin(me, nv, N), p1 = part_begin(me + 1, nv, N);
-      const int64_t per = (p1 - p0 + G - 1) / G;
-      const int64_t v0 = p0 + (int64_t)b * per;
-      const int64_t v1 = v0 + per < p1 ? v0 + per : p1;
+      int64_t v0, v1;
+      cta_chunk(part_begin(me, nv, N), part_begin(me + 1, nv, N), b, G, v0, v1);
       int seg = advance_segment(0, ((v0 + threadIdx.x) << 2) < a.n ? (v0 + threadIdx.x) << 2 : 0, s_end);
       for (int64_t v = v0 + threadIdx.x; v < v1; v += (int64_t)U * kThreads)
         reduce_slots<N, U>(s_in, s_end, seg, v, v1, kThreads, own, second);
@@ -407,10 +423,8 @@ __global__ void __launch_bounds__(kThreads, 2) twoshot_kernel(const __grid_const
       if (threadIdx.x > 0 && threadIdx.x < N) {
         const int k = threadIdx.x;
         const int p = me + k >= N ? me + k - N : me + k;
-        const int64_t q0 = part_begin(p, nv, N), q1 = part_begin(p + 1, nv, N);
-        const int64_t per = (q1 - q0 + G - 1) / G;
-        const int64_t c0 = q0 + (int64_t)b * per;
-        const int64_t c1 = c0 + per < q1 ? c0 + per : q1;
+        int64_t c0, c1;
+        cta_chunk(part_begin(p, nv, N), part_begin(p + 1, nv, N), b, G, c0, c1);
         s_lo[k] = c0;
         s_len[k] = c1 > c0 ? c1 - c0 : 0;
       }

@@ -13,7 +13,7 @@
 //
 // Every NVLink byte is a store (2 (N-1)/N x M out per rank); all loads are local.  Rows:
 // slot[parity] of each rank viewed as bf16 [N src][stride], stride = one part of 16-B slots
-// (8 bf16) + the n % 8 tail; gather area = the second capacity pair of the IPC region.
+// (8 bf16, + kPartAlign for part_begin's rounding) + the n % 8 tail; gather area = the second capacity pair of the IPC region.
 #pragma once
 
 #include "bf16.cuh"
@@ -22,7 +22,7 @@
 namespace mgw {
 
 __host__ __device__ __forceinline__ int64_t b16_push_stride(int64_t n, int world) {
-  return ((n / kB16 + world - 1) / world + 1) * kB16;
+  return ((n / kB16 + world - 1) / world + kPartAlign + 1) * kB16;  // as push_stride()
 }
 
 template <int N>

@@ -280,9 +280,8 @@ __device__ __forceinline__ void b16_oneshot_body(const FusedArgs& f, const int c
   kernel_prologue<N>(a, epoch, parity, s_in, s_end);
   const uint16_t* const* in = reinterpret_cast<const uint16_t* const*>(s_in);
   const int64_t nv = a.n / kB16;
-  const int64_t per = (nv + ctas - 1) / ctas;
-  const int64_t v0 = (int64_t)cta * per;
-  const int64_t v1 = v0 + per < nv ? v0 + per : nv;
+  int64_t v0, v1;
+  cta_chunk(0, nv, cta, ctas, v0, v1);
   const bool last = cta == ctas - 1;
   if (!(a.flags & kSkipPack))
     b16_pack_range(f, const_cast<uint16_t*>(in[a.rank]), v0, v1, last ? nv * kB16 : 0, last ? a.n : 0);

@@ -284,9 +284,8 @@ __device__ __forceinline__ void fused_oneshot_body(const FusedArgs& f, const int
   kernel_prologue<N>(a, epoch, parity, s_in, s_end);
   MGW_EXPECT(a.slot_stride == 0 || a.n * 4 <= a.slot_stride);  // fp32 bucket fits its slot
   const int64_t nv = a.n >> 2;
-  const int64_t per = (nv + ctas - 1) / ctas;
-  const int64_t v0 = (int64_t)cta * per;
-  const int64_t v1 = v0 + per < nv ? v0 + per : nv;
+  int64_t v0, v1;
+  cta_chunk(0, nv, cta, ctas, v0, v1);
   const bool last = cta == ctas - 1;
   float* mine = const_cast<float*>(s_in[a.rank]);
   phase_mark(a, 0, cta);
@@ -320,10 +319,8 @@ __device__ __forceinline__ void part_chunks(int64_t nv, int b, int G, PartChunks
   pc.longest = 0;
 #pragma unroll
   for (int p = 0; p < N; ++p) {
-    const int64_t q0 = part_begin(p, nv, N), q1 = part_begin(p + 1, nv, N);
-    const int64_t per = (q1 - q0 + G - 1) / G;
-    const int64_t c0 = q0 + (int64_t)b * per;
-    const int64_t c1 = c0 + per < q1 ? c0 + per : q1;
+    int64_t c0, c1;
+    cta_chunk(part_begin(p, nv, N), part_begin(p + 1, nv, N), b, G, c0, c1);
     pc.lo[p] = c0;
     pc.len[p] = c1 > c0 ? c1 - c0 : 0;
     pc.longest = pc.len[p] > pc.longest ? pc.len[p] : pc.longest;

@@ -283,7 +283,7 @@ int resolve_fused_algo(const mgw_comm* c, int64_t n, int algo) {
   int chosen = pick_fused_algo(c, n, algo);
   if (chosen == MGW_ALGO_PUSH_ONESHOT && c->world * round_up(n, 16) * 4 > c->slot_bytes) chosen = MGW_ALGO_ONESHOT;
   if ((chosen == MGW_ALGO_PUSH || chosen == MGW_ALGO_PUSH_PIPE) &&
-      c->world * (((n / 4 + c->world - 1) / c->world + 1) * 4) * 4 > c->slot_bytes)
+      c->world * push_stride(n / 4, c->world) * 4 > c->slot_bytes)
     chosen = MGW_ALGO_TWOSHOT;
   return chosen;
 }
@@ -404,7 +404,7 @@ int comm_allreduce_fused(mgw_comm* c, const Row* host_rows, const Row* dev_rows,
     PushArgs x;
     memset(&x, 0, sizeof(x));
     x.f = f;
-    x.stride = one ? round_up(n, 16) : ((n / 4 + c->world - 1) / c->world + 1) * 4;
+    x.stride = one ? round_up(n, 16) : push_stride(n / 4, c->world);
     for (int s = 0; s < c->world; ++s) {
       x.gather[s] = c->peer[s] + kSlotOff + 2 * c->slot_bytes;
       x.pipe[s] = reinterpret_cast<uint64_t*>(c->peer[s] + kPipeOff);
@@ -878,7 +878,7 @@ int mgw_group_allreduce_fused(mgw_comm* const* comms, void* const* tables, const
       const bool one = chosen == MGW_ALGO_PUSH_ONESHOT;
       PushArgs& x = gp->args[r];
       x.f = f;
-      x.stride = one ? round_up(n, 16) : ((n / 4 + world - 1) / world + 1) * 4;
+      x.stride = one ? round_up(n, 16) : push_stride(n / 4, world);
       for (int q = 0; q < world; ++q) {
         x.gather[q] = c->peer[q] + kSlotOff + 2 * c->slot_bytes;
         x.pipe[q] = reinterpret_cast<uint64_t*>(c->peer[q] + kPipeOff);
@@ -1233,7 +1233,7 @@ int mgw_allreduce_emulated(float* const* ins, float* const* outs, int world, int
 static int push_emulated(void* const* tables, int world, int64_t n, float scale, cudaStream_t s, bool oneshot,
                          bool pipe = false) {
   if (world < 2) return set_error(MGW_EINVAL, "push exchanges need >= 2 ranks");
-  const int64_t stride = oneshot ? round_up(n, 16) : ((n / 4 + world - 1) / world + 1) * 4;
+  const int64_t stride = oneshot ? round_up(n, 16) : push_stride(n / 4, world);
   char* mem = nullptr;
   const size_t in_bytes = (size_t)round_up((int64_t)world * stride * 4, 256);
   const size_t g_bytes = oneshot ? in_bytes : (size_t)round_up(n * 4, 256);

@@ -34,8 +34,10 @@ struct PushArgs {
   int subs;                    // pipelined two-shot: sub-chunks per CTA chunk
 };
 
-__device__ __forceinline__ int64_t push_stride(int64_t nv, int world) {
-  return ((nv + world - 1) / world + 1) * 4;  // one part of 16-B slots + the n % 4 tail
+// incoming row stride in floats: the longest part (ceil(nv / world) + kPartAlign slots,
+// part_begin rounds down) + one slot for the n % 4 tail
+__host__ __device__ __forceinline__ int64_t push_stride(int64_t nv, int world) {
+  return ((nv + world - 1) / world + kPartAlign + 1) * 4;
 }
 
 template <int N>
@@ -223,9 +225,8 @@ __device__ __forceinline__ void push_oneshot_body(const PushArgs& x, const int c
   }
   __syncthreads();
   const int64_t nv = a.n >> 2;
-  const int64_t per = (nv + ctas - 1) / ctas;
-  const int64_t v0 = (int64_t)cta * per;
-  const int64_t v1 = v0 + per < nv ? v0 + per : nv;
+  int64_t v0, v1;
+  cta_chunk(0, nv, cta, ctas, v0, v1);
   const bool last = cta == ctas - 1;
   const float scale = f.scale;
   const bool scaled = scale != 1.0f;
