@@ -1,0 +1,358 @@
+// ll128.cuh -- flag-in-line two-shot ("LL128"): the push two-shot's data movement with no
+// barrier at all.  Same result as ring_allreduce (allreduce_net.py:370-411) on the group
+// bucket (:499-509), bit for bit.
+//
+// The push two-shot (push.cuh) pays two CTA barriers per call; each is a system-scope
+// release (the CTA stalls until every NVLink store it issued is acknowledged) plus a flag
+// round trip, and a phase cannot start on any data until the slowest peer CTA signalled.
+// Here data and flag travel together: a 128-B line = 8 lanes x 16 B, lanes 0..6 carry 7
+// 16-B slots of the bucket, lane 7 carries the flag (epoch << 32 | collective tag) twice.
+// One warp store instruction writes whole lines (a group of 8 consecutive lanes per line),
+// and NVLink delivers a warp's 128-B line as one write, so a reader that sees the flag of a
+// line (loaded by the same warp instruction as the other 7 lanes) sees its payload -- the
+// NVLink LL128 contract of NCCL's protocol of that name.  Readers only poll local memory.
+//
+//   phase 1  CTA b stores its line range of every part p (scaled) into rank p's incoming
+//            row `me`                                  (lines: 2 (N-1)/N x M x 8/7 out)
+//   phase 2  CTA b polls its line range of its own part in the N local rows, folds in the
+//            reference order (fold start = the element's `_segments` segment), writes its
+//            tensors and stores result lines into every peer's gather row `me`
+//   phase 3  CTA b polls its line range of every peer part in its gather rows and writes
+//            its tensors.
+//
+// Every CTA depends only on the same CTA index of its peers (same part / line split), so
+// the grid need not be co-resident across ranks.  Areas: incoming lines = slot[parity] of
+// the IPC region ([N src][row_lines]), gather lines = gather[parity] ([N part][row_lines]):
+// the slots every other kernel uses, with the same reuse distance 2 by parity (a pull
+// kernel of call k may still be reading a peer's slot[parity k] when this rank starts
+// call k + 1).  The flag's epoch tells calls apart; lines must fit one slot.
+// Disagreement: CTA 0 pushes the LL header (barrier word of CTA 0) and polls check the
+// source's header, so a peer in another collective fails fast as for LL.
+#pragma once
+
+#include "ll.cuh"
+
+namespace mgw {
+
+constexpr int kL128Lanes = 8;                          // 16-B lanes per 128-B line
+constexpr int kL128Vec = kL128Lanes - 1;               // payload 16-B slots per line
+constexpr int kL128Step = kThreads / kL128Lanes;       // lines per CTA step (64)
+constexpr int kL128Words = 2 * kL128Lanes;             // u64 words per line
+
+struct L128Args {
+  FusedArgs f;
+  char* in[kMaxRanks];       // rank r's slot 0: incoming lines [N src][row_lines] (parity 1 at slot_stride)
+  char* gat[kMaxRanks];      // rank r's gather area 0: result lines [N part][row_lines]
+  uint64_t* hdr[kMaxRanks];  // header words (CTA 0's arrive flags), as LLArgs::hdr
+  int64_t hdr_stride;        // words from parity 0 to parity 1 of hdr
+  int64_t row_lines;         // lines per row (the longest part)
+};
+
+// 16-B slots of a bucket of n elements (the last one partial when n % 4 != 0)
+__host__ __device__ __forceinline__ int64_t l128_slots(int64_t n) { return (n + 3) / 4; }
+// lines per row: the longest part (part_begin rounds down to kPartAlign) in lines
+__host__ __device__ __forceinline__ int64_t l128_row_lines(int64_t n, int world) {
+  const int64_t part = (l128_slots(n) + world - 1) / world + kPartAlign;
+  return (part + kL128Vec - 1) / kL128Vec;
+}
+
+__device__ __forceinline__ void st_volatile_v2(uint64_t* p, uint64_t a, uint64_t b) {
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+
+__device__ __forceinline__ void ld_volatile_v2(const uint64_t* p, uint64_t& a, uint64_t& b) {
+  asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+
+__device__ __forceinline__ uint64_t l128_lo(float4 v) {
+  return (uint64_t)__float_as_uint(v.x) | ((uint64_t)__float_as_uint(v.y) << 32);
+}
+__device__ __forceinline__ uint64_t l128_hi(float4 v) {
+  return (uint64_t)__float_as_uint(v.z) | ((uint64_t)__float_as_uint(v.w) << 32);
+}
+__device__ __forceinline__ float l128_elem(uint64_t lo, uint64_t hi, int j) {
+  const uint64_t w = j < 2 ? lo : hi;
+  return __uint_as_float((uint32_t)(j & 1 ? w >> 32 : w));
+}
+
+// Warp-collective: poll until every active group's line (this lane's 16 B at `p`) carries
+// `expect` in its flag lane.  Returns a warp-uniform status.  Slow path every 16 spins: a
+// flag of this epoch with another tag, or the source's header of this epoch with another
+// tag (a peer in a different collective), the abort flag, the timeout.
+__device__ __forceinline__ int l128_poll(const uint64_t* p, bool active, uint64_t expect, const uint64_t* hdr,
+                                         const ArArgs& a, uint64_t& w0, uint64_t& w1) {
+  const int flag_lane = (threadIdx.x & 31) | (kL128Lanes - 1);
+  const uint32_t epoch = (uint32_t)(expect >> 32);
+  uint64_t start = 0;
+  for (uint32_t spin = 0;; ++spin) {
+    if (active) ld_volatile_v2(p, w0, w1);
+    const uint64_t flag = __shfl_sync(0xffffffffu, w1, flag_lane);
+    if (__all_sync(0xffffffffu, !active || flag == expect)) return MGW_DEV_OK;
+    if ((spin & 15) == 15) {
+      int st = MGW_DEV_OK;
+      if (active && flag != expect && (uint32_t)(flag >> 32) == epoch) st = MGW_DEV_MISMATCH;
+      if (active && st == MGW_DEV_OK) {
+        const uint64_t h = ld_relaxed_sys_u64(hdr);
+        if ((uint32_t)(h >> 32) == epoch && (uint32_t)h != a.tag) st = MGW_DEV_MISMATCH;
+      }
+      if (st == MGW_DEV_OK && load_relaxed_sys32(a.abort_flag[a.rank]) != 0u) st = MGW_DEV_PEER_ABORT;
+      if (spin == 15) start = global_ns();
+      if (st == MGW_DEV_OK && global_ns() - start > a.timeout_ns) st = MGW_DEV_TIMEOUT;
+      // warp-uniform: the largest code any lane saw (mismatch 1 < abort < timeout order is
+      // irrelevant -- any error ends the call)
+      const int any = __reduce_max_sync(0xffffffffu, st);
+      if (any != MGW_DEV_OK) return any;
+    }
+  }
+}
+
+// the fold of one 16-B slot from the N sources' words, starting at source `seg`
+// (static register indexing: the rotation is unrolled per start)
+template <int N>
+__device__ __forceinline__ float4 l128_fold4(const uint64_t (&lo)[N], const uint64_t (&hi)[N], int seg) {
+  float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int s = 0; s < N; ++s) {
+    if (s == seg) {
+      float r[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float acc = l128_elem(lo[s], hi[s], j);
+#pragma unroll
+        for (int kk = 1; kk < N; ++kk) {
+          const int src = (s + kk) % N;
+          acc = __fadd_rn(acc, l128_elem(lo[src], hi[src], j));
+        }
+        r[j] = acc;
+      }
+      y = make_float4(r[0], r[1], r[2], r[3]);
+    }
+  }
+  return y;
+}
+
+template <int N>
+__device__ __forceinline__ float l128_fold1(const uint64_t (&lo)[N], const uint64_t (&hi)[N], int seg, int j) {
+  float out = 0.f;
+#pragma unroll
+  for (int s = 0; s < N; ++s) {
+    if (s == seg) {
+      float acc = l128_elem(lo[s], hi[s], j);
+#pragma unroll
+      for (int kk = 1; kk < N; ++kk) {
+        const int src = (s + kk) % N;
+        acc = __fadd_rn(acc, l128_elem(lo[src], hi[src], j));
+      }
+      out = acc;
+    }
+  }
+  return out;
+}
+
+// bucket slot v (elements 4v ..) from the layer tensors, scaled; zeros past n
+__device__ __forceinline__ float4 l128_load(const FusedArgs& f, int& k, int64_t v, float scale, bool scaled) {
+  const int64_t e = v << 2;
+  bool fast;
+  const float* tp = fused_tensor(f, k, e, fast);
+  if (fast) {
+    const float4 x = *reinterpret_cast<const float4*>(tp);
+    return scaled ? fmul4(x, scale) : x;
+  }
+  float r[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    float x = 0.f;
+    if (e + j < f.ar.n) {
+      x = *fused_tensor1(f, k, e + j);
+      if (scaled) x = __fmul_rn(x, scale);
+    }
+    r[j] = x;
+  }
+  return make_float4(r[0], r[1], r[2], r[3]);
+}
+
+// bucket slot v into the layer tensors (elements past n dropped)
+__device__ __forceinline__ void l128_store(const FusedArgs& f, int& k, int64_t v, uint64_t lo, uint64_t hi) {
+  const int64_t e = v << 2;
+  bool fast;
+  float* tp = fused_tensor(f, k, e, fast);
+  if (fast) {
+    *reinterpret_cast<float4*>(tp) = make_float4(l128_elem(lo, hi, 0), l128_elem(lo, hi, 1), l128_elem(lo, hi, 2),
+                                                 l128_elem(lo, hi, 3));
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    if (e + j < f.ar.n) *fused_tensor1(f, k, e + j) = l128_elem(lo, hi, j);
+}
+
+template <int N>
+__device__ __forceinline__ void ll128_body(const L128Args& x, const int cta, const int ctas) {
+  const FusedArgs& f = x.f;
+  const ArArgs& a = f.ar;
+  grid_dep_wait();
+  stamp_enter(a.stamp);
+  __shared__ int64_t s_end[kMaxRanks];
+  __shared__ int64_t s_part[kMaxRanks + 1];
+  const uint32_t epoch = load_volatile32(a.state) + 1u;
+  const int parity = (int)(epoch & 1u);
+  const int me = a.rank;
+  const int64_t n = a.n;
+  const int64_t slots = l128_slots(n);
+  if (threadIdx.x < N) {
+    const int t = threadIdx.x;
+    const int64_t q = n / N, r = n % N;
+    s_end[t] = (int64_t)(t + 1) * q + (t + 1 < r ? t + 1 : r);  // end of reference segment t
+  }
+  if (threadIdx.x <= N) s_part[threadIdx.x] = part_begin(threadIdx.x, slots, N);
+  // kSkipPack / kSkipPhase1 / kSkipPhase2 run one phase per launch (emulated ranks on one
+  // device, tests only: every launch polls lines that earlier launches wrote)
+  const bool do_push = !(a.flags & kSkipPack), do_fold = !(a.flags & kSkipPhase1),
+             do_unpack = !(a.flags & kSkipPhase2);
+  if (do_push && cta == 0 && threadIdx.x < N)
+    st_relaxed_sys_u64(x.hdr[threadIdx.x] + parity * x.hdr_stride + me, ((uint64_t)epoch << 32) | a.tag);
+  __syncthreads();
+  const uint64_t expect = ((uint64_t)epoch << 32) | a.tag;
+  const int sub = threadIdx.x & (kL128Lanes - 1);  // lane within the line
+  const int grp = threadIdx.x / kL128Lanes;        // line within the CTA step
+  const bool carrier = sub < kL128Vec;             // payload lane (lane 7 = flag)
+  const int64_t rl = x.row_lines;
+  const float scale = f.scale;
+  const bool scaled = scale != 1.0f;
+  const uint64_t* hdr_mine = x.hdr[me] + parity * x.hdr_stride;
+  MGW_EXPECT(a.slot_stride == 0 || (int64_t)N * rl * 128 <= a.slot_stride);
+  const int64_t poff = (int64_t)parity * a.slot_stride;
+  auto in_of = [&](int r) { return reinterpret_cast<uint64_t*>(x.in[r] + poff); };
+  auto gat_of = [&](int r) { return reinterpret_cast<uint64_t*>(x.gat[r] + poff); };
+  int status = MGW_DEV_OK;
+
+  phase_mark(a, 0, cta);
+  // ---- phase 1: my line range of every part p into rank p's incoming row `me`
+  if (do_push) {
+    int k = 0;
+    bool k_set = false;
+#pragma unroll 1
+    for (int p = 0; p < N; ++p) {
+      const int64_t q0 = s_part[p], q1 = s_part[p + 1];
+      int64_t l0, l1;
+      cta_chunk(0, (q1 - q0 + kL128Vec - 1) / kL128Vec, cta, ctas, l0, l1);
+      uint64_t* row = in_of(p) + (int64_t)me * rl * kL128Words + sub * 2;
+      for (int64_t base = l0; base < l1; base += kL128Step) {
+        const int64_t l = base + grp;
+        const int64_t v = q0 + l * kL128Vec + sub;
+        const bool live = l < l1 && carrier && v < q1;
+        float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (live) {
+          if (!k_set) {
+            k = fused_row_covering(f, v << 2);
+            k_set = true;
+          }
+          y = l128_load(f, k, v, scale, scaled);
+        }
+        __syncwarp();
+        if (l < l1) st_volatile_v2(row + l * kL128Words, carrier ? l128_lo(y) : expect, carrier ? l128_hi(y) : expect);
+      }
+    }
+  }
+  phase_mark(a, 1, cta);
+  // ---- phase 2: fold my line range of my part from the N local rows; write my tensors and
+  //      every peer's gather row `me`
+  if (do_fold) {
+    const int64_t q0 = s_part[me], q1 = s_part[me + 1];
+    int64_t l0, l1;
+    cta_chunk(0, (q1 - q0 + kL128Vec - 1) / kL128Vec, cta, ctas, l0, l1);
+    const uint64_t* in = in_of(me) + sub * 2;
+    int seg = 0, k = 0;
+    bool k_set = false;
+    for (int64_t base = l0; base < l1 && status == MGW_DEV_OK; base += kL128Step) {
+      const int64_t l = base + grp;
+      const bool active = l < l1;
+      const int64_t v = q0 + l * kL128Vec + sub;
+      uint64_t lo[N], hi[N];
+#pragma unroll
+      for (int s = 0; s < N; ++s) {
+        lo[s] = hi[s] = 0;
+        if (active) ld_volatile_v2(in + ((int64_t)s * rl + l) * kL128Words, lo[s], hi[s]);
+      }
+#pragma unroll
+      for (int s = 0; s < N; ++s) {
+        const uint64_t flag = __shfl_sync(0xffffffffu, hi[s], (threadIdx.x & 31) | (kL128Lanes - 1));
+        if (!__all_sync(0xffffffffu, !active || flag == expect)) {
+          const int st = l128_poll(in + ((int64_t)s * rl + l) * kL128Words, active, expect, hdr_mine + s, a, lo[s], hi[s]);
+          if (st != MGW_DEV_OK) status = st;
+        }
+      }
+      if (status != MGW_DEV_OK) break;
+      const bool live = active && carrier && v < q1;
+      float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (live) {
+        const int64_t e = v << 2;
+        seg = advance_segment(seg, e, s_end);
+        if (e + 3 < s_end[seg]) {
+          y = l128_fold4<N>(lo, hi, seg);
+        } else {  // the slot straddles a segment boundary, or is the partial last slot
+          float r[4];
+          int s2 = seg;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            r[j] = 0.f;
+            if (e + j < n) {
+              s2 = advance_segment(s2, e + j, s_end);
+              r[j] = l128_fold1<N>(lo, hi, s2, j);
+            }
+          }
+          y = make_float4(r[0], r[1], r[2], r[3]);
+        }
+        if (!k_set) {
+          k = fused_row_covering(f, e);
+          k_set = true;
+        }
+        l128_store(f, k, v, l128_lo(y), l128_hi(y));
+      }
+      __syncwarp();
+      const uint64_t w0 = carrier ? l128_lo(y) : expect, w1 = carrier ? l128_hi(y) : expect;
+#pragma unroll
+      for (int q = 0; q < N; ++q)
+        if (q != me && active) st_volatile_v2(gat_of(q) + ((int64_t)me * rl + l) * kL128Words + sub * 2, w0, w1);
+    }
+  }
+  phase_mark(a, 2, cta);
+  // ---- phase 3: every peer part's result lines from my gather rows into my tensors
+  if (do_unpack) {
+    int k = 0;
+    bool k_set = false;
+#pragma unroll 1
+    for (int p = 0; p < N && status == MGW_DEV_OK; ++p) {
+      if (p == me) continue;
+      const int64_t q0 = s_part[p], q1 = s_part[p + 1];
+      int64_t l0, l1;
+      cta_chunk(0, (q1 - q0 + kL128Vec - 1) / kL128Vec, cta, ctas, l0, l1);
+      const uint64_t* g = gat_of(me) + (int64_t)p * rl * kL128Words + sub * 2;
+      for (int64_t base = l0; base < l1; base += kL128Step) {
+        const int64_t l = base + grp;
+        const bool active = l < l1;
+        uint64_t w0 = 0, w1 = 0;
+        const int st = l128_poll(g + l * kL128Words, active, expect, hdr_mine + p, a, w0, w1);
+        if (st != MGW_DEV_OK) {
+          status = st;
+          break;
+        }
+        const int64_t v = q0 + l * kL128Vec + sub;
+        if (active && carrier && v < q1) {
+          if (!k_set) {
+            k = fused_row_covering(f, v << 2);
+            k_set = true;
+          }
+          l128_store(f, k, v, w0, w1);
+        }
+      }
+    }
+  }
+  if (status != MGW_DEV_OK && (threadIdx.x & 31) == 0) ll_report(a, status);
+  phase_mark(a, 3, cta);
+  finish_call(a, ctas);
+}
+
+MGW_DEFINE_KERNELS(ll128, L128Args)
+
+}  // namespace mgw

@@ -281,6 +281,8 @@ constexpr int64_t kB16PushMinBytes = 8ll << 20;  // bf16 AUTO: push two-shot at 
 
 int resolve_fused_algo(const mgw_comm* c, int64_t n, int algo) {
   int chosen = pick_fused_algo(c, n, algo);
+  if (chosen == MGW_ALGO_LL128 && (c->world == 1 || c->world * l128_row_lines(n, c->world) * 128 > c->slot_bytes))
+    chosen = MGW_ALGO_PUSH;  // one rank, or the lines do not fit one slot
   if (chosen == MGW_ALGO_PUSH_ONESHOT && c->world * round_up(n, 16) * 4 > c->slot_bytes) chosen = MGW_ALGO_ONESHOT;
   if ((chosen == MGW_ALGO_PUSH || chosen == MGW_ALGO_PUSH_PIPE) &&
       c->world * push_stride(n / 4, c->world) * 4 > c->slot_bytes)
@@ -299,6 +301,7 @@ int resolve_b16_algo(const mgw_comm* c, int64_t n, int algo) {
       algo = c->world > 1 && n * 2 >= kB16PushMinBytes ? MGW_ALGO_PUSH : MGW_ALGO_TWOSHOT;
   }
   if (algo == MGW_ALGO_LL && c->world == 1) algo = MGW_ALGO_ONESHOT;
+  if (algo == MGW_ALGO_LL128) algo = MGW_ALGO_PUSH;  // LL128 lines carry fp32 only
   if (algo == MGW_ALGO_PUSH && (c->world == 1 || c->world * b16_push_stride(n, c->world) * 2 > c->slot_bytes))
     algo = MGW_ALGO_TWOSHOT;  // one rank, or the incoming rows do not fit the slot
   return algo;
@@ -396,6 +399,18 @@ int comm_allreduce_fused(mgw_comm* c, const Row* host_rows, const Row* dev_rows,
     }
     l.hdr_stride = (int64_t)kMaxBlocks * kMaxRanks;
     return launch_ll(l, c->max_ctas, stream);
+  }
+  if (chosen == MGW_ALGO_LL128) {
+    L128Args x;
+    memset(&x, 0, sizeof(x));
+    x.f = f;
+    for (int s = 0; s < c->world; ++s) {
+      x.in[s] = c->peer[s] + kSlotOff;
+      x.gat[s] = c->peer[s] + kSlotOff + 2 * c->slot_bytes;
+      x.hdr[s] = reinterpret_cast<uint64_t*>(c->peer[s] + kArriveOff);
+    }
+    x.hdr_stride = (int64_t)kMaxBlocks * kMaxRanks;
+    return launch_ll128(x, c->max_ctas, stream, c->vec_per_cta);
   }
   if (chosen == MGW_ALGO_PUSH_ONESHOT || chosen == MGW_ALGO_PUSH || chosen == MGW_ALGO_PUSH_PIPE) {
     // incoming rows: one 64-B aligned row per source (one-shot), or one part + tail per
@@ -831,18 +846,20 @@ int mgw_group_allreduce_fused(mgw_comm* const* comms, void* const* tables, const
   if (chosen < 0) return MGW_OK;
   if (chosen == MGW_ALGO_NVLS) return set_error(MGW_EINVAL, "NVLS has no rank-group launch");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const bool ll = chosen == MGW_ALGO_LL,
+  const bool ll = chosen == MGW_ALGO_LL, l128 = chosen == MGW_ALGO_LL128,
              push = chosen == MGW_ALGO_PUSH || chosen == MGW_ALGO_PUSH_ONESHOT || chosen == MGW_ALGO_PUSH_PIPE;
   // the argument blocks are large (8 ranks x ~1.5 KB): build them on the heap
   std::unique_ptr<RankGroup<FusedArgs>> gf(new RankGroup<FusedArgs>());
   std::unique_ptr<RankGroup<PushArgs>> gp(new RankGroup<PushArgs>());
   std::unique_ptr<RankGroup<LLArgs>> gl(new RankGroup<LLArgs>());
+  std::unique_ptr<RankGroup<L128Args>> g8(new RankGroup<L128Args>());
+  memset(g8.get(), 0, sizeof(*g8));
   memset(gf.get(), 0, sizeof(*gf));
   memset(gp.get(), 0, sizeof(*gp));
   memset(gl.get(), 0, sizeof(*gl));
   int first = 0;
   for (int r = 0; r < world; ++r) {
-    gf->first[r] = gp->first[r] = gl->first[r] = first;
+    gf->first[r] = gp->first[r] = gl->first[r] = g8->first[r] = first;
     if (n_elem[r] < 0) continue;
     const mgw_comm* c = comms[r];
     const mgw_table_t* t = as_table(tables[r]);
@@ -868,6 +885,16 @@ int mgw_group_allreduce_fused(mgw_comm* const* comms, void* const* tables, const
       l.hdr_stride = (int64_t)kMaxBlocks * kMaxRanks;
       if (n > (b16 ? 2 : 1) * kLLElems) return set_error(MGW_EINVAL, "LL bucket of %lld elements too large", (long long)n);
       grid = b16 ? plan_ll_b16(l, c->max_ctas) : plan_ll(l, c->max_ctas);
+    } else if (l128) {
+      L128Args& x = g8->args[r];
+      x.f = f;
+      for (int q = 0; q < world; ++q) {
+        x.in[q] = c->peer[q] + kSlotOff;
+        x.gat[q] = c->peer[q] + kSlotOff + 2 * c->slot_bytes;
+        x.hdr[q] = reinterpret_cast<uint64_t*>(c->peer[q] + kArriveOff);
+      }
+      x.hdr_stride = (int64_t)kMaxBlocks * kMaxRanks;
+      grid = plan_ll128(x, c->max_ctas, c->vec_per_cta);
     } else if (push && b16) {
       PushArgs& x = gp->args[r];
       x.f = f;
@@ -892,10 +919,11 @@ int mgw_group_allreduce_fused(mgw_comm* const* comms, void* const* tables, const
     }
     first += grid;
   }
-  for (int r = world; r <= kMaxRanks; ++r) gf->first[r] = gp->first[r] = gl->first[r] = first;
+  for (int r = world; r <= kMaxRanks; ++r) gf->first[r] = gp->first[r] = gl->first[r] = g8->first[r] = first;
   if (first > 2 * kSMs)
     return set_error(MGW_EINVAL, "rank group needs %d co-resident CTAs (> %d): lower the CTA caps", first, 2 * kSMs);
   if (ll) return b16 ? launch_ll_b16_group(*gl, world, s) : launch_ll_group(*gl, world, s);
+  if (l128) return launch_ll128_group(*g8, world, s);
   if (push && b16) return launch_b16_push_group(*gp, world, s);
   if (push)
     return launch_push_group(*gp, world, chosen == MGW_ALGO_PUSH_ONESHOT ? 1 : (chosen == MGW_ALGO_PUSH_PIPE ? 2 : 0), s);
@@ -926,8 +954,9 @@ int mgw_checked_violations(int reset, uint64_t* total, int* checked) {
   *checked = 0;
 #endif
   unsigned long long sum = 0;
-  int (*getters[])(unsigned long long*, bool) = {violations_allreduce, violations_bf16, violations_fused, violations_ll,
-                                                 violations_nvls,      violations_push, violations_rows};
+  int (*getters[])(unsigned long long*, bool) = {violations_allreduce, violations_bf16, violations_fused,
+                                                 violations_ll,        violations_ll128, violations_nvls,
+                                                 violations_push,      violations_rows};
   for (auto get : getters) {
     unsigned long long v = 0;
     if (get(&v, reset != 0) != MGW_OK) return set_error(MGW_ECUDA, "reading the checked-build violation counters");
@@ -1001,7 +1030,7 @@ int mgw_allreduce(mgw_comm* c, int64_t n_elem, int algo, void* stream) {
 int mgw_allreduce_fused(mgw_comm* c, const void* table, int n_rows, int64_t n_elem, float scale, int algo,
                         void* stream) {
   if (!c) return set_error(MGW_EINVAL, "comm is null");
-  if (algo < MGW_ALGO_AUTO || algo > MGW_ALGO_PUSH_PIPE) return set_error(MGW_EINVAL, "unknown algorithm %d", algo);
+  if (algo < MGW_ALGO_AUTO || algo > MGW_ALGO_LL128) return set_error(MGW_EINVAL, "unknown algorithm %d", algo);
   int rc = check_table(table, n_rows, n_elem);
   if (rc) return rc;
   const mgw_table_t* t = as_table(table);
@@ -1376,6 +1405,71 @@ static int ll_emulated(void* const* tables, int world, int64_t n, float scale, c
   return rc;
 }
 
+// LL128 two-shot with emulated ranks on one device: every rank's phase 1 (line stores), then
+// every rank's phase 2 (poll + fold + result lines), then phase 3 -- each launch polls only
+// lines that earlier, completed launches wrote, so no launch ever waits on another.
+static int ll128_emulated(void* const* tables, int world, int64_t n, float scale, cudaStream_t s) {
+  if (world < 2) return set_error(MGW_EINVAL, "LL128 needs >= 2 ranks");
+  const size_t area = (size_t)world * l128_row_lines(n, world) * 128;
+  const size_t hdr_bytes = 2 * kMaxRanks * sizeof(uint64_t);
+  const size_t per_rank = 2 * area + hdr_bytes + 256;
+  char* mem = nullptr;
+  MGW_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&mem), (size_t)world * per_rank, s));
+  int rc = MGW_OK;
+  {
+    cudaError_t e = cudaMemsetAsync(mem, 0, (size_t)world * per_rank, s);
+    if (e != cudaSuccess) rc = set_error(MGW_ECUDA, "memset: %s", cudaGetErrorString(e));
+  }
+  L128Args x;
+  memset(&x, 0, sizeof(x));
+  for (int r = 0; r < world; ++r) {
+    char* base = mem + (size_t)r * per_rank;
+    x.in[r] = base;
+    x.gat[r] = base + area;
+    x.hdr[r] = reinterpret_cast<uint64_t*>(base + 2 * area);
+    x.f.ar.abort_flag[r] = reinterpret_cast<uint32_t*>(base + 2 * area + hdr_bytes);
+  }
+  x.hdr_stride = kMaxRanks;
+  x.f.ar.n = n;
+  x.f.ar.world = world;
+  x.f.ar.timeout_ns = 2000000000ull;
+  x.f.scale = scale;
+  const int step_flags[3] = {kSkipPhase1 | kSkipPhase2, kSkipPack | kSkipPhase2, kSkipPack | kSkipPhase1};
+  for (int step = 0; step < 3 && rc == MGW_OK; ++step) {
+    for (int r = 0; r < world && rc == MGW_OK; ++r) {
+      char* ctl = mem + (size_t)r * per_rank + 2 * area + hdr_bytes;  // [abort u32][state u32 x2][err i32]
+      // every launch of rank r sees call counter 0 -> epoch 1 (finish_call advances it)
+      cudaError_t e = cudaMemsetAsync(ctl + 4, 0, 8, s);
+      if (e != cudaSuccess) rc = set_error(MGW_ECUDA, "memset: %s", cudaGetErrorString(e));
+      const mgw_table_t* t = as_table(tables[r]);
+      const int n_rows = (int)t->host.size();
+      x.f.use_inline = n_rows <= kInlineRows;
+      if (x.f.use_inline)
+        for (int k = 0; k < n_rows; ++k) x.f.inline_rows[k] = t->host[k];
+      x.f.rows = t->dev;
+      x.f.n_rows = n_rows;
+      x.f.ar.rank = r;
+      x.f.ar.state = reinterpret_cast<uint32_t*>(ctl + 4);
+      x.f.ar.err = reinterpret_cast<int*>(ctl + 12);
+      x.f.ar.flags = step_flags[step];
+      if (rc == MGW_OK) rc = launch_ll128(x, 2 * kSMs, s, nullptr);
+    }
+  }
+  int bad = 0;
+  for (int r = 0; r < world && rc == MGW_OK; ++r) {  // any device error word set?
+    int w = 0;
+    cudaError_t e = cudaMemcpyAsync(&w, mem + (size_t)r * per_rank + 2 * area + hdr_bytes + 12, 4,
+                                    cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) rc = set_error(MGW_ECUDA, "LL128 emulation: %s", cudaGetErrorString(e));
+    bad |= w;
+  }
+  cudaError_t e = cudaFreeAsync(mem, s);
+  if (rc == MGW_OK && e != cudaSuccess) rc = set_error(MGW_ECUDA, "cudaFreeAsync: %s", cudaGetErrorString(e));
+  if (rc == MGW_OK && bad) rc = set_error(MGW_EPROTO, "emulated LL128 exchange raised device error %d", bad);
+  return rc;
+}
+
 int mgw_allreduce_fused_emulated(void* const* tables, float* const* slots, int world, int64_t n, float scale, int algo,
                                  void* stream) {
   if (!tables || !slots || world < 1 || world > kMaxRanks || n < 0)
@@ -1387,6 +1481,14 @@ int mgw_allreduce_fused_emulated(void* const* tables, float* const* slots, int w
       if (rc) return rc;
     }
     return n == 0 ? MGW_OK : ll_emulated(tables, world, n, scale, static_cast<cudaStream_t>(stream), false);
+  }
+  if (algo == MGW_ALGO_LL128) {
+    for (int r = 0; r < world; ++r) {
+      const mgw_table_t* t = as_table(tables[r]);
+      int rc = check_table(tables[r], t ? (int)t->host.size() : 0, n);
+      if (rc) return rc;
+    }
+    return n == 0 ? MGW_OK : ll128_emulated(tables, world, n, scale, static_cast<cudaStream_t>(stream));
   }
   if (algo == MGW_ALGO_PUSH || algo == MGW_ALGO_PUSH_ONESHOT || algo == MGW_ALGO_PUSH_PIPE) {
     for (int r = 0; r < world; ++r) {

@@ -43,7 +43,8 @@ def main() -> int:
     _, session = open_session_dist(capacity_bytes=max(sizes) + (1 << 20))
     comm = session.comm
     ids = {"oneshot": _native.ALGO_ONESHOT, "twoshot": _native.ALGO_TWOSHOT, "push": _native.ALGO_PUSH,
-           "push_pipe": _native.ALGO_PUSH_PIPE, "push_oneshot": _native.ALGO_PUSH_ONESHOT, "auto": _native.ALGO_AUTO}
+           "push_pipe": _native.ALGO_PUSH_PIPE, "push_oneshot": _native.ALGO_PUSH_ONESHOT, "auto": _native.ALGO_AUTO,
+           "ll128": _native.ALGO_LL128}
     out = {"world": world, "sizes": sizes, "bus_gbs": {}, "us": {}}
     for name in args.algos.split(","):
         for graph in (False, True):

@@ -76,7 +76,8 @@ def every_algorithm_task(config, session, *, arrays):
         for key, vals in arrays[config.rank].items():
             n = vals.size
             for name, algo in (("ll", _native.ALGO_LL), ("one", _native.ALGO_ONESHOT), ("two", _native.ALGO_TWOSHOT),
-                               ("push", _native.ALGO_PUSH), ("push1", _native.ALGO_PUSH_ONESHOT)):
+                               ("push", _native.ALGO_PUSH), ("push1", _native.ALGO_PUSH_ONESHOT),
+                               ("ll128", _native.ALGO_LL128)):
                 t = torch.from_numpy(vals.copy()).to(session.device)
                 table = _native.DeviceTable([(t.data_ptr(), n, 0)])
                 _native.call("mgw_allreduce_fused", session.comm, table.ptr, 1, n, ctypes.c_float(1.0), algo, h)
@@ -320,7 +321,7 @@ def stress_task(config, session, *, iterations=300, seed=2024):
     rng = np.random.default_rng(seed)
     n_ranks = config.n_workers
     algos_f32 = [_native.ALGO_AUTO, _native.ALGO_LL, _native.ALGO_ONESHOT, _native.ALGO_TWOSHOT, _native.ALGO_PUSH,
-                 _native.ALGO_PUSH_ONESHOT]
+                 _native.ALGO_PUSH_ONESHOT, _native.ALGO_LL128]
     algos_b16 = [_native.ALGO_AUTO, _native.ALGO_LL, _native.ALGO_ONESHOT, _native.ALGO_TWOSHOT]
     h = session.stream.cuda_stream
     failures = []
@@ -339,7 +340,10 @@ def stress_task(config, session, *, iterations=300, seed=2024):
             dtype = torch.bfloat16 if bf16 else torch.float32
             idx = torch.arange(n, device=session.device)
             pattern = (idx % 5).to(torch.float32)
-            x = (pattern + float(config.rank + 1)).to(dtype)
+            # fp32: an iteration-dependent offset, so a stale line of an earlier call in the
+            # same area can never pass for this call's data
+            it_off = 0.0 if bf16 else 16.0 * (it % 11)
+            x = (pattern + float(config.rank + 1) + it_off).to(dtype)
             rows = []
             views = []
             for lo, hi in zip(bounds[:-1], bounds[1:]):
@@ -350,7 +354,7 @@ def stress_task(config, session, *, iterations=300, seed=2024):
             fn = "mgw_allreduce_fused_bf16" if bf16 else "mgw_allreduce_fused"
             _native.call(fn, session.comm, table.ptr, len(rows), n, ctypes.c_float(1.0), algo, h)
             got = torch.cat(views).float()
-            want = pattern * n_ranks + n_ranks * (n_ranks + 1) / 2
+            want = pattern * n_ranks + n_ranks * (n_ranks + 1) / 2 + n_ranks * it_off
             session.stream.synchronize()
             table.close()
             if not torch.equal(got, want):

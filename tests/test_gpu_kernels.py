@@ -191,7 +191,8 @@ def _fused_emulated(torch, per_rank_tensors, counts, algo, scale=1.0):
 
 
 @pytest.mark.parametrize("algo", [_native.ALGO_ONESHOT, _native.ALGO_TWOSHOT, _native.ALGO_PUSH,
-                                  _native.ALGO_PUSH_ONESHOT, _native.ALGO_LL, _native.ALGO_PUSH_PIPE])
+                                  _native.ALGO_PUSH_ONESHOT, _native.ALGO_LL, _native.ALGO_PUSH_PIPE,
+                                  _native.ALGO_LL128])
 @pytest.mark.parametrize("n_ranks", [2, 3, 4, 8])
 @pytest.mark.parametrize("shift", [0, 1])
 def test_fused_exchange_bit_exact(torch_cuda, algo, n_ranks, shift):

@@ -28,7 +28,7 @@ from paper_1811_11141_b200.allreduce_net import LocalGroup, ProtocolError, group
 pytestmark = pytest.mark.gpu
 
 ALGOS_F32 = [_native.ALGO_LL, _native.ALGO_ONESHOT, _native.ALGO_TWOSHOT, _native.ALGO_PUSH_ONESHOT,
-             _native.ALGO_PUSH, _native.ALGO_PUSH_PIPE]
+             _native.ALGO_PUSH, _native.ALGO_PUSH_PIPE, _native.ALGO_LL128]
 ALGOS_B16 = [_native.ALGO_LL, _native.ALGO_ONESHOT, _native.ALGO_TWOSHOT, _native.ALGO_PUSH]
 
 
@@ -165,6 +165,7 @@ CASES = {
     "length_ll": dict(n_of=lambda r: 1000 + r, algo=_native.ALGO_LL),
     "length_push": dict(n_of=lambda r: 3_000_000 + 4 * r, algo=_native.ALGO_PUSH),
     "length_pipe": dict(n_of=lambda r: 3_000_000 + 4 * r, algo=_native.ALGO_PUSH_PIPE),
+    "length_ll128": dict(n_of=lambda r: 3_000_000 + 4 * r, algo=_native.ALGO_LL128),
     "group": dict(n_of=lambda r: 100_000, tags=lambda w: [group_tag(3 + r) for r in range(w)]),
     "iteration": dict(n_of=lambda r: 100_000, tags=lambda w: [group_tag(3, r) for r in range(w)]),
     "scale": dict(n_of=lambda r: 100_000, algo=_native.ALGO_ONESHOT, scales=lambda w: [1.0 / (r + 1) for r in range(w)]),

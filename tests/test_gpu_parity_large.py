@@ -35,7 +35,8 @@ pytestmark = pytest.mark.gpu
 
 A = _native
 F32_ALGOS = {"ll": A.ALGO_LL, "oneshot": A.ALGO_ONESHOT, "twoshot": A.ALGO_TWOSHOT,
-             "push_oneshot": A.ALGO_PUSH_ONESHOT, "push": A.ALGO_PUSH, "push_pipe": A.ALGO_PUSH_PIPE}
+             "push_oneshot": A.ALGO_PUSH_ONESHOT, "push": A.ALGO_PUSH, "push_pipe": A.ALGO_PUSH_PIPE,
+             "ll128": A.ALGO_LL128}
 B16_ALGOS = {"ll": A.ALGO_LL, "oneshot": A.ALGO_ONESHOT, "twoshot": A.ALGO_TWOSHOT, "push": A.ALGO_PUSH}
 LL_ELEMS = 262_144
 
@@ -163,7 +164,7 @@ def get_case(torch, case, n_ranks, bf16=False):
 def f32_algos(case, n_ranks):
     counts, _ = layout(case, n_ranks)
     n = sum(counts)
-    out = ["oneshot", "twoshot", "push", "push_pipe"]
+    out = ["oneshot", "twoshot", "push", "push_pipe", "ll128"]
     if n <= LL_ELEMS:
         out.append("ll")
     if 4 * n <= (16 << 20):
