@@ -28,6 +28,7 @@ def main() -> int:
     ap.add_argument("--bf16", action="store_true", help="bf16 gradients (fp32 accumulation) vs NCCL bf16")
     ap.add_argument("--max-ctas", default="", help="comma list of CTA caps to sweep for the listed algorithms")
     ap.add_argument("--per-cta", default="", help="comma list of two-shot / push slots per CTA to sweep")
+    ap.add_argument("--per-cta-algos", default="", help="algorithms of the --per-cta sweep (default: --algos)")
     args = ap.parse_args()
     import torch
 
@@ -39,7 +40,7 @@ def main() -> int:
 
     rank, world, local = bench._dist_setup(A())
     device = torch.device("cuda", local)
-    sizes = [int(m) << 20 for m in args.mib.split(",")]
+    sizes = [int(float(m) * (1 << 20)) for m in args.mib.split(",")]
     _, session = open_session_dist(capacity_bytes=max(sizes) + (1 << 20))
     comm = session.comm
     ids = {"oneshot": _native.ALGO_ONESHOT, "twoshot": _native.ALGO_TWOSHOT, "push": _native.ALGO_PUSH,
@@ -67,7 +68,7 @@ def main() -> int:
     _native.call("mgw_set_option", _native.OPT_WIDE_MIN_BYTES, 112 << 20)
     for per in [int(v) for v in args.per_cta.split(",") if v]:
         _native.call("mgw_comm_set_tuning", comm, 1, per)
-        for name in args.algos.split(","):
+        for name in (args.per_cta_algos or args.algos).split(","):
             t = bench._exchange_times(comm, world, device, sizes, kind=(5 if args.bf16 else 4) | 256, algo=ids[name],
                                       repeats=args.reps)
             key = f"{name}_per{per}@graph"
