@@ -422,6 +422,11 @@ class RingSession:
             c.rounds += 1
             c.payload_bytes_received += 2 * w * n * (world - 1)
             c.payload_bytes_sent += 2 * w * n * (world - 1)
+        elif algo == _native.ALGO_LL128:  # the two-shot's bytes in 128-B lines of 112 B payload
+            c.rounds += 2
+            mine = sizes[rank]
+            c.payload_bytes_received += w * ((world - 1) * mine + n - mine) * 8 // 7
+            c.payload_bytes_sent += w * ((n - mine) + (world - 1) * mine) * 8 // 7
         elif algo in (_native.ALGO_ONESHOT, _native.ALGO_PUSH_ONESHOT):
             c.rounds += 1
             c.payload_bytes_received += w * n * (world - 1)
@@ -474,6 +479,9 @@ def _auto_rule(session: RingSession, n: int, fused: bool = False) -> int:
     if fused and 4 * n <= ll_max_bytes(session.config.n_workers):
         return _native.ALGO_LL
     if fused:
+        world = session.config.n_workers
+        if (1 << 20) <= 4 * n <= ((32 << 20) if world == 2 else (16 << 20)):
+            return _native.ALGO_LL128
         push_ok = 4 * n <= (1 << 30)
         if session.config.n_workers == 2:
             if 4 * n <= (16 << 20):

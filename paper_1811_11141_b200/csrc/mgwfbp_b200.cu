@@ -254,6 +254,8 @@ int pick_algo(const mgw_comm* c, int64_t n, int algo) {
 
 // fused group exchange: LL push for small buckets, else pull one-shot / two-shot;
 // NVLS only when enabled (not bit-exact with the reference order)
+constexpr int64_t kLL128MinBytes = 1ll << 20;  // AUTO: LL128 from here (after LL's ceiling)
+
 int pick_fused_algo(const mgw_comm* c, int64_t n, int algo) {
   if (algo != MGW_ALGO_AUTO) return algo;
   if (c->nvls_bound && c->nvls_min_bytes > 0 && n * 4 >= c->nvls_min_bytes && (size_t)n * 4 <= c->nvls_bytes)
@@ -267,6 +269,12 @@ int pick_fused_algo(const mgw_comm* c, int64_t n, int algo) {
   // 1000-layer SyncEASGD bucket, 6.75 GB: 42.4 vs 20.8 ms at N = 4; VGG-16's 553 MB still
   // favours push, profiles/profiles_n4_r01_final.json).
   const int64_t bytes = n * 4;
+  // the flag-in-line two-shot (ll128.cuh) from 1 MiB: no barriers, 2 (N-1)/N x M x 8/7 out
+  // (profiles/ll128_sweep_n{2,4}_r02.json, graph-timed at N = 4: 1 MiB 11.8 vs 15.4 us,
+  // 4 MiB 18.2 vs 27.9, 16 MiB 56.3 vs 58.5; level with the push two-shot at 32 MiB,
+  // which stays above 16 MiB; at N = 2 it wins to 32 MiB)
+  if (c->world > 1 && bytes >= kLL128MinBytes && bytes <= (c->world == 2 ? (32ll << 20) : (16ll << 20)))
+    return MGW_ALGO_LL128;
   const bool push_ok = bytes <= (1ll << 30);
   if (c->world == 2)
     return bytes <= (16ll << 20) ? MGW_ALGO_PUSH_ONESHOT : (push_ok ? MGW_ALGO_PUSH : MGW_ALGO_TWOSHOT);

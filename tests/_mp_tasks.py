@@ -498,3 +498,33 @@ def wide_push_task(config, session, *, n32, n16):
         out["b16_bad"] = int(np.count_nonzero(got != want16))
         table.close()
     return out
+
+
+def algo_mismatch_task(config, session):
+    """Rank 0 runs the LL128 two-shot, the others the push two-shot, on the same 8 MB
+    bucket: LL128's line polls meet the push barrier words (and the LL header the push
+    barrier polls for) -> ProtocolError on every rank, no timeout."""
+    import ctypes
+    import time
+
+    import torch
+
+    from paper_1811_11141_b200 import ProtocolError, _native
+
+    _native.call("mgw_comm_set_timeout_ms", session.comm, 20000)
+    n = 2_000_000
+    algo = _native.ALGO_LL128 if config.rank == 0 else _native.ALGO_PUSH
+    h = session.stream.cuda_stream
+    with torch.cuda.device(session.device), torch.cuda.stream(session.stream):
+        t = torch.ones(n, device=session.device)
+        table = _native.DeviceTable([(t.data_ptr(), n, 0)])
+        t0 = time.perf_counter()
+        try:
+            _native.call("mgw_allreduce_fused", session.comm, table.ptr, 1, n, ctypes.c_float(1.0), algo, h)
+            session.stream.synchronize()
+            session.raise_if_failed()
+            return time.perf_counter() - t0, None
+        except ProtocolError as exc:
+            return time.perf_counter() - t0, str(exc)
+        finally:
+            table.close()

@@ -271,7 +271,8 @@ def test_randomized_stress_every_algorithm_and_dtype():
             assert n_bad == 0, (n, r, first)
 
 
-@pytest.mark.parametrize("task", ["cta_cap_mismatch_task", "swapped_groups_task", "iteration_mismatch_task"])
+@pytest.mark.parametrize("task", ["cta_cap_mismatch_task", "swapped_groups_task", "iteration_mismatch_task",
+                                  "algo_mismatch_task"])
 def test_settings_disagreement_raises_fast(task):
     """Per-rank CTA caps, swapped group order, different iterations: every rank raises
     ProtocolError within a second (the collective tag in every barrier flag / LL header,
