@@ -1,6 +1,7 @@
 // ll128.cuh -- flag-in-line two-shot ("LL128"): the push two-shot's data movement with no
 // barrier at all.  Same result as ring_allreduce (allreduce_net.py:370-411) on the group
-// bucket (:499-509), bit for bit.
+// bucket (:499-509), bit for bit; fp32 (4 per 16-B slot, scaled at pack) and bf16 (8 per
+// slot, fp32 accumulation, scaled and rounded once by the part's owner, as bf16.cuh).
 //
 // The push two-shot (push.cuh) pays two CTA barriers per call; each is a system-scope
 // release (the CTA stalls until every NVLink store it issued is acknowledged) plus a flag
@@ -30,6 +31,7 @@
 // source's header, so a peer in another collective fails fast as for LL.
 #pragma once
 
+#include "bf16.cuh"
 #include "ll.cuh"
 
 namespace mgw {
@@ -48,11 +50,11 @@ struct L128Args {
   int64_t row_lines;         // lines per row (the longest part)
 };
 
-// 16-B slots of a bucket of n elements (the last one partial when n % 4 != 0)
-__host__ __device__ __forceinline__ int64_t l128_slots(int64_t n) { return (n + 3) / 4; }
+// 16-B slots of a bucket of n elements (4 fp32 / 8 bf16; the last one partial)
+__host__ __device__ __forceinline__ int64_t l128_slots(int64_t n, bool b16) { return b16 ? (n + 7) / 8 : (n + 3) / 4; }
 // lines per row: the longest part (part_begin rounds down to kPartAlign) in lines
-__host__ __device__ __forceinline__ int64_t l128_row_lines(int64_t n, int world) {
-  const int64_t part = (l128_slots(n) + world - 1) / world + kPartAlign;
+__host__ __device__ __forceinline__ int64_t l128_row_lines(int64_t n, int world, bool b16) {
+  const int64_t part = (l128_slots(n, b16) + world - 1) / world + kPartAlign;
   return (part + kL128Vec - 1) / kL128Vec;
 }
 
@@ -62,17 +64,6 @@ __device__ __forceinline__ void st_volatile_v2(uint64_t* p, uint64_t a, uint64_t
 
 __device__ __forceinline__ void ld_volatile_v2(const uint64_t* p, uint64_t& a, uint64_t& b) {
   asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
-}
-
-__device__ __forceinline__ uint64_t l128_lo(float4 v) {
-  return (uint64_t)__float_as_uint(v.x) | ((uint64_t)__float_as_uint(v.y) << 32);
-}
-__device__ __forceinline__ uint64_t l128_hi(float4 v) {
-  return (uint64_t)__float_as_uint(v.z) | ((uint64_t)__float_as_uint(v.w) << 32);
-}
-__device__ __forceinline__ float l128_elem(uint64_t lo, uint64_t hi, int j) {
-  const uint64_t w = j < 2 ? lo : hi;
-  return __uint_as_float((uint32_t)(j & 1 ? w >> 32 : w));
 }
 
 // Warp-collective: poll until every active group's line (this lane's 16 B at `p`) carries
@@ -98,50 +89,37 @@ __device__ __forceinline__ int l128_poll(const uint64_t* p, bool active, uint64_
       if (st == MGW_DEV_OK && load_relaxed_sys32(a.abort_flag[a.rank]) != 0u) st = MGW_DEV_PEER_ABORT;
       if (spin == 15) start = global_ns();
       if (st == MGW_DEV_OK && global_ns() - start > a.timeout_ns) st = MGW_DEV_TIMEOUT;
-      // warp-uniform: the largest code any lane saw (mismatch 1 < abort < timeout order is
-      // irrelevant -- any error ends the call)
-      const int any = __reduce_max_sync(0xffffffffu, st);
+      const int any = __reduce_max_sync(0xffffffffu, st);  // warp-uniform: any error ends the call
       if (any != MGW_DEV_OK) return any;
     }
   }
 }
 
-// the fold of one 16-B slot from the N sources' words, starting at source `seg`
-// (static register indexing: the rotation is unrolled per start)
-template <int N>
-__device__ __forceinline__ float4 l128_fold4(const uint64_t (&lo)[N], const uint64_t (&hi)[N], int seg) {
-  float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-  for (int s = 0; s < N; ++s) {
-    if (s == seg) {
-      float r[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        float acc = l128_elem(lo[s], hi[s], j);
-#pragma unroll
-        for (int kk = 1; kk < N; ++kk) {
-          const int src = (s + kk) % N;
-          acc = __fadd_rn(acc, l128_elem(lo[src], hi[src], j));
-        }
-        r[j] = acc;
-      }
-      y = make_float4(r[0], r[1], r[2], r[3]);
-    }
+// Element j of a 16-B slot held as two u64 words: fp32 (4 per slot) or bf16 (8 per slot,
+// exactly upcast).
+template <bool B16>
+__device__ __forceinline__ float l128_get(uint64_t lo, uint64_t hi, int j) {
+  if (B16) {
+    const uint64_t w = j < 4 ? lo : hi;
+    return __uint_as_float((uint32_t)((w >> (16 * (j & 3))) & 0xFFFFu) << 16);
   }
-  return y;
+  const uint64_t w = j < 2 ? lo : hi;
+  return __uint_as_float((uint32_t)(j & 1 ? w >> 32 : w));
 }
 
-template <int N>
-__device__ __forceinline__ float l128_fold1(const uint64_t (&lo)[N], const uint64_t (&hi)[N], int seg, int j) {
+// the reference fold of element j from the N sources' words, starting at source `seg`
+// (static register indexing: the rotation is unrolled per start)
+template <int N, bool B16>
+__device__ __forceinline__ float l128_fold_elem(const uint64_t (&lo)[N], const uint64_t (&hi)[N], int seg, int j) {
   float out = 0.f;
 #pragma unroll
   for (int s = 0; s < N; ++s) {
     if (s == seg) {
-      float acc = l128_elem(lo[s], hi[s], j);
+      float acc = l128_get<B16>(lo[s], hi[s], j);
 #pragma unroll
       for (int kk = 1; kk < N; ++kk) {
         const int src = (s + kk) % N;
-        acc = __fadd_rn(acc, l128_elem(lo[src], hi[src], j));
+        acc = __fadd_rn(acc, l128_get<B16>(lo[src], hi[src], j));
       }
       out = acc;
     }
@@ -149,45 +127,130 @@ __device__ __forceinline__ float l128_fold1(const uint64_t (&lo)[N], const uint6
   return out;
 }
 
-// bucket slot v (elements 4v ..) from the layer tensors, scaled; zeros past n
-__device__ __forceinline__ float4 l128_load(const FusedArgs& f, int& k, int64_t v, float scale, bool scaled) {
+// The reduced slot at bucket element e: every element folded from its segment's start
+// (one rotation for the whole slot when it lies in one segment); bf16: scaled and
+// rounded once here (fp32 was scaled at pack, as the reference packs).  Padding
+// elements past n come out 0.
+template <int N, bool B16>
+__device__ __forceinline__ void l128_fold_slot(const uint64_t (&lo)[N], const uint64_t (&hi)[N], int seg, int64_t e,
+                                               int64_t n, const int64_t* s_end, float scale, bool scaled,
+                                               uint64_t& olo, uint64_t& ohi) {
+  constexpr int K = B16 ? 8 : 4;
+  float r[K];
+  if (e + K - 1 < s_end[seg]) {
+#pragma unroll
+    for (int j = 0; j < K; ++j) r[j] = 0.f;
+#pragma unroll
+    for (int s = 0; s < N; ++s) {
+      if (s == seg) {
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          float acc = l128_get<B16>(lo[s], hi[s], j);
+#pragma unroll
+          for (int kk = 1; kk < N; ++kk) {
+            const int src = (s + kk) % N;
+            acc = __fadd_rn(acc, l128_get<B16>(lo[src], hi[src], j));
+          }
+          r[j] = acc;
+        }
+      }
+    }
+  } else {  // the slot straddles a segment boundary, or is the partial last slot
+    int s2 = seg;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      r[j] = 0.f;
+      if (e + j < n) {
+        s2 = advance_segment(s2, e + j, s_end);
+        r[j] = l128_fold_elem<N, B16>(lo, hi, s2, j);
+      }
+    }
+  }
+  if (B16) {
+    uint64_t w[2] = {0, 0};
+#pragma unroll
+    for (int j = 0; j < K; ++j)
+      w[j >> 2] |= (uint64_t)f32_to_b16(scaled ? __fmul_rn(r[j], scale) : r[j]) << (16 * (j & 3));
+    olo = w[0];
+    ohi = w[1];
+  } else {
+    olo = (uint64_t)__float_as_uint(r[0]) | ((uint64_t)__float_as_uint(r[1]) << 32);
+    ohi = (uint64_t)__float_as_uint(r[2]) | ((uint64_t)__float_as_uint(r[3]) << 32);
+  }
+}
+
+// bucket slot v from the layer tensors (fp32: scaled; bf16: raw); zeros past n
+template <bool B16>
+__device__ __forceinline__ void l128_load(const FusedArgs& f, int& k, int64_t v, float scale, bool scaled,
+                                          uint64_t& lo, uint64_t& hi) {
+  if (B16) {
+    const int64_t e = v * kB16;
+    bool fast;
+    const uint16_t* tp = b16_tensor(f, k, e, fast);
+    if (fast) {
+      const uint4 x = *reinterpret_cast<const uint4*>(tp);
+      lo = (uint64_t)x.x | ((uint64_t)x.y << 32);
+      hi = (uint64_t)x.z | ((uint64_t)x.w << 32);
+      return;
+    }
+    uint64_t w[2] = {0, 0};
+#pragma unroll
+    for (int j = 0; j < kB16; ++j)
+      if (e + j < f.ar.n) w[j >> 2] |= (uint64_t)*b16_tensor1(f, k, e + j) << (16 * (j & 3));
+    lo = w[0];
+    hi = w[1];
+    return;
+  }
   const int64_t e = v << 2;
   bool fast;
   const float* tp = fused_tensor(f, k, e, fast);
+  float r[4];
   if (fast) {
     const float4 x = *reinterpret_cast<const float4*>(tp);
-    return scaled ? fmul4(x, scale) : x;
-  }
-  float r[4];
+    r[0] = x.x, r[1] = x.y, r[2] = x.z, r[3] = x.w;
+  } else {
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    float x = 0.f;
-    if (e + j < f.ar.n) {
-      x = *fused_tensor1(f, k, e + j);
-      if (scaled) x = __fmul_rn(x, scale);
-    }
-    r[j] = x;
+    for (int j = 0; j < 4; ++j) r[j] = e + j < f.ar.n ? *fused_tensor1(f, k, e + j) : 0.f;
   }
-  return make_float4(r[0], r[1], r[2], r[3]);
+  if (scaled)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) r[j] = __fmul_rn(r[j], scale);
+  lo = (uint64_t)__float_as_uint(r[0]) | ((uint64_t)__float_as_uint(r[1]) << 32);
+  hi = (uint64_t)__float_as_uint(r[2]) | ((uint64_t)__float_as_uint(r[3]) << 32);
 }
 
 // bucket slot v into the layer tensors (elements past n dropped)
+template <bool B16>
 __device__ __forceinline__ void l128_store(const FusedArgs& f, int& k, int64_t v, uint64_t lo, uint64_t hi) {
+  if (B16) {
+    const int64_t e = v * kB16;
+    bool fast;
+    uint16_t* tp = b16_tensor(f, k, e, fast);
+    if (fast) {
+      *reinterpret_cast<uint4*>(tp) = make_uint4((uint32_t)lo, (uint32_t)(lo >> 32), (uint32_t)hi, (uint32_t)(hi >> 32));
+      return;
+    }
+#pragma unroll
+    for (int j = 0; j < kB16; ++j)
+      if (e + j < f.ar.n) *b16_tensor1(f, k, e + j) = (uint16_t)((j < 4 ? lo : hi) >> (16 * (j & 3)));
+    return;
+  }
   const int64_t e = v << 2;
   bool fast;
   float* tp = fused_tensor(f, k, e, fast);
   if (fast) {
-    *reinterpret_cast<float4*>(tp) = make_float4(l128_elem(lo, hi, 0), l128_elem(lo, hi, 1), l128_elem(lo, hi, 2),
-                                                 l128_elem(lo, hi, 3));
+    *reinterpret_cast<float4*>(tp) = make_float4(l128_get<false>(lo, hi, 0), l128_get<false>(lo, hi, 1),
+                                                 l128_get<false>(lo, hi, 2), l128_get<false>(lo, hi, 3));
     return;
   }
 #pragma unroll
   for (int j = 0; j < 4; ++j)
-    if (e + j < f.ar.n) *fused_tensor1(f, k, e + j) = l128_elem(lo, hi, j);
+    if (e + j < f.ar.n) *fused_tensor1(f, k, e + j) = l128_get<false>(lo, hi, j);
 }
 
-template <int N>
-__device__ __forceinline__ void ll128_body(const L128Args& x, const int cta, const int ctas) {
+template <int N, bool B16>
+__device__ __forceinline__ void ll128_any_body(const L128Args& x, const int cta, const int ctas) {
+  constexpr int K = B16 ? kB16 : 4;  // elements per 16-B slot
   const FusedArgs& f = x.f;
   const ArArgs& a = f.ar;
   grid_dep_wait();
@@ -198,7 +261,7 @@ __device__ __forceinline__ void ll128_body(const L128Args& x, const int cta, con
   const int parity = (int)(epoch & 1u);
   const int me = a.rank;
   const int64_t n = a.n;
-  const int64_t slots = l128_slots(n);
+  const int64_t slots = l128_slots(n, B16);
   if (threadIdx.x < N) {
     const int t = threadIdx.x;
     const int64_t q = n / N, r = n % N;
@@ -241,16 +304,16 @@ __device__ __forceinline__ void ll128_body(const L128Args& x, const int cta, con
         const int64_t l = base + grp;
         const int64_t v = q0 + l * kL128Vec + sub;
         const bool live = l < l1 && carrier && v < q1;
-        float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
+        uint64_t lo = 0, hi = 0;
         if (live) {
           if (!k_set) {
-            k = fused_row_covering(f, v << 2);
+            k = fused_row_covering(f, v * K);
             k_set = true;
           }
-          y = l128_load(f, k, v, scale, scaled);
+          l128_load<B16>(f, k, v, scale, scaled, lo, hi);
         }
         __syncwarp();
-        if (l < l1) st_volatile_v2(row + l * kL128Words, carrier ? l128_lo(y) : expect, carrier ? l128_hi(y) : expect);
+        if (l < l1) st_volatile_v2(row + l * kL128Words, carrier ? lo : expect, carrier ? hi : expect);
       }
     }
   }
@@ -284,33 +347,19 @@ __device__ __forceinline__ void ll128_body(const L128Args& x, const int cta, con
       }
       if (status != MGW_DEV_OK) break;
       const bool live = active && carrier && v < q1;
-      float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
+      uint64_t ylo = 0, yhi = 0;
       if (live) {
-        const int64_t e = v << 2;
+        const int64_t e = v * K;
         seg = advance_segment(seg, e, s_end);
-        if (e + 3 < s_end[seg]) {
-          y = l128_fold4<N>(lo, hi, seg);
-        } else {  // the slot straddles a segment boundary, or is the partial last slot
-          float r[4];
-          int s2 = seg;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            r[j] = 0.f;
-            if (e + j < n) {
-              s2 = advance_segment(s2, e + j, s_end);
-              r[j] = l128_fold1<N>(lo, hi, s2, j);
-            }
-          }
-          y = make_float4(r[0], r[1], r[2], r[3]);
-        }
+        l128_fold_slot<N, B16>(lo, hi, seg, e, n, s_end, scale, scaled, ylo, yhi);
         if (!k_set) {
           k = fused_row_covering(f, e);
           k_set = true;
         }
-        l128_store(f, k, v, l128_lo(y), l128_hi(y));
+        l128_store<B16>(f, k, v, ylo, yhi);
       }
       __syncwarp();
-      const uint64_t w0 = carrier ? l128_lo(y) : expect, w1 = carrier ? l128_hi(y) : expect;
+      const uint64_t w0 = carrier ? ylo : expect, w1 = carrier ? yhi : expect;
 #pragma unroll
       for (int q = 0; q < N; ++q)
         if (q != me && active) st_volatile_v2(gat_of(q) + ((int64_t)me * rl + l) * kL128Words + sub * 2, w0, w1);
@@ -340,10 +389,10 @@ __device__ __forceinline__ void ll128_body(const L128Args& x, const int cta, con
         const int64_t v = q0 + l * kL128Vec + sub;
         if (active && carrier && v < q1) {
           if (!k_set) {
-            k = fused_row_covering(f, v << 2);
+            k = fused_row_covering(f, v * K);
             k_set = true;
           }
-          l128_store(f, k, v, w0, w1);
+          l128_store<B16>(f, k, v, w0, w1);
         }
       }
     }
@@ -353,6 +402,16 @@ __device__ __forceinline__ void ll128_body(const L128Args& x, const int cta, con
   finish_call(a, ctas);
 }
 
+template <int N>
+__device__ __forceinline__ void ll128_body(const L128Args& x, const int cta, const int ctas) {
+  ll128_any_body<N, false>(x, cta, ctas);
+}
+template <int N>
+__device__ __forceinline__ void b16_ll128_body(const L128Args& x, const int cta, const int ctas) {
+  ll128_any_body<N, true>(x, cta, ctas);
+}
+
 MGW_DEFINE_KERNELS(ll128, L128Args)
+MGW_DEFINE_KERNELS(b16_ll128, L128Args)
 
 }  // namespace mgw

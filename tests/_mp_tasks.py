@@ -229,7 +229,7 @@ def bf16_task(config, session, *, sizes):
         t = vals.to(session.device)
         ring_allreduce(GradientBuffer(1, 1, t), config, session)
         out[("auto", n)] = t.view(torch.int16).cpu().numpy().view(np.uint16)
-        algos = [("one", _native.ALGO_ONESHOT), ("two", _native.ALGO_TWOSHOT)]
+        algos = [("one", _native.ALGO_ONESHOT), ("two", _native.ALGO_TWOSHOT), ("ll128", _native.ALGO_LL128)]
         if n <= 131072:
             algos.append(("ll", _native.ALGO_LL))
         for name, algo in algos:
@@ -322,7 +322,7 @@ def stress_task(config, session, *, iterations=300, seed=2024):
     n_ranks = config.n_workers
     algos_f32 = [_native.ALGO_AUTO, _native.ALGO_LL, _native.ALGO_ONESHOT, _native.ALGO_TWOSHOT, _native.ALGO_PUSH,
                  _native.ALGO_PUSH_ONESHOT, _native.ALGO_LL128]
-    algos_b16 = [_native.ALGO_AUTO, _native.ALGO_LL, _native.ALGO_ONESHOT, _native.ALGO_TWOSHOT]
+    algos_b16 = [_native.ALGO_AUTO, _native.ALGO_LL, _native.ALGO_ONESHOT, _native.ALGO_TWOSHOT, _native.ALGO_LL128]
     h = session.stream.cuda_stream
     failures = []
     with torch.cuda.device(session.device), torch.cuda.stream(session.stream):

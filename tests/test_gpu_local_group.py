@@ -29,7 +29,7 @@ pytestmark = pytest.mark.gpu
 
 ALGOS_F32 = [_native.ALGO_LL, _native.ALGO_ONESHOT, _native.ALGO_TWOSHOT, _native.ALGO_PUSH_ONESHOT,
              _native.ALGO_PUSH, _native.ALGO_PUSH_PIPE, _native.ALGO_LL128]
-ALGOS_B16 = [_native.ALGO_LL, _native.ALGO_ONESHOT, _native.ALGO_TWOSHOT, _native.ALGO_PUSH]
+ALGOS_B16 = [_native.ALGO_LL, _native.ALGO_ONESHOT, _native.ALGO_TWOSHOT, _native.ALGO_PUSH, _native.ALGO_LL128]
 
 
 @pytest.fixture(scope="module")

@@ -244,6 +244,7 @@ def test_bf16_exchange_over_ipc_vs_oracle():
                 assert np.array_equal(res[r][("auto", size)], want1), (n, size, r)
                 assert np.array_equal(res[r][("one", size)], want_half), (n, size, r, "one")
                 assert np.array_equal(res[r][("two", size)], want_half), (n, size, r, "two")
+                assert np.array_equal(res[r][("ll128", size)], want_half), (n, size, r, "ll128")
                 if size <= 131072:
                     assert np.array_equal(res[r][("ll", size)], want_half), (n, size, r, "ll")
 

@@ -37,7 +37,8 @@ A = _native
 F32_ALGOS = {"ll": A.ALGO_LL, "oneshot": A.ALGO_ONESHOT, "twoshot": A.ALGO_TWOSHOT,
              "push_oneshot": A.ALGO_PUSH_ONESHOT, "push": A.ALGO_PUSH, "push_pipe": A.ALGO_PUSH_PIPE,
              "ll128": A.ALGO_LL128}
-B16_ALGOS = {"ll": A.ALGO_LL, "oneshot": A.ALGO_ONESHOT, "twoshot": A.ALGO_TWOSHOT, "push": A.ALGO_PUSH}
+B16_ALGOS = {"ll": A.ALGO_LL, "oneshot": A.ALGO_ONESHOT, "twoshot": A.ALGO_TWOSHOT, "push": A.ALGO_PUSH,
+             "ll128": A.ALGO_LL128}
 LL_ELEMS = 262_144
 
 
@@ -184,7 +185,7 @@ def test_fp32_bucket_bit_exact(torch_cuda, case, n_ranks, algo):
 
 
 B16_CASES = [(c, n, a) for c in ("ll_ceiling", "mib16", "r50_bucket", "vgg_fc6") for n in (2, 4, 8)
-             for a in (["oneshot", "twoshot", "push"] + (["ll"] if sum(layout(c, n)[0]) <= 2 * LL_ELEMS else []))]
+             for a in (["oneshot", "twoshot", "push", "ll128"] + (["ll"] if sum(layout(c, n)[0]) <= 2 * LL_ELEMS else []))]
 
 
 @pytest.mark.parametrize("case,n_ranks,algo", B16_CASES, ids=[f"{c}-N{n}-{a}" for c, n, a in B16_CASES])
