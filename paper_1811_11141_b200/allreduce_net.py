@@ -476,12 +476,12 @@ def _algo_for(session: RingSession, n: int, fused: bool = False, elem_bytes: int
 
 def _auto_rule(session: RingSession, n: int, fused: bool = False) -> int:
     """Host mirror of pick_fused_algo / pick_algo at the default thresholds."""
-    if fused and 4 * n <= ll_max_bytes(session.config.n_workers):
-        return _native.ALGO_LL
     if fused:
         world = session.config.n_workers
         if (1 << 20) <= 4 * n <= ((32 << 20) if world == 2 else (16 << 20)):
             return _native.ALGO_LL128
+        if 4 * n <= ll_max_bytes(world):
+            return _native.ALGO_LL
         push_ok = 4 * n <= (1 << 30)
         if session.config.n_workers == 2:
             if 4 * n <= (16 << 20):

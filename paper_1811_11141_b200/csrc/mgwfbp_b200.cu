@@ -254,13 +254,13 @@ int pick_algo(const mgw_comm* c, int64_t n, int algo) {
 
 // fused group exchange: LL push for small buckets, else pull one-shot / two-shot;
 // NVLS only when enabled (not bit-exact with the reference order)
-constexpr int64_t kLL128MinBytes = 1ll << 20;  // AUTO: LL128 from here (after LL's ceiling)
+constexpr int64_t kLL128MinBytes = 1ll << 20;  // AUTO: LL128 from here (before LL's ceiling)
+inline int64_t ll128_max_bytes(const mgw_comm* c) { return c->world == 2 ? (32ll << 20) : (16ll << 20); }
 
 int pick_fused_algo(const mgw_comm* c, int64_t n, int algo) {
   if (algo != MGW_ALGO_AUTO) return algo;
   if (c->nvls_bound && c->nvls_min_bytes > 0 && n * 4 >= c->nvls_min_bytes && (size_t)n * 4 <= c->nvls_bytes)
     return MGW_ALGO_NVLS;
-  if (c->world > 1 && n * 4 <= c->ll_max_bytes && n <= kLLElems) return MGW_ALGO_LL;
   // engine-mode sweeps (profiles/grid_{push,large,push1}_n*_r01.json): at N = 2 the push
   // one-shot wins up to 16 MB and the push two-shot above; at N >= 3 the push one-shot up
   // to 512 KB, the pull one-shot to 8 MB / (N - 1), the pull two-shot to 8 MB and the
@@ -272,9 +272,9 @@ int pick_fused_algo(const mgw_comm* c, int64_t n, int algo) {
   // the flag-in-line two-shot (ll128.cuh) from 1 MiB: no barriers, 2 (N-1)/N x M x 8/7 out
   // (profiles/ll128_sweep_n{2,4}_r02.json, graph-timed at N = 4: 1 MiB 11.8 vs 15.4 us,
   // 4 MiB 18.2 vs 27.9, 16 MiB 56.3 vs 58.5; level with the push two-shot at 32 MiB,
-  // which stays above 16 MiB; at N = 2 it wins to 32 MiB)
-  if (c->world > 1 && bytes >= kLL128MinBytes && bytes <= (c->world == 2 ? (32ll << 20) : (16ll << 20)))
-    return MGW_ALGO_LL128;
+  // which stays above 16 MiB; at N = 2 it wins to 32 MiB, and from 1 MiB over the LL one-shot)
+  if (c->world > 1 && bytes >= kLL128MinBytes && bytes <= ll128_max_bytes(c)) return MGW_ALGO_LL128;
+  if (c->world > 1 && n * 4 <= c->ll_max_bytes && n <= kLLElems) return MGW_ALGO_LL;
   const bool push_ok = bytes <= (1ll << 30);
   if (c->world == 2)
     return bytes <= (16ll << 20) ? MGW_ALGO_PUSH_ONESHOT : (push_ok ? MGW_ALGO_PUSH : MGW_ALGO_TWOSHOT);
@@ -301,7 +301,11 @@ int resolve_fused_algo(const mgw_comm* c, int64_t n, int algo) {
 // bf16 group exchange: LL for small buckets, else pull one-shot / two-shot
 int resolve_b16_algo(const mgw_comm* c, int64_t n, int algo) {
   if (algo == MGW_ALGO_AUTO) {
-    if (c->world > 1 && n * 2 <= c->ll_max_bytes && n <= 2 * kLLElems)
+    // bf16 crossovers as fp32 (profiles/ll128_bf16_sweep_n{2,4}_r02.json): LL128 for
+    // 1 MiB .. 16 MiB (N >= 3) / 32 MiB (N = 2), LL below, push two-shot above
+    if (c->world > 1 && n * 2 >= kLL128MinBytes && n * 2 <= ll128_max_bytes(c))
+      algo = MGW_ALGO_LL128;
+    else if (c->world > 1 && n * 2 <= c->ll_max_bytes && n <= 2 * kLLElems)
       algo = MGW_ALGO_LL;
     else if (n * 2 <= c->oneshot_max_bytes)
       algo = MGW_ALGO_ONESHOT;
