@@ -66,6 +66,7 @@ extern "C" {
 #define MGW_ALGO_PUSH_ONESHOT 6 /* push-based one-shot (fused path only): stores out, local fold */
 #define MGW_ALGO_PUSH_PIPE 7 /* pipelined push two-shot (fused path only): per-sub-chunk flags overlap the phases */
 #define MGW_ALGO_LL128 8 /* flag-in-line two-shot (fused fp32 and bf16 paths): 128-B lines, 7 x 16 B payload + flag, no barrier */
+#define MGW_ALGO_LL128_ONESHOT 9 /* flag-in-line one-shot (fused paths): the whole bucket to every rank in 128-B lines, one hop */
 
 /* schedule flags */
 #define MGW_SCHED_FILL 1u  /* "backward" writes fill_values into each layer before its deadline */

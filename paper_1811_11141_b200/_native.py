@@ -19,7 +19,7 @@ LIB_PATH = LIB_DIR / "libmgwfbp_b200.so"
 
 MGW_OK, MGW_EINVAL, MGW_EPROTO, MGW_ECUDA = 0, 1, 2, 3
 (ALGO_AUTO, ALGO_ONESHOT, ALGO_TWOSHOT, ALGO_LL, ALGO_NVLS, ALGO_PUSH, ALGO_PUSH_ONESHOT, ALGO_PUSH_PIPE,
- ALGO_LL128) = range(9)
+ ALGO_LL128, ALGO_LL128_ONESHOT) = range(10)
 SCHED_FILL, SCHED_GRAPH, SCHED_HOSTIO, SCHED_FUSED, SCHED_PDL, SCHED_BF16 = 1, 2, 4, 8, 16, 32
 OPT_WIDE_MIN_BYTES = 4  # mgw_set_option key: push two-shot buckets >= this launch 512 CTAs (0 = off)
 OPT_LOCAL_MIN_SLOTS = 3  # mgw_set_option key: single-rank group kernel minimum slots per CTA

@@ -52,7 +52,7 @@ struct ArArgs {
 // at any barrier raises MGW_DEV_MISMATCH on every rank within one flag round trip.
 enum TagKind : uint32_t {
   kTagOneshot = 1, kTagTwoshot, kTagFusedOneshot, kTagFusedTwoshot, kTagLL, kTagNvls, kTagPush, kTagPushOneshot,
-  kTagB16Oneshot, kTagB16Twoshot, kTagB16LL, kTagPushPipe, kTagB16Push, kTagLL128, kTagB16LL128
+  kTagB16Oneshot, kTagB16Twoshot, kTagB16LL, kTagPushPipe, kTagB16Push, kTagLL128, kTagB16LL128, kTagLL128One, kTagB16LL128One
 };
 
 inline uint32_t tag_mix(uint32_t h, uint32_t k) {  // murmur3 block step

@@ -23,7 +23,7 @@ int launch_ll(const LLArgs& l, int max_ctas, cudaStream_t stream);
 int launch_ll_b16(const LLArgs& l, int max_ctas, cudaStream_t stream);
 int launch_b16(const FusedArgs& f, int algo, int max_ctas, cudaStream_t stream);
 int launch_b16_push(const PushArgs& x, int max_ctas, cudaStream_t stream);
-int launch_ll128(const L128Args& x, int max_ctas, cudaStream_t stream, const int64_t* per_cta, bool b16);
+int launch_ll128(const L128Args& x, int max_ctas, cudaStream_t stream, const int64_t* per_cta, bool b16, bool one);
 int launch_nvls(const NvlsArgs& x, int max_ctas, cudaStream_t stream, const int64_t* per_cta);
 
 // plan_*: the grid a launch uses for these arguments and settings; stamps the collective
@@ -36,7 +36,7 @@ int plan_ll(LLArgs& l, int max_ctas);
 int plan_ll_b16(LLArgs& l, int max_ctas);
 int plan_b16(FusedArgs& f, int algo, int max_ctas);
 int plan_b16_push(PushArgs& x, int max_ctas);
-int plan_ll128(L128Args& x, int max_ctas, const int64_t* per_cta, bool b16);
+int plan_ll128(L128Args& x, int max_ctas, const int64_t* per_cta, bool b16, bool one);
 
 // Rank-group launches: every rank's planned CTAs in ONE cooperative launch on one device
 // (co-residency guaranteed, so ranks that wait on one another always run together).
@@ -47,7 +47,7 @@ int launch_ll_group(const RankGroup<LLArgs>& g, int world, cudaStream_t stream);
 int launch_b16_group(const RankGroup<FusedArgs>& g, int world, int algo, cudaStream_t stream);
 int launch_ll_b16_group(const RankGroup<LLArgs>& g, int world, cudaStream_t stream);
 int launch_b16_push_group(const RankGroup<PushArgs>& g, int world, cudaStream_t stream);
-int launch_ll128_group(const RankGroup<L128Args>& g, int world, cudaStream_t stream, bool b16);
+int launch_ll128_group(const RankGroup<L128Args>& g, int world, cudaStream_t stream, bool b16, bool one);
 
 template <class Args>
 inline int launch_cooperative(void (*kernel)(const RankGroup<Args>), const RankGroup<Args>& g, cudaStream_t stream) {

@@ -52,8 +52,10 @@ struct L128Args {
 
 // 16-B slots of a bucket of n elements (4 fp32 / 8 bf16; the last one partial)
 __host__ __device__ __forceinline__ int64_t l128_slots(int64_t n, bool b16) { return b16 ? (n + 7) / 8 : (n + 3) / 4; }
-// lines per row: the longest part (part_begin rounds down to kPartAlign) in lines
-__host__ __device__ __forceinline__ int64_t l128_row_lines(int64_t n, int world, bool b16) {
+// lines per row: the longest part (part_begin rounds down to kPartAlign) in lines; the
+// one-shot's row holds the whole bucket
+__host__ __device__ __forceinline__ int64_t l128_row_lines(int64_t n, int world, bool b16, bool one = false) {
+  if (one) return (l128_slots(n, b16) + kL128Vec - 1) / kL128Vec;
   const int64_t part = (l128_slots(n, b16) + world - 1) / world + kPartAlign;
   return (part + kL128Vec - 1) / kL128Vec;
 }
@@ -248,7 +250,10 @@ __device__ __forceinline__ void l128_store(const FusedArgs& f, int& k, int64_t v
     if (e + j < f.ar.n) *fused_tensor1(f, k, e + j) = l128_get<false>(lo, hi, j);
 }
 
-template <int N, bool B16>
+// ONE = the one-shot: every rank pushes its whole bucket (one line range per CTA) into
+// every rank's incoming row `me` and folds its line range of the whole bucket from the N
+// local rows -- one NVLink hop, (N-1) x M x 8/7 out, no gather phase.
+template <int N, bool B16, bool ONE>
 __device__ __forceinline__ void ll128_any_body(const L128Args& x, const int cta, const int ctas) {
   constexpr int K = B16 ? kB16 : 4;  // elements per 16-B slot
   const FusedArgs& f = x.f;
@@ -267,7 +272,7 @@ __device__ __forceinline__ void ll128_any_body(const L128Args& x, const int cta,
     const int64_t q = n / N, r = n % N;
     s_end[t] = (int64_t)(t + 1) * q + (t + 1 < r ? t + 1 : r);  // end of reference segment t
   }
-  if (threadIdx.x <= N) s_part[threadIdx.x] = part_begin(threadIdx.x, slots, N);
+  if (threadIdx.x <= N) s_part[threadIdx.x] = part_begin(threadIdx.x, slots, N);  // (the one-shot: unused)
   // kSkipPack / kSkipPhase1 / kSkipPhase2 run one phase per launch (emulated ranks on one
   // device, tests only: every launch polls lines that earlier launches wrote)
   const bool do_push = !(a.flags & kSkipPack), do_fold = !(a.flags & kSkipPhase1),
@@ -290,8 +295,37 @@ __device__ __forceinline__ void ll128_any_body(const L128Args& x, const int cta,
   int status = MGW_DEV_OK;
 
   phase_mark(a, 0, cta);
-  // ---- phase 1: my line range of every part p into rank p's incoming row `me`
-  if (do_push) {
+  // ---- phase 1: my line range of every part p into rank p's incoming row `me` (one-shot:
+  //      my line range of the whole bucket into every rank's row `me`)
+  if (do_push && ONE) {
+    int k = 0;
+    bool k_set = false;
+    int64_t l0, l1;
+    cta_chunk(0, (slots + kL128Vec - 1) / kL128Vec, cta, ctas, l0, l1);
+    for (int64_t base = l0; base < l1; base += kL128Step) {
+      const int64_t l = base + grp;
+      const int64_t v = l * kL128Vec + sub;
+      const bool live = l < l1 && carrier && v < slots;
+      uint64_t lo = 0, hi = 0;
+      if (live) {
+        if (!k_set) {
+          k = fused_row_covering(f, v * K);
+          k_set = true;
+        }
+        l128_load<B16>(f, k, v, scale, scaled, lo, hi);
+      }
+      if (!carrier) lo = hi = expect;
+      __syncwarp();
+      if (l < l1) {
+#pragma unroll
+        for (int r = 0; r < N; ++r) {
+          const int q = me + 1 + r < N ? me + 1 + r : me + 1 + r - N;  // peers first, mine last
+          st_volatile_v2(in_of(q) + ((int64_t)me * rl + l) * kL128Words + sub * 2, lo, hi);
+        }
+      }
+    }
+  }
+  if (do_push && !ONE) {
     int k = 0;
     bool k_set = false;
 #pragma unroll 1
@@ -321,7 +355,7 @@ __device__ __forceinline__ void ll128_any_body(const L128Args& x, const int cta,
   // ---- phase 2: fold my line range of my part from the N local rows; write my tensors and
   //      every peer's gather row `me`
   if (do_fold) {
-    const int64_t q0 = s_part[me], q1 = s_part[me + 1];
+    const int64_t q0 = ONE ? 0 : s_part[me], q1 = ONE ? slots : s_part[me + 1];
     int64_t l0, l1;
     cta_chunk(0, (q1 - q0 + kL128Vec - 1) / kL128Vec, cta, ctas, l0, l1);
     const uint64_t* in = in_of(me) + sub * 2;
@@ -358,6 +392,7 @@ __device__ __forceinline__ void ll128_any_body(const L128Args& x, const int cta,
         }
         l128_store<B16>(f, k, v, ylo, yhi);
       }
+      if (ONE) continue;  // the one-shot has every part: no result lines
       __syncwarp();
       const uint64_t w0 = carrier ? ylo : expect, w1 = carrier ? yhi : expect;
 #pragma unroll
@@ -367,7 +402,7 @@ __device__ __forceinline__ void ll128_any_body(const L128Args& x, const int cta,
   }
   phase_mark(a, 2, cta);
   // ---- phase 3: every peer part's result lines from my gather rows into my tensors
-  if (do_unpack) {
+  if (do_unpack && !ONE) {
     int k = 0;
     bool k_set = false;
 #pragma unroll 1
@@ -404,14 +439,24 @@ __device__ __forceinline__ void ll128_any_body(const L128Args& x, const int cta,
 
 template <int N>
 __device__ __forceinline__ void ll128_body(const L128Args& x, const int cta, const int ctas) {
-  ll128_any_body<N, false>(x, cta, ctas);
+  ll128_any_body<N, false, false>(x, cta, ctas);
 }
 template <int N>
 __device__ __forceinline__ void b16_ll128_body(const L128Args& x, const int cta, const int ctas) {
-  ll128_any_body<N, true>(x, cta, ctas);
+  ll128_any_body<N, true, false>(x, cta, ctas);
+}
+template <int N>
+__device__ __forceinline__ void ll128_one_body(const L128Args& x, const int cta, const int ctas) {
+  ll128_any_body<N, false, true>(x, cta, ctas);
+}
+template <int N>
+__device__ __forceinline__ void b16_ll128_one_body(const L128Args& x, const int cta, const int ctas) {
+  ll128_any_body<N, true, true>(x, cta, ctas);
 }
 
 MGW_DEFINE_KERNELS(ll128, L128Args)
 MGW_DEFINE_KERNELS(b16_ll128, L128Args)
+MGW_DEFINE_KERNELS(ll128_one, L128Args)
+MGW_DEFINE_KERNELS(b16_ll128_one, L128Args)
 
 }  // namespace mgw

@@ -289,6 +289,9 @@ constexpr int64_t kB16PushMinBytes = 8ll << 20;  // bf16 AUTO: push two-shot at 
 
 int resolve_fused_algo(const mgw_comm* c, int64_t n, int algo) {
   int chosen = pick_fused_algo(c, n, algo);
+  if (chosen == MGW_ALGO_LL128_ONESHOT &&
+      (c->world == 1 || c->world * l128_row_lines(n, c->world, false, true) * 128 > c->slot_bytes))
+    chosen = MGW_ALGO_LL128;  // one rank, or the whole-bucket lines do not fit one slot
   if (chosen == MGW_ALGO_LL128 && (c->world == 1 || c->world * l128_row_lines(n, c->world, false) * 128 > c->slot_bytes))
     chosen = MGW_ALGO_PUSH;  // one rank, or the lines do not fit one slot
   if (chosen == MGW_ALGO_PUSH_ONESHOT && c->world * round_up(n, 16) * 4 > c->slot_bytes) chosen = MGW_ALGO_ONESHOT;
@@ -313,6 +316,9 @@ int resolve_b16_algo(const mgw_comm* c, int64_t n, int algo) {
       algo = c->world > 1 && n * 2 >= kB16PushMinBytes ? MGW_ALGO_PUSH : MGW_ALGO_TWOSHOT;
   }
   if (algo == MGW_ALGO_LL && c->world == 1) algo = MGW_ALGO_ONESHOT;
+  if (algo == MGW_ALGO_LL128_ONESHOT &&
+      (c->world == 1 || c->world * l128_row_lines(n, c->world, true, true) * 128 > c->slot_bytes))
+    algo = MGW_ALGO_LL128;
   if (algo == MGW_ALGO_LL128 && (c->world == 1 || c->world * l128_row_lines(n, c->world, true) * 128 > c->slot_bytes))
     algo = MGW_ALGO_PUSH;  // one rank, or the lines do not fit one slot
   if (algo == MGW_ALGO_PUSH && (c->world == 1 || c->world * b16_push_stride(n, c->world) * 2 > c->slot_bytes))
@@ -413,7 +419,7 @@ int comm_allreduce_fused(mgw_comm* c, const Row* host_rows, const Row* dev_rows,
     l.hdr_stride = (int64_t)kMaxBlocks * kMaxRanks;
     return launch_ll(l, c->max_ctas, stream);
   }
-  if (chosen == MGW_ALGO_LL128) {
+  if (chosen == MGW_ALGO_LL128 || chosen == MGW_ALGO_LL128_ONESHOT) {
     L128Args x;
     memset(&x, 0, sizeof(x));
     x.f = f;
@@ -423,7 +429,7 @@ int comm_allreduce_fused(mgw_comm* c, const Row* host_rows, const Row* dev_rows,
       x.hdr[s] = reinterpret_cast<uint64_t*>(c->peer[s] + kArriveOff);
     }
     x.hdr_stride = (int64_t)kMaxBlocks * kMaxRanks;
-    return launch_ll128(x, c->max_ctas, stream, c->vec_per_cta, false);
+    return launch_ll128(x, c->max_ctas, stream, c->vec_per_cta, false, chosen == MGW_ALGO_LL128_ONESHOT);
   }
   if (chosen == MGW_ALGO_PUSH_ONESHOT || chosen == MGW_ALGO_PUSH || chosen == MGW_ALGO_PUSH_PIPE) {
     // incoming rows: one 64-B aligned row per source (one-shot), or one part + tail per
@@ -535,7 +541,7 @@ int comm_allreduce_fused_bf16(mgw_comm* c, const Row* host_rows, const Row* dev_
     l.hdr_stride = (int64_t)kMaxBlocks * kMaxRanks;
     return launch_ll_b16(l, c->max_ctas, stream);
   }
-  if (algo == MGW_ALGO_LL128) {
+  if (algo == MGW_ALGO_LL128 || algo == MGW_ALGO_LL128_ONESHOT) {
     L128Args x;
     memset(&x, 0, sizeof(x));
     x.f = f;
@@ -545,7 +551,7 @@ int comm_allreduce_fused_bf16(mgw_comm* c, const Row* host_rows, const Row* dev_
       x.hdr[s] = reinterpret_cast<uint64_t*>(c->peer[s] + kArriveOff);
     }
     x.hdr_stride = (int64_t)kMaxBlocks * kMaxRanks;
-    return launch_ll128(x, c->max_ctas, stream, c->vec_per_cta, true);
+    return launch_ll128(x, c->max_ctas, stream, c->vec_per_cta, true, algo == MGW_ALGO_LL128_ONESHOT);
   }
   if (algo == MGW_ALGO_PUSH) {
     PushArgs x;
@@ -871,7 +877,8 @@ int mgw_group_allreduce_fused(mgw_comm* const* comms, void* const* tables, const
   if (chosen < 0) return MGW_OK;
   if (chosen == MGW_ALGO_NVLS) return set_error(MGW_EINVAL, "NVLS has no rank-group launch");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const bool ll = chosen == MGW_ALGO_LL, l128 = chosen == MGW_ALGO_LL128,
+  const bool ll = chosen == MGW_ALGO_LL, l128 = chosen == MGW_ALGO_LL128 || chosen == MGW_ALGO_LL128_ONESHOT,
+             l128_one = chosen == MGW_ALGO_LL128_ONESHOT,
              push = chosen == MGW_ALGO_PUSH || chosen == MGW_ALGO_PUSH_ONESHOT || chosen == MGW_ALGO_PUSH_PIPE;
   // the argument blocks are large (8 ranks x ~1.5 KB): build them on the heap
   std::unique_ptr<RankGroup<FusedArgs>> gf(new RankGroup<FusedArgs>());
@@ -919,7 +926,7 @@ int mgw_group_allreduce_fused(mgw_comm* const* comms, void* const* tables, const
         x.hdr[q] = reinterpret_cast<uint64_t*>(c->peer[q] + kArriveOff);
       }
       x.hdr_stride = (int64_t)kMaxBlocks * kMaxRanks;
-      grid = plan_ll128(x, c->max_ctas, c->vec_per_cta, b16);
+      grid = plan_ll128(x, c->max_ctas, c->vec_per_cta, b16, l128_one);
     } else if (push && b16) {
       PushArgs& x = gp->args[r];
       x.f = f;
@@ -948,7 +955,7 @@ int mgw_group_allreduce_fused(mgw_comm* const* comms, void* const* tables, const
   if (first > 2 * kSMs)
     return set_error(MGW_EINVAL, "rank group needs %d co-resident CTAs (> %d): lower the CTA caps", first, 2 * kSMs);
   if (ll) return b16 ? launch_ll_b16_group(*gl, world, s) : launch_ll_group(*gl, world, s);
-  if (l128) return launch_ll128_group(*g8, world, s, b16);
+  if (l128) return launch_ll128_group(*g8, world, s, b16, l128_one);
   if (push && b16) return launch_b16_push_group(*gp, world, s);
   if (push)
     return launch_push_group(*gp, world, chosen == MGW_ALGO_PUSH_ONESHOT ? 1 : (chosen == MGW_ALGO_PUSH_PIPE ? 2 : 0), s);
@@ -1055,7 +1062,7 @@ int mgw_allreduce(mgw_comm* c, int64_t n_elem, int algo, void* stream) {
 int mgw_allreduce_fused(mgw_comm* c, const void* table, int n_rows, int64_t n_elem, float scale, int algo,
                         void* stream) {
   if (!c) return set_error(MGW_EINVAL, "comm is null");
-  if (algo < MGW_ALGO_AUTO || algo > MGW_ALGO_LL128) return set_error(MGW_EINVAL, "unknown algorithm %d", algo);
+  if (algo < MGW_ALGO_AUTO || algo > MGW_ALGO_LL128_ONESHOT) return set_error(MGW_EINVAL, "unknown algorithm %d", algo);
   int rc = check_table(table, n_rows, n_elem);
   if (rc) return rc;
   const mgw_table_t* t = as_table(table);
@@ -1075,7 +1082,7 @@ int mgw_allreduce_fused_bf16(mgw_comm* c, const void* table, int n_rows, int64_t
                              void* stream) {
   if (!c) return set_error(MGW_EINVAL, "comm is null");
   if (algo != MGW_ALGO_AUTO && algo != MGW_ALGO_ONESHOT && algo != MGW_ALGO_TWOSHOT && algo != MGW_ALGO_LL &&
-      algo != MGW_ALGO_PUSH && algo != MGW_ALGO_LL128)
+      algo != MGW_ALGO_PUSH && algo != MGW_ALGO_LL128 && algo != MGW_ALGO_LL128_ONESHOT)
     return set_error(MGW_EINVAL, "bf16 buckets support AUTO, LL, one-shot, two-shot, push two-shot and LL128 (got %d)",
                      algo);
   int rc = check_table(table, n_rows, n_elem);
@@ -1434,9 +1441,9 @@ static int ll_emulated(void* const* tables, int world, int64_t n, float scale, c
 // LL128 two-shot with emulated ranks on one device: every rank's phase 1 (line stores), then
 // every rank's phase 2 (poll + fold + result lines), then phase 3 -- each launch polls only
 // lines that earlier, completed launches wrote, so no launch ever waits on another.
-static int ll128_emulated(void* const* tables, int world, int64_t n, float scale, cudaStream_t s, bool b16) {
+static int ll128_emulated(void* const* tables, int world, int64_t n, float scale, cudaStream_t s, bool b16, bool one) {
   if (world < 2) return set_error(MGW_EINVAL, "LL128 needs >= 2 ranks");
-  const size_t area = (size_t)world * l128_row_lines(n, world, b16) * 128;
+  const size_t area = (size_t)world * l128_row_lines(n, world, b16, one) * 128;
   const size_t hdr_bytes = 2 * kMaxRanks * sizeof(uint64_t);
   const size_t per_rank = 2 * area + hdr_bytes + 256;
   char* mem = nullptr;
@@ -1478,7 +1485,7 @@ static int ll128_emulated(void* const* tables, int world, int64_t n, float scale
       x.f.ar.state = reinterpret_cast<uint32_t*>(ctl + 4);
       x.f.ar.err = reinterpret_cast<int*>(ctl + 12);
       x.f.ar.flags = step_flags[step];
-      if (rc == MGW_OK) rc = launch_ll128(x, 2 * kSMs, s, nullptr, b16);
+      if (rc == MGW_OK) rc = launch_ll128(x, 2 * kSMs, s, nullptr, b16, one);
     }
   }
   int bad = 0;
@@ -1508,13 +1515,15 @@ int mgw_allreduce_fused_emulated(void* const* tables, float* const* slots, int w
     }
     return n == 0 ? MGW_OK : ll_emulated(tables, world, n, scale, static_cast<cudaStream_t>(stream), false);
   }
-  if (algo == MGW_ALGO_LL128) {
+  if (algo == MGW_ALGO_LL128 || algo == MGW_ALGO_LL128_ONESHOT) {
     for (int r = 0; r < world; ++r) {
       const mgw_table_t* t = as_table(tables[r]);
       int rc = check_table(tables[r], t ? (int)t->host.size() : 0, n);
       if (rc) return rc;
     }
-    return n == 0 ? MGW_OK : ll128_emulated(tables, world, n, scale, static_cast<cudaStream_t>(stream), false);
+    return n == 0 ? MGW_OK
+                  : ll128_emulated(tables, world, n, scale, static_cast<cudaStream_t>(stream), false,
+                                   algo == MGW_ALGO_LL128_ONESHOT);
   }
   if (algo == MGW_ALGO_PUSH || algo == MGW_ALGO_PUSH_ONESHOT || algo == MGW_ALGO_PUSH_PIPE) {
     for (int r = 0; r < world; ++r) {
@@ -1587,13 +1596,15 @@ int mgw_allreduce_fused_bf16_emulated(void* const* tables, void* const* slots, i
     }
     return n == 0 ? MGW_OK : ll_emulated(tables, world, n, scale, static_cast<cudaStream_t>(stream), true);
   }
-  if (algo == MGW_ALGO_LL128) {
+  if (algo == MGW_ALGO_LL128 || algo == MGW_ALGO_LL128_ONESHOT) {
     for (int r = 0; r < world; ++r) {
       const mgw_table_t* t = as_table(tables[r]);
       int rc = check_table(tables[r], t ? (int)t->host.size() : 0, n);
       if (rc) return rc;
     }
-    return n == 0 ? MGW_OK : ll128_emulated(tables, world, n, scale, static_cast<cudaStream_t>(stream), true);
+    return n == 0 ? MGW_OK
+                  : ll128_emulated(tables, world, n, scale, static_cast<cudaStream_t>(stream), true,
+                                   algo == MGW_ALGO_LL128_ONESHOT);
   }
   if (algo == MGW_ALGO_PUSH) {
     for (int r = 0; r < world; ++r) {

@@ -45,7 +45,7 @@ def main() -> int:
     comm = session.comm
     ids = {"oneshot": _native.ALGO_ONESHOT, "twoshot": _native.ALGO_TWOSHOT, "push": _native.ALGO_PUSH,
            "push_pipe": _native.ALGO_PUSH_PIPE, "push_oneshot": _native.ALGO_PUSH_ONESHOT, "auto": _native.ALGO_AUTO,
-           "ll128": _native.ALGO_LL128}
+           "ll128": _native.ALGO_LL128, "ll128_one": _native.ALGO_LL128_ONESHOT, "ll": _native.ALGO_LL}
     out = {"world": world, "sizes": sizes, "bus_gbs": {}, "us": {}}
     for name in args.algos.split(","):
         for graph in (False, True):

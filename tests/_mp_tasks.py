@@ -77,7 +77,7 @@ def every_algorithm_task(config, session, *, arrays):
             n = vals.size
             for name, algo in (("ll", _native.ALGO_LL), ("one", _native.ALGO_ONESHOT), ("two", _native.ALGO_TWOSHOT),
                                ("push", _native.ALGO_PUSH), ("push1", _native.ALGO_PUSH_ONESHOT),
-                               ("ll128", _native.ALGO_LL128)):
+                               ("ll128", _native.ALGO_LL128), ("ll128_1", _native.ALGO_LL128_ONESHOT)):
                 t = torch.from_numpy(vals.copy()).to(session.device)
                 table = _native.DeviceTable([(t.data_ptr(), n, 0)])
                 _native.call("mgw_allreduce_fused", session.comm, table.ptr, 1, n, ctypes.c_float(1.0), algo, h)
@@ -321,8 +321,9 @@ def stress_task(config, session, *, iterations=300, seed=2024):
     rng = np.random.default_rng(seed)
     n_ranks = config.n_workers
     algos_f32 = [_native.ALGO_AUTO, _native.ALGO_LL, _native.ALGO_ONESHOT, _native.ALGO_TWOSHOT, _native.ALGO_PUSH,
-                 _native.ALGO_PUSH_ONESHOT, _native.ALGO_LL128]
-    algos_b16 = [_native.ALGO_AUTO, _native.ALGO_LL, _native.ALGO_ONESHOT, _native.ALGO_TWOSHOT, _native.ALGO_LL128]
+                 _native.ALGO_PUSH_ONESHOT, _native.ALGO_LL128, _native.ALGO_LL128_ONESHOT]
+    algos_b16 = [_native.ALGO_AUTO, _native.ALGO_LL, _native.ALGO_ONESHOT, _native.ALGO_TWOSHOT, _native.ALGO_LL128,
+                 _native.ALGO_LL128_ONESHOT]
     h = session.stream.cuda_stream
     failures = []
     with torch.cuda.device(session.device), torch.cuda.stream(session.stream):

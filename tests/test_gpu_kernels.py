@@ -192,7 +192,7 @@ def _fused_emulated(torch, per_rank_tensors, counts, algo, scale=1.0):
 
 @pytest.mark.parametrize("algo", [_native.ALGO_ONESHOT, _native.ALGO_TWOSHOT, _native.ALGO_PUSH,
                                   _native.ALGO_PUSH_ONESHOT, _native.ALGO_LL, _native.ALGO_PUSH_PIPE,
-                                  _native.ALGO_LL128])
+                                  _native.ALGO_LL128, _native.ALGO_LL128_ONESHOT])
 @pytest.mark.parametrize("n_ranks", [2, 3, 4, 8])
 @pytest.mark.parametrize("shift", [0, 1])
 def test_fused_exchange_bit_exact(torch_cuda, algo, n_ranks, shift):
@@ -239,7 +239,7 @@ def test_fused_exchange_many_rows_from_device_table(torch_cuda):
 
 
 @pytest.mark.parametrize("algo", [_native.ALGO_ONESHOT, _native.ALGO_TWOSHOT, _native.ALGO_LL, _native.ALGO_PUSH,
-                                  _native.ALGO_LL128])
+                                  _native.ALGO_LL128, _native.ALGO_LL128_ONESHOT])
 @pytest.mark.parametrize("n_ranks", [1, 2, 3, 4, 5, 8])
 @pytest.mark.parametrize("shift,scale", [(0, 1.0), (1, 1.0), (3, 0.125)])
 def test_bf16_exchange_bit_exact(torch_cuda, algo, n_ranks, shift, scale):
@@ -247,7 +247,7 @@ def test_bf16_exchange_bit_exact(torch_cuda, algo, n_ranks, shift, scale):
     equals the oracle (reference fold over upcast inputs, rounded once), bit for bit, for odd
     row sizes, misaligned tensors, segment-straddling slots and an n % 8 tail."""
     torch = torch_cuda
-    if algo in (_native.ALGO_LL, _native.ALGO_PUSH, _native.ALGO_LL128) and n_ranks == 1:
+    if algo in (_native.ALGO_LL, _native.ALGO_PUSH, _native.ALGO_LL128, _native.ALGO_LL128_ONESHOT) and n_ranks == 1:
         pytest.skip("LL / push / LL128 need >= 2 ranks")
     counts = [9408, 4096, 1001, 3, 36864, 17, 2049, 8, 7]  # layer high first
     total = sum(counts)

@@ -28,8 +28,9 @@ from paper_1811_11141_b200.allreduce_net import LocalGroup, ProtocolError, group
 pytestmark = pytest.mark.gpu
 
 ALGOS_F32 = [_native.ALGO_LL, _native.ALGO_ONESHOT, _native.ALGO_TWOSHOT, _native.ALGO_PUSH_ONESHOT,
-             _native.ALGO_PUSH, _native.ALGO_PUSH_PIPE, _native.ALGO_LL128]
-ALGOS_B16 = [_native.ALGO_LL, _native.ALGO_ONESHOT, _native.ALGO_TWOSHOT, _native.ALGO_PUSH, _native.ALGO_LL128]
+             _native.ALGO_PUSH, _native.ALGO_PUSH_PIPE, _native.ALGO_LL128, _native.ALGO_LL128_ONESHOT]
+ALGOS_B16 = [_native.ALGO_LL, _native.ALGO_ONESHOT, _native.ALGO_TWOSHOT, _native.ALGO_PUSH, _native.ALGO_LL128,
+             _native.ALGO_LL128_ONESHOT]
 
 
 @pytest.fixture(scope="module")
@@ -166,6 +167,7 @@ CASES = {
     "length_push": dict(n_of=lambda r: 3_000_000 + 4 * r, algo=_native.ALGO_PUSH),
     "length_pipe": dict(n_of=lambda r: 3_000_000 + 4 * r, algo=_native.ALGO_PUSH_PIPE),
     "length_ll128": dict(n_of=lambda r: 3_000_000 + 4 * r, algo=_native.ALGO_LL128),
+    "length_ll128_one": dict(n_of=lambda r: 100_000 + 4 * r, algo=_native.ALGO_LL128_ONESHOT),
     "group": dict(n_of=lambda r: 100_000, tags=lambda w: [group_tag(3 + r) for r in range(w)]),
     "iteration": dict(n_of=lambda r: 100_000, tags=lambda w: [group_tag(3, r) for r in range(w)]),
     "scale": dict(n_of=lambda r: 100_000, algo=_native.ALGO_ONESHOT, scales=lambda w: [1.0 / (r + 1) for r in range(w)]),

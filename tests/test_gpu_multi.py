@@ -106,7 +106,7 @@ def test_every_algorithm_bit_exact_over_ipc():
         for size in (1, 17, 1001, 4099):
             want = g[f"out_N{n}_n{size}"].view("<u4")
             for r in range(n):
-                for variant in ("fused_ll", "fused_one", "fused_two", "fused_push", "fused_push1", "fused_ll128", "plain_one",
+                for variant in ("fused_ll", "fused_one", "fused_two", "fused_push", "fused_push1", "fused_ll128", "fused_ll128_1", "plain_one",
                                 "plain_two", "gate_ll", "gate_two"):
                     got = results[r][f"n{size}_{variant}"].view("<u4")
                     assert np.array_equal(got, want), (n, size, r, variant)
@@ -118,7 +118,7 @@ def test_fused_algorithms_large_multirow_vs_oracle():
 
     sizes = (4099, 16705, 40000, 65536, 131075, 262144)  # up to the LL area's 1 MB per source
     algos = (_native.ALGO_LL, _native.ALGO_ONESHOT, _native.ALGO_TWOSHOT, _native.ALGO_PUSH, _native.ALGO_PUSH_ONESHOT,
-             _native.ALGO_LL128)
+             _native.ALGO_LL128, _native.ALGO_LL128_ONESHOT)
     for n in _worlds():
         res = run_workers(n, partial(_mp_tasks.sizes_task, sizes=sizes, algos=algos))
         for size in sizes:

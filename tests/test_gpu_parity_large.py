@@ -36,9 +36,9 @@ pytestmark = pytest.mark.gpu
 A = _native
 F32_ALGOS = {"ll": A.ALGO_LL, "oneshot": A.ALGO_ONESHOT, "twoshot": A.ALGO_TWOSHOT,
              "push_oneshot": A.ALGO_PUSH_ONESHOT, "push": A.ALGO_PUSH, "push_pipe": A.ALGO_PUSH_PIPE,
-             "ll128": A.ALGO_LL128}
+             "ll128": A.ALGO_LL128, "ll128_one": A.ALGO_LL128_ONESHOT}
 B16_ALGOS = {"ll": A.ALGO_LL, "oneshot": A.ALGO_ONESHOT, "twoshot": A.ALGO_TWOSHOT, "push": A.ALGO_PUSH,
-             "ll128": A.ALGO_LL128}
+             "ll128": A.ALGO_LL128, "ll128_one": A.ALGO_LL128_ONESHOT}
 LL_ELEMS = 262_144
 
 
@@ -169,7 +169,7 @@ def f32_algos(case, n_ranks):
     if n <= LL_ELEMS:
         out.append("ll")
     if 4 * n <= (16 << 20):
-        out.append("push_oneshot")
+        out.extend(["push_oneshot", "ll128_one"])
     return out
 
 
@@ -185,7 +185,8 @@ def test_fp32_bucket_bit_exact(torch_cuda, case, n_ranks, algo):
 
 
 B16_CASES = [(c, n, a) for c in ("ll_ceiling", "mib16", "r50_bucket", "vgg_fc6") for n in (2, 4, 8)
-             for a in (["oneshot", "twoshot", "push", "ll128"] + (["ll"] if sum(layout(c, n)[0]) <= 2 * LL_ELEMS else []))]
+             for a in (["oneshot", "twoshot", "push", "ll128"] + (["ll"] if sum(layout(c, n)[0]) <= 2 * LL_ELEMS else [])
+                       + (["ll128_one"] if sum(layout(c, n)[0]) <= (8 << 20) else []))]
 
 
 @pytest.mark.parametrize("case,n_ranks,algo", B16_CASES, ids=[f"{c}-N{n}-{a}" for c, n, a in B16_CASES])
