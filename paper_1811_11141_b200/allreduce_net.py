@@ -427,6 +427,10 @@ class RingSession:
             mine = sizes[rank]
             c.payload_bytes_received += w * ((world - 1) * mine + n - mine) * 8 // 7
             c.payload_bytes_sent += w * ((n - mine) + (world - 1) * mine) * 8 // 7
+        elif algo == _native.ALGO_LL128_ONESHOT:  # (N-1) x M in 128-B lines of 112 B payload
+            c.rounds += 1
+            c.payload_bytes_received += w * n * (world - 1) * 8 // 7
+            c.payload_bytes_sent += w * n * (world - 1) * 8 // 7
         elif algo in (_native.ALGO_ONESHOT, _native.ALGO_PUSH_ONESHOT):
             c.rounds += 1
             c.payload_bytes_received += w * n * (world - 1)
@@ -478,7 +482,12 @@ def _auto_rule(session: RingSession, n: int, fused: bool = False) -> int:
     """Host mirror of pick_fused_algo / pick_algo at the default thresholds."""
     if fused:
         world = session.config.n_workers
-        if (1 << 20) <= 4 * n <= ((32 << 20) if world == 2 else (16 << 20)):
+        nbytes = 4 * n
+        if world == 2 and (512 << 10) <= nbytes <= (8 << 20):
+            return _native.ALGO_LL128_ONESHOT
+        if 2 < world <= 4 and (256 << 10) <= nbytes < (1 << 20):
+            return _native.ALGO_LL128_ONESHOT
+        if (1 << 20) <= nbytes <= ((32 << 20) if world == 2 else (16 << 20)):
             return _native.ALGO_LL128
         if 4 * n <= ll_max_bytes(world):
             return _native.ALGO_LL

@@ -256,6 +256,17 @@ int pick_algo(const mgw_comm* c, int64_t n, int algo) {
 // NVLS only when enabled (not bit-exact with the reference order)
 constexpr int64_t kLL128MinBytes = 1ll << 20;  // AUTO: LL128 from here (before LL's ceiling)
 inline int64_t ll128_max_bytes(const mgw_comm* c) { return c->world == 2 ? (32ll << 20) : (16ll << 20); }
+// AUTO's LL128 choice for a bucket of `bytes` (fp32 or bf16 alike), 0 = neither: the
+// one-shot (one hop, (N-1) x M x 8/7 out) for mid-size buckets, the two-shot from 1 MiB
+// (profiles/ll128_one_n{2,4}_r02.json, graph-timed: N=4 256 KiB 7.5 vs LL 8.8 us, 512 KiB
+// 9.0 vs 11.4; N=2 1 MiB 7.3 vs 9.0, 4 MiB 13.1 vs 14.5, 8 MiB 20.7 vs 21.0).  N > 4: the
+// one-shot's (N-1) x M is unmeasured there, so only the two-shot.
+inline int ll128_pick(const mgw_comm* c, int64_t bytes) {
+  if (c->world == 2 && bytes >= (512ll << 10) && bytes <= (8ll << 20)) return MGW_ALGO_LL128_ONESHOT;
+  if (c->world > 2 && c->world <= 4 && bytes >= (256ll << 10) && bytes < kLL128MinBytes) return MGW_ALGO_LL128_ONESHOT;
+  if (bytes >= kLL128MinBytes && bytes <= ll128_max_bytes(c)) return MGW_ALGO_LL128;
+  return 0;
+}
 
 int pick_fused_algo(const mgw_comm* c, int64_t n, int algo) {
   if (algo != MGW_ALGO_AUTO) return algo;
@@ -273,7 +284,10 @@ int pick_fused_algo(const mgw_comm* c, int64_t n, int algo) {
   // (profiles/ll128_sweep_n{2,4}_r02.json, graph-timed at N = 4: 1 MiB 11.8 vs 15.4 us,
   // 4 MiB 18.2 vs 27.9, 16 MiB 56.3 vs 58.5; level with the push two-shot at 32 MiB,
   // which stays above 16 MiB; at N = 2 it wins to 32 MiB, and from 1 MiB over the LL one-shot)
-  if (c->world > 1 && bytes >= kLL128MinBytes && bytes <= ll128_max_bytes(c)) return MGW_ALGO_LL128;
+  if (c->world > 1) {
+    const int l128 = ll128_pick(c, bytes);
+    if (l128) return l128;
+  }
   if (c->world > 1 && n * 4 <= c->ll_max_bytes && n <= kLLElems) return MGW_ALGO_LL;
   const bool push_ok = bytes <= (1ll << 30);
   if (c->world == 2)
@@ -304,10 +318,11 @@ int resolve_fused_algo(const mgw_comm* c, int64_t n, int algo) {
 // bf16 group exchange: LL for small buckets, else pull one-shot / two-shot
 int resolve_b16_algo(const mgw_comm* c, int64_t n, int algo) {
   if (algo == MGW_ALGO_AUTO) {
-    // bf16 crossovers as fp32 (profiles/ll128_bf16_sweep_n{2,4}_r02.json): LL128 for
-    // 1 MiB .. 16 MiB (N >= 3) / 32 MiB (N = 2), LL below, push two-shot above
-    if (c->world > 1 && n * 2 >= kLL128MinBytes && n * 2 <= ll128_max_bytes(c))
-      algo = MGW_ALGO_LL128;
+    // bf16 crossovers as fp32 in bytes (profiles/ll128_bf16_sweep_n{2,4}_r02.json): LL128
+    // one-/two-shot (ll128_pick), LL below, push two-shot above
+    const int l128 = c->world > 1 ? ll128_pick(c, n * 2) : 0;
+    if (l128)
+      algo = l128;
     else if (c->world > 1 && n * 2 <= c->ll_max_bytes && n <= 2 * kLLElems)
       algo = MGW_ALGO_LL;
     else if (n * 2 <= c->oneshot_max_bytes)

@@ -41,7 +41,8 @@ def main() -> int:
     rank, world, local = bench._dist_setup(A())
     device = torch.device("cuda", local)
     sizes = [int(float(m) * (1 << 20)) for m in args.mib.split(",")]
-    _, session = open_session_dist(capacity_bytes=max(sizes) + (1 << 20))
+    # the one-shot kinds hold N incoming rows of the whole bucket (LL128: in 128-B lines of 112 B)
+    _, session = open_session_dist(capacity_bytes=max(sizes) * world * 8 // 7 + (1 << 20))
     comm = session.comm
     ids = {"oneshot": _native.ALGO_ONESHOT, "twoshot": _native.ALGO_TWOSHOT, "push": _native.ALGO_PUSH,
            "push_pipe": _native.ALGO_PUSH_PIPE, "push_oneshot": _native.ALGO_PUSH_ONESHOT, "auto": _native.ALGO_AUTO,
