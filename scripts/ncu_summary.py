@@ -92,7 +92,7 @@ def main() -> int:
         tpath = ROOT / "profiles" / "roofline_traffic.json"
         traffic = json.loads(tpath.read_text()) if tpath.exists() else {}
         for spec in args.traffic:
-            key, pat = spec.split("=", 1)
+            key, pat = spec.rsplit("=", 1)  # keys may hold "=" (e.g. "(N=1)"), kernel regexes do not
             hits = [v for k, v in kernels.items() if re.search(pat, k)]
             if hits:
                 traffic[key] = hits[0]["dram_bytes_per_launch"]
