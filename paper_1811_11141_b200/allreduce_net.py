@@ -823,6 +823,7 @@ class LocalGroup:
             sess = RingSession(self.configs[r], self._comms[r], capacity_bytes=capacity_bytes, timeout=timeout)
             sess._local_group = True
             self.sessions.append(sess)
+        self.device = torch.device("cuda", device)
         self.stream = torch.cuda.Stream(device=device)
 
     @property
@@ -866,6 +867,61 @@ class LocalGroup:
             except ProtocolError as exc:
                 errors.append(exc)
         return errors
+
+    def bench_allreduce(self, sizes: list[int], *, repeats: int = 5, warmups: int = 3,
+                        algo: int = _native.ALGO_AUTO) -> list[Measurement]:
+        """``bench_allreduce`` (allreduce_net.py:414-445 semantics) for the in-process group:
+        median device time of one fused group exchange per payload size, every rank's CTAs
+        in one cooperative launch.  Each sample is 8 back-to-back group launches under one
+        CUDA event pair, queued behind a short device spin so host launch latency stays out;
+        every size is checked once for the exact sum N(N+1)/2."""
+        if repeats < 1:
+            raise ValueError("repeats must be >= 1")
+        for nbytes in sizes:
+            if not isinstance(nbytes, int) or nbytes <= 0 or nbytes % 4:
+                raise ValueError(f"sizes must be positive multiples of 4 bytes, got {nbytes!r}")
+            if nbytes > self.sessions[0].capacity_bytes:
+                raise ValueError(f"size {nbytes} exceeds the session capacity of {self.sessions[0].capacity_bytes} B")
+        torch = self.torch
+        world = self.n_workers
+        out: list[Measurement] = []
+        loop = 8
+        for nbytes in sizes:
+            n = nbytes // 4
+            bufs = [torch.empty(n, dtype=torch.float32, device=self.device) for _ in range(world)]
+            tables = [_native.DeviceTable([(b.data_ptr(), n, 0)]) for b in bufs]
+            args = ((ctypes.c_void_p * world)(*self._comms), (ctypes.c_void_p * world)(*[t.ptr for t in tables]),
+                    (ctypes.c_int64 * world)(*([n] * world)), (ctypes.c_float * world)(*([1.0] * world)), world,
+                    int(algo), 4, self.stream.cuda_stream)
+            try:
+                self.stream.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(self.stream):
+                    for _ in range(warmups):
+                        _native.call("mgw_group_allreduce_fused", *args)
+                    times = []
+                    for _ in range(repeats):
+                        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        _native.call("mgw_spin_ns", 2_000_000, self.stream.cuda_stream)
+                        start.record(self.stream)
+                        for _ in range(loop):
+                            _native.call("mgw_group_allreduce_fused", *args)
+                        end.record(self.stream)
+                        end.synchronize()
+                        times.append(start.elapsed_time(end) * 1e-3 / loop)
+                    for r, b in enumerate(bufs):
+                        b.fill_(float(r + 1))
+                    _native.call("mgw_group_allreduce_fused", *args)
+                    self.stream.synchronize()
+                for sess in self.sessions:
+                    sess.raise_if_failed()
+                for b in bufs:
+                    if not bool((b == float(world * (world + 1) // 2)).all()):
+                        raise RuntimeError(f"wrong all-reduce result at {nbytes} B")
+            finally:
+                for t in tables:
+                    t.close()
+            out.append(Measurement(nbytes=nbytes, seconds=statistics.median(times), n_nodes=world))
+        return out
 
     def clear_errors(self) -> None:
         for sess in self.sessions:

@@ -228,3 +228,22 @@ def test_absent_peer_times_out(torch_cuda):
         assert 0.4 < dt < 3.0
     finally:
         grp.close()
+
+
+@pytest.mark.parametrize("n_ranks", [2, 4])
+def test_bench_allreduce_local_group(torch_cuda, group, n_ranks):
+    """``bench_allreduce`` (allreduce_net.py:414-445 contract) through the real protocol on one
+    GPU: one Measurement per size, positive and growing with size, exact sums checked
+    inside, and the (a, b) fit of the reference's cost model is positive."""
+    from paper_1811_11141_b200 import fit_ab
+
+    grp = group(n_ranks)
+    sizes = [4096, 65536, 1 << 20, 4 << 20, 16 << 20]
+    ms = grp.bench_allreduce(sizes, repeats=3, warmups=2)
+    assert [m.nbytes for m in ms] == sizes and all(m.n_nodes == n_ranks for m in ms)
+    assert all(m.seconds > 0 for m in ms)
+    assert ms[-1].seconds > ms[0].seconds
+    model = fit_ab(ms)
+    assert model.a > 0 and model.b > 0
+    with pytest.raises(ValueError):
+        grp.bench_allreduce([6])
