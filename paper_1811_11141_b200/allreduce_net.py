@@ -422,15 +422,15 @@ class RingSession:
             c.rounds += 1
             c.payload_bytes_received += 2 * w * n * (world - 1)
             c.payload_bytes_sent += 2 * w * n * (world - 1)
-        elif algo == _native.ALGO_LL128:  # the two-shot's bytes in 128-B lines of 112 B payload
+        elif algo == _native.ALGO_LL128:  # the two-shot's bytes in 128-B lines of 120 B payload
             c.rounds += 2
             mine = sizes[rank]
-            c.payload_bytes_received += w * ((world - 1) * mine + n - mine) * 8 // 7
-            c.payload_bytes_sent += w * ((n - mine) + (world - 1) * mine) * 8 // 7
-        elif algo == _native.ALGO_LL128_ONESHOT:  # (N-1) x M in 128-B lines of 112 B payload
+            c.payload_bytes_received += w * ((world - 1) * mine + n - mine) * 16 // 15
+            c.payload_bytes_sent += w * ((n - mine) + (world - 1) * mine) * 16 // 15
+        elif algo == _native.ALGO_LL128_ONESHOT:  # (N-1) x M in 128-B lines of 120 B payload
             c.rounds += 1
-            c.payload_bytes_received += w * n * (world - 1) * 8 // 7
-            c.payload_bytes_sent += w * n * (world - 1) * 8 // 7
+            c.payload_bytes_received += w * n * (world - 1) * 16 // 15
+            c.payload_bytes_sent += w * n * (world - 1) * 16 // 15
         elif algo in (_native.ALGO_ONESHOT, _native.ALGO_PUSH_ONESHOT):
             c.rounds += 1
             c.payload_bytes_received += w * n * (world - 1)

@@ -5,13 +5,13 @@
 
 namespace mgw {
 
-// lines per CTA: at least one full CTA step (64 lines = 7 KB of payload per part), grid up
-// to the CTA cap.  Two-shot: lines of one part; one-shot: lines of the whole bucket.
+// lines per CTA: at least one full CTA step (64 lines = 7.5 KB of payload per part), grid
+// up to the CTA cap.  Two-shot: lines of one part; one-shot: lines of the whole bucket.
 int plan_ll128(L128Args& x, int max_ctas, const int64_t* per_cta, bool b16, bool one) {
   max_ctas = max_ctas < kMaxBlocks ? max_ctas : kMaxBlocks;
   const int w = x.f.ar.world > 0 ? x.f.ar.world : 1;
   const int64_t slots = l128_slots(x.f.ar.n, b16);
-  const int64_t lines = ((one ? slots : slots / w) + kL128Vec - 1) / kL128Vec;
+  const int64_t lines = l128_lines(one ? slots : slots / w);
   const int64_t per = per_cta && per_cta[1] > 0 ? (per_cta[1] + kL128Vec - 1) / kL128Vec : kL128Step;
   const int grid = grid_for(lines, per, max_ctas);
   x.row_lines = l128_row_lines(x.f.ar.n, w, b16, one);

@@ -7,14 +7,15 @@
 // release (the CTA stalls until every NVLink store it issued is acknowledged) plus a flag
 // round trip, and a phase cannot start on any data until the slowest peer CTA signalled.
 // Here data and flag travel together: a 128-B line = 8 lanes x 16 B, lanes 0..6 carry 7
-// 16-B slots of the bucket, lane 7 carries the flag (epoch << 32 | collective tag) twice.
+// 16-B slots of the bucket, lane 7 carries 8 B of payload (half of a slot shared by a pair
+// of lines) and the flag (epoch << 32 | collective tag): 120 B of payload per line.
 // One warp store instruction writes whole lines (a group of 8 consecutive lanes per line),
 // and NVLink delivers a warp's 128-B line as one write, so a reader that sees the flag of a
 // line (loaded by the same warp instruction as the other 7 lanes) sees its payload -- the
 // NVLink LL128 contract of NCCL's protocol of that name.  Readers only poll local memory.
 //
 //   phase 1  CTA b stores its line range of every part p (scaled) into rank p's incoming
-//            row `me`                                  (lines: 2 (N-1)/N x M x 8/7 out)
+//            row `me`                                  (lines: 2 (N-1)/N x M x 16/15 out)
 //   phase 2  CTA b polls its line range of its own part in the N local rows, folds in the
 //            reference order (fold start = the element's `_segments` segment), writes its
 //            tensors and stores result lines into every peer's gather row `me`
@@ -37,9 +38,31 @@
 namespace mgw {
 
 constexpr int kL128Lanes = 8;                          // 16-B lanes per 128-B line
-constexpr int kL128Vec = kL128Lanes - 1;               // payload 16-B slots per line
-constexpr int kL128Step = kThreads / kL128Lanes;       // lines per CTA step (64)
+constexpr int kL128Vec = kL128Lanes - 1;               // whole 16-B slots per line (lanes 0..6)
+constexpr int kL128PairSlots = 2 * kL128Vec + 1;       // 16-B slots per line pair (15)
+constexpr int kL128Step = kThreads / kL128Lanes;       // lines per CTA step (64 = 32 pairs)
 constexpr int kL128Words = 2 * kL128Lanes;             // u64 words per line
+
+// Lines come in pairs: lanes 0..6 of the even line carry slots 0..6 of the pair, lanes
+// 0..6 of the odd line slots 7..13, and lane 7 of each line carries one 8-B half of slot
+// 14 next to its flag word -- 240 B of payload per 256 B (16/15 on the wire instead of
+// 8/7), every tensor access still a 16-B aligned slot.  Slot of (line l, lane sub)
+// relative to its part:
+__host__ __device__ __forceinline__ int64_t l128_slot(int64_t l, int sub) {
+  const int64_t base = (l >> 1) * kL128PairSlots;
+  return sub < kL128Vec ? base + (l & 1) * kL128Vec + sub : base + 2 * kL128Vec;
+}
+// lines holding `slots` 16-B slots (whole pairs)
+__host__ __device__ __forceinline__ int64_t l128_lines(int64_t slots) {
+  return 2 * ((slots + kL128PairSlots - 1) / kL128PairSlots);
+}
+// CTA b's line range [l0, l1) of a part of `slots` slots: whole pairs, so a warp's groups
+// 2k and 2k+1 always hold the two lines of one pair
+__device__ __forceinline__ void l128_cta_lines(int64_t slots, int b, int ctas, int64_t& l0, int64_t& l1) {
+  cta_chunk(0, l128_lines(slots) / 2, b, ctas, l0, l1);
+  l0 *= 2;
+  l1 *= 2;
+}
 
 struct L128Args {
   FusedArgs f;
@@ -55,9 +78,8 @@ __host__ __device__ __forceinline__ int64_t l128_slots(int64_t n, bool b16) { re
 // lines per row: the longest part (part_begin rounds down to kPartAlign) in lines; the
 // one-shot's row holds the whole bucket
 __host__ __device__ __forceinline__ int64_t l128_row_lines(int64_t n, int world, bool b16, bool one = false) {
-  if (one) return (l128_slots(n, b16) + kL128Vec - 1) / kL128Vec;
-  const int64_t part = (l128_slots(n, b16) + world - 1) / world + kPartAlign;
-  return (part + kL128Vec - 1) / kL128Vec;
+  if (one) return l128_lines(l128_slots(n, b16));
+  return l128_lines((l128_slots(n, b16) + world - 1) / world + kPartAlign);
 }
 
 __device__ __forceinline__ void st_volatile_v2(uint64_t* p, uint64_t a, uint64_t b) {
@@ -252,7 +274,7 @@ __device__ __forceinline__ void l128_store(const FusedArgs& f, int& k, int64_t v
 
 // ONE = the one-shot: every rank pushes its whole bucket (one line range per CTA) into
 // every rank's incoming row `me` and folds its line range of the whole bucket from the N
-// local rows -- one NVLink hop, (N-1) x M x 8/7 out, no gather phase.
+// local rows -- one NVLink hop, (N-1) x M x 16/15 out, no gather phase.
 template <int N, bool B16, bool ONE>
 __device__ __forceinline__ void ll128_any_body(const L128Args& x, const int cta, const int ctas) {
   constexpr int K = B16 ? kB16 : 4;  // elements per 16-B slot
@@ -282,8 +304,12 @@ __device__ __forceinline__ void ll128_any_body(const L128Args& x, const int cta,
   __syncthreads();
   const uint64_t expect = ((uint64_t)epoch << 32) | a.tag;
   const int sub = threadIdx.x & (kL128Lanes - 1);  // lane within the line
-  const int grp = threadIdx.x / kL128Lanes;        // line within the CTA step
-  const bool carrier = sub < kL128Vec;             // payload lane (lane 7 = flag)
+  const int grp = threadIdx.x / kL128Lanes;        // line within the CTA step (pairs: 2k, 2k+1)
+  const bool shared_lane = sub == kL128Vec;        // lane 7: half of the pair's slot 14 + flag
+  const bool odd = grp & 1;                        // the pair's second line (high half of slot 14)
+  // the words lane `sub` puts on the wire for slot words (lo, hi)
+  auto wire_lo = [&](uint64_t lo, uint64_t hi) { return shared_lane ? (odd ? hi : lo) : lo; };
+  auto wire_hi = [&](uint64_t hi) { return shared_lane ? expect : hi; };
   const int64_t rl = x.row_lines;
   const float scale = f.scale;
   const bool scaled = scale != 1.0f;
@@ -301,11 +327,11 @@ __device__ __forceinline__ void ll128_any_body(const L128Args& x, const int cta,
     int k = 0;
     bool k_set = false;
     int64_t l0, l1;
-    cta_chunk(0, (slots + kL128Vec - 1) / kL128Vec, cta, ctas, l0, l1);
+    l128_cta_lines(slots, cta, ctas, l0, l1);
     for (int64_t base = l0; base < l1; base += kL128Step) {
       const int64_t l = base + grp;
-      const int64_t v = l * kL128Vec + sub;
-      const bool live = l < l1 && carrier && v < slots;
+      const int64_t v = l128_slot(l, sub);
+      const bool live = l < l1 && v < slots;
       uint64_t lo = 0, hi = 0;
       if (live) {
         if (!k_set) {
@@ -314,13 +340,13 @@ __device__ __forceinline__ void ll128_any_body(const L128Args& x, const int cta,
         }
         l128_load<B16>(f, k, v, scale, scaled, lo, hi);
       }
-      if (!carrier) lo = hi = expect;
+      const uint64_t w0 = wire_lo(lo, hi), w1 = wire_hi(hi);
       __syncwarp();
       if (l < l1) {
 #pragma unroll
         for (int r = 0; r < N; ++r) {
           const int q = me + 1 + r < N ? me + 1 + r : me + 1 + r - N;  // peers first, mine last
-          st_volatile_v2(in_of(q) + ((int64_t)me * rl + l) * kL128Words + sub * 2, lo, hi);
+          st_volatile_v2(in_of(q) + ((int64_t)me * rl + l) * kL128Words + sub * 2, w0, w1);
         }
       }
     }
@@ -332,12 +358,12 @@ __device__ __forceinline__ void ll128_any_body(const L128Args& x, const int cta,
     for (int p = 0; p < N; ++p) {
       const int64_t q0 = s_part[p], q1 = s_part[p + 1];
       int64_t l0, l1;
-      cta_chunk(0, (q1 - q0 + kL128Vec - 1) / kL128Vec, cta, ctas, l0, l1);
+      l128_cta_lines(q1 - q0, cta, ctas, l0, l1);
       uint64_t* row = in_of(p) + (int64_t)me * rl * kL128Words + sub * 2;
       for (int64_t base = l0; base < l1; base += kL128Step) {
         const int64_t l = base + grp;
-        const int64_t v = q0 + l * kL128Vec + sub;
-        const bool live = l < l1 && carrier && v < q1;
+        const int64_t v = q0 + l128_slot(l, sub);
+        const bool live = l < l1 && v < q1;
         uint64_t lo = 0, hi = 0;
         if (live) {
           if (!k_set) {
@@ -346,8 +372,9 @@ __device__ __forceinline__ void ll128_any_body(const L128Args& x, const int cta,
           }
           l128_load<B16>(f, k, v, scale, scaled, lo, hi);
         }
+        const uint64_t w0 = wire_lo(lo, hi), w1 = wire_hi(hi);
         __syncwarp();
-        if (l < l1) st_volatile_v2(row + l * kL128Words, carrier ? lo : expect, carrier ? hi : expect);
+        if (l < l1) st_volatile_v2(row + l * kL128Words, w0, w1);
       }
     }
   }
@@ -357,14 +384,14 @@ __device__ __forceinline__ void ll128_any_body(const L128Args& x, const int cta,
   if (do_fold) {
     const int64_t q0 = ONE ? 0 : s_part[me], q1 = ONE ? slots : s_part[me + 1];
     int64_t l0, l1;
-    cta_chunk(0, (q1 - q0 + kL128Vec - 1) / kL128Vec, cta, ctas, l0, l1);
+    l128_cta_lines(q1 - q0, cta, ctas, l0, l1);
     const uint64_t* in = in_of(me) + sub * 2;
     int seg = 0, k = 0;
     bool k_set = false;
     for (int64_t base = l0; base < l1 && status == MGW_DEV_OK; base += kL128Step) {
       const int64_t l = base + grp;
       const bool active = l < l1;
-      const int64_t v = q0 + l * kL128Vec + sub;
+      const int64_t v = q0 + l128_slot(l, sub);
       uint64_t lo[N], hi[N];
 #pragma unroll
       for (int s = 0; s < N; ++s) {
@@ -380,7 +407,16 @@ __device__ __forceinline__ void ll128_any_body(const L128Args& x, const int cta,
         }
       }
       if (status != MGW_DEV_OK) break;
-      const bool live = active && carrier && v < q1;
+      // lane 7: rebuild slot 14 from its own half and the partner line's (lane ^ 8)
+#pragma unroll
+      for (int s = 0; s < N; ++s) {
+        const uint64_t other = __shfl_xor_sync(0xffffffffu, lo[s], kL128Lanes);
+        if (shared_lane) {
+          hi[s] = odd ? lo[s] : other;
+          lo[s] = odd ? other : lo[s];
+        }
+      }
+      const bool live = active && v < q1;
       uint64_t ylo = 0, yhi = 0;
       if (live) {
         const int64_t e = v * K;
@@ -390,11 +426,11 @@ __device__ __forceinline__ void ll128_any_body(const L128Args& x, const int cta,
           k = fused_row_covering(f, e);
           k_set = true;
         }
-        l128_store<B16>(f, k, v, ylo, yhi);
+        if (!(shared_lane && odd)) l128_store<B16>(f, k, v, ylo, yhi);  // slot 14: the even line's lane
       }
       if (ONE) continue;  // the one-shot has every part: no result lines
+      const uint64_t w0 = wire_lo(ylo, yhi), w1 = wire_hi(yhi);
       __syncwarp();
-      const uint64_t w0 = carrier ? ylo : expect, w1 = carrier ? yhi : expect;
 #pragma unroll
       for (int q = 0; q < N; ++q)
         if (q != me && active) st_volatile_v2(gat_of(q) + ((int64_t)me * rl + l) * kL128Words + sub * 2, w0, w1);
@@ -410,7 +446,7 @@ __device__ __forceinline__ void ll128_any_body(const L128Args& x, const int cta,
       if (p == me) continue;
       const int64_t q0 = s_part[p], q1 = s_part[p + 1];
       int64_t l0, l1;
-      cta_chunk(0, (q1 - q0 + kL128Vec - 1) / kL128Vec, cta, ctas, l0, l1);
+      l128_cta_lines(q1 - q0, cta, ctas, l0, l1);
       const uint64_t* g = gat_of(me) + (int64_t)p * rl * kL128Words + sub * 2;
       for (int64_t base = l0; base < l1; base += kL128Step) {
         const int64_t l = base + grp;
@@ -421,8 +457,10 @@ __device__ __forceinline__ void ll128_any_body(const L128Args& x, const int cta,
           status = st;
           break;
         }
-        const int64_t v = q0 + l * kL128Vec + sub;
-        if (active && carrier && v < q1) {
+        const int64_t v = q0 + l128_slot(l, sub);
+        const uint64_t other = __shfl_xor_sync(0xffffffffu, w0, kL128Lanes);  // slot 14's other half
+        if (shared_lane) w1 = other;  // the even line's lane 7 writes slot 14: (own half, odd half)
+        if (active && v < q1 && !(shared_lane && odd)) {
           if (!k_set) {
             k = fused_row_covering(f, v * K);
             k_set = true;

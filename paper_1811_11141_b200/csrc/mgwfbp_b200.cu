@@ -257,7 +257,7 @@ int pick_algo(const mgw_comm* c, int64_t n, int algo) {
 constexpr int64_t kLL128MinBytes = 1ll << 20;  // AUTO: LL128 from here (before LL's ceiling)
 inline int64_t ll128_max_bytes(const mgw_comm* c) { return c->world == 2 ? (32ll << 20) : (16ll << 20); }
 // AUTO's LL128 choice for a bucket of `bytes` (fp32 or bf16 alike), 0 = neither: the
-// one-shot (one hop, (N-1) x M x 8/7 out) for mid-size buckets, the two-shot from 1 MiB
+// one-shot (one hop, (N-1) x M x 16/15 out) for mid-size buckets, the two-shot from 1 MiB
 // (profiles/ll128_one_n{2,4}_r02.json, graph-timed: N=4 256 KiB 7.5 vs LL 8.8 us, 512 KiB
 // 9.0 vs 11.4; N=2 1 MiB 7.3 vs 9.0, 4 MiB 13.1 vs 14.5, 8 MiB 20.7 vs 21.0).  N > 4: the
 // one-shot's (N-1) x M is unmeasured there, so only the two-shot.
@@ -280,7 +280,7 @@ int pick_fused_algo(const mgw_comm* c, int64_t n, int algo) {
   // 1000-layer SyncEASGD bucket, 6.75 GB: 42.4 vs 20.8 ms at N = 4; VGG-16's 553 MB still
   // favours push, profiles/profiles_n4_r01_final.json).
   const int64_t bytes = n * 4;
-  // the flag-in-line two-shot (ll128.cuh) from 1 MiB: no barriers, 2 (N-1)/N x M x 8/7 out
+  // the flag-in-line two-shot (ll128.cuh) from 1 MiB: no barriers, 2 (N-1)/N x M x 16/15 out
   // (profiles/ll128_sweep_n{2,4}_r02.json, graph-timed at N = 4: 1 MiB 11.8 vs 15.4 us,
   // 4 MiB 18.2 vs 27.9, 16 MiB 56.3 vs 58.5; level with the push two-shot at 32 MiB,
   // which stays above 16 MiB; at N = 2 it wins to 32 MiB, and from 1 MiB over the LL one-shot)
