@@ -485,7 +485,7 @@ def _auto_rule(session: RingSession, n: int, fused: bool = False) -> int:
         nbytes = 4 * n
         if world == 2 and (512 << 10) <= nbytes <= (8 << 20):
             return _native.ALGO_LL128_ONESHOT
-        if 2 < world <= 4 and (256 << 10) <= nbytes < (1 << 20):
+        if 2 < world <= 4 and (256 << 10) <= nbytes <= (1 << 20):
             return _native.ALGO_LL128_ONESHOT
         if (1 << 20) <= nbytes <= ((32 << 20) if world == 2 else (16 << 20)):
             return _native.ALGO_LL128
