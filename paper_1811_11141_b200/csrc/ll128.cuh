@@ -94,12 +94,16 @@ __device__ __forceinline__ void ld_volatile_v2(const uint64_t* p, uint64_t& a, u
 // `expect` in its flag lane.  Returns a warp-uniform status.  Slow path every 16 spins: a
 // flag of this epoch with another tag, or the source's header of this epoch with another
 // tag (a peer in a different collective), the abort flag, the timeout.
+#ifndef MGW_L128_BACKOFF_NS
+#define MGW_L128_BACKOFF_NS 0  // A/B: sleep between re-polls of a line that has not arrived
+#endif
 __device__ __forceinline__ int l128_poll(const uint64_t* p, bool active, uint64_t expect, const uint64_t* hdr,
                                          const ArArgs& a, uint64_t& w0, uint64_t& w1) {
   const int flag_lane = (threadIdx.x & 31) | (kL128Lanes - 1);
   const uint32_t epoch = (uint32_t)(expect >> 32);
   uint64_t start = 0;
   for (uint32_t spin = 0;; ++spin) {
+    if (MGW_L128_BACKOFF_NS > 0 && spin > 0) __nanosleep(MGW_L128_BACKOFF_NS);
     if (active) ld_volatile_v2(p, w0, w1);
     const uint64_t flag = __shfl_sync(0xffffffffu, w1, flag_lane);
     if (__all_sync(0xffffffffu, !active || flag == expect)) return MGW_DEV_OK;
