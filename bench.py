@@ -304,7 +304,9 @@ def _algo_mix(session, group_bytes):
     from paper_1811_11141_b200.allreduce_net import _algo_for
 
     names = {_native.ALGO_LL: "ll", _native.ALGO_ONESHOT: "oneshot", _native.ALGO_TWOSHOT: "twoshot",
-             _native.ALGO_PUSH: "push_twoshot", _native.ALGO_PUSH_ONESHOT: "push_oneshot"}
+             _native.ALGO_PUSH: "push_twoshot", _native.ALGO_PUSH_ONESHOT: "push_oneshot",
+             _native.ALGO_PUSH_PIPE: "push_pipe", _native.ALGO_NVLS: "nvls", _native.ALGO_LL128: "ll128_twoshot",
+             _native.ALGO_LL128_ONESHOT: "ll128_oneshot"}
     mix = collections.Counter(names.get(_algo_for(session, b // 4, fused=True), "other") for b in group_bytes if b)
     return dict(sorted(mix.items()))
 
