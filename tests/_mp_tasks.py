@@ -306,7 +306,7 @@ def absent_peer_task(config, session):
     return "completed"
 
 
-def stress_task(config, session, *, iterations=300, seed=2024):
+def stress_task(config, session, *, iterations=300, seed=2024, only=None, max_n=1 << 21):
     """A seeded stream of collectives with random sizes, row splits, dtypes and algorithms
     (the same on every rank), back to back on one communicator: integer-valued payloads
     must come back exactly.  Exercises slot-parity / LL-area / gather-area reuse across
@@ -324,12 +324,15 @@ def stress_task(config, session, *, iterations=300, seed=2024):
                  _native.ALGO_PUSH_ONESHOT, _native.ALGO_LL128, _native.ALGO_LL128_ONESHOT]
     algos_b16 = [_native.ALGO_AUTO, _native.ALGO_LL, _native.ALGO_ONESHOT, _native.ALGO_TWOSHOT, _native.ALGO_LL128,
                  _native.ALGO_LL128_ONESHOT]
+    if only is not None:  # a restricted algorithm set (e.g. the LL128 kernels only)
+        algos_f32 = [a for a in algos_f32 if a in only]
+        algos_b16 = [a for a in algos_b16 if a in only]
     h = session.stream.cuda_stream
     failures = []
     with torch.cuda.device(session.device), torch.cuda.stream(session.stream):
         for it in range(iterations):
             bf16 = bool(rng.random() < 0.25)
-            n = int(rng.choice([1, 7, 63, 1000, 4097]) if rng.random() < 0.3 else rng.integers(1, 1 << 21))
+            n = int(rng.choice([1, 7, 63, 1000, 4097]) if rng.random() < 0.3 else rng.integers(1, max_n))
             if bf16:
                 algo = int(rng.choice(algos_b16))
             else:
