@@ -42,6 +42,11 @@ constexpr int kL128Vec = kL128Lanes - 1;               // whole 16-B slots per l
 constexpr int kL128PairSlots = 2 * kL128Vec + 1;       // 16-B slots per line pair (15)
 constexpr int kL128Step = kThreads / kL128Lanes;       // lines per CTA step (64 = 32 pairs)
 constexpr int kL128Words = 2 * kL128Lanes;             // u64 words per line
+#ifndef MGW_L128_ROUND_LINES
+#define MGW_L128_ROUND_LINES 128
+#endif
+constexpr int64_t kL128Round = MGW_L128_ROUND_LINES;   // lines per part per round (a multiple of kL128Step)
+static_assert(kL128Round % kL128Step == 0, "rounds are whole CTA steps");
 
 // Lines come in pairs: lanes 0..6 of the even line carry slots 0..6 of the pair, lanes
 // 0..6 of the odd line slots 7..13, and lane 7 of each line carries one 8-B half of slot
@@ -324,158 +329,157 @@ __device__ __forceinline__ void ll128_any_body(const L128Args& x, const int cta,
   auto gat_of = [&](int r) { return reinterpret_cast<uint64_t*>(x.gat[r] + poff); };
   int status = MGW_DEV_OK;
 
-  phase_mark(a, 0, cta);
-  // ---- phase 1: my line range of every part p into rank p's incoming row `me` (one-shot:
-  //      my line range of the whole bucket into every rank's row `me`)
-  if (do_push && ONE) {
-    int k = 0;
-    bool k_set = false;
-    int64_t l0, l1;
-    l128_cta_lines(slots, cta, ctas, l0, l1);
-    for (int64_t base = l0; base < l1; base += kL128Step) {
-      const int64_t l = base + grp;
-      const int64_t v = l128_slot(l, sub);
-      const bool live = l < l1 && v < slots;
-      uint64_t lo = 0, hi = 0;
-      if (live) {
-        if (!k_set) {
-          k = fused_row_covering(f, v * K);
-          k_set = true;
-        }
-        l128_load<B16>(f, k, v, scale, scaled, lo, hi);
-      }
-      const uint64_t w0 = wire_lo(lo, hi), w1 = wire_hi(hi);
-      __syncwarp();
-      if (l < l1) {
-#pragma unroll
-        for (int r = 0; r < N; ++r) {
-          const int q = me + 1 + r < N ? me + 1 + r : me + 1 + r - N;  // peers first, mine last
-          st_volatile_v2(in_of(q) + ((int64_t)me * rl + l) * kL128Words + sub * 2, w0, w1);
-        }
-      }
-    }
-  }
-  if (do_push && !ONE) {
-    int k = 0;
-    bool k_set = false;
-#pragma unroll 1
-    for (int p = 0; p < N; ++p) {
-      const int64_t q0 = s_part[p], q1 = s_part[p + 1];
-      int64_t l0, l1;
-      l128_cta_lines(q1 - q0, cta, ctas, l0, l1);
-      uint64_t* row = in_of(p) + (int64_t)me * rl * kL128Words + sub * 2;
-      for (int64_t base = l0; base < l1; base += kL128Step) {
-        const int64_t l = base + grp;
-        const int64_t v = q0 + l128_slot(l, sub);
-        const bool live = l < l1 && v < q1;
-        uint64_t lo = 0, hi = 0;
-        if (live) {
-          if (!k_set) {
-            k = fused_row_covering(f, v * K);
-            k_set = true;
-          }
-          l128_load<B16>(f, k, v, scale, scaled, lo, hi);
-        }
-        const uint64_t w0 = wire_lo(lo, hi), w1 = wire_hi(hi);
-        __syncwarp();
-        if (l < l1) st_volatile_v2(row + l * kL128Words, w0, w1);
-      }
-    }
-  }
-  phase_mark(a, 1, cta);
-  // ---- phase 2: fold my line range of my part from the N local rows; write my tensors and
-  //      every peer's gather row `me`
-  if (do_fold) {
-    const int64_t q0 = ONE ? 0 : s_part[me], q1 = ONE ? slots : s_part[me + 1];
-    int64_t l0, l1;
+  // line range [l0, l1) of this CTA in part p (one-shot: the whole bucket)
+  auto range_of = [&](int p, int64_t& q0, int64_t& q1, int64_t& l0, int64_t& l1) {
+    q0 = ONE ? 0 : s_part[p];
+    q1 = ONE ? slots : s_part[p + 1];
     l128_cta_lines(q1 - q0, cta, ctas, l0, l1);
-    const uint64_t* in = in_of(me) + sub * 2;
-    int seg = 0, k = 0;
-    bool k_set = false;
-    for (int64_t base = l0; base < l1 && status == MGW_DEV_OK; base += kL128Step) {
-      const int64_t l = base + grp;
-      const bool active = l < l1;
-      const int64_t v = q0 + l128_slot(l, sub);
-      uint64_t lo[N], hi[N];
-#pragma unroll
-      for (int s = 0; s < N; ++s) {
-        lo[s] = hi[s] = 0;
-        if (active) ld_volatile_v2(in + ((int64_t)s * rl + l) * kL128Words, lo[s], hi[s]);
-      }
-#pragma unroll
-      for (int s = 0; s < N; ++s) {
-        const uint64_t flag = __shfl_sync(0xffffffffu, hi[s], (threadIdx.x & 31) | (kL128Lanes - 1));
-        if (!__all_sync(0xffffffffu, !active || flag == expect)) {
-          const int st = l128_poll(in + ((int64_t)s * rl + l) * kL128Words, active, expect, hdr_mine + s, a, lo[s], hi[s]);
-          if (st != MGW_DEV_OK) status = st;
-        }
-      }
-      if (status != MGW_DEV_OK) break;
-      // lane 7: rebuild slot 14 from its own half and the partner line's (lane ^ 8)
-#pragma unroll
-      for (int s = 0; s < N; ++s) {
-        const uint64_t other = __shfl_xor_sync(0xffffffffu, lo[s], kL128Lanes);
-        if (shared_lane) {
-          hi[s] = odd ? lo[s] : other;
-          lo[s] = odd ? other : lo[s];
-        }
-      }
-      const bool live = active && v < q1;
-      uint64_t ylo = 0, yhi = 0;
-      if (live) {
-        const int64_t e = v * K;
-        seg = advance_segment(seg, e, s_end);
-        l128_fold_slot<N, B16>(lo, hi, seg, e, n, s_end, scale, scaled, ylo, yhi);
-        if (!k_set) {
-          k = fused_row_covering(f, e);
-          k_set = true;
-        }
-        if (!(shared_lane && odd)) l128_store<B16>(f, k, v, ylo, yhi);  // slot 14: the even line's lane
-      }
-      if (ONE) continue;  // the one-shot has every part: no result lines
-      const uint64_t w0 = wire_lo(ylo, yhi), w1 = wire_hi(yhi);
-      __syncwarp();
-#pragma unroll
-      for (int q = 0; q < N; ++q)
-        if (q != me && active) st_volatile_v2(gat_of(q) + ((int64_t)me * rl + l) * kL128Words + sub * 2, w0, w1);
-    }
+  };
+  // The CTA walks its line ranges in rounds of kL128Round lines per part, all three phases
+  // per round: a CTA's local phase 3 of round r then overlaps the NVLink pushes of round
+  // r + 1 (its own and other CTAs'), instead of every CTA pushing, then folding, then
+  // copying in lock-step (profiles/ll128_rounds_n4_r02.json).  Round r of a phase only waits
+  // on round r of the same CTA index on the peers, so there is no cycle.
+  int64_t span = 0;
+  for (int p = 0; p < (ONE ? 1 : N); ++p) {
+    int64_t q0, q1, l0, l1;
+    range_of(p, q0, q1, l0, l1);
+    span = l1 - l0 > span ? l1 - l0 : span;
   }
-  phase_mark(a, 2, cta);
-  // ---- phase 3: every peer part's result lines from my gather rows into my tensors
-  if (do_unpack && !ONE) {
-    int k = 0;
-    bool k_set = false;
+  int seg = 0, k2 = 0;
+  bool k2_set = false;
+  phase_mark(a, 0, cta);
+  for (int64_t off = 0; off < span && status == MGW_DEV_OK; off += kL128Round) {
+    // ---- phase 1: this round's lines of every part p into rank p's incoming row `me`
+    //      (one-shot: this round's lines of the whole bucket into every rank's row `me`)
+    if (do_push) {
 #pragma unroll 1
-    for (int p = 0; p < N && status == MGW_DEV_OK; ++p) {
-      if (p == me) continue;
-      const int64_t q0 = s_part[p], q1 = s_part[p + 1];
-      int64_t l0, l1;
-      l128_cta_lines(q1 - q0, cta, ctas, l0, l1);
-      const uint64_t* g = gat_of(me) + (int64_t)p * rl * kL128Words + sub * 2;
-      for (int64_t base = l0; base < l1; base += kL128Step) {
-        const int64_t l = base + grp;
-        const bool active = l < l1;
-        uint64_t w0 = 0, w1 = 0;
-        const int st = l128_poll(g + l * kL128Words, active, expect, hdr_mine + p, a, w0, w1);
-        if (st != MGW_DEV_OK) {
-          status = st;
-          break;
-        }
-        const int64_t v = q0 + l128_slot(l, sub);
-        const uint64_t other = __shfl_xor_sync(0xffffffffu, w0, kL128Lanes);  // slot 14's other half
-        if (shared_lane) w1 = other;  // the even line's lane 7 writes slot 14: (own half, odd half)
-        if (active && v < q1 && !(shared_lane && odd)) {
-          if (!k_set) {
-            k = fused_row_covering(f, v * K);
-            k_set = true;
+      for (int p = 0; p < (ONE ? 1 : N); ++p) {
+        int64_t q0, q1, l0, l1;
+        range_of(p, q0, q1, l0, l1);
+        const int64_t r0 = l0 + off, r1 = l0 + off + kL128Round < l1 ? l0 + off + kL128Round : l1;
+        int k = 0;
+        bool k_set = false;
+        for (int64_t base = r0; base < r1; base += kL128Step) {
+          const int64_t l = base + grp;
+          const int64_t v = q0 + l128_slot(l, sub);
+          const bool live = l < r1 && v < q1;
+          uint64_t lo = 0, hi = 0;
+          if (live) {
+            if (!k_set) {
+              k = fused_row_covering(f, v * K);
+              k_set = true;
+            }
+            l128_load<B16>(f, k, v, scale, scaled, lo, hi);
           }
-          l128_store<B16>(f, k, v, w0, w1);
+          const uint64_t w0 = wire_lo(lo, hi), w1 = wire_hi(hi);
+          __syncwarp();
+          if (l < r1) {
+            if (ONE) {
+#pragma unroll
+              for (int r = 0; r < N; ++r) {
+                const int q = me + 1 + r < N ? me + 1 + r : me + 1 + r - N;  // peers first, mine last
+                st_volatile_v2(in_of(q) + ((int64_t)me * rl + l) * kL128Words + sub * 2, w0, w1);
+              }
+            } else {
+              st_volatile_v2(in_of(p) + ((int64_t)me * rl + l) * kL128Words + sub * 2, w0, w1);
+            }
+          }
+        }
+      }
+    }
+    // ---- phase 2: fold this round's lines of my part from the N local rows; write my
+    //      tensors and every peer's gather row `me`
+    if (do_fold) {
+      int64_t q0, q1, l0, l1;
+      range_of(ONE ? 0 : me, q0, q1, l0, l1);
+      const int64_t r0 = l0 + off, r1 = l0 + off + kL128Round < l1 ? l0 + off + kL128Round : l1;
+      const uint64_t* in = in_of(me) + sub * 2;
+      for (int64_t base = r0; base < r1 && status == MGW_DEV_OK; base += kL128Step) {
+        const int64_t l = base + grp;
+        const bool active = l < r1;
+        const int64_t v = q0 + l128_slot(l, sub);
+        uint64_t lo[N], hi[N];
+#pragma unroll
+        for (int s = 0; s < N; ++s) {
+          lo[s] = hi[s] = 0;
+          if (active) ld_volatile_v2(in + ((int64_t)s * rl + l) * kL128Words, lo[s], hi[s]);
+        }
+#pragma unroll
+        for (int s = 0; s < N; ++s) {
+          const uint64_t flag = __shfl_sync(0xffffffffu, hi[s], (threadIdx.x & 31) | (kL128Lanes - 1));
+          if (!__all_sync(0xffffffffu, !active || flag == expect)) {
+            const int st =
+                l128_poll(in + ((int64_t)s * rl + l) * kL128Words, active, expect, hdr_mine + s, a, lo[s], hi[s]);
+            if (st != MGW_DEV_OK) status = st;
+          }
+        }
+        if (status != MGW_DEV_OK) break;
+        // lane 7: rebuild slot 14 from its own half and the partner line's (lane ^ 8)
+#pragma unroll
+        for (int s = 0; s < N; ++s) {
+          const uint64_t other = __shfl_xor_sync(0xffffffffu, lo[s], kL128Lanes);
+          if (shared_lane) {
+            hi[s] = odd ? lo[s] : other;
+            lo[s] = odd ? other : lo[s];
+          }
+        }
+        const bool live = active && v < q1;
+        uint64_t ylo = 0, yhi = 0;
+        if (live) {
+          const int64_t e = v * K;
+          seg = advance_segment(seg, e, s_end);
+          l128_fold_slot<N, B16>(lo, hi, seg, e, n, s_end, scale, scaled, ylo, yhi);
+          if (!k2_set) {
+            k2 = fused_row_covering(f, e);
+            k2_set = true;
+          }
+          if (!(shared_lane && odd)) l128_store<B16>(f, k2, v, ylo, yhi);  // slot 14: the even line's lane
+        }
+        if (ONE) continue;  // the one-shot has every part: no result lines
+        const uint64_t w0 = wire_lo(ylo, yhi), w1 = wire_hi(yhi);
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < N; ++q)
+          if (q != me && active) st_volatile_v2(gat_of(q) + ((int64_t)me * rl + l) * kL128Words + sub * 2, w0, w1);
+      }
+    }
+    // ---- phase 3: this round's lines of every peer part from my gather rows into my tensors
+    if (do_unpack && !ONE) {
+#pragma unroll 1
+      for (int p = 0; p < N && status == MGW_DEV_OK; ++p) {
+        if (p == me) continue;
+        int64_t q0, q1, l0, l1;
+        range_of(p, q0, q1, l0, l1);
+        const int64_t r0 = l0 + off, r1 = l0 + off + kL128Round < l1 ? l0 + off + kL128Round : l1;
+        const uint64_t* g = gat_of(me) + (int64_t)p * rl * kL128Words + sub * 2;
+        int k = 0;
+        bool k_set = false;
+        for (int64_t base = r0; base < r1; base += kL128Step) {
+          const int64_t l = base + grp;
+          const bool active = l < r1;
+          uint64_t w0 = 0, w1 = 0;
+          const int st = l128_poll(g + l * kL128Words, active, expect, hdr_mine + p, a, w0, w1);
+          if (st != MGW_DEV_OK) {
+            status = st;
+            break;
+          }
+          const int64_t v = q0 + l128_slot(l, sub);
+          const uint64_t other = __shfl_xor_sync(0xffffffffu, w0, kL128Lanes);  // slot 14's other half
+          if (shared_lane) w1 = other;  // the even line's lane 7 writes slot 14: (own half, odd half)
+          if (active && v < q1 && !(shared_lane && odd)) {
+            if (!k_set) {
+              k = fused_row_covering(f, v * K);
+              k_set = true;
+            }
+            l128_store<B16>(f, k, v, w0, w1);
+          }
         }
       }
     }
   }
   if (status != MGW_DEV_OK && (threadIdx.x & 31) == 0) ll_report(a, status);
-  phase_mark(a, 3, cta);
+  phase_mark(a, 1, cta);
   finish_call(a, ctas);
 }
 
