@@ -292,7 +292,6 @@ __device__ __forceinline__ void ll128_any_body(const L128Args& x, const int cta,
   grid_dep_wait();
   stamp_enter(a.stamp);
   __shared__ int64_t s_end[kMaxRanks];
-  __shared__ int64_t s_part[kMaxRanks + 1];
   const uint32_t epoch = load_volatile32(a.state) + 1u;
   const int parity = (int)(epoch & 1u);
   const int me = a.rank;
@@ -303,7 +302,6 @@ __device__ __forceinline__ void ll128_any_body(const L128Args& x, const int cta,
     const int64_t q = n / N, r = n % N;
     s_end[t] = (int64_t)(t + 1) * q + (t + 1 < r ? t + 1 : r);  // end of reference segment t
   }
-  if (threadIdx.x <= N) s_part[threadIdx.x] = part_begin(threadIdx.x, slots, N);  // (the one-shot: unused)
   // kSkipPack / kSkipPhase1 / kSkipPhase2 run one phase per launch (emulated ranks on one
   // device, tests only: every launch polls lines that earlier launches wrote)
   const bool do_push = !(a.flags & kSkipPack), do_fold = !(a.flags & kSkipPhase1),
@@ -329,23 +327,40 @@ __device__ __forceinline__ void ll128_any_body(const L128Args& x, const int cta,
   auto gat_of = [&](int r) { return reinterpret_cast<uint64_t*>(x.gat[r] + poff); };
   int status = MGW_DEV_OK;
 
-  // line range [l0, l1) of this CTA in part p (one-shot: the whole bucket)
-  auto range_of = [&](int p, int64_t& q0, int64_t& q1, int64_t& l0, int64_t& l1) {
-    q0 = ONE ? 0 : s_part[p];
-    q1 = ONE ? slots : s_part[p + 1];
+  // line range [l0, l1) of this CTA in part p (one-shot: the whole bucket), computed once
+  // per CTA into shared memory (the 64-bit divisions cost ~1 us per thread if repeated)
+  __shared__ int64_t s_rng[kMaxRanks][4];
+  __shared__ int64_t s_span;
+  if (threadIdx.x < (ONE ? 1 : N)) {
+    const int p = threadIdx.x;
+    const int64_t q0 = ONE ? 0 : part_begin(p, slots, N), q1 = ONE ? slots : part_begin(p + 1, slots, N);
+    int64_t l0, l1;
     l128_cta_lines(q1 - q0, cta, ctas, l0, l1);
+    s_rng[p][0] = q0;
+    s_rng[p][1] = q1;
+    s_rng[p][2] = l0;
+    s_rng[p][3] = l1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t span = 0;
+    for (int p = 0; p < (ONE ? 1 : N); ++p) span = s_rng[p][3] - s_rng[p][2] > span ? s_rng[p][3] - s_rng[p][2] : span;
+    s_span = span;
+  }
+  __syncthreads();
+  auto range_of = [&](int p, int64_t& q0, int64_t& q1, int64_t& l0, int64_t& l1) {
+    const int r = ONE ? 0 : p;
+    q0 = s_rng[r][0];
+    q1 = s_rng[r][1];
+    l0 = s_rng[r][2];
+    l1 = s_rng[r][3];
   };
   // The CTA walks its line ranges in rounds of kL128Round lines per part, all three phases
   // per round: a CTA's local phase 3 of round r then overlaps the NVLink pushes of round
   // r + 1 (its own and other CTAs'), instead of every CTA pushing, then folding, then
   // copying in lock-step (profiles/ll128_rounds_n4_r02.json).  Round r of a phase only waits
   // on round r of the same CTA index on the peers, so there is no cycle.
-  int64_t span = 0;
-  for (int p = 0; p < (ONE ? 1 : N); ++p) {
-    int64_t q0, q1, l0, l1;
-    range_of(p, q0, q1, l0, l1);
-    span = l1 - l0 > span ? l1 - l0 : span;
-  }
+  const int64_t span = s_span;
   int seg = 0, k2 = 0;
   bool k2_set = false;
   phase_mark(a, 0, cta);
