@@ -483,11 +483,11 @@ def _auto_rule(session: RingSession, n: int, fused: bool = False) -> int:
     if fused:
         world = session.config.n_workers
         nbytes = 4 * n
-        if world == 2 and (512 << 10) <= nbytes <= (8 << 20):
+        if world == 2 and (512 << 10) <= nbytes <= (16 << 20):
             return _native.ALGO_LL128_ONESHOT
         if 2 < world <= 4 and (256 << 10) <= nbytes <= (1 << 20):
             return _native.ALGO_LL128_ONESHOT
-        if (1 << 20) <= nbytes <= ((32 << 20) if world == 2 else (16 << 20)):
+        if (1 << 20) <= nbytes <= ((128 << 20) if world == 2 else ((64 << 20) if world <= 4 else (16 << 20))):
             return _native.ALGO_LL128
         if 4 * n <= ll_max_bytes(world):
             return _native.ALGO_LL

@@ -43,10 +43,19 @@ constexpr int kL128PairSlots = 2 * kL128Vec + 1;       // 16-B slots per line pa
 constexpr int kL128Step = kThreads / kL128Lanes;       // lines per CTA step (64 = 32 pairs)
 constexpr int kL128Words = 2 * kL128Lanes;             // u64 words per line
 #ifndef MGW_L128_ROUND_LINES
-#define MGW_L128_ROUND_LINES 128
+#define MGW_L128_ROUND_LINES 0  // A/B: a fixed round (multiple of 64 lines); 0 = by the CTA's span
 #endif
-constexpr int64_t kL128Round = MGW_L128_ROUND_LINES;   // lines per part per round (a multiple of kL128Step)
-static_assert(kL128Round % kL128Step == 0, "rounds are whole CTA steps");
+static_assert(MGW_L128_ROUND_LINES % kL128Step == 0, "rounds are whole CTA steps");
+// Lines per part per round for a CTA whose longest part range is `span` lines: about four
+// rounds, 64 or 128 lines (same-box A/B at N = 4, profiles/ll128_rounds_r02.json:
+// 16 MiB 2 x 64 -> 505 GB/s vs 478 in one round, 32 MiB 4 x 64 -> 542, 64 MiB 4 x 128 -> 578,
+// 128 MiB 8 x 128 -> 585).  Every rank derives the same span, so the same rounds: a CTA's
+// round r only ever waits on round r of the same CTA index elsewhere.
+__device__ __forceinline__ int64_t l128_round_lines(int64_t span, bool one) {
+  if (MGW_L128_ROUND_LINES > 0) return MGW_L128_ROUND_LINES;
+  if (one) return 2 * kL128Step;  // the one-shot: 128 (N = 2, 4 / 8 MiB: 334 / 431 vs 313 / 410 GB/s at 64)
+  return span / 4 > kL128Step ? 2 * kL128Step : kL128Step;
+}
 
 // Lines come in pairs: lanes 0..6 of the even line carry slots 0..6 of the pair, lanes
 // 0..6 of the odd line slots 7..13, and lane 7 of each line carries one 8-B half of slot
@@ -355,16 +364,17 @@ __device__ __forceinline__ void ll128_any_body(const L128Args& x, const int cta,
     l0 = s_rng[r][2];
     l1 = s_rng[r][3];
   };
-  // The CTA walks its line ranges in rounds of kL128Round lines per part, all three phases
+  // The CTA walks its line ranges in rounds (l128_round_lines) of lines per part, all three phases
   // per round: a CTA's local phase 3 of round r then overlaps the NVLink pushes of round
   // r + 1 (its own and other CTAs'), instead of every CTA pushing, then folding, then
   // copying in lock-step (profiles/ll128_rounds_n4_r02.json).  Round r of a phase only waits
   // on round r of the same CTA index on the peers, so there is no cycle.
   const int64_t span = s_span;
+  const int64_t round = l128_round_lines(span, ONE);
   int seg = 0, k2 = 0;
   bool k2_set = false;
   phase_mark(a, 0, cta);
-  for (int64_t off = 0; off < span && status == MGW_DEV_OK; off += kL128Round) {
+  for (int64_t off = 0; off < span && status == MGW_DEV_OK; off += round) {
     // ---- phase 1: this round's lines of every part p into rank p's incoming row `me`
     //      (one-shot: this round's lines of the whole bucket into every rank's row `me`)
     if (do_push) {
@@ -372,7 +382,7 @@ __device__ __forceinline__ void ll128_any_body(const L128Args& x, const int cta,
       for (int p = 0; p < (ONE ? 1 : N); ++p) {
         int64_t q0, q1, l0, l1;
         range_of(p, q0, q1, l0, l1);
-        const int64_t r0 = l0 + off, r1 = l0 + off + kL128Round < l1 ? l0 + off + kL128Round : l1;
+        const int64_t r0 = l0 + off, r1 = l0 + off + round < l1 ? l0 + off + round : l1;
         int k = 0;
         bool k_set = false;
         for (int64_t base = r0; base < r1; base += kL128Step) {
@@ -408,7 +418,7 @@ __device__ __forceinline__ void ll128_any_body(const L128Args& x, const int cta,
     if (do_fold) {
       int64_t q0, q1, l0, l1;
       range_of(ONE ? 0 : me, q0, q1, l0, l1);
-      const int64_t r0 = l0 + off, r1 = l0 + off + kL128Round < l1 ? l0 + off + kL128Round : l1;
+      const int64_t r0 = l0 + off, r1 = l0 + off + round < l1 ? l0 + off + round : l1;
       const uint64_t* in = in_of(me) + sub * 2;
       for (int64_t base = r0; base < r1 && status == MGW_DEV_OK; base += kL128Step) {
         const int64_t l = base + grp;
@@ -466,7 +476,7 @@ __device__ __forceinline__ void ll128_any_body(const L128Args& x, const int cta,
         if (p == me) continue;
         int64_t q0, q1, l0, l1;
         range_of(p, q0, q1, l0, l1);
-        const int64_t r0 = l0 + off, r1 = l0 + off + kL128Round < l1 ? l0 + off + kL128Round : l1;
+        const int64_t r0 = l0 + off, r1 = l0 + off + round < l1 ? l0 + off + round : l1;
         const uint64_t* g = gat_of(me) + (int64_t)p * rl * kL128Words + sub * 2;
         int k = 0;
         bool k_set = false;

@@ -255,15 +255,17 @@ int pick_algo(const mgw_comm* c, int64_t n, int algo) {
 // fused group exchange: LL push for small buckets, else pull one-shot / two-shot;
 // NVLS only when enabled (not bit-exact with the reference order)
 constexpr int64_t kLL128MinBytes = 1ll << 20;  // AUTO: LL128 from here (before LL's ceiling)
-inline int64_t ll128_max_bytes(const mgw_comm* c) { return c->world == 2 ? (32ll << 20) : (16ll << 20); }
+inline int64_t ll128_max_bytes(const mgw_comm* c) {
+  return c->world == 2 ? (128ll << 20) : (c->world <= 4 ? (64ll << 20) : (16ll << 20));
+}
 // AUTO's LL128 choice for a bucket of `bytes` (fp32 or bf16 alike), 0 = neither: the
-// one-shot (one hop, (N-1) x M x 16/15 out) for mid-size buckets, the two-shot above
-// (profiles/ll128_pairs_n{2,4}_r02.json, graph-timed bus GB/s: N=4 256 KiB 51 vs LL 35,
-// 1 MiB one-shot 140 vs two-shot 132, 2 MiB two-shot 236 vs one-shot 194, 16 MiB two-shot
-// 489 vs push 431, 32 MiB push 507 vs 494; N=2 one-shot to 8 MiB, two-shot to 32 MiB).
-// N > 4: the one-shot's (N-1) x M is unmeasured there, so only the two-shot.
+// one-shot (one hop, (N-1) x M x 16/15 out) for mid-size buckets, the two-shot (in rounds)
+// above, the push two-shot beyond (profiles/ll128_rounds_r02.json, graph-timed bus
+// GB/s, N=4: 1 MiB one-shot 140 vs two-shot 134, 2 MiB two-shot 235 vs 195, 16 MiB 505 vs
+// push 431, 64 MiB 578 vs 557, 128 MiB 585 vs the wide push 590; N=2: one-shot to 16 MiB,
+// two-shot to 128 MiB).  N > 4: unmeasured here, so only the two-shot, to 16 MiB.
 inline int ll128_pick(const mgw_comm* c, int64_t bytes) {
-  if (c->world == 2 && bytes >= (512ll << 10) && bytes <= (8ll << 20)) return MGW_ALGO_LL128_ONESHOT;
+  if (c->world == 2 && bytes >= (512ll << 10) && bytes <= (16ll << 20)) return MGW_ALGO_LL128_ONESHOT;
   if (c->world > 2 && c->world <= 4 && bytes >= (256ll << 10) && bytes <= kLL128MinBytes) return MGW_ALGO_LL128_ONESHOT;
   if (bytes >= kLL128MinBytes && bytes <= ll128_max_bytes(c)) return MGW_ALGO_LL128;
   return 0;

@@ -117,12 +117,12 @@ def test_auto_algorithm_rule_mirrors_the_native_choice():
         return _algo_for(SimpleNamespace(config=SimpleNamespace(n_workers=world)), nbytes // 4, fused=True)
 
     assert algo(2, 4096) == algo(2, 256 << 10) == _native.ALGO_LL
-    assert algo(2, 512 << 10) == algo(2, 8 << 20) == _native.ALGO_LL128_ONESHOT
-    assert algo(2, 16 << 20) == algo(2, 32 << 20) == _native.ALGO_LL128
-    assert algo(2, 64 << 20) == _native.ALGO_PUSH and algo(2, 2 << 30) == _native.ALGO_TWOSHOT
+    assert algo(2, 512 << 10) == algo(2, 16 << 20) == _native.ALGO_LL128_ONESHOT
+    assert algo(2, 32 << 20) == algo(2, 128 << 20) == _native.ALGO_LL128
+    assert algo(2, 256 << 20) == _native.ALGO_PUSH and algo(2, 2 << 30) == _native.ALGO_TWOSHOT
     assert algo(4, 128 << 10) == _native.ALGO_LL and algo(4, 256 << 10) == algo(4, 1 << 20) == _native.ALGO_LL128_ONESHOT
-    assert algo(4, 2 << 20) == algo(4, 16 << 20) == _native.ALGO_LL128
-    assert algo(4, 32 << 20) == algo(4, 64 << 20) == _native.ALGO_PUSH
+    assert algo(4, 2 << 20) == algo(4, 64 << 20) == _native.ALGO_LL128
+    assert algo(4, 128 << 20) == _native.ALGO_PUSH
     assert algo(8, 256 << 10) == _native.ALGO_LL and algo(8, 512 << 10) == _native.ALGO_PUSH_ONESHOT
     assert algo(8, 1 << 20) == _native.ALGO_LL128 and algo(8, 2 << 30) == _native.ALGO_TWOSHOT
     assert algo(8, 20 << 20) == _native.ALGO_PUSH
