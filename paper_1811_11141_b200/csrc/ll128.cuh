@@ -367,7 +367,7 @@ __device__ __forceinline__ void ll128_any_body(const L128Args& x, const int cta,
   // The CTA walks its line ranges in rounds (l128_round_lines) of lines per part, all three phases
   // per round: a CTA's local phase 3 of round r then overlaps the NVLink pushes of round
   // r + 1 (its own and other CTAs'), instead of every CTA pushing, then folding, then
-  // copying in lock-step (profiles/ll128_rounds_n4_r02.json).  Round r of a phase only waits
+  // copying in lock-step (profiles/ll128_rounds_r02.json).  Round r of a phase only waits
   // on round r of the same CTA index on the peers, so there is no cycle.
   const int64_t span = s_span;
   const int64_t round = l128_round_lines(span, ONE);
