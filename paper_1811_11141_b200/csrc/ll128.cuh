@@ -1,5 +1,5 @@
-// ll128.cuh -- flag-in-line two-shot ("LL128"): the push two-shot's data movement with no
-// barrier at all.  Same result as ring_allreduce (allreduce_net.py:370-411) on the group
+// ll128.cuh -- flag-in-line two-shot and one-shot ("LL128"): the push kernels' data movement
+// with no barrier at all.  Same result as ring_allreduce (allreduce_net.py:370-411) on the group
 // bucket (:499-509), bit for bit; fp32 (4 per 16-B slot, scaled at pack) and bf16 (8 per
 // slot, fp32 accumulation, scaled and rounded once by the part's owner, as bf16.cuh).
 //
@@ -21,6 +21,10 @@
 //            tensors and stores result lines into every peer's gather row `me`
 //   phase 3  CTA b polls its line range of every peer part in its gather rows and writes
 //            its tensors.
+// A CTA runs the three phases per round of 64-128 lines per part (l128_round_lines), so its
+// local copies overlap the NVLink traffic of the next round.  The one-shot (ONE) pushes its
+// line range of the whole bucket to every rank and folds the whole bucket locally: phases
+// 1-2 only, (N-1) x M x 16/15 out, one hop.
 //
 // Every CTA depends only on the same CTA index of its peers (same part / line split), so
 // the grid need not be co-resident across ranks.  Areas: incoming lines = slot[parity] of
