@@ -65,7 +65,7 @@ extern "C" {
 #define MGW_ALGO_PUSH 5 /* push-based two-shot (fused path only): every NVLink byte is a store */
 #define MGW_ALGO_PUSH_ONESHOT 6 /* push-based one-shot (fused path only): stores out, local fold */
 #define MGW_ALGO_PUSH_PIPE 7 /* pipelined push two-shot (fused path only): per-sub-chunk flags overlap the phases */
-#define MGW_ALGO_LL128 8 /* flag-in-line two-shot (fused fp32 and bf16 paths): 128-B lines, 7 x 16 B payload + flag, no barrier */
+#define MGW_ALGO_LL128 8 /* flag-in-line two-shot (fused fp32 and bf16 paths): 128-B lines of 120 B payload + flag, no barrier */
 #define MGW_ALGO_LL128_ONESHOT 9 /* flag-in-line one-shot (fused paths): the whole bucket to every rank in 128-B lines, one hop */
 
 /* schedule flags */

@@ -6,6 +6,7 @@ import ctypes
 
 import pytest
 
+from conftest import ROOT
 from paper_1811_11141_b200 import _native
 
 
@@ -93,3 +94,26 @@ def test_group_tag_mixes_layer_and_iteration():
     tags = {group_tag(low, it) for low in range(1, 60) for it in range(0, 50)}
     assert len(tags) == 59 * 50
     assert all(0 <= t < 1 << 32 for t in tags)
+
+
+def test_python_constants_match_the_header():
+    """Every MGW_ALGO_* / MGW_SCHED_* / MGW_OPT_* / MGW_DEV_* / status code the header
+    defines has the same value in _native (the ctypes binding a reference user imports)."""
+    import re
+
+    from paper_1811_11141_b200 import _native
+
+    header = (ROOT / "include" / "mgwfbp_b200.h").read_text()
+    defs = dict(re.findall(r"#define (MGW_[A-Z0-9_]+) (\d+)u?\b", header))
+    prefixes = {"MGW_ALGO_": "ALGO_", "MGW_SCHED_": "SCHED_", "MGW_OPT_": "OPT_", "MGW_DEV_": "DEV_"}
+    checked = 0
+    for name, value in defs.items():
+        for cprefix, pyprefix in prefixes.items():
+            if name.startswith(cprefix):
+                py = pyprefix + name[len(cprefix):]
+                assert hasattr(_native, py), py
+                assert getattr(_native, py) == int(value), (name, value, getattr(_native, py))
+                checked += 1
+    for name in ("MGW_OK", "MGW_EINVAL", "MGW_EPROTO", "MGW_ECUDA"):
+        assert getattr(_native, name) == int(defs[name]), name
+    assert checked >= 20
