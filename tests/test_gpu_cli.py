@@ -1,7 +1,7 @@
 """The CLI data verbs on GPUs (the reference's test_cli.py:163-204 for bench / emulate /
 worker, here over NVLink): `bench` writes the measurement CSV, `emulate` reports verified
 iterations, a hand-launched `worker` pair meets and measures, and a worker whose peer never
-comes exits 2 (ring failure) -- the last one needs a single GPU only."""
+comes exits 2 (ring failure) -- that one, and `bench --local-group`, need a single GPU only."""
 
 from __future__ import annotations
 
@@ -38,6 +38,19 @@ def test_bench_verb_writes_csv(tmp_path, two_gpus):
     ms = load_measurements(out)
     assert [m.nbytes for m in ms] == [4096, 65536, 1048576]
     assert all(m.n_nodes == 2 and 0 < m.seconds < 1e-2 for m in ms)
+
+
+def test_bench_verb_local_group_on_one_gpu(tmp_path):
+    """`bench --local-group`: the reference's bench verb through the real protocol with every
+    rank's CTAs in one cooperative launch on a single GPU (exact sums checked inside)."""
+    out = tmp_path / "bench.csv"
+    proc = _run(["bench", "--nodes", "4", "--local-group", "--sizes", "4096,65536,1048576,4194304", "--repeats", "2",
+                 "--warmups", "1", "--out", str(out)])
+    assert proc.returncode == 0, proc.stderr
+    ms = load_measurements(out)
+    assert [m.nbytes for m in ms] == [4096, 65536, 1048576, 4194304]
+    assert all(m.n_nodes == 4 and 0 < m.seconds < 1e-2 for m in ms)
+    assert "fitted: a=" in proc.stdout
 
 
 def test_emulate_verb_verified(tmp_path, two_gpus):
