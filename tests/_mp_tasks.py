@@ -459,7 +459,7 @@ def emulate_bf16_task(config, session, *, profile, plan):
 
 def wide_push_task(config, session, *, n32, n16):
     """Buckets above the wide-grid threshold (push two-shot at 512 CTAs, a second partial
-    wave): fp32 in three ragged rows and bf16 through AUTO (= the bf16 push), each rank
+    wave): fp32 in three ragged rows and bf16, both on the push two-shot, each rank
     regenerating every rank's seeded input to check its result against the oracle in place
     (the arrays are too large to ship back).  Returns mismatch counts."""
     import ctypes
@@ -495,7 +495,7 @@ def wide_push_task(config, session, *, n32, n16):
         t = torch.from_numpy(ins16[config.rank].view(np.int16).copy()).view(torch.bfloat16).to(session.device)
         table = _native.DeviceTable([(t.data_ptr(), n16, 0)])
         _native.call("mgw_allreduce_fused_bf16", session.comm, table.ptr, 1, n16, ctypes.c_float(0.5),
-                     _native.ALGO_AUTO, h)
+                     _native.ALGO_PUSH, h)
         session.stream.synchronize()
         session.raise_if_failed()
         got = t.view(torch.int16).cpu().numpy().view(np.uint16)

@@ -307,7 +307,7 @@ def test_emulate_bf16_engine_verified():
 
 def test_wide_push_grid_above_threshold_vs_oracle():
     """Buckets >= 112 MiB launch the push two-shot with 512 CTAs (two waves over the 296
-    resident): still bit-exact vs the oracle, fp32 (ragged rows) and bf16 (AUTO -> push)."""
+    resident): still bit-exact vs the oracle, fp32 (ragged rows) and bf16."""
     n32 = (112 << 20) // 4 + 12_347
     n16 = (112 << 20) // 2 + 9_001
     n = min(_worlds())
